@@ -1,0 +1,543 @@
+// extern "C" boundary (include/blws_cuda.h): handles, status codes, copies.
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <unordered_set>
+
+#include "../../include/blws_cuda.h"
+#include "host.hpp"
+#include "ops.cuh"
+
+using namespace blws;
+
+struct blws_context {
+    std::unique_ptr<Context> ctx;
+};
+struct blws_rng {
+    Rng rng;
+};
+struct blws_operator {
+    blws_context* owner;
+    std::unique_ptr<LinearOperator> op;
+    bool dense = true;
+};
+struct blws_warm_start {
+    blws_context* owner;
+    DWarm w;
+};
+struct blws_svd_backend {
+    blws_context* owner;
+    std::unique_ptr<SvdBackend> b;
+};
+
+namespace {
+thread_local std::string g_err;
+
+template <typename F>
+int guard(F&& f) {
+    try {
+        f();
+        return BLWS_OK;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return BLWS_INVALID_ARGUMENT;
+    } catch (const CudaError& e) {
+        g_err = e.what();
+        return BLWS_CUDA_ERROR;
+    } catch (const std::bad_alloc& e) {
+        g_err = std::string("allocation failed: ") + e.what();
+        return BLWS_CUDA_ERROR;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return BLWS_NUMERICAL_FAILURE;
+    }
+}
+
+void need(bool c, const char* msg) {
+    if (!c) throw std::invalid_argument(msg);
+}
+
+blws_warm_start* wrap(blws_context* owner, DWarm w) { return new blws_warm_start{owner, std::move(w)}; }
+
+void copy_in(Context& ctx, View dst, const double* src, Index ld, int where) {
+    if (where == BLWS_HOST)
+        upload(ctx, dst, src, ld);
+    else
+        copy(ctx, dst, View{const_cast<double*>(src), dst.rows, dst.cols, ld});
+}
+
+void copy_out(Context& ctx, View src, double* dst, Index ld, int where) {
+    if (!dst) return;
+    if (where == BLWS_HOST)
+        download(ctx, src, dst, ld);
+    else
+        copy(ctx, View{dst, src.rows, src.cols, ld}, src);
+}
+
+void put_stats(const SolverStats& s, blws_solver_stats* o, int64_t* pr, int64_t* mh, double* rh, int64_t cap) {
+    if (o) {
+        o->iterations = s.iterations;
+        o->wall_time_s = s.wall_time_s;
+        o->matvec_count = s.matvec_count;
+        o->matvec_init = s.matvec_init;
+        o->rel_err = s.rel_err;
+        o->rank_hat = s.rank_hat;
+        o->e_l0 = s.e_l0;
+        o->e_nnz = s.e_nnz;
+        o->converged = s.converged ? 1 : 0;
+    }
+    for (int64_t i = 0; i < std::min<int64_t>(cap, static_cast<int64_t>(s.predicted_ranks.size())); ++i)
+        if (pr) pr[i] = s.predicted_ranks[i];
+    for (int64_t i = 0; i < std::min<int64_t>(cap, static_cast<int64_t>(s.matvec_history.size())); ++i)
+        if (mh) mh[i] = s.matvec_history[i];
+    for (int64_t i = 0; i < std::min<int64_t>(cap, static_cast<int64_t>(s.residual_history.size())); ++i)
+        if (rh) rh[i] = s.residual_history[i];
+}
+}  // namespace
+
+extern "C" {
+
+const char* blws_last_error(void) { return g_err.c_str(); }
+int blws_abi_version(void) { return 1; }
+
+// ---------------------------------------------------------------- context
+int blws_context_create(int device, blws_context** out) {
+    return guard([&] {
+        need(out != nullptr, "blws_context_create: null out");
+        auto c = std::make_unique<blws_context>();
+        c->ctx = std::make_unique<Context>(device);
+        *out = c.release();
+    });
+}
+int blws_context_destroy(blws_context* ctx) {
+    return guard([&] { delete ctx; });
+}
+int blws_context_synchronize(blws_context* ctx) {
+    return guard([&] { ctx->ctx->sync(); });
+}
+void* blws_context_stream(blws_context* ctx) { return ctx ? ctx->ctx->stream() : nullptr; }
+int64_t blws_context_launches(const blws_context* ctx) { return ctx ? ctx->ctx->launches() : 0; }
+int blws_context_set_profiling(blws_context* ctx, int on) {
+    return guard([&] { ctx->ctx->set_profiling(on != 0); });
+}
+int blws_context_region_stats(blws_context* ctx, int region, double* total_ms, int64_t* count, double* flops,
+                              double* bytes) {
+    return guard([&] {
+        need(region >= 0 && region < 8, "region out of range");
+        ctx->ctx->region_stats(region, total_ms, count, flops, bytes);
+    });
+}
+int blws_context_region_reset(blws_context* ctx) {
+    return guard([&] { ctx->ctx->region_reset(); });
+}
+int blws_fp64_peak(blws_context* ctx, int mode, double* tflops) {
+    return guard([&] { *tflops = fp64_peak_tflops(*ctx->ctx, mode); });
+}
+
+// -------------------------------------------------------------------- rng
+int blws_rng_create(uint64_t seed, blws_rng** out) {
+    return guard([&] { *out = new blws_rng{Rng(seed)}; });
+}
+int blws_rng_destroy(blws_rng* r) {
+    delete r;
+    return BLWS_OK;
+}
+int blws_rng_split(const blws_rng* r, uint64_t tag, blws_rng** out) {
+    return guard([&] { *out = new blws_rng{r->rng.split(tag)}; });
+}
+uint64_t blws_rng_next_u64(blws_rng* r) { return r->rng.next_u64(); }
+double blws_rng_uniform(blws_rng* r, double lo, double hi) { return r->rng.uniform(lo, hi); }
+uint64_t blws_rng_uniform_index(blws_rng* r, uint64_t n) { return r->rng.uniform_index(n); }
+double blws_rng_normal(blws_rng* r) { return r->rng.normal(); }
+int blws_rng_gaussian_matrix(blws_rng* r, int64_t rows, int64_t cols, double* out) {
+    return guard([&] { r->rng.gaussian_matrix(rows, cols, out, rows); });
+}
+int64_t blws_sample_distinct(int64_t n, int64_t s, blws_rng* r, int64_t* out) {
+    // Floyd's algorithm (synth.hpp:23-33); the accepted set decides each step,
+    // so a bitmap gives the same draws as the reference's hash set.
+    std::vector<std::uint64_t> bits(static_cast<size_t>((n + 63) / 64), 0);
+    auto test_set = [&](int64_t t) {
+        std::uint64_t& w = bits[static_cast<size_t>(t >> 6)];
+        const std::uint64_t mask = 1ull << (t & 63);
+        const bool had = (w & mask) != 0;
+        w |= mask;
+        return had;
+    };
+    for (int64_t j = n - s; j < n; ++j) {
+        const auto t = static_cast<int64_t>(r->rng.uniform_index(static_cast<uint64_t>(j + 1)));
+        if (test_set(t)) test_set(j);
+    }
+    int64_t c = 0;
+    for (int64_t w = 0; w < static_cast<int64_t>(bits.size()); ++w) {
+        std::uint64_t x = bits[static_cast<size_t>(w)];
+        while (x) {
+            out[c++] = w * 64 + __builtin_ctzll(x);
+            x &= x - 1;
+        }
+    }
+    return c;
+}
+
+// -------------------------------------------------------------- operators
+int blws_dense_operator_create(blws_context* ctx, int64_t m, int64_t n, const double* w, int64_t ldw, int where,
+                               int borrow, blws_operator** out) {
+    return guard([&] {
+        need(m > 0 && n > 0 && w && ldw >= m, "DenseOperator: bad shape");
+        Context& c = *ctx->ctx;
+        auto h = std::make_unique<blws_operator>();
+        h->owner = ctx;
+        if (where == BLWS_DEVICE && borrow) {
+            need(ldw % 2 == 0 && reinterpret_cast<uintptr_t>(w) % 16 == 0,
+                 "DenseOperator: borrowed W needs an even leading dimension and 16-byte alignment");
+            auto op = std::make_unique<DenseOperator>(c, m, n, const_cast<double*>(w), ldw);
+            op->check_finite();
+            h->op = std::move(op);
+        } else {
+            auto op = std::make_unique<DenseOperator>(c, m, n);
+            if (where == BLWS_HOST)
+                op->assign_host(w, ldw);
+            else
+                op->assign_device(w, ldw);
+            h->op = std::move(op);
+        }
+        *out = h.release();
+    });
+}
+int blws_dense_operator_assign(blws_operator* op, const double* w, int64_t ldw, int where) {
+    return guard([&] {
+        need(op->dense, "assign: not a dense operator");
+        auto* d = static_cast<DenseOperator*>(op->op.get());
+        if (where == BLWS_HOST)
+            d->assign_host(w, ldw);
+        else
+            d->assign_device(w, ldw);
+    });
+}
+int blws_sparse_operator_create(blws_context* ctx, int64_t m, int64_t n, int64_t nnz, const int64_t* colptr,
+                                const int32_t* rowidx, const double* values, blws_operator** out) {
+    return guard([&] {
+        need(m > 0 && n > 0 && nnz >= 0, "SparseOperator: bad shape");
+        auto h = std::make_unique<blws_operator>();
+        h->owner = ctx;
+        h->dense = false;
+        h->op = std::make_unique<SparseOperator>(*ctx->ctx, m, n, nnz, colptr, rowidx, values);
+        *out = h.release();
+    });
+}
+int blws_sparse_operator_assign_values(blws_operator* op, const double* values, int64_t nnz, int where) {
+    return guard([&] {
+        need(!op->dense, "assign_values: not a sparse operator");
+        auto* s = static_cast<SparseOperator*>(op->op.get());
+        need(nnz == s->nnz(), "SparseOperator: value count does not match pattern");
+        if (where == BLWS_HOST) {
+            for (int64_t i = 0; i < nnz; ++i)
+                if (!std::isfinite(values[i])) throw std::invalid_argument("SparseOperator: non-finite entries");
+            s->assign_values_host(values);
+        } else {
+            s->assign_values_device(values);
+        }
+    });
+}
+int blws_operator_destroy(blws_operator* op) {
+    return guard([&] { delete op; });
+}
+int64_t blws_operator_rows(const blws_operator* op) { return op->op->rows(); }
+int64_t blws_operator_cols(const blws_operator* op) { return op->op->cols(); }
+int64_t blws_operator_application_count(const blws_operator* op) { return op->op->application_count(); }
+int blws_operator_apply_pair_block(blws_operator* op, int64_t b, const double* left, const double* right,
+                                   double* top, double* bot) {
+    return guard([&] {
+        Context& c = op->op->ctx();
+        const Index m = op->op->rows(), n = op->op->cols();
+        DMat l(c, m, b), r(c, n, b), t(c, m, b), bt(c, n, b);
+        upload(c, l.view(), left, m);
+        upload(c, r.view(), right, n);
+        op->op->apply_pair_block(l.view(), r.view(), t.view(), bt.view());
+        download(c, t.view(), top, m);
+        download(c, bt.view(), bot, n);
+    });
+}
+
+// ------------------------------------------------------------- warm start
+int blws_warm_start_create(blws_context* ctx, int64_t m, int64_t n, int64_t r, const double* u, int64_t ldu,
+                           const double* v, int64_t ldv, const double* sigma, int where, blws_warm_start** out) {
+    return guard([&] {
+        need(m > 0 && n > 0 && r >= 0, "WarmStart: bad shape");
+        Context& c = *ctx->ctx;
+        DWarm w = make_warm(c, m, n, r);
+        if (r > 0) {
+            copy_in(c, w.u(), u, ldu, where);
+            copy_in(c, w.v(), v, ldv, where);
+            std::copy(sigma, sigma + r, w.sigma.begin());
+        }
+        *out = wrap(ctx, std::move(w));
+    });
+}
+int blws_warm_start_copy(const blws_warm_start* src, blws_warm_start** out) {
+    return guard([&] { *out = wrap(src->owner, copy_warm(*src->owner->ctx, src->w, src->w.rank())); });
+}
+int64_t blws_warm_start_rank(const blws_warm_start* w) { return w->w.rank(); }
+int blws_warm_start_get(const blws_warm_start* w, double* u, int64_t ldu, double* v, int64_t ldv, double* sigma,
+                        int where) {
+    return guard([&] {
+        Context& c = *w->owner->ctx;
+        copy_out(c, w->w.u(), u, ldu, where);
+        copy_out(c, w->w.v(), v, ldv, where);
+        if (sigma) std::copy(w->w.sigma.begin(), w->w.sigma.end(), sigma);
+        c.sync();
+    });
+}
+int blws_warm_start_destroy(blws_warm_start* w) {
+    return guard([&] { delete w; });
+}
+
+// ---------------------------------------------------------- block lanczos
+int blws_svd(blws_operator* w, const blws_warm_start* warm, int64_t k, int64_t r, blws_rng* rng,
+             blws_warm_start** out, int* flags) {
+    return guard([&] {
+        need(w && warm && rng && out, "blws_svd: null argument");
+        auto res = blws::blws_svd(*w->op, warm->w, k, r, rng->rng);
+        if (flags) *flags = (res.padded ? 1 : 0) | (res.k_raised ? 2 : 0) | (res.terminated_early ? 4 : 0);
+        *out = wrap(w->owner, std::move(res.warm));
+    });
+}
+int blws_adapt_subspace(blws_context* ctx, const blws_warm_start* warm, int64_t r_new, int64_t m, int64_t n,
+                        blws_rng* rng, blws_warm_start** out) {
+    return guard([&] {
+        DWarm o = blws::adapt_subspace(*ctx->ctx, warm ? &warm->w : nullptr, r_new, m, n, rng->rng);
+        *out = wrap(ctx, std::move(o));
+    });
+}
+int blws_block_lanczos_procedure(blws_operator* w, int64_t b, const double* x1, int64_t k, double* q, double* t,
+                                 int64_t* built, int* terminated_early) {
+    return guard([&] {
+        Context& c = w->op->ctx();
+        const Stack geo{w->op->rows(), w->op->cols()};
+        const Index dim = geo.m + geo.n;
+        DMat x(c, geo.ld(), b, true);
+        upload(c, View{x.data(), geo.m, b, x.ld}, x1, dim);
+        upload(c, View{x.data() + geo.mp(), geo.n, b, x.ld}, x1 + geo.m, dim);
+        auto f = blws::block_lanczos_procedure(*w->op, x.view(), k);
+        const Index cols = f.built * b;
+        download(c, View{f.q.data(), geo.m, cols, f.q.ld}, q, dim);
+        download(c, View{f.q.data() + geo.mp(), geo.n, cols, f.q.ld}, q + geo.m, dim);
+        std::vector<double> tt(static_cast<size_t>(cols * cols), 0.0);
+        std::vector<double> blk(static_cast<size_t>(b * b));
+        for (Index l = 0; l < f.built; ++l) {
+            download(c, f.m[l].view(), blk.data(), b);
+            for (Index j = 0; j < b; ++j)
+                for (Index i = 0; i < b; ++i) tt[(l * b + i) + (l * b + j) * cols] = blk[i + j * b];
+            if (l + 1 < f.built) {
+                download(c, f.b[l].view(), blk.data(), b);
+                for (Index j = 0; j < b; ++j)
+                    for (Index i = 0; i < b; ++i) {
+                        tt[(l * b + b + i) + (l * b + j) * cols] = blk[i + j * b];
+                        tt[(l * b + j) + (l * b + b + i) * cols] = blk[i + j * b];
+                    }
+            }
+        }
+        std::copy(tt.begin(), tt.end(), t);
+        *built = f.built;
+        *terminated_early = f.terminated_early ? 1 : 0;
+    });
+}
+
+// ---------------------------------------------------------------- lanczos
+int blws_lanczos_partial_svd(blws_operator* w, int64_t r, double tol, int64_t max_k, uint64_t seed,
+                             blws_warm_start** out, int64_t stats[4]) {
+    return guard([&] {
+        LanczosOptions o;
+        o.tol = tol;
+        o.max_k = max_k;
+        o.seed = seed;
+        auto res = blws::lanczos_partial_svd(*w->op, r, o);
+        if (stats) {
+            stats[0] = res.stats.steps;
+            stats[1] = res.stats.restarts;
+            stats[2] = res.stats.converged;
+            stats[3] = res.stats.all_converged ? 1 : 0;
+        }
+        *out = wrap(w->owner, std::move(res.uv));
+    });
+}
+int blws_spectral_norm(blws_operator* w, double tol, uint64_t seed, double* out) {
+    return guard([&] { *out = blws::spectral_norm(*w->op, tol, seed); });
+}
+
+// ------------------------------------------------- dense kernels (device)
+int blws_thin_qr(blws_context* ctx, int64_t rows, int64_t cols, const double* m, double* q, double* r,
+                 int64_t* rank) {
+    return guard([&] {
+        need(rows > 0 && cols > 0, "thin_qr: empty matrix");
+        need(rows >= cols, "thin_qr: requires rows >= cols");
+        for (int64_t i = 0; i < rows * cols; ++i)
+            if (!std::isfinite(m[i])) throw std::invalid_argument("thin_qr: non-finite entries");
+        Context& c = *ctx->ctx;
+        DMat x(c, rows, cols), rr(c, cols, cols);
+        upload(c, x.view(), m, rows);
+        View rv = rr.view();
+        *rank = blws::thin_qr(c, x.view(), &rv);
+        download(c, x.view(), q, rows);
+        if (r) download(c, rr.view(), r, cols);
+    });
+}
+int blws_sym_evd(blws_context* ctx, int64_t n, const double* t, double* values, double* vectors) {
+    return guard([&] {
+        need(n > 0, "sym_evd_small: not square");
+        need(n <= 4096, "sym_evd_small: too large");
+        double nrm = 0, asym = 0;
+        for (int64_t j = 0; j < n; ++j)
+            for (int64_t i = 0; i < n; ++i) {
+                const double a = t[i + j * n];
+                if (!std::isfinite(a)) throw std::invalid_argument("sym_evd_small: non-finite entries");
+                nrm += a * a;
+                const double d = a - t[j + i * n];
+                asym += d * d;
+            }
+        if (std::sqrt(asym) > 1e-10 * std::sqrt(nrm) && nrm > 0)
+            throw std::invalid_argument("sym_evd_small: input is not symmetric");
+        Context& c = *ctx->ctx;
+        DMat a(c, n, n), s(c, n, n), vec(c, n, n);
+        upload(c, a.view(), t, n);
+        blws::symmetrize(c, s.view(), a.view());
+        DBuf<double> vals(c, static_cast<size_t>(n));
+        sym_evd_jacobi(c, s.view(), vals.get(), vec.view());
+        c.read(vals.get(), values, n);
+        download(c, vec.view(), vectors, n);
+    });
+}
+int blws_sym_evd_tridiagonal_top(blws_context* ctx, int64_t n, const double* d, const double* e, int64_t want,
+                                 double* values, double* vectors) {
+    return guard([&] {
+        need(n > 0, "sym_evd_tridiagonal: empty");
+        need(n <= 4096, "sym_evd_tridiagonal: too large");
+        need(want >= 1 && want <= n, "sym_evd_tridiagonal: bad want");
+        Context& c = *ctx->ctx;
+        DBuf<double> dd(c, static_cast<size_t>(n)), ee(c, static_cast<size_t>(std::max<int64_t>(n - 1, 1))),
+            vals(c, static_cast<size_t>(want));
+        c.write(dd.get(), d, n);
+        if (n > 1) c.write(ee.get(), e, n - 1);
+        DMat vec(c, n, want);
+        tridiag_eig_top(c, n, dd.get(), ee.get(), want, vals.get(), vec.view());
+        c.read(vals.get(), values, want);
+        download(c, vec.view(), vectors, n);
+    });
+}
+int blws_dgemm(blws_context* ctx, int ta, int tb, int64_t m, int64_t n, int64_t k, double alpha, const double* a,
+               int64_t lda, const double* b, int64_t ldb, double beta, double* c, int64_t ldc) {
+    return guard([&] { gemm(*ctx->ctx, ta != 0, tb != 0, m, n, k, alpha, a, lda, b, ldb, beta, c, ldc); });
+}
+
+// ------------------------------------------------------------ backend/svt
+int blws_svd_backend_create(blws_context* ctx, int kind, int64_t block_steps, double ritz_tol, int64_t max_k,
+                            int64_t seed_margin, uint64_t seed, blws_svd_backend** out) {
+    return guard([&] {
+        need(kind == BLWS_BACKEND_LANCZOS || kind == BLWS_BACKEND_BLWS,
+             "SvdBackend: kind must be lanczos (1) or blws (2); exact-full is the CPU test oracle");
+        SvdBackend::Options o;
+        o.block_steps = block_steps;
+        o.ritz_tol = ritz_tol;
+        o.max_k = max_k;
+        o.seed_margin = seed_margin;
+        o.seed = seed;
+        *out = new blws_svd_backend{ctx, std::make_unique<SvdBackend>(*ctx->ctx, static_cast<SvdBackend::Kind>(kind), o)};
+    });
+}
+int blws_svd_backend_destroy(blws_svd_backend* b) {
+    return guard([&] { delete b; });
+}
+int blws_svd_backend_warm_state(const blws_svd_backend* b, blws_warm_start** out) {
+    return guard([&] {
+        const auto& w = b->b->warm_state();
+        *out = w ? wrap(b->owner, copy_warm(*b->owner->ctx, *w, w->rank())) : nullptr;
+    });
+}
+int blws_svd_backend_set_warm_state(blws_svd_backend* b, const blws_warm_start* w) {
+    return guard([&] { b->b->set_warm(copy_warm(*b->owner->ctx, w->w, w->w.rank())); });
+}
+int blws_svt(blws_operator* w, double eps, blws_svd_backend* backend, blws_rank_predictor* pred, int64_t* history,
+             int64_t history_cap, int64_t* history_len, blws_warm_start** out, int64_t* achieved_rank,
+             int* all_above_threshold) {
+    return guard([&] {
+        RankPredictor p;
+        p.r = pred->r;
+        p.increment = pred->increment;
+        p.max_rank = pred->max_rank;
+        auto res = blws::svt(*w->op, eps, *backend->b, p);
+        pred->r = p.r;
+        if (history && history_len && *history_len < history_cap) history[(*history_len)++] = p.history.back();
+        if (achieved_rank) *achieved_rank = res.achieved_rank;
+        if (all_above_threshold) *all_above_threshold = res.all_above_threshold ? 1 : 0;
+        if (out) *out = wrap(w->owner, std::move(res.trip));
+    });
+}
+
+// ---------------------------------------------------------------- solvers
+int blws_rpca_adm(blws_context* ctx, int64_t m, const double* d, int64_t ldd, int where, double lambda,
+                  blws_svd_backend* backend, const blws_rpca_options* opts, const double* truth, double* a_out,
+                  double* e_out, blws_solver_stats* stats, int64_t* predicted_ranks, int64_t* matvec_history,
+                  double* residual_history, int64_t hist_cap) {
+    return guard([&] {
+        need(m > 0 && d && ldd >= m, "rpca_adm: bad D");
+        Context& c = *ctx->ctx;
+        RpcaOptions o;
+        if (opts) {
+            o.tol_outer = opts->tol_outer;
+            o.max_iter = opts->max_iter;
+            o.rho = opts->rho;
+            o.mu_max_factor = opts->mu_max_factor;
+            o.initial_rank = opts->initial_rank;
+            o.rank_increment = opts->rank_increment;
+        }
+        const Index ld = std::max<Index>(2, round_up(m, 2));
+        if (where == BLWS_DEVICE && ldd % 2 == 0) {
+            auto s = blws::rpca_adm(c, m, d, ldd, lambda, *backend->b, o, truth, a_out, e_out);
+            put_stats(s, stats, predicted_ranks, matvec_history, residual_history, hist_cap);
+            return;
+        }
+        DMat dd(c, m, m, false);
+        copy_in(c, dd.view(), d, ldd, where);
+        DMat tr, a, e;
+        if (truth) {
+            tr = DMat(c, m, m, false);
+            copy_in(c, tr.view(), truth, ldd, where);
+        }
+        if (a_out) a = DMat(c, m, m, false);
+        if (e_out) e = DMat(c, m, m, false);
+        auto s = blws::rpca_adm(c, m, dd.data(), ld, lambda, *backend->b, o, truth ? tr.data() : nullptr,
+                                a_out ? a.data() : nullptr, e_out ? e.data() : nullptr);
+        if (a_out) copy_out(c, a.view(), a_out, ldd, where);
+        if (e_out) copy_out(c, e.view(), e_out, ldd, where);
+        c.sync();
+        put_stats(s, stats, predicted_ranks, matvec_history, residual_history, hist_cap);
+    });
+}
+
+int blws_mc_svt(blws_context* ctx, int64_t m, int64_t n, int64_t nnz, const int64_t* colptr, const int32_t* rowidx,
+                const double* values, double tau, double delta, blws_svd_backend* backend, const blws_mc_options* opts,
+                const double* truth_ml, const double* truth_mr, int64_t r_true, double* u, double* sigma, double* v,
+                int64_t cap, int64_t* rank, blws_solver_stats* stats, int64_t* predicted_ranks,
+                int64_t* matvec_history, double* residual_history, int64_t hist_cap) {
+    return guard([&] {
+        Context& c = *ctx->ctx;
+        McOptions o;
+        if (opts) {
+            o.tol_outer = opts->tol_outer;
+            o.max_iter = opts->max_iter;
+            o.initial_rank = opts->initial_rank;
+            o.rank_increment = opts->rank_increment;
+        }
+        auto sol = blws::mc_svt(c, m, n, nnz, colptr, rowidx, values, tau, delta, *backend->b, o, truth_ml, truth_mr,
+                                r_true);
+        const Index k = sol.uv.rank();
+        if (rank) *rank = k;
+        if (k > cap) throw std::invalid_argument("mc_svt: output capacity too small");
+        if (u) download(c, sol.uv.u(), u, m);
+        if (v) download(c, sol.uv.v(), v, n);
+        if (sigma) std::copy(sol.uv.sigma.begin(), sol.uv.sigma.end(), sigma);
+        put_stats(sol.stats, stats, predicted_ranks, matvec_history, residual_history, hist_cap);
+    });
+}
+
+}  // extern "C"

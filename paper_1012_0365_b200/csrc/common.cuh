@@ -1,0 +1,156 @@
+// Shared device/host infrastructure for the B200 BLWS library.
+//
+// Layout conventions: every matrix is column-major fp64 with an
+// even leading dimension so that 16-byte cp.async / vector accesses stay
+// aligned. A "stacked panel" holds an (m+n) x b block of the augmented
+// operator [[0,W],[W^T,0]] (block_lanczos.hpp, augmented_operator.hpp): rows
+// [0, m) are the top (W's row space, U), rows [mp, mp+n) the bottom (W's column
+// space, V), with mp = round_up(m, 2); padding rows are kept at exactly zero.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace blws {
+
+using Index = std::int64_t;
+
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct NumericalError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+#define BLWS_CUDA(call)                                                                         \
+    do {                                                                                        \
+        cudaError_t _e = (call);                                                                \
+        if (_e != cudaSuccess)                                                                  \
+            throw ::blws::CudaError(std::string(#call) + ": " + cudaGetErrorString(_e) + " (" + \
+                                    __FILE__ + ":" + std::to_string(__LINE__) + ")");           \
+    } while (0)
+
+inline Index round_up(Index x, Index a) { return (x + a - 1) / a * a; }
+inline Index ceil_div(Index x, Index a) { return (x + a - 1) / a; }
+
+/// Per-solve device context: one stream, stream-ordered pool allocations,
+/// pinned staging for the small device->host reads the control flow needs,
+/// and a counter of kernel launches issued through it.
+class Context {
+public:
+    explicit Context(int device);
+    ~Context();
+    Context(const Context&) = delete;
+    Context& operator=(const Context&) = delete;
+
+    cudaStream_t stream() const { return stream_; }
+    int device() const { return device_; }
+    int sm_count() const { return sms_; }
+
+    void* alloc(size_t bytes);
+    void free(void* p);
+    void sync();
+    /// Copies `count` doubles device->host through pinned staging and waits.
+    void read(const double* dev, double* host, size_t count);
+    void read_i64(const std::int64_t* dev, std::int64_t* host, size_t count);
+    void write(double* dev, const double* host, size_t count);
+    void note_launch(std::int64_t n = 1) { launches_ += n; }
+    /// Optional CUDA-event timing of named regions (bench roofline evidence).
+    void set_profiling(bool on) { profiling_ = on; }
+    bool profiling() const { return profiling_; }
+    void region_begin(int id);
+    void region_end(int id, double flops, double bytes);
+    /// total ms, count, flops, bytes of region `id` (syncs; resolves events)
+    void region_stats(int id, double* ms, std::int64_t* count, double* flops, double* bytes);
+    void region_reset();
+    std::int64_t launches() const { return launches_; }
+    void check_launch(const char* what);
+
+private:
+    int device_ = 0;
+    int sms_ = 148;
+    cudaStream_t stream_ = nullptr;
+    void* pinned_ = nullptr;
+    size_t pinned_bytes_ = 0;
+    std::int64_t launches_ = 0;
+    bool profiling_ = false;
+    struct Region {
+        std::vector<cudaEvent_t> begin, end;
+        double flops = 0, bytes = 0, ms = 0;
+        std::int64_t count = 0;
+    };
+    Region regions_[8];
+    void ensure_pinned(size_t bytes);
+};
+
+/// Owning device buffer of doubles (or raw bytes), freed stream-ordered.
+template <typename T>
+class DBuf {
+public:
+    DBuf() = default;
+    DBuf(Context& ctx, size_t count) : ctx_(&ctx), n_(count) {
+        if (count) p_ = static_cast<T*>(ctx.alloc(sizeof(T) * count));
+    }
+    ~DBuf() { reset(); }
+    DBuf(DBuf&& o) noexcept : ctx_(o.ctx_), p_(o.p_), n_(o.n_) {
+        o.p_ = nullptr;
+        o.n_ = 0;
+    }
+    DBuf& operator=(DBuf&& o) noexcept {
+        if (this != &o) {
+            reset();
+            ctx_ = o.ctx_;
+            p_ = o.p_;
+            n_ = o.n_;
+            o.p_ = nullptr;
+            o.n_ = 0;
+        }
+        return *this;
+    }
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    void reset() {
+        if (p_ && ctx_) ctx_->free(p_);
+        p_ = nullptr;
+        n_ = 0;
+    }
+    T* get() const { return p_; }
+    size_t size() const { return n_; }
+
+private:
+    Context* ctx_ = nullptr;
+    T* p_ = nullptr;
+    size_t n_ = 0;
+};
+
+/// Non-owning column-major view.
+struct View {
+    double* p = nullptr;
+    Index rows = 0, cols = 0, ld = 0;
+    double* col(Index j) const { return p + j * ld; }
+    View sub(Index r0, Index c0, Index nr, Index nc) const { return View{p + r0 + c0 * ld, nr, nc, ld}; }
+    View left(Index k) const { return View{p, rows, k, ld}; }
+    View cols_range(Index c0, Index k) const { return View{p + c0 * ld, rows, k, ld}; }
+};
+
+/// Owning column-major matrix on the device (even leading dimension).
+struct DMat {
+    DBuf<double> buf;
+    Index rows = 0, cols = 0, ld = 0;
+    DMat() = default;
+    DMat(Context& ctx, Index r, Index c, bool zero = true);
+    View view() const { return View{buf.get(), rows, cols, ld}; }
+    double* data() const { return buf.get(); }
+};
+
+/// Geometry of a stacked (augmented) panel for an m x n operator.
+struct Stack {
+    Index m = 0, n = 0;
+    Index mp() const { return round_up(m, 2); }
+    Index ld() const { return mp() + round_up(n, 2); }
+};
+
+}  // namespace blws

@@ -1,0 +1,142 @@
+// Device context: stream, stream-ordered pool allocator, pinned staging.
+#include <cstring>
+
+#include "common.cuh"
+
+namespace blws {
+
+Context::Context(int device) : device_(device) {
+    BLWS_CUDA(cudaSetDevice(device));
+    BLWS_CUDA(cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, device));
+    BLWS_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    // keep freed blocks cached in the default pool between calls
+    cudaMemPool_t pool;
+    BLWS_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    std::uint64_t threshold = UINT64_MAX;
+    BLWS_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold));
+    ensure_pinned(1 << 20);
+}
+
+void Context::region_begin(int id) {
+    if (!profiling_) return;
+    cudaEvent_t e;
+    BLWS_CUDA(cudaEventCreate(&e));
+    BLWS_CUDA(cudaEventRecord(e, stream_));
+    regions_[id].begin.push_back(e);
+}
+
+void Context::region_end(int id, double flops, double bytes) {
+    if (!profiling_) return;
+    cudaEvent_t e;
+    BLWS_CUDA(cudaEventCreate(&e));
+    BLWS_CUDA(cudaEventRecord(e, stream_));
+    regions_[id].end.push_back(e);
+    regions_[id].flops += flops;
+    regions_[id].bytes += bytes;
+    regions_[id].count += 1;
+}
+
+void Context::region_stats(int id, double* ms, std::int64_t* count, double* flops, double* bytes) {
+    Region& r = regions_[id];
+    if (!r.begin.empty()) BLWS_CUDA(cudaEventSynchronize(r.end.back()));
+    for (size_t i = 0; i < r.begin.size(); ++i) {
+        float t = 0;
+        BLWS_CUDA(cudaEventElapsedTime(&t, r.begin[i], r.end[i]));
+        r.ms += t;
+        cudaEventDestroy(r.begin[i]);
+        cudaEventDestroy(r.end[i]);
+    }
+    r.begin.clear();
+    r.end.clear();
+    *ms = r.ms;
+    *count = r.count;
+    *flops = r.flops;
+    *bytes = r.bytes;
+}
+
+void Context::region_reset() {
+    for (auto& r : regions_) {
+        for (auto e : r.begin) cudaEventDestroy(e);
+        for (auto e : r.end) cudaEventDestroy(e);
+        r = Region{};
+    }
+}
+
+Context::~Context() {
+    region_reset();
+    if (stream_) {
+        cudaStreamSynchronize(stream_);
+        cudaStreamDestroy(stream_);
+    }
+    if (pinned_) cudaFreeHost(pinned_);
+}
+
+void Context::ensure_pinned(size_t bytes) {
+    if (bytes <= pinned_bytes_) return;
+    if (pinned_) {
+        BLWS_CUDA(cudaStreamSynchronize(stream_));
+        BLWS_CUDA(cudaFreeHost(pinned_));
+    }
+    pinned_bytes_ = std::max(bytes, pinned_bytes_ * 2);
+    BLWS_CUDA(cudaMallocHost(&pinned_, pinned_bytes_));
+}
+
+void* Context::alloc(size_t bytes) {
+    void* p = nullptr;
+    BLWS_CUDA(cudaMallocAsync(&p, bytes, stream_));
+    return p;
+}
+
+void Context::free(void* p) { cudaFreeAsync(p, stream_); }
+
+void Context::sync() { BLWS_CUDA(cudaStreamSynchronize(stream_)); }
+
+void Context::check_launch(const char* what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void Context::read(const double* dev, double* host, size_t count) {
+    if (!count) return;
+    const size_t bytes = count * sizeof(double);
+    if (bytes > (64u << 20)) {  // large reads go straight to pageable memory
+        BLWS_CUDA(cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, stream_));
+        sync();
+        return;
+    }
+    ensure_pinned(bytes);
+    BLWS_CUDA(cudaMemcpyAsync(pinned_, dev, bytes, cudaMemcpyDeviceToHost, stream_));
+    sync();
+    std::memcpy(host, pinned_, bytes);
+}
+
+void Context::read_i64(const std::int64_t* dev, std::int64_t* host, size_t count) {
+    if (!count) return;
+    const size_t bytes = count * sizeof(std::int64_t);
+    ensure_pinned(bytes);
+    BLWS_CUDA(cudaMemcpyAsync(pinned_, dev, bytes, cudaMemcpyDeviceToHost, stream_));
+    sync();
+    std::memcpy(host, pinned_, bytes);
+}
+
+void Context::write(double* dev, const double* host, size_t count) {
+    if (!count) return;
+    const size_t bytes = count * sizeof(double);
+    if (bytes > (64u << 20)) {
+        BLWS_CUDA(cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, stream_));
+        sync();
+        return;
+    }
+    ensure_pinned(bytes);
+    // the staging buffer may still feed an earlier async copy
+    BLWS_CUDA(cudaStreamSynchronize(stream_));
+    std::memcpy(pinned_, host, bytes);
+    BLWS_CUDA(cudaMemcpyAsync(dev, pinned_, bytes, cudaMemcpyHostToDevice, stream_));
+}
+
+DMat::DMat(Context& ctx, Index r, Index c, bool zero) : rows(r), cols(c), ld(std::max<Index>(round_up(r, 2), 2)) {
+    buf = DBuf<double>(ctx, static_cast<size_t>(ld * std::max<Index>(c, 1)));
+    if (zero) BLWS_CUDA(cudaMemsetAsync(buf.get(), 0, sizeof(double) * buf.size(), ctx.stream()));
+}
+
+}  // namespace blws

@@ -1,0 +1,212 @@
+// DMMA GEMM kernels (K1 block products W*X / W^T*X, K2 Grams, K5 Ritz lift).
+#include <algorithm>
+
+#include "dgemm.cuh"
+#include "ops.cuh"
+
+namespace blws {
+using namespace gemm_detail;
+
+namespace {
+
+/// Plain GEMM: partial = true writes the raw split-K partial sum into
+/// ws + blockIdx.z * M * N (ld M); otherwise C = alpha*acc + beta*C.
+template <bool TA, bool TB, int VEC>
+__global__ void __launch_bounds__(THREADS) dgemm_kernel(const double* __restrict__ A, long lda,
+                                                        const double* __restrict__ B, long ldb, double* C, long ldc,
+                                                        long M, long N, long K, long kchunk, double alpha,
+                                                        double beta, double* ws) {
+    extern __shared__ __align__(16) double smem[];
+    const long m0 = static_cast<long>(blockIdx.x) * BM, n0 = static_cast<long>(blockIdx.y) * BN;
+    const long kbeg = static_cast<long>(blockIdx.z) * kchunk;
+    const long kend = min(K, kbeg + kchunk);
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    mainloop<TA, TB, VEC>(acc, smem, A, lda, B, ldb, M, N, m0, n0, kbeg, kend);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane >> 2, t = lane & 3;
+    const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
+    double* P = ws ? ws + static_cast<long>(blockIdx.z) * M * N : nullptr;
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi) {
+        const long row = m0 + wm + mi * 8 + g;
+        if (row >= M) continue;
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const long col = n0 + wn + ni * 8 + 2 * t + e;
+                if (col >= N) continue;
+                const double v = acc[mi][ni][e];
+                if (P) {
+                    P[row + col * M] = v;
+                } else {
+                    double* c = C + row + col * ldc;
+                    *c = beta == 0.0 ? alpha * v : alpha * v + beta * *c;
+                }
+            }
+    }
+}
+
+/// C = alpha * sum_z ws[z] + beta * C  (ws slices are M x N, ld M)
+__global__ void splitk_reduce(const double* __restrict__ ws, long M, long N, int S, double alpha, double beta,
+                              double* C, long ldc) {
+    const long total = M * N;
+    for (long idx = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<long>(gridDim.x) * blockDim.x) {
+        double s = 0.0;
+        for (int z = 0; z < S; ++z) s += ws[z * total + idx];
+        const long i = idx % M, j = idx / M;
+        double* c = C + i + j * ldc;
+        *c = beta == 0.0 ? alpha * s : alpha * s + beta * *c;
+    }
+}
+
+__global__ void scale_kernel(double* C, long ldc, long M, long N, double beta) {
+    const long total = M * N;
+    for (long idx = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<long>(gridDim.x) * blockDim.x) {
+        const long i = idx % M, j = idx / M;
+        C[i + j * ldc] = beta == 0.0 ? 0.0 : beta * C[i + j * ldc];
+    }
+}
+
+template <bool TA, bool TB, int VEC>
+void launch(Context& ctx, dim3 grid, const double* A, long lda, const double* B, long ldb, double* C, long ldc,
+            long M, long N, long K, long kchunk, double alpha, double beta, double* ws) {
+    constexpr int bytes = smem_bytes<TA, TB>();
+    static bool configured = false;  // per-instantiation, per process
+    if (!configured) {
+        BLWS_CUDA(cudaFuncSetAttribute(dgemm_kernel<TA, TB, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+        configured = true;
+    }
+    dgemm_kernel<TA, TB, VEC><<<grid, THREADS, bytes, ctx.stream()>>>(A, lda, B, ldb, C, ldc, M, N, K, kchunk, alpha,
+                                                                      beta, ws);
+    ctx.note_launch();
+    ctx.check_launch("dgemm_kernel");
+}
+
+template <int VEC>
+void dispatch(Context& ctx, bool ta, bool tb, dim3 grid, const double* A, long lda, const double* B, long ldb,
+              double* C, long ldc, long M, long N, long K, long kchunk, double alpha, double beta, double* ws) {
+    if (!ta && !tb) launch<false, false, VEC>(ctx, grid, A, lda, B, ldb, C, ldc, M, N, K, kchunk, alpha, beta, ws);
+    else if (ta && !tb) launch<true, false, VEC>(ctx, grid, A, lda, B, ldb, C, ldc, M, N, K, kchunk, alpha, beta, ws);
+    else if (!ta && tb) launch<false, true, VEC>(ctx, grid, A, lda, B, ldb, C, ldc, M, N, K, kchunk, alpha, beta, ws);
+    else launch<true, true, VEC>(ctx, grid, A, lda, B, ldb, C, ldc, M, N, K, kchunk, alpha, beta, ws);
+}
+
+}  // namespace
+
+void gemm(Context& ctx, bool ta, bool tb, Index M, Index N, Index K, double alpha, const double* A, Index lda,
+          const double* B, Index ldb, double beta, double* C, Index ldc) {
+    if (M <= 0 || N <= 0) return;
+    if (K <= 0 || alpha == 0.0) {
+        const long total = M * N;
+        scale_kernel<<<static_cast<unsigned>(std::min<long>(1024, (total + 255) / 256)), 256, 0, ctx.stream()>>>(
+            C, ldc, M, N, beta);
+        ctx.note_launch();
+        ctx.check_launch("scale_kernel");
+        return;
+    }
+    const Index tiles = ceil_div(M, BM) * ceil_div(N, BN);
+    const Index ktiles = ceil_div(K, BK);
+    // enough CTAs for ~2 waves of 3 resident CTAs/SM, each split >= 8 k-tiles
+    const Index want = 3 * static_cast<Index>(ctx.sm_count());
+    Index S = 1;
+    if (tiles < want) S = std::min<Index>(ceil_div(want, tiles), std::max<Index>(1, ktiles / 8));
+    S = std::max<Index>(1, std::min<Index>(S, 64));
+    const Index kchunk = ceil_div(ktiles, S) * BK;
+    S = ceil_div(K, kchunk);
+    const bool aligned = (lda % 2 == 0) && (ldb % 2 == 0) && (reinterpret_cast<uintptr_t>(A) % 16 == 0) &&
+                         (reinterpret_cast<uintptr_t>(B) % 16 == 0);
+    dim3 grid(static_cast<unsigned>(ceil_div(M, BM)), static_cast<unsigned>(ceil_div(N, BN)),
+              static_cast<unsigned>(S));
+    DBuf<double> ws;
+    if (S > 1) ws = DBuf<double>(ctx, static_cast<size_t>(S * M * N));
+    if (aligned)
+        dispatch<2>(ctx, ta, tb, grid, A, lda, B, ldb, C, ldc, M, N, K, kchunk, alpha, beta, ws.get());
+    else
+        dispatch<1>(ctx, ta, tb, grid, A, lda, B, ldb, C, ldc, M, N, K, kchunk, alpha, beta, ws.get());
+    if (S > 1) {
+        const long total = M * N;
+        splitk_reduce<<<static_cast<unsigned>(std::min<long>(2048, (total + 255) / 256)), 256, 0, ctx.stream()>>>(
+            ws.get(), M, N, static_cast<int>(S), alpha, beta, C, ldc);
+        ctx.note_launch();
+        ctx.check_launch("splitk_reduce");
+    }
+}
+
+}  // namespace blws
+
+// ---------------------------------------------------------------------------
+// FP64 peak microbenchmarks (roofline denominator; MEASURED_PEAKS.json has no
+// FP64 figure). mode 0: DMMA m8n8k4 chains; mode 1: DFMA chains.
+namespace blws {
+namespace {
+
+__global__ void __launch_bounds__(256) fp64_dmma_peak_k(double* sink, int iters) {
+    double acc[8][2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i][0] = acc[i][1] = 0.0;
+    double a = 1.0 + threadIdx.x * 1e-9, b = 1.0 - threadIdx.x * 1e-9;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) gemm_detail::dmma(acc[i], a, b);
+    }
+    double s = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += acc[i][0] + acc[i][1];
+    if (s == 12345.678) sink[0] = s;
+}
+
+__global__ void __launch_bounds__(256) fp64_dfma_peak_k(double* sink, int iters) {
+    double acc[8];
+    double a = 1.0 + threadIdx.x * 1e-9, b = 1.0 - threadIdx.x * 1e-9;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = i;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] = fma(acc[i], a, b);
+    }
+    double s = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += acc[i];
+    if (s == 12345.678) sink[0] = s;
+}
+
+}  // namespace
+
+double fp64_peak_tflops(Context& ctx, int mode) {
+    DBuf<double> sink(ctx, 1);
+    const int blocks = ctx.sm_count() * 4, threads = 256, iters = 20000;
+    cudaEvent_t e0, e1;
+    BLWS_CUDA(cudaEventCreate(&e0));
+    BLWS_CUDA(cudaEventCreate(&e1));
+    double best = 0;
+    for (int rep = 0; rep < 3; ++rep) {
+        BLWS_CUDA(cudaEventRecord(e0, ctx.stream()));
+        if (mode == 0)
+            fp64_dmma_peak_k<<<blocks, threads, 0, ctx.stream()>>>(sink.get(), iters);
+        else
+            fp64_dfma_peak_k<<<blocks, threads, 0, ctx.stream()>>>(sink.get(), iters);
+        BLWS_CUDA(cudaEventRecord(e1, ctx.stream()));
+        BLWS_CUDA(cudaEventSynchronize(e1));
+        ctx.note_launch();
+        float ms = 0;
+        BLWS_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        // DMMA: 8x8x4 = 256 FMA per warp-instruction; DFMA: 1 FMA per thread-instruction
+        const double warps = static_cast<double>(blocks) * threads / 32.0;
+        const double flops = mode == 0 ? warps * iters * 8 * 256 * 2.0
+                                       : static_cast<double>(blocks) * threads * iters * 8 * 2.0;
+        best = std::max(best, flops / (ms * 1e-3) / 1e12);
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return best;
+}
+
+}  // namespace blws

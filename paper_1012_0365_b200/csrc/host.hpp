@@ -1,0 +1,281 @@
+// Host-side control flow of the BLWS hot path on the device.
+//
+// The algorithm objects mirror the reference's C++ API
+// (/root/reference/proj/include/blws): same names, same control flow, same
+// constants, same RNG draw order. All matrices live on the device; the host
+// reads back only the scalars and small vectors the control flow branches on.
+#pragma once
+#include <cstdint>
+#include <memory>
+#include <optional>
+#include <random>
+#include <vector>
+
+#include "common.cuh"
+
+namespace blws {
+
+// ------------------------------------------------------------------ rng
+/// Bit-exact restatement of blws::Rng (core/rng.hpp:17-90). Draws happen on the
+/// host so the device path consumes exactly the reference's stream.
+class Rng {
+public:
+    explicit Rng(std::uint64_t seed) : engine_(seed), seed_(seed) {}
+    Rng split(std::uint64_t tag) const { return Rng(seed_ ^ (0x9e3779b97f4a7c15ull * (tag + 1))); }
+    std::uint64_t next_u64() { return engine_(); }
+    double uniform() { return static_cast<double>(engine_() >> 11) * 0x1.0p-53; }
+    double uniform(double lo, double hi) { return lo + (hi - lo) * uniform(); }
+    std::uint64_t uniform_index(std::uint64_t n);
+    double normal();
+    /// Column-major rows x cols draws (rng.hpp:63-68).
+    void gaussian_matrix(Index rows, Index cols, double* out, Index ld);
+    std::vector<double> gaussian_vector(Index n);
+    std::vector<double> unit_vector(Index n);
+
+private:
+    std::mt19937_64 engine_;
+    std::uint64_t seed_ = 0;
+    double spare_ = 0.0;
+    bool have_spare_ = false;
+};
+
+// ------------------------------------------------------------- operators
+/// Device-resident W with the reference's application counter
+/// (core/linear_operator.hpp:20-98). Only the paired products the augmented
+/// view needs are exposed (augmented_operator.hpp:39-57).
+class LinearOperator {
+public:
+    explicit LinearOperator(Context& ctx) : ctx_(ctx) {}
+    virtual ~LinearOperator() = default;
+    virtual Index rows() const = 0;
+    virtual Index cols() const = 0;
+    Context& ctx() const { return ctx_; }
+
+    /// (top, bot) = (W * right, W^T * left); counts right.cols (linear_operator.hpp:57-61).
+    void apply_pair_block(View left, View right, View top, View bot) {
+        count_ += right.cols;
+        pair_block_impl(left, right, top, bot);
+    }
+    /// Single-vector paired apply; counts 1 (linear_operator.hpp:51-54).
+    void apply_pair(const double* left, const double* right, double* top, double* bot) {
+        count_ += 1;
+        pair_impl(left, right, top, bot);
+    }
+    std::int64_t application_count() const { return count_; }
+
+protected:
+    virtual void pair_block_impl(View left, View right, View top, View bot) = 0;
+    virtual void pair_impl(const double* left, const double* right, double* top, double* bot) = 0;
+    Context& ctx_;
+
+private:
+    std::int64_t count_ = 0;
+};
+
+/// DenseOperator (linear_operator.hpp:102-131): column-major W on the device,
+/// either owned or borrowed (a caller-owned device buffer).
+class DenseOperator final : public LinearOperator {
+public:
+    DenseOperator(Context& ctx, Index m, Index n);
+    /// Borrow caller memory (ld must be even, 16-byte aligned).
+    DenseOperator(Context& ctx, Index m, Index n, double* dev, Index ld);
+    Index rows() const override { return m_; }
+    Index cols() const override { return n_; }
+    View w() const { return View{p_, m_, n_, ld_}; }
+    /// Host upload with the reference's non-finite check (:113-116).
+    void assign_host(const double* w, Index ldw);
+    /// Device copy with the non-finite check.
+    void assign_device(const double* w, Index ldw);
+    /// Non-finite scan of the held matrix (throws std::invalid_argument).
+    void check_finite();
+
+protected:
+    void pair_block_impl(View left, View right, View top, View bot) override;
+    void pair_impl(const double* left, const double* right, double* top, double* bot) override;
+
+private:
+    Index m_, n_, ld_;
+    DBuf<double> own_;
+    double* p_ = nullptr;
+};
+
+/// SparseOperator (linear_operator.hpp:136-169): the pattern in CSR (for W*x)
+/// and CSC (= CSR of W^T, for W^T*x); values are assigned in compressed (CSC)
+/// order like the reference and scattered to CSR order on the device.
+class SparseOperator final : public LinearOperator {
+public:
+    SparseOperator(Context& ctx, Index m, Index n, Index nnz, const std::int64_t* colptr, const std::int32_t* rowidx,
+                   const double* values_host);
+    Index rows() const override { return m_; }
+    Index cols() const override { return n_; }
+    Index nnz() const { return nnz_; }
+    void assign_values_device(const double* vals_csc);
+    void assign_values_host(const double* vals_csc);
+    const double* val_csc() const { return val_csc_.get(); }
+    const std::int32_t* rowidx_csc() const { return rowidx_.get(); }
+    const std::int32_t* colof_csc() const { return colof_.get(); }
+
+protected:
+    void pair_block_impl(View left, View right, View top, View bot) override;
+    void pair_impl(const double* left, const double* right, double* top, double* bot) override;
+
+private:
+    Index m_, n_, nnz_;
+    DBuf<std::int64_t> rowptr_, colptr_, perm_;  // perm: csr position -> csc position
+    DBuf<std::int32_t> colidx_, rowidx_, colof_;
+    DBuf<double> val_csr_, val_csc_;
+    DBuf<double> scratch_;
+};
+
+// ------------------------------------------------------------ warm start
+/// WarmStart (block_lanczos.hpp:45-52): U (m x b) and V (n x b) kept as one
+/// stacked panel (top / bottom), sigma on the host.
+struct DWarm {
+    Stack geo;
+    DMat uv;  // geo.ld() x b
+    std::vector<double> sigma;
+    Index rank() const { return static_cast<Index>(sigma.size()); }
+    View u() const { return View{uv.data(), geo.m, rank(), uv.ld}; }
+    View v() const { return View{uv.data() + geo.mp(), geo.n, rank(), uv.ld}; }
+    View panel() const { return View{uv.data(), uv.ld, rank(), uv.ld}; }
+};
+DWarm make_warm(Context& ctx, Index m, Index n, Index b);
+DWarm copy_warm(Context& ctx, const DWarm& w, Index cols);
+
+// ------------------------------------------------------------ dense pieces
+/// thin_qr (core/qr.hpp:24-47) as CholQR2 (shifted CholQR3 fallback) in place:
+/// X <- Q, R (b x b, optional) upper with positive diagonal; returns the rank,
+/// counted as diag(R) > 1e-12 ||X||_F.
+Index thin_qr(Context& ctx, View x, View* r_out);
+
+/// Upload / download a host column-major block into a device view.
+void upload(Context& ctx, View dst, const double* host, Index ldh);
+void download(Context& ctx, View src, double* host, Index ldh);
+
+// ------------------------------------------------------------ block lanczos
+struct BlwsResult {
+    DWarm warm;
+    bool padded = false, k_raised = false, terminated_early = false;
+};
+/// adapt_subspace (block_lanczos.hpp:157-187).
+DWarm adapt_subspace(Context& ctx, const DWarm* warm, Index r_new, Index m, Index n, Rng& rng);
+/// blws_svd (block_lanczos.hpp:204-261).
+BlwsResult blws_svd(LinearOperator& w, const DWarm& warm, Index k, Index r, Rng& rng);
+
+/// Factorisation for tests: block_lanczos_procedure on the augmented view.
+struct BlockLanczos {
+    DMat q;
+    std::vector<DMat> m, b;
+    Index built = 0;
+    bool terminated_early = false;
+};
+BlockLanczos block_lanczos_procedure(LinearOperator& w, View x1, Index k);
+
+// ------------------------------------------------------------------ lanczos
+struct LanczosStats {
+    Index steps = 0, restarts = 0, converged = 0;
+    bool all_converged = false;
+};
+struct LanczosOptions {
+    double tol = 1e-8;
+    Index max_k = 0;
+    std::uint64_t seed = 0x1a2c705u;
+};
+struct PartialSvd {
+    DWarm uv;  // sigma + stacked U/V (not re-orthonormalised, as the reference)
+    LanczosStats stats;
+};
+/// lanczos_partial_svd (lanczos.hpp:289-329) on the augmented view.
+PartialSvd lanczos_partial_svd(LinearOperator& w, Index r, const LanczosOptions& opts);
+/// spectral_norm (lanczos.hpp:332-340).
+double spectral_norm(LinearOperator& w, double tol = 1e-6, std::uint64_t seed = 0xb1f);
+
+// --------------------------------------------------------------------- svt
+struct RankPredictor {
+    Index r = 10, increment = 5, max_rank = 1;
+    std::vector<Index> history;
+};
+RankPredictor predict_rank(RankPredictor p, Index achieved, bool all_above);  // svt.hpp:58-64
+
+class SvdBackend {
+public:
+    enum class Kind { ExactFull = 0, Lanczos = 1, Blws = 2 };
+    struct Options {
+        Index block_steps = 2;
+        double ritz_tol = 1e-8;
+        Index max_k = 0;
+        Index seed_margin = 5;
+        std::uint64_t seed = 0xb10c;
+    };
+    SvdBackend(Context& ctx, Kind k, Options o);
+    struct Triplets {
+        DWarm own;                    // cold Lanczos result (Lanczos kind)
+        const DWarm* held = nullptr;  // the backend's warm start (Blws kind)
+        Index converged = 0;
+        bool hit_cap = false;
+        const DWarm& get() const { return held ? *held : own; }
+    };
+    /// SvdBackend::compute (svt.hpp:104-186); ExactFull is not provided on the device.
+    Triplets compute(LinearOperator& w, Index r);
+    Kind kind() const { return kind_; }
+    const std::optional<DWarm>& warm_state() const { return warm_; }
+    void set_warm(DWarm w) { warm_ = std::move(w); }
+
+private:
+    Context& ctx_;
+    Kind kind_;
+    Options opt_;
+    std::optional<DWarm> warm_;
+    Rng rng_;
+    Index growth_streak_ = 0;
+};
+
+struct SvtResult {
+    DWarm trip;               // first `achieved` triplets, sigma already shrunk
+    DBuf<double> sigma_dev;   // shrunk sigma on the device
+    Index achieved_rank = 0;
+    bool all_above_threshold = false;
+};
+/// svt (svt.hpp:216-254).
+SvtResult svt(LinearOperator& w, double eps, SvdBackend& backend, RankPredictor& predictor);
+
+// ----------------------------------------------------------------- solvers
+struct SolverStats {
+    Index iterations = 0;
+    double wall_time_s = 0;
+    std::int64_t matvec_count = 0, matvec_init = 0;
+    double rel_err = -1;
+    Index rank_hat = 0;
+    std::int64_t e_l0 = -1, e_nnz = 0;
+    bool converged = false;
+    std::vector<Index> predicted_ranks;
+    std::vector<std::int64_t> matvec_history;
+    std::vector<double> residual_history;
+};
+struct RpcaOptions {
+    double tol_outer = 1e-7;
+    Index max_iter = 1000;
+    double rho = 1.5;
+    double mu_max_factor = 1e7;
+    Index initial_rank = 10, rank_increment = 5;
+};
+/// rpca_adm (solvers.hpp:72-157). d / truth / a_out / e_out are device
+/// pointers with leading dimension ldd (truth, a_out, e_out may be null).
+SolverStats rpca_adm(Context& ctx, Index m, const double* d, Index ldd, double lambda, SvdBackend& backend,
+                     const RpcaOptions& opts, const double* truth, double* a_out, double* e_out);
+
+struct McOptions {
+    double tol_outer = 1e-4;
+    Index max_iter = 500;
+    Index initial_rank = 10, rank_increment = 5;
+};
+struct McSolution {
+    DWarm uv;  // sigma = shrunk values
+    SolverStats stats;
+};
+/// mc_svt (solvers.hpp:202-270); the observation is host CSC.
+McSolution mc_svt(Context& ctx, Index m, Index n, Index nnz, const std::int64_t* colptr, const std::int32_t* rowidx,
+                  const double* vals, double tau, double delta, SvdBackend& backend, const McOptions& opts,
+                  const double* truth_ml, const double* truth_mr, Index r_true);
+
+}  // namespace blws

@@ -1,0 +1,817 @@
+// Operators, CholQR thin_qr, block Lanczos / BLWS and the cold Lanczos reseed.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <stdexcept>
+
+#include "host.hpp"
+#include "ops.cuh"
+
+namespace blws {
+
+// =================================================================== Rng
+std::uint64_t Rng::uniform_index(std::uint64_t n) {
+    const std::uint64_t limit = UINT64_MAX - UINT64_MAX % n;
+    std::uint64_t x;
+    do {
+        x = engine_();
+    } while (x >= limit);
+    return x % n;
+}
+
+double Rng::normal() {
+    if (have_spare_) {
+        have_spare_ = false;
+        return spare_;
+    }
+    double u1, u2;
+    do {
+        u1 = uniform();
+    } while (u1 <= 0.0);
+    u2 = uniform();
+    const double r = std::sqrt(-2.0 * std::log(u1));
+    const double theta = 6.283185307179586476925287 * u2;
+    spare_ = r * std::sin(theta);
+    have_spare_ = true;
+    return r * std::cos(theta);
+}
+
+void Rng::gaussian_matrix(Index rows, Index cols, double* out, Index ld) {
+    for (Index j = 0; j < cols; ++j)
+        for (Index i = 0; i < rows; ++i) out[i + j * ld] = normal();
+}
+
+std::vector<double> Rng::gaussian_vector(Index n) {
+    std::vector<double> v(static_cast<size_t>(n));
+    for (auto& x : v) x = normal();
+    return v;
+}
+
+std::vector<double> Rng::unit_vector(Index n) {
+    auto v = gaussian_vector(n);
+    double s = 0;
+    for (double x : v) s += x * x;
+    const double nv = std::sqrt(s);
+    for (auto& x : v) x /= nv;
+    return v;
+}
+
+// ============================================================ small kernels
+namespace {
+
+constexpr int kT = 256;
+inline unsigned gridn(long total, long cap = 4096) {
+    return static_cast<unsigned>(std::max<long>(1, std::min<long>(cap, (total + kT - 1) / kT)));
+}
+
+__global__ void nonfinite_count_k(const double* x, long rows, long cols, long ld, int* flag) {
+    const long total = rows * cols;
+    int bad = 0;
+    for (long idx = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<long>(gridDim.x) * blockDim.x)
+        if (!isfinite(x[idx % rows + (idx / rows) * ld])) bad = 1;
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
+// warp per row SpMV: y[i] = sum_p val[p] x[col[p]]
+__global__ void csr_spmv_k(long rows, const std::int64_t* __restrict__ ptr, const std::int32_t* __restrict__ idx,
+                           const double* __restrict__ val, const double* __restrict__ x, double* y) {
+    const long warps = (static_cast<long>(gridDim.x) * blockDim.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    for (long i = (blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x) >> 5; i < rows; i += warps) {
+        double s = 0.0;
+        for (long p = ptr[i] + lane; p < ptr[i + 1]; p += 32) s += val[p] * x[idx[p]];
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) y[i] = s;
+    }
+}
+
+// r -= alpha[l] q_l + coup[l] q_{l-1}
+__global__ void lanczos_three_term_k(double* r, const double* q, long ld, long l, const double* alpha,
+                                     const double* coup, long n) {
+    const double a = alpha[l];
+    const double b = l > 0 ? coup[l] : 0.0;
+    const double* ql = q + l * ld;
+    const double* qp = l > 0 ? q + (l - 1) * ld : q;
+    for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long>(gridDim.x) * blockDim.x) {
+        double v = r[i] - a * ql[i];
+        if (l > 0) v -= b * qp[i];
+        r[i] = v;
+    }
+}
+
+// beta = ||r|| (from sumsq), breakdown test, next_dir = r / beta; state[0] =
+// first broken step (or -1), state[1] = tau (set at step 0).
+__global__ void lanczos_finalize_k(const double* r, double* next, long n, long l, long dim, const double* rsq,
+                                   const double* alpha, double* lastbeta, double* coup, long cap, double* state) {
+    const double beta = sqrt(rsq[0]);
+    __shared__ int broken;
+    if (threadIdx.x == 0) {
+        if (l == 0) state[1] = 1e-12 * fabs(alpha[0]);
+        const bool already = state[0] >= 0.0;
+        const bool now = beta <= state[1] || (l + 1) >= dim;
+        if (!already && now) state[0] = static_cast<double>(l);
+        broken = already || now;
+        lastbeta[l] = beta;
+        if (!broken && l + 1 < cap) coup[l + 1] = beta;
+    }
+    __syncthreads();
+    const double inv = broken ? 0.0 : 1.0 / beta;
+    for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long>(gridDim.x) * blockDim.x)
+        next[i] = broken ? 0.0 : r[i] * inv;
+}
+
+__global__ void scale_by_inv_sqrt_k(double* x, long n, const double* ss) {
+    const double inv = 1.0 / sqrt(ss[0]);
+    for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long>(gridDim.x) * blockDim.x)
+        x[i] *= inv;
+}
+
+__global__ void shift_for_cholqr3_k(const double* ss, double factor, double* out) { out[0] = factor * ss[0]; }
+
+}  // namespace
+
+// ======================================================== upload / download
+void upload(Context& ctx, View dst, const double* host, Index ldh) {
+    if (dst.rows * dst.cols == 0) return;
+    BLWS_CUDA(cudaMemcpy2DAsync(dst.p, sizeof(double) * dst.ld, host, sizeof(double) * ldh,
+                                sizeof(double) * dst.rows, dst.cols, cudaMemcpyHostToDevice, ctx.stream()));
+    ctx.sync();
+}
+
+void download(Context& ctx, View src, double* host, Index ldh) {
+    if (src.rows * src.cols == 0) return;
+    BLWS_CUDA(cudaMemcpy2DAsync(host, sizeof(double) * ldh, src.p, sizeof(double) * src.ld,
+                                sizeof(double) * src.rows, src.cols, cudaMemcpyDeviceToHost, ctx.stream()));
+    ctx.sync();
+}
+
+static void check_finite_view(Context& ctx, View v, const char* what) {
+    DBuf<int> flag(ctx, 1);
+    BLWS_CUDA(cudaMemsetAsync(flag.get(), 0, sizeof(int), ctx.stream()));
+    if (v.rows * v.cols > 0) {
+        nonfinite_count_k<<<gridn(v.rows * v.cols), kT, 0, ctx.stream()>>>(v.p, v.rows, v.cols, v.ld, flag.get());
+        ctx.note_launch();
+        ctx.check_launch("nonfinite");
+    }
+    int h = 0;
+    BLWS_CUDA(cudaMemcpyAsync(&h, flag.get(), sizeof(int), cudaMemcpyDeviceToHost, ctx.stream()));
+    ctx.sync();
+    if (h) throw std::invalid_argument(what);
+}
+
+// ======================================================== DenseOperator
+DenseOperator::DenseOperator(Context& ctx, Index m, Index n)
+    : LinearOperator(ctx), m_(m), n_(n), ld_(std::max<Index>(2, round_up(m, 2))) {
+    own_ = DBuf<double>(ctx, static_cast<size_t>(ld_ * std::max<Index>(n, 1)));
+    BLWS_CUDA(cudaMemsetAsync(own_.get(), 0, sizeof(double) * own_.size(), ctx.stream()));
+    p_ = own_.get();
+}
+
+DenseOperator::DenseOperator(Context& ctx, Index m, Index n, double* dev, Index ld)
+    : LinearOperator(ctx), m_(m), n_(n), ld_(ld), p_(dev) {}
+
+void DenseOperator::check_finite() { check_finite_view(ctx_, w(), "DenseOperator: non-finite entries"); }
+
+void DenseOperator::assign_host(const double* w_host, Index ldw) {
+    upload(ctx_, w(), w_host, ldw);
+    check_finite();
+}
+
+void DenseOperator::assign_device(const double* w_dev, Index ldw) {
+    if (w_dev != p_) copy(ctx_, w(), View{const_cast<double*>(w_dev), m_, n_, ldw});
+    check_finite();
+}
+
+void DenseOperator::pair_block_impl(View left, View right, View top, View bot) {
+    const Index b = right.cols;
+    // K1: region 0 times the paired product (both GEMMs incl. split-K reduce)
+    ctx_.region_begin(0);
+    gemm(ctx_, false, false, m_, b, n_, 1.0, p_, ld_, right.p, right.ld, 0.0, top.p, top.ld);
+    gemm(ctx_, true, false, n_, b, m_, 1.0, p_, ld_, left.p, left.ld, 0.0, bot.p, bot.ld);
+    ctx_.region_end(0, 4.0 * static_cast<double>(m_) * n_ * b, 16.0 * static_cast<double>(m_) * n_);
+}
+
+void DenseOperator::pair_impl(const double* left, const double* right, double* top, double* bot) {
+    gemv(ctx_, false, m_, n_, 1.0, p_, ld_, right, 0.0, top);
+    gemv(ctx_, true, m_, n_, 1.0, p_, ld_, left, 0.0, bot);
+}
+
+// ======================================================== SparseOperator
+SparseOperator::SparseOperator(Context& ctx, Index m, Index n, Index nnz, const std::int64_t* colptr,
+                               const std::int32_t* rowidx, const double* values)
+    : LinearOperator(ctx), m_(m), n_(n), nnz_(nnz) {
+    for (Index i = 0; i < nnz; ++i)
+        if (!std::isfinite(values[i])) throw std::invalid_argument("SparseOperator: non-finite entries");
+    // CSC -> CSR with the position permutation
+    std::vector<std::int64_t> rowptr(static_cast<size_t>(m + 1), 0), perm(static_cast<size_t>(nnz));
+    std::vector<std::int32_t> colidx(static_cast<size_t>(nnz)), colof(static_cast<size_t>(nnz));
+    for (Index p = 0; p < nnz; ++p) ++rowptr[static_cast<size_t>(rowidx[p]) + 1];
+    for (Index i = 0; i < m; ++i) rowptr[i + 1] += rowptr[i];
+    std::vector<std::int64_t> next(rowptr.begin(), rowptr.end() - 1);
+    for (Index j = 0; j < n; ++j)
+        for (std::int64_t p = colptr[j]; p < colptr[j + 1]; ++p) {
+            const std::int64_t q = next[static_cast<size_t>(rowidx[p])]++;
+            colidx[static_cast<size_t>(q)] = static_cast<std::int32_t>(j);
+            perm[static_cast<size_t>(q)] = p;
+            colof[static_cast<size_t>(p)] = static_cast<std::int32_t>(j);
+        }
+    auto up64 = [&](DBuf<std::int64_t>& d, const std::int64_t* h, size_t c) {
+        d = DBuf<std::int64_t>(ctx, std::max<size_t>(c, 1));
+        BLWS_CUDA(cudaMemcpyAsync(d.get(), h, sizeof(std::int64_t) * c, cudaMemcpyHostToDevice, ctx.stream()));
+    };
+    auto up32 = [&](DBuf<std::int32_t>& d, const std::int32_t* h, size_t c) {
+        d = DBuf<std::int32_t>(ctx, std::max<size_t>(c, 1));
+        BLWS_CUDA(cudaMemcpyAsync(d.get(), h, sizeof(std::int32_t) * c, cudaMemcpyHostToDevice, ctx.stream()));
+    };
+    up64(rowptr_, rowptr.data(), rowptr.size());
+    up64(colptr_, colptr, static_cast<size_t>(n + 1));
+    up64(perm_, perm.data(), perm.size());
+    up32(colidx_, colidx.data(), colidx.size());
+    up32(rowidx_, rowidx, static_cast<size_t>(nnz));
+    up32(colof_, colof.data(), colof.size());
+    val_csr_ = DBuf<double>(ctx, std::max<size_t>(nnz, 1));
+    val_csc_ = DBuf<double>(ctx, std::max<size_t>(nnz, 1));
+    ctx.sync();
+    assign_values_host(values);
+}
+
+void SparseOperator::assign_values_host(const double* vals) {
+    BLWS_CUDA(cudaMemcpyAsync(val_csc_.get(), vals, sizeof(double) * nnz_, cudaMemcpyHostToDevice, ctx_.stream()));
+    gather_values(ctx_, nnz_, val_csr_.get(), val_csc_.get(), perm_.get());
+    ctx_.sync();
+}
+
+void SparseOperator::assign_values_device(const double* vals) {
+    if (vals != val_csc_.get())
+        BLWS_CUDA(cudaMemcpyAsync(val_csc_.get(), vals, sizeof(double) * nnz_, cudaMemcpyDeviceToDevice,
+                                  ctx_.stream()));
+    gather_values(ctx_, nnz_, val_csr_.get(), val_csc_.get(), perm_.get());
+}
+
+void SparseOperator::pair_block_impl(View left, View right, View top, View bot) {
+    const Index b = right.cols;
+    const size_t need = static_cast<size_t>(std::max(m_, n_) * b);
+    if (scratch_.size() < need) scratch_ = DBuf<double>(ctx_, need);
+    csr_spmm(ctx_, m_, rowptr_.get(), colidx_.get(), val_csr_.get(), n_, b, right.p, right.ld, top.p, top.ld,
+             scratch_.get());
+    csr_spmm(ctx_, n_, colptr_.get(), rowidx_.get(), val_csc_.get(), m_, b, left.p, left.ld, bot.p, bot.ld,
+             scratch_.get());
+}
+
+void SparseOperator::pair_impl(const double* left, const double* right, double* top, double* bot) {
+    csr_spmv_k<<<gridn(m_ * 32, 8192), kT, 0, ctx_.stream()>>>(m_, rowptr_.get(), colidx_.get(), val_csr_.get(),
+                                                                right, top);
+    ctx_.note_launch();
+    csr_spmv_k<<<gridn(n_ * 32, 8192), kT, 0, ctx_.stream()>>>(n_, colptr_.get(), rowidx_.get(), val_csc_.get(),
+                                                                left, bot);
+    ctx_.note_launch();
+    ctx_.check_launch("csr_spmv");
+}
+
+// ======================================================== warm start
+DWarm make_warm(Context& ctx, Index m, Index n, Index b) {
+    DWarm w;
+    w.geo = Stack{m, n};
+    w.uv = DMat(ctx, w.geo.ld(), std::max<Index>(b, 1), true);
+    w.uv.cols = b;
+    w.sigma.assign(static_cast<size_t>(b), 0.0);
+    return w;
+}
+
+DWarm copy_warm(Context& ctx, const DWarm& src, Index cols) {
+    DWarm w = make_warm(ctx, src.geo.m, src.geo.n, cols);
+    copy(ctx, w.panel().left(cols), src.panel().left(cols));
+    w.sigma.assign(src.sigma.begin(), src.sigma.begin() + cols);
+    return w;
+}
+
+// ======================================================== thin_qr (CholQR)
+namespace {
+
+struct CholStep {
+    DMat r, rinv;
+    bool ok = false;
+    double dmin = 0, dmax = 0;
+};
+
+// One Cholesky-QR pass: G = X^T X (+ shift), R = chol(G), X <- X R^{-1}.
+CholStep cholqr_pass(Context& ctx, View x, const double* shift_dev) {
+    const Index b = x.cols;
+    CholStep s;
+    s.r = DMat(ctx, b, b, false);
+    gemm(ctx, true, false, b, b, x.rows, 1.0, x.p, x.ld, x.p, x.ld, 0.0, s.r.data(), s.r.ld);
+    if (shift_dev) add_diagonal(ctx, s.r.view(), shift_dev);
+    DBuf<int> status(ctx, 1);
+    DBuf<double> diag(ctx, 2);
+    potrf_upper(ctx, s.r.view(), status.get(), diag.get());
+    int st = 0;
+    double dd[2] = {0, 0};
+    BLWS_CUDA(cudaMemcpyAsync(&st, status.get(), sizeof(int), cudaMemcpyDeviceToHost, ctx.stream()));
+    ctx.read(diag.get(), dd, 2);
+    s.ok = st == 0;
+    if (!s.ok) return s;
+    s.dmin = dd[0];
+    s.dmax = dd[1];
+    s.rinv = DMat(ctx, b, b, false);
+    trtri_upper(ctx, s.rinv.view(), s.r.view());
+    DMat tmp(ctx, x.rows, b, false);
+    gemm(ctx, false, false, x.rows, b, b, 1.0, x.p, x.ld, s.rinv.data(), s.rinv.ld, 0.0, tmp.data(), tmp.ld);
+    copy(ctx, x, tmp.view());
+    return s;
+}
+
+}  // namespace
+
+Index thin_qr(Context& ctx, View x, View* r_out) {
+    const Index rows = x.rows, b = x.cols;
+    if (rows == 0 || b == 0) throw std::invalid_argument("thin_qr: empty matrix");
+    if (rows < b) throw std::invalid_argument("thin_qr: requires rows >= cols");
+    DBuf<double> ss(ctx, 1);
+    sumsq(ctx, x, ss.get());
+    double hss = 0;
+    ctx.read(ss.get(), &hss, 1);
+    if (!std::isfinite(hss)) throw std::invalid_argument("thin_qr: non-finite entries");
+    // keep the input for the shifted fallback
+    DMat x0(ctx, rows, b, false);
+    copy(ctx, x0.view(), x);
+    std::vector<CholStep> steps;
+    CholStep s1 = cholqr_pass(ctx, x, nullptr);
+    const bool ill = !s1.ok || !(s1.dmin > 0) || s1.dmax / s1.dmin > 1e6;
+    if (!ill) {
+        steps.push_back(std::move(s1));
+        steps.push_back(cholqr_pass(ctx, x, nullptr));
+        if (!steps.back().ok) throw NumericalError("thin_qr: CholQR2 second pass failed");
+    } else {
+        // shifted CholQR3 (Fukaya et al.): s = 11 (rows*b + b(b+1)) u ||X||_F^2
+        copy(ctx, x, x0.view());
+        DBuf<double> shift(ctx, 1);
+        const double factor = 11.0 * (static_cast<double>(rows) * b + static_cast<double>(b) * (b + 1)) * 1.1102230246251565e-16;
+        shift_for_cholqr3_k<<<1, 1, 0, ctx.stream()>>>(ss.get(), factor, shift.get());
+        ctx.note_launch();
+        CholStep a = cholqr_pass(ctx, x, shift.get());
+        if (!a.ok) {
+            if (hss == 0.0) {
+                // all-zero input: Q undefined, rank 0 (R = 0)
+                if (r_out) fill(ctx, *r_out, 0.0);
+                return 0;
+            }
+            throw NumericalError("thin_qr: shifted CholQR failed");
+        }
+        steps.push_back(std::move(a));
+        for (int k = 0; k < 2; ++k) {
+            CholStep c = cholqr_pass(ctx, x, nullptr);
+            if (!c.ok) {
+                // Q columns already orthonormal to working precision except for
+                // the null directions; keep what we have
+                break;
+            }
+            steps.push_back(std::move(c));
+        }
+    }
+    // R = R_last * ... * R_1
+    DMat r = std::move(steps.back().r);
+    for (int k = static_cast<int>(steps.size()) - 2; k >= 0; --k) {
+        DMat t(ctx, b, b, false);
+        gemm(ctx, false, false, b, b, b, 1.0, r.data(), r.ld, steps[k].r.data(), steps[k].r.ld, 0.0, t.data(), t.ld);
+        r = std::move(t);
+    }
+    DBuf<std::int64_t> rank(ctx, 1);
+    count_diag_above(ctx, r.view(), ss.get(), 1e-12, rank.get());
+    std::int64_t hr = 0;
+    ctx.read_i64(rank.get(), &hr, 1);
+    if (r_out) copy(ctx, *r_out, r.view());
+    return hr;
+}
+
+// ======================================================== adapt_subspace
+DWarm adapt_subspace(Context& ctx, const DWarm* warm, Index r_new, Index m, Index n, Rng& rng) {
+    if (r_new < 1 || r_new > std::min(m, n)) throw std::invalid_argument("adapt_subspace: r_new out of range");
+    if (!warm || warm->rank() == 0) {
+        DWarm out = make_warm(ctx, m, n, r_new);
+        std::vector<double> h(static_cast<size_t>(std::max(m, n) * r_new));
+        rng.gaussian_matrix(m, r_new, h.data(), m);
+        upload(ctx, out.u(), h.data(), m);
+        rng.gaussian_matrix(n, r_new, h.data(), n);
+        upload(ctx, out.v(), h.data(), n);
+        View u = out.u(), v = out.v();
+        thin_qr(ctx, u, nullptr);
+        thin_qr(ctx, v, nullptr);
+        return out;
+    }
+    const Index r_old = warm->rank();
+    if (r_new == r_old) return copy_warm(ctx, *warm, r_old);
+    if (r_new < r_old) return copy_warm(ctx, *warm, r_new);
+    const Index add = r_new - r_old;
+    DWarm out = make_warm(ctx, m, n, r_new);
+    copy(ctx, out.panel().left(r_old), warm->panel().left(r_old));
+    std::vector<double> h(static_cast<size_t>(std::max(m, n) * add));
+    rng.gaussian_matrix(m, add, h.data(), m);
+    upload(ctx, out.u().cols_range(r_old, add), h.data(), m);
+    rng.gaussian_matrix(n, add, h.data(), n);
+    upload(ctx, out.v().cols_range(r_old, add), h.data(), n);
+    View u = out.u(), v = out.v();
+    thin_qr(ctx, u, nullptr);
+    thin_qr(ctx, v, nullptr);
+    std::copy(warm->sigma.begin(), warm->sigma.end(), out.sigma.begin());
+    return out;
+}
+
+// ======================================================== block lanczos
+namespace {
+
+/// Augmented block apply (augmented_operator.hpp:50-57): Z = [[0,W],[W^T,0]] X.
+void aug_apply(LinearOperator& w, const Stack& geo, View x, View z) {
+    View xt{x.p, geo.m, x.cols, x.ld}, xb{x.p + geo.mp(), geo.n, x.cols, x.ld};
+    View zt{z.p, geo.m, z.cols, z.ld}, zb{z.p + geo.mp(), geo.n, z.cols, z.ld};
+    w.apply_pair_block(xt, xb, zt, zb);
+}
+
+double read_scalar(Context& ctx, const double* d) {
+    double h = 0;
+    ctx.read(d, &h, 1);
+    return h;
+}
+
+}  // namespace
+
+// block_lanczos.hpp:70-126 on the augmented view; x1 is a stacked panel.
+BlockLanczos block_lanczos_procedure(LinearOperator& w, View x1, Index k) {
+    Context& ctx = w.ctx();
+    const Stack geo{w.rows(), w.cols()};
+    const Index dim = geo.m + geo.n, bs = x1.cols, ld = geo.ld();
+    if (k < 1) throw std::invalid_argument("block_lanczos_procedure: k must be >= 1");
+    if (bs < 1 || x1.rows != ld) throw std::invalid_argument("block_lanczos_procedure: bad initial block");
+    if (k * bs > dim) throw std::invalid_argument("block_lanczos_procedure: k*b exceeds dimension");
+    DBuf<double> sc(ctx, 4);
+    {
+        DMat g(ctx, bs, bs, false);
+        gemm(ctx, true, false, bs, bs, ld, 1.0, x1.p, x1.ld, x1.p, x1.ld, 0.0, g.data(), g.ld);
+        sumsq_minus_identity(ctx, g.view(), sc.get());
+        if (std::sqrt(read_scalar(ctx, sc.get())) > 1e-8)
+            throw std::invalid_argument("block_lanczos_procedure: X1 not orthonormal");
+    }
+    BlockLanczos out;
+    out.q = DMat(ctx, ld, k * bs, true);
+    View Q = out.q.view();
+    copy(ctx, Q.cols_range(0, bs), x1);
+    DMat z(ctx, ld, bs, true);
+    DMat mtmp(ctx, bs, bs, false);
+    auto block = [&](Index l) { return View{Q.p + l * bs * Q.ld, ld, bs, Q.ld}; };
+
+    aug_apply(w, geo, block(0), z.view());
+    sumsq(ctx, z.view(), sc.get());
+    double scale = std::sqrt(read_scalar(ctx, sc.get()));
+    gemm(ctx, true, false, bs, bs, ld, 1.0, Q.p, Q.ld, z.data(), z.ld, 0.0, mtmp.data(), mtmp.ld);
+    out.m.emplace_back(ctx, bs, bs, false);
+    symmetrize(ctx, out.m.back().view(), mtmp.view());
+    out.built = 1;
+    for (Index l = 1; l < k; ++l) {
+        View xc = block(l - 1);
+        // R = Z - X_l M_l - X_{l-1} B_{l-1}^T, in place in z
+        gemm(ctx, false, false, ld, bs, bs, -1.0, xc.p, xc.ld, out.m.back().data(), out.m.back().ld, 1.0, z.data(),
+             z.ld);
+        if (l > 1) {
+            View xp = block(l - 2);
+            gemm(ctx, false, true, ld, bs, bs, -1.0, xp.p, xp.ld, out.b.back().data(), out.b.back().ld, 1.0,
+                 z.data(), z.ld);
+        }
+        sumsq(ctx, z.view(), sc.get());
+        const double rn = std::sqrt(read_scalar(ctx, sc.get()));
+        if (rn <= 1e-10 * scale) {  // kBlockBreakdownTol (block_lanczos.hpp:64, :103)
+            out.terminated_early = true;
+            break;
+        }
+        View xn = block(l);
+        copy(ctx, xn, z.view());
+        DMat rb(ctx, bs, bs, true);
+        View rv = rb.view();
+        const Index rank = thin_qr(ctx, xn, &rv);
+        if (rank < bs) {
+            fill(ctx, xn, 0.0);
+            out.terminated_early = true;
+            break;
+        }
+        out.b.push_back(std::move(rb));
+        ++out.built;
+        aug_apply(w, geo, xn, z.view());
+        sumsq(ctx, z.view(), sc.get());
+        scale = std::max(scale, std::sqrt(read_scalar(ctx, sc.get())));
+        gemm(ctx, true, false, bs, bs, ld, 1.0, xn.p, xn.ld, z.data(), z.ld, 0.0, mtmp.data(), mtmp.ld);
+        out.m.emplace_back(ctx, bs, bs, false);
+        symmetrize(ctx, out.m.back().view(), mtmp.view());
+    }
+    out.q.cols = out.built * bs;
+    return out;
+}
+
+// block_lanczos.hpp:204-261
+BlwsResult blws_svd(LinearOperator& w, const DWarm& warm, Index k, Index r, Rng& rng) {
+    Context& ctx = w.ctx();
+    const Index m = w.rows(), n = w.cols();
+    const Index bs = warm.rank();
+    if (bs < 1) throw std::invalid_argument("blws_svd: empty warm start (seed via adapt_subspace)");
+    if (r < 1 || r > std::min(m, n)) throw std::invalid_argument("blws_svd: bad r");
+    if (warm.geo.m != m || warm.geo.n != n) throw std::invalid_argument("blws_svd: warm start does not match operator");
+    BlwsResult out;
+    Index k_eff = k;
+    if (r > k_eff * bs) {
+        k_eff = (r + bs - 1) / bs;
+        out.k_raised = true;
+    }
+    k_eff = std::min(k_eff, (m + n) / bs);
+    k_eff = std::max<Index>(k_eff, 1);
+    const Stack geo{m, n};
+
+    // X1 = qr([U; V] / sqrt(2)).q -- Q is invariant under the positive scale,
+    // so the 1/sqrt(2) is folded away.
+    DMat x1(ctx, geo.ld(), bs, false);
+    copy(ctx, x1.view(), warm.panel());
+    {
+        View xv = x1.view();
+        thin_qr(ctx, xv, nullptr);
+    }
+    BlockLanczos fac = block_lanczos_procedure(w, x1.view(), k_eff);
+    out.terminated_early = fac.terminated_early;
+    const Index d = fac.built * bs;
+
+    // T = embed() (block_lanczos.hpp:28-40), EVD descending (small_dense.hpp:24-43)
+    DMat t(ctx, d, d, true);
+    for (Index l = 0; l < fac.built; ++l) {
+        place_block(ctx, t.view().sub(l * bs, l * bs, bs, bs), fac.m[l].view(), false);
+        if (l + 1 < fac.built) {
+            place_block(ctx, t.view().sub(l * bs + bs, l * bs, bs, bs), fac.b[l].view(), false);
+            place_block(ctx, t.view().sub(l * bs, l * bs + bs, bs, bs), fac.b[l].view(), true);
+        }
+    }
+    DBuf<double> vals(ctx, static_cast<size_t>(d));
+    DMat vecs(ctx, d, d, false);
+    sym_evd_jacobi(ctx, t.view(), vals.get(), vecs.view());
+    std::vector<double> hv(static_cast<size_t>(d));
+    ctx.read(vals.get(), hv.data(), d);
+    for (double v : hv)
+        if (!std::isfinite(v)) throw NumericalError("sym_evd_small: failed to converge");
+
+    // keep the strictly positive part (block_lanczos.hpp:233-238); avail = d >= r
+    const Index avail = std::min(k_eff * bs, d);
+    const double floor = d > 0 ? 1e-12 * std::fabs(hv[0]) : 0.0;
+    Index keep = 0;
+    while (keep < avail && keep < r && hv[static_cast<size_t>(keep)] > floor) ++keep;
+
+    DWarm next = make_warm(ctx, m, n, keep);
+    if (keep > 0) {
+        // Ritz lift of the kept columns only, sqrt(2) unpack fused (:240-248)
+        gemm(ctx, false, false, geo.ld(), keep, d, std::sqrt(2.0), fac.q.data(), fac.q.ld, vecs.data(), vecs.ld, 0.0,
+             next.uv.data(), next.uv.ld);
+        std::copy(hv.begin(), hv.begin() + keep, next.sigma.begin());
+        View u = next.u(), v = next.v();
+        thin_qr(ctx, u, nullptr);
+        thin_qr(ctx, v, nullptr);
+    }
+    if (keep < r) {
+        next = adapt_subspace(ctx, keep > 0 ? &next : nullptr, r, m, n, rng);
+        out.padded = true;
+    }
+    out.warm = std::move(next);
+    return out;
+}
+
+// ======================================================== Lanczos (reseed)
+namespace {
+
+/// LanczosRun (lanczos.hpp:85-183) on the augmented view. Steps run on the
+/// device without host round trips; breakdown is latched on the device and
+/// read back at the Ritz checkpoints.
+class DeviceLanczos {
+public:
+    DeviceLanczos(LinearOperator& w, const std::vector<double>& q1_logical, Index cap)
+        : w_(w), ctx_(w.ctx()), geo_{w.rows(), w.cols()}, dim_(geo_.m + geo_.n), ld_(geo_.ld()), cap_(cap) {
+        q_ = DMat(ctx_, ld_, cap_, true);
+        next_ = DMat(ctx_, ld_, 1, true);
+        r_ = DMat(ctx_, ld_, 1, true);
+        alpha_ = DBuf<double>(ctx_, static_cast<size_t>(cap_));
+        lastbeta_ = DBuf<double>(ctx_, static_cast<size_t>(cap_));
+        coup_ = DBuf<double>(ctx_, static_cast<size_t>(cap_ + 1));
+        state_ = DBuf<double>(ctx_, 2);
+        coef_ = DBuf<double>(ctx_, static_cast<size_t>(cap_));
+        ss_ = DBuf<double>(ctx_, 1);
+        BLWS_CUDA(cudaMemsetAsync(coup_.get(), 0, sizeof(double) * coup_.size(), ctx_.stream()));
+        const double st[2] = {-1.0, 0.0};
+        ctx_.write(state_.get(), st, 2);
+        set_logical(next_.data(), q1_logical);
+    }
+
+    Index cols() const { return cols_; }
+    bool breakdown() const { return breakdown_; }
+    double residual_norm() const { return last_beta_; }
+    View basis() const { return View{q_.data(), ld_, cols_, q_.ld}; }
+
+    /// Launch steps until `target` columns; returns after syncing the state.
+    void step_to(Index target) {
+        while (cols_ < target) {
+            launch_step(cols_);
+            ++cols_;
+        }
+        sync_state();
+    }
+
+    /// restart (lanczos.hpp:144-160)
+    bool restart(Rng& rng) {
+        if (cols_ >= dim_) return false;
+        for (int attempt = 0; attempt < 3; ++attempt) {
+            std::vector<double> v = rng.gaussian_vector(dim_);
+            double s = 0;
+            for (double x : v) s += x * x;
+            const double n0 = std::sqrt(s);
+            for (auto& x : v) x /= n0;
+            set_logical(r_.data(), v);
+            reorth(r_.data());
+            reorth(r_.data());
+            sumsq(ctx_, r_.view(), ss_.get());
+            double nv2 = 0;
+            ctx_.read(ss_.get(), &nv2, 1);
+            const double nv = std::sqrt(nv2);
+            if (nv > 1e-8) {
+                copy(ctx_, next_.view(), r_.view(), 1.0 / nv);
+                const double zero = 0.0;
+                ctx_.write(coup_.get() + cols_, &zero, 1);  // recorded coupling is zero
+                const double st[1] = {-1.0};
+                ctx_.write(state_.get(), st, 1);
+                breakdown_ = false;
+                return true;
+            }
+        }
+        return false;
+    }
+
+    void read_tridiagonal(std::vector<double>& alpha, std::vector<double>& coup) {
+        alpha.resize(static_cast<size_t>(cols_));
+        coup.resize(static_cast<size_t>(std::max<Index>(cols_ - 1, 0)));
+        ctx_.read(alpha_.get(), alpha.data(), cols_);
+        if (cols_ > 1) ctx_.read(coup_.get() + 1, coup.data(), cols_ - 1);
+    }
+    const double* alpha_dev() const { return alpha_.get(); }
+    const double* coup_dev() const { return coup_.get(); }
+
+private:
+    void set_logical(double* dst, const std::vector<double>& v) {
+        std::vector<double> h(static_cast<size_t>(ld_), 0.0);
+        std::copy(v.begin(), v.begin() + geo_.m, h.begin());
+        std::copy(v.begin() + geo_.m, v.end(), h.begin() + geo_.mp());
+        BLWS_CUDA(cudaMemcpyAsync(dst, h.data(), sizeof(double) * ld_, cudaMemcpyHostToDevice, ctx_.stream()));
+        ctx_.sync();
+    }
+
+    // r -= Q (Q^T r) over the current basis
+    void reorth(double* r) {
+        if (cols_ == 0) return;
+        gemv(ctx_, true, ld_, cols_, 1.0, q_.data(), q_.ld, r, 0.0, coef_.get());
+        gemv(ctx_, false, ld_, cols_, -1.0, q_.data(), q_.ld, coef_.get(), 1.0, r);
+    }
+
+    void launch_step(Index l) {
+        double* ql = q_.data() + l * q_.ld;
+        BLWS_CUDA(cudaMemcpyAsync(ql, next_.data(), sizeof(double) * ld_, cudaMemcpyDeviceToDevice, ctx_.stream()));
+        // r = A q_l: (W q_bot ; W^T q_top)
+        w_.apply_pair(ql, ql + geo_.mp(), r_.data(), r_.data() + geo_.mp());
+        dot(ctx_, ld_, ql, r_.data(), alpha_.get() + l);
+        lanczos_three_term_k<<<gridn(ld_), kT, 0, ctx_.stream()>>>(r_.data(), q_.data(), q_.ld, l, alpha_.get(),
+                                                                   coup_.get(), ld_);
+        ctx_.note_launch();
+        // full reorthogonalisation, twice (lanczos.hpp:123-126); basis includes column l
+        const Index c = l + 1;
+        for (int pass = 0; pass < 2; ++pass) {
+            gemv(ctx_, true, ld_, c, 1.0, q_.data(), q_.ld, r_.data(), 0.0, coef_.get());
+            gemv(ctx_, false, ld_, c, -1.0, q_.data(), q_.ld, coef_.get(), 1.0, r_.data());
+        }
+        sumsq(ctx_, r_.view(), ss_.get());
+        lanczos_finalize_k<<<gridn(ld_), kT, 0, ctx_.stream()>>>(r_.data(), next_.data(), ld_, l, dim_, ss_.get(),
+                                                                 alpha_.get(), lastbeta_.get(), coup_.get(), cap_,
+                                                                 state_.get());
+        ctx_.note_launch();
+        ctx_.check_launch("lanczos step");
+    }
+
+    void sync_state() {
+        double st[2];
+        ctx_.read(state_.get(), st, 2);
+        const Index first_broken = st[0] >= 0 ? static_cast<Index>(st[0]) : -1;
+        if (first_broken >= 0 && first_broken + 1 < cols_) cols_ = first_broken + 1;
+        breakdown_ = first_broken >= 0;
+        if (cols_ > 0) ctx_.read(lastbeta_.get() + cols_ - 1, &last_beta_, 1);
+    }
+
+    LinearOperator& w_;
+    Context& ctx_;
+    Stack geo_;
+    Index dim_, ld_, cap_;
+    DMat q_, next_, r_;
+    DBuf<double> alpha_, lastbeta_, coup_, state_, coef_, ss_;
+    Index cols_ = 0;
+    bool breakdown_ = false;
+    double last_beta_ = 0;
+};
+
+struct Checkpoint {
+    std::vector<double> values;  // top `want`, descending
+    DMat vecs;                   // cols x want
+    Index converged = 0;
+};
+
+// ritz_checkpoint (lanczos.hpp:191-207), top min(r, cols) pairs
+Checkpoint ritz_checkpoint(Context& ctx, DeviceLanczos& run, Index r, double tol) {
+    Checkpoint cp;
+    const Index k = run.cols();
+    const Index want = std::min(r, k);
+    DBuf<double> vals(ctx, static_cast<size_t>(want));
+    cp.vecs = DMat(ctx, k, want, false);
+    tridiag_eig_top(ctx, k, run.alpha_dev(), run.coup_dev() + 1, want, vals.get(), cp.vecs.view());
+    cp.values.resize(static_cast<size_t>(want));
+    ctx.read(vals.get(), cp.values.data(), want);
+    std::vector<double> last(static_cast<size_t>(want));
+    BLWS_CUDA(cudaMemcpy2DAsync(last.data(), sizeof(double), cp.vecs.data() + (k - 1), sizeof(double) * cp.vecs.ld,
+                                sizeof(double), want, cudaMemcpyDeviceToHost, ctx.stream()));
+    ctx.sync();
+    const double scale = std::fabs(cp.values[0]);
+    const double limit = tol * scale;
+    for (Index j = 0; j < want; ++j) {
+        const double res = run.residual_norm() * std::fabs(last[static_cast<size_t>(j)]);
+        if (res <= limit)
+            ++cp.converged;
+        else
+            break;
+    }
+    return cp;
+}
+
+}  // namespace
+
+// lanczos.hpp:209-252 (partial_evd_impl) + :289-329 (lanczos_partial_svd)
+PartialSvd lanczos_partial_svd(LinearOperator& w, Index r, const LanczosOptions& opts) {
+    Context& ctx = w.ctx();
+    const Index m = w.rows(), n = w.cols();
+    if (r < 1 || r > std::min(m, n)) throw std::invalid_argument("lanczos_partial_svd: bad r");
+    const Index dim = m + n;
+    Rng seed_rng = Rng(opts.seed).split(13);
+    std::vector<double> top = seed_rng.unit_vector(m);
+    std::vector<double> q1(static_cast<size_t>(dim), 0.0);
+    std::copy(top.begin(), top.end(), q1.begin());
+
+    Index max_k = opts.max_k > 0 ? std::min(opts.max_k, dim) : std::min(dim, 10 * r + 20);
+    max_k = std::max(max_k, std::min(dim, r));
+    DeviceLanczos run(w, q1, max_k);
+    Rng rng = Rng(opts.seed).split(11);
+    LanczosStats stats;
+    Index k_target = std::min(max_k, std::max<Index>(2 * r, 10));
+    while (true) {
+        if (!run.breakdown() && run.cols() < k_target) {
+            run.step_to(k_target);
+            continue;
+        }
+        Checkpoint cp = ritz_checkpoint(ctx, run, r, opts.tol);
+        bool done = cp.converged >= r || run.cols() >= max_k;
+        if (!done) {
+            if (run.breakdown()) {
+                if (run.restart(rng))
+                    ++stats.restarts;
+                else
+                    done = true;
+            } else {
+                k_target = std::min(max_k, 2 * k_target);
+            }
+        }
+        if (done) {
+            const Index avail = std::min(r, run.cols());
+            Index keep = 0;
+            while (keep < avail && cp.values[static_cast<size_t>(keep)] > 0.0) ++keep;
+            PartialSvd out;
+            out.uv = make_warm(ctx, m, n, keep);
+            if (keep > 0) {
+                View B = run.basis();
+                gemm(ctx, false, false, B.rows, keep, B.cols, std::sqrt(2.0), B.p, B.ld, cp.vecs.data(), cp.vecs.ld,
+                     0.0, out.uv.uv.data(), out.uv.uv.ld);
+                std::copy(cp.values.begin(), cp.values.begin() + keep, out.uv.sigma.begin());
+            }
+            stats.steps = run.cols();
+            stats.converged = std::min(cp.converged, avail);
+            stats.all_converged = avail == r && cp.converged >= r;
+            out.stats = stats;
+            out.stats.converged = std::min(out.stats.converged, keep);
+            out.stats.all_converged = stats.all_converged && keep == r;
+            return out;
+        }
+    }
+}
+
+double spectral_norm(LinearOperator& w, double tol, std::uint64_t seed) {
+    LanczosOptions o;
+    o.tol = tol;
+    o.seed = seed;
+    auto svd = lanczos_partial_svd(w, 1, o);
+    return svd.uv.rank() > 0 ? svd.uv.sigma[0] : 0.0;
+}
+
+}  // namespace blws

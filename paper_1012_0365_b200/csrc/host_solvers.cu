@@ -1,0 +1,533 @@
+// SvdBackend / svt and the RPCA (inexact ALM) and MC (SVT) solvers.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <sstream>
+#include <stdexcept>
+
+#include "dgemm.cuh"
+#include "host.hpp"
+#include "ops.cuh"
+
+namespace blws {
+
+// ================================================================== svt
+RankPredictor predict_rank(RankPredictor p, Index achieved, bool all_above) {
+    const Index next = achieved + (all_above ? p.increment : 1);
+    p.r = std::clamp<Index>(next, 1, p.max_rank);
+    p.history.push_back(p.r);
+    return p;
+}
+
+SvdBackend::SvdBackend(Context& ctx, Kind k, Options o) : ctx_(ctx), kind_(k), opt_(o), rng_(o.seed) {
+    if (k == Kind::ExactFull)
+        throw std::invalid_argument("SvdBackend: ExactFull is the dense test oracle and has no device path");
+}
+
+// svt.hpp:104-186
+SvdBackend::Triplets SvdBackend::compute(LinearOperator& w, Index r) {
+    const Index p = std::min(w.rows(), w.cols());
+    if (r < 1 || r > p) throw std::invalid_argument("SvdBackend: bad r");
+    Triplets t;
+    if (kind_ == Kind::Lanczos) {
+        LanczosOptions lo;
+        lo.tol = opt_.ritz_tol;
+        lo.max_k = opt_.max_k;
+        lo.seed = rng_.next_u64();
+        auto svd = lanczos_partial_svd(w, r, lo);
+        t.own = std::move(svd.uv);
+        t.converged = svd.stats.converged;
+        t.hit_cap = !svd.stats.all_converged;
+        return t;
+    }
+    const Index held = warm_ ? warm_->rank() : 0;
+    if (held < r) {
+        const Index margin = opt_.seed_margin * (Index(1) << std::min<Index>(growth_streak_, 5));
+        ++growth_streak_;
+        const Index r_seed = std::min(p, r + margin);
+        LanczosOptions lo;
+        lo.tol = opt_.ritz_tol;
+        lo.max_k = opt_.max_k;
+        lo.seed = rng_.next_u64();
+        auto svd = lanczos_partial_svd(w, r_seed, lo);
+        DWarm ws = std::move(svd.uv);
+        if (ws.rank() < r_seed) ws = adapt_subspace(ctx_, ws.rank() > 0 ? &ws : nullptr, r_seed, w.rows(), w.cols(), rng_);
+        warm_ = std::move(ws);
+        t.held = &*warm_;
+        t.converged = svd.stats.converged;
+        t.hit_cap = !svd.stats.all_converged;
+        return t;
+    }
+    if (r < held) growth_streak_ = 0;
+    if (held > r + 2 * opt_.seed_margin)
+        warm_ = adapt_subspace(ctx_, &*warm_, r + opt_.seed_margin, w.rows(), w.cols(), rng_);
+    auto res = blws_svd(w, *warm_, opt_.block_steps, warm_->rank(), rng_);
+    warm_ = std::move(res.warm);
+    t.held = &*warm_;
+    t.converged = res.padded ? std::min(r, warm_->rank()) : warm_->rank();
+    return t;
+}
+
+// svt.hpp:216-254
+SvtResult svt(LinearOperator& w, double eps, SvdBackend& backend, RankPredictor& predictor) {
+    if (eps < 0.0) throw std::invalid_argument("svt: negative threshold");
+    Context& ctx = w.ctx();
+    const Index p = std::min(w.rows(), w.cols());
+    Index r = std::clamp<Index>(predictor.r, 1, p);
+    SvdBackend::Triplets t;
+    bool all_above = false;
+    while (true) {
+        t = backend.compute(w, r);
+        const DWarm& tr = t.get();
+        const Index have = tr.rank();
+        const bool smallest_above = have > 0 && tr.sigma[static_cast<size_t>(have - 1)] > eps;
+        if (!smallest_above || std::max(r, have) >= p) {
+            all_above = smallest_above;
+            break;
+        }
+        r = std::min<Index>(std::max(r, have) + predictor.increment, p);
+    }
+    const DWarm& tr = t.get();
+    if (t.hit_cap && t.converged == 0 && tr.rank() > 0 && tr.sigma[0] > eps) {
+        std::ostringstream msg;
+        msg << "svt: partial SVD backend hit its step cap with no converged triplet (requested " << r << " of " << p
+            << ")";
+        throw NumericalError(msg.str());
+    }
+    Index achieved = 0;
+    while (achieved < tr.rank() && tr.sigma[static_cast<size_t>(achieved)] > eps) ++achieved;
+    SvtResult out;
+    out.trip = copy_warm(ctx, tr, achieved);
+    for (Index j = 0; j < achieved; ++j) out.trip.sigma[static_cast<size_t>(j)] -= eps;
+    out.sigma_dev = DBuf<double>(ctx, static_cast<size_t>(std::max<Index>(achieved, 1)));
+    if (achieved > 0) ctx.write(out.sigma_dev.get(), out.trip.sigma.data(), achieved);
+    out.achieved_rank = achieved;
+    out.all_above_threshold = all_above;
+    predictor = predict_rank(predictor, achieved, all_above);
+    return out;
+}
+
+// ============================================================ device kernels
+namespace {
+
+constexpr int kT = 256;
+inline unsigned gridn(long total, long cap = 4096) {
+    return static_cast<unsigned>(std::max<long>(1, std::min<long>(cap, (total + kT - 1) / kT)));
+}
+
+__device__ __forceinline__ double shrink_d(double x, double eps) { return x > eps ? x - eps : (x < -eps ? x + eps : 0.0); }
+
+// W = D - E + Y / mu (solvers.hpp:112), non-finite flag
+__global__ void form_w_k(const double* D, const double* E, const double* Y, double* W, long m, long ld, double mu,
+                         int* bad) {
+    const long total = m * m;
+    int b = 0;
+    for (long idx = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<long>(gridDim.x) * blockDim.x) {
+        const long o = idx % m + (idx / m) * ld;
+        const double w = D[o] - E[o] + Y[o] / mu;
+        W[o] = w;
+        b |= !isfinite(w);
+    }
+    if (__syncthreads_or(b) && threadIdx.x == 0) atomicOr(bad, 1);
+}
+
+// Y = D / s
+__global__ void scale_into_k(const double* D, double* Y, long m, long ld, double s) {
+    const long total = m * m;
+    for (long idx = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<long>(gridDim.x) * blockDim.x) {
+        const long o = idx % m + (idx / m) * ld;
+        Y[o] = D[o] / s;
+    }
+}
+
+__global__ void maxabs_partial_k(const double* x, long m, long ld, double* partial) {
+    const long total = m * m;
+    double v = 0.0;
+    for (long idx = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<long>(gridDim.x) * blockDim.x)
+        v = fmax(v, fabs(x[idx % m + (idx / m) * ld]));
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    __shared__ double sh[32];
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) v = fmax(v, sh[w]);
+        partial[blockIdx.x] = v;
+    }
+}
+
+// e_l0 = #|E| > tol, nnz = #E != 0 (solvers.hpp:400-409)
+__global__ void e_counts_k(const double* E, long m, long ld, double tol, unsigned long long* out) {
+    const long total = m * m;
+    unsigned long long l0 = 0, nz = 0;
+    for (long idx = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<long>(gridDim.x) * blockDim.x) {
+        const double v = E[idx % m + (idx / m) * ld];
+        l0 += fabs(v) > tol;
+        nz += v != 0.0;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        l0 += __shfl_xor_sync(0xffffffffu, l0, o);
+        nz += __shfl_xor_sync(0xffffffffu, nz, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(out, l0);
+        atomicAdd(out + 1, nz);
+    }
+}
+
+/// K7: fused rank-r reconstruction + ALM update (solvers.hpp:114-124):
+///   a = (U diag(s)) V^T            (DMMA mainloop, K = r)
+///   e = shrink(D - a + Y/mu, lambda/mu); res = D - a - e; Y += mu res
+///   W = D - e + Y/mu_next;  E = e;  partial ||res||^2, non-finite(W)
+/// One pass over D, Y (read) and Y, W, E (write): 40 B per element.
+__global__ void __launch_bounds__(gemm_detail::THREADS) alm_fused_k(const double* __restrict__ us, long ldu,
+                                                                   const double* __restrict__ v, long ldv, long m,
+                                                                   long r, const double* __restrict__ D, double* Y,
+                                                                   double* W, double* E, long ld, double mu,
+                                                                   double mu_next, double lambda_mu, double* partial,
+                                                                   int* bad) {
+    using namespace gemm_detail;
+    extern __shared__ __align__(16) double smem[];
+    const long m0 = static_cast<long>(blockIdx.x) * BM, n0 = static_cast<long>(blockIdx.y) * BN;
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    mainloop<false, true, 2>(acc, smem, us, ldu, v, ldv, m, m, m0, n0, 0, r);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane >> 2, t = lane & 3;
+    const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
+    double ss = 0.0;
+    int nonfinite = 0;
+    const double inv_mu = 1.0 / mu, inv_mu_next = 1.0 / mu_next;
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi) {
+        const long row = m0 + wm + mi * 8 + g;
+        if (row >= m) continue;
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+            for (int e2 = 0; e2 < 2; ++e2) {
+                const long col = n0 + wn + ni * 8 + 2 * t + e2;
+                if (col >= m) continue;
+                const long o = row + col * ld;
+                const double a = acc[mi][ni][e2];
+                const double d = D[o];
+                const double y = Y[o];
+                const double dma = d - a;
+                const double e = shrink_d(dma + y * inv_mu, lambda_mu);
+                const double res = dma - e;
+                const double yn = y + mu * res;
+                const double w = (d - e) + yn * inv_mu_next;
+                Y[o] = yn;
+                E[o] = e;
+                W[o] = w;
+                ss += res * res;
+                nonfinite |= !isfinite(w);
+            }
+    }
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    __shared__ double sh[4];
+    __syncthreads();
+    if (lane == 0) sh[warp] = ss;
+    if (__syncthreads_or(nonfinite) && threadIdx.x == 0) atomicOr(bad, 1);
+    if (threadIdx.x == 0) partial[blockIdx.x + static_cast<long>(blockIdx.y) * gridDim.x] = (sh[0] + sh[1]) + (sh[2] + sh[3]);
+}
+
+// K9: a_p = sum_c us[i,c] v[j,c] over CSC positions p (solvers.hpp:181-196, :247);
+// resid_p = obs_p - a_p; per-block partial ||resid||^2.
+__global__ void mc_sampled_k(long nnz, const std::int32_t* __restrict__ rowidx, const std::int32_t* __restrict__ colof,
+                             const double* __restrict__ ust, const double* __restrict__ vt, long r,
+                             const double* __restrict__ obs, double* resid, double* partial) {
+    double ss = 0.0;
+    for (long p = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; p < nnz;
+         p += static_cast<long>(gridDim.x) * blockDim.x) {
+        const double* a = ust + static_cast<long>(rowidx[p]) * r;
+        const double* b = vt + static_cast<long>(colof[p]) * r;
+        double s0 = 0.0, s1 = 0.0;
+        long c = 0;
+        for (; c + 1 < r; c += 2) {
+            s0 += a[c] * b[c];
+            s1 += a[c + 1] * b[c + 1];
+        }
+        if (c < r) s0 += a[c] * b[c];
+        const double res = obs[p] - (s0 + s1);
+        resid[p] = res;
+        ss += res * res;
+    }
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    __shared__ double sh[32];
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = ss;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) s += sh[w];
+        partial[blockIdx.x] = s;
+    }
+}
+
+__global__ void row_major_scaled_k(const double* X, long ld, long rows, long cols, const double* s, double* out) {
+    const long total = rows * cols;
+    for (long idx = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<long>(gridDim.x) * blockDim.x) {
+        const long i = idx / cols, c = idx % cols;
+        out[idx] = X[i + c * ld] * (s ? s[c] : 1.0);
+    }
+}
+
+__global__ void vec_axpy_k(long n, double* y, const double* x, double a) {
+    for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long>(gridDim.x) * blockDim.x)
+        y[i] += a * x[i];
+}
+
+__global__ void vec_scale_k(long n, double* y, const double* x, double a) {
+    for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long>(gridDim.x) * blockDim.x)
+        y[i] = a * x[i];
+}
+
+double sum_partials(Context& ctx, const double* part, Index count) {
+    DBuf<double> out(ctx, 1);
+    reduce_partials(ctx, part, count, out.get());
+    double h = 0;
+    ctx.read(out.get(), &h, 1);
+    return h;
+}
+
+double frob(Context& ctx, View x) {
+    DBuf<double> s(ctx, 1);
+    sumsq(ctx, x, s.get());
+    double h = 0;
+    ctx.read(s.get(), &h, 1);
+    return std::sqrt(h);
+}
+
+}  // namespace
+
+// ============================================================ rpca_adm
+SolverStats rpca_adm(Context& ctx, Index m, const double* d_in, Index ldd, double lambda_in, SvdBackend& backend,
+                     const RpcaOptions& opts, const double* truth, double* a_out, double* e_out) {
+    const auto t0 = std::chrono::steady_clock::now();
+    SolverStats stats;
+    const Index ld = std::max<Index>(2, round_up(m, 2));
+    DMat D(ctx, m, m, false);
+    copy(ctx, D.view(), View{const_cast<double*>(d_in), m, m, ldd});
+    {
+        DenseOperator probe(ctx, m, m, D.data(), D.ld);
+        try {
+            probe.check_finite();
+        } catch (const std::invalid_argument&) {
+            throw std::invalid_argument("rpca_adm: D has non-finite entries");
+        }
+    }
+    const double lambda = lambda_in > 0.0 ? lambda_in : 1.0 / std::sqrt(static_cast<double>(m));
+    const double norm_d_fro = frob(ctx, D.view());
+    if (norm_d_fro == 0.0) {
+        if (a_out) fill(ctx, View{a_out, m, m, ldd}, 0.0);
+        if (e_out) fill(ctx, View{e_out, m, m, ldd}, 0.0);
+        stats.converged = true;
+        stats.e_l0 = 0;
+        return stats;
+    }
+    DMat Wm(ctx, m, m, false), Y(ctx, m, m, false), E(ctx, m, m, true);
+    copy(ctx, Wm.view(), D.view());
+    DenseOperator op(ctx, m, m, Wm.data(), Wm.ld);
+    const double norm2_d = spectral_norm(op);
+    double mu = 1.25 / norm2_d;
+    const double mu_max = mu * opts.mu_max_factor;
+    double dmax = 0;
+    {
+        const unsigned blocks = gridn(m * m, 1024);
+        DBuf<double> part(ctx, blocks);
+        maxabs_partial_k<<<blocks, kT, 0, ctx.stream()>>>(D.data(), m, ld, part.get());
+        ctx.note_launch();
+        std::vector<double> h(blocks);
+        ctx.read(part.get(), h.data(), blocks);
+        for (double x : h) dmax = std::max(dmax, x);
+    }
+    const double dual_scale = std::max(norm2_d, dmax / lambda);
+    scale_into_k<<<gridn(m * m), kT, 0, ctx.stream()>>>(D.data(), Y.data(), m, ld, dual_scale);
+    ctx.note_launch();
+
+    RankPredictor predictor;
+    predictor.r = opts.initial_rank;
+    predictor.increment = opts.rank_increment;
+    predictor.max_rank = m;
+    stats.matvec_init = op.application_count();
+    std::int64_t mark = stats.matvec_init;
+    Index last_rank = 0;
+    DBuf<int> bad(ctx, 1);
+    // first W = D - E + Y/mu (later ones come out of the fused kernel)
+    BLWS_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(int), ctx.stream()));
+    form_w_k<<<gridn(m * m), kT, 0, ctx.stream()>>>(D.data(), E.data(), Y.data(), Wm.data(), m, ld, mu, bad.get());
+    ctx.note_launch();
+    using namespace gemm_detail;
+    const dim3 grid(static_cast<unsigned>(ceil_div(m, BM)), static_cast<unsigned>(ceil_div(m, BN)));
+    DBuf<double> part(ctx, static_cast<size_t>(grid.x) * grid.y);
+    constexpr int smem = smem_bytes<false, true>();
+    BLWS_CUDA(cudaFuncSetAttribute(alm_fused_k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    SvtResult prox;
+    for (Index it = 1; it <= opts.max_iter; ++it) {
+        int hbad = 0;
+        BLWS_CUDA(cudaMemcpyAsync(&hbad, bad.get(), sizeof(int), cudaMemcpyDeviceToHost, ctx.stream()));
+        ctx.sync();
+        if (hbad) throw std::invalid_argument("DenseOperator: non-finite entries");
+        prox = svt(op, 1.0 / mu, backend, predictor);
+        last_rank = prox.achieved_rank;
+        const Index r = prox.achieved_rank;
+        DMat us(ctx, m, std::max<Index>(r, 1), false);
+        if (r > 0) scale_columns(ctx, us.view().left(r), prox.trip.u(), prox.sigma_dev.get());
+        const double mu_next = std::min(opts.rho * mu, mu_max);
+        BLWS_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(int), ctx.stream()));
+        alm_fused_k<<<grid, THREADS, smem, ctx.stream()>>>(us.data(), us.ld, prox.trip.v().p, prox.trip.uv.ld, m, r,
+                                                           D.data(), Y.data(), Wm.data(), E.data(), ld, mu, mu_next,
+                                                           lambda / mu, part.get(), bad.get());
+        ctx.note_launch();
+        ctx.check_launch("alm_fused_k");
+        mu = mu_next;
+        stats.matvec_history.push_back(op.application_count() - mark);
+        mark = op.application_count();
+        const double feas = std::sqrt(sum_partials(ctx, part.get(), static_cast<Index>(grid.x) * grid.y)) / norm_d_fro;
+        stats.residual_history.push_back(feas);
+        stats.iterations = it;
+        if (feas <= opts.tol_outer) {
+            stats.converged = true;
+            break;
+        }
+    }
+    // A = U diag(s) V^T of the last prox; E, e_l0, rel_err
+    const Index r = prox.achieved_rank;
+    DMat A(ctx, m, m, false);
+    if (r > 0) {
+        DMat us(ctx, m, r, false);
+        scale_columns(ctx, us.view(), prox.trip.u(), prox.sigma_dev.get());
+        gemm(ctx, false, true, m, m, r, 1.0, us.data(), us.ld, prox.trip.v().p, prox.trip.uv.ld, 0.0, A.data(), A.ld);
+    } else {
+        fill(ctx, A.view(), 0.0);
+    }
+    {
+        DBuf<unsigned long long> cnt(ctx, 2);
+        BLWS_CUDA(cudaMemsetAsync(cnt.get(), 0, 2 * sizeof(unsigned long long), ctx.stream()));
+        e_counts_k<<<gridn(m * m, 1024), kT, 0, ctx.stream()>>>(E.data(), m, ld, 1e-8 * dmax, cnt.get());
+        ctx.note_launch();
+        unsigned long long h[2];
+        BLWS_CUDA(cudaMemcpyAsync(h, cnt.get(), sizeof(h), cudaMemcpyDeviceToHost, ctx.stream()));
+        ctx.sync();
+        stats.e_l0 = static_cast<std::int64_t>(h[0]);
+        stats.e_nnz = static_cast<std::int64_t>(h[1]);
+    }
+    if (truth) {
+        DMat diff(ctx, m, m, false);
+        copy(ctx, diff.view(), A.view());
+        axpy(ctx, diff.view(), View{const_cast<double*>(truth), m, m, ldd}, -1.0);
+        stats.rel_err = frob(ctx, diff.view()) / frob(ctx, View{const_cast<double*>(truth), m, m, ldd});
+    }
+    if (a_out) copy(ctx, View{a_out, m, m, ldd}, A.view());
+    if (e_out) copy(ctx, View{e_out, m, m, ldd}, E.view());
+    ctx.sync();
+    stats.rank_hat = last_rank;
+    stats.matvec_count = op.application_count();
+    stats.predicted_ranks = predictor.history;
+    stats.wall_time_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return stats;
+}
+
+// ============================================================ mc_svt
+McSolution mc_svt(Context& ctx, Index m, Index n, Index nnz, const std::int64_t* colptr, const std::int32_t* rowidx,
+                  const double* vals, double tau_in, double delta_in, SvdBackend& backend, const McOptions& opts,
+                  const double* truth_ml, const double* truth_mr, Index r_true) {
+    const auto t0 = std::chrono::steady_clock::now();
+    if (nnz == 0) throw std::invalid_argument("mc_svt: empty observation set");
+    for (Index i = 0; i < nnz; ++i)
+        if (!std::isfinite(vals[i])) throw std::invalid_argument("mc_svt: non-finite observations");
+    const double tau = tau_in > 0.0 ? tau_in : 5.0 * static_cast<double>(m);
+    const double delta = delta_in > 0.0 ? delta_in
+                                        : 1.2 * static_cast<double>(m) * static_cast<double>(n) / static_cast<double>(nnz);
+    SparseOperator op(ctx, m, n, nnz, colptr, rowidx, vals);
+    const double norm2_pd = spectral_norm(op);
+    const double k0 = std::ceil(tau / (delta * norm2_pd));
+    DBuf<double> obs(ctx, static_cast<size_t>(nnz)), y(ctx, static_cast<size_t>(nnz)), resid(ctx, static_cast<size_t>(nnz));
+    BLWS_CUDA(cudaMemcpyAsync(obs.get(), op.val_csc(), sizeof(double) * nnz, cudaMemcpyDeviceToDevice, ctx.stream()));
+    double obs_norm = 0;
+    {
+        DBuf<double> s(ctx, 1);
+        sumsq(ctx, View{obs.get(), nnz, 1, nnz}, s.get());
+        ctx.read(s.get(), &obs_norm, 1);
+        obs_norm = std::sqrt(obs_norm);
+    }
+    vec_scale_k<<<gridn(nnz), kT, 0, ctx.stream()>>>(nnz, y.get(), obs.get(), k0 * delta);
+    ctx.note_launch();
+
+    RankPredictor predictor;
+    predictor.r = opts.initial_rank;
+    predictor.increment = opts.rank_increment;
+    predictor.max_rank = std::min(m, n);
+    McSolution sol;
+    SolverStats& stats = sol.stats;
+    stats.matvec_init = op.application_count();
+    std::int64_t mark = stats.matvec_init;
+    const unsigned blocks = gridn(nnz, 2048);
+    DBuf<double> part(ctx, blocks);
+    for (Index it = 1; it <= opts.max_iter; ++it) {
+        op.assign_values_device(y.get());
+        SvtResult prox = svt(op, tau, backend, predictor);
+        stats.rank_hat = prox.achieved_rank;
+        const Index r = prox.achieved_rank;
+        DBuf<double> ust(ctx, static_cast<size_t>(std::max<Index>(m * r, 1))), vt(ctx, static_cast<size_t>(std::max<Index>(n * r, 1)));
+        if (r > 0) {
+            row_major_scaled_k<<<gridn(m * r), kT, 0, ctx.stream()>>>(prox.trip.u().p, prox.trip.uv.ld, m, r,
+                                                                      prox.sigma_dev.get(), ust.get());
+            row_major_scaled_k<<<gridn(n * r), kT, 0, ctx.stream()>>>(prox.trip.v().p, prox.trip.uv.ld, n, r, nullptr,
+                                                                      vt.get());
+            ctx.note_launch(2);
+        }
+        mc_sampled_k<<<blocks, kT, 0, ctx.stream()>>>(nnz, op.rowidx_csc(), op.colof_csc(), ust.get(), vt.get(), r,
+                                                      obs.get(), resid.get(), part.get());
+        ctx.note_launch();
+        ctx.check_launch("mc_sampled_k");
+        sol.uv = std::move(prox.trip);
+        stats.matvec_history.push_back(op.application_count() - mark);
+        mark = op.application_count();
+        const double rel = std::sqrt(sum_partials(ctx, part.get(), blocks)) / obs_norm;
+        stats.residual_history.push_back(rel);
+        stats.iterations = it;
+        if (rel <= opts.tol_outer) {
+            stats.converged = true;
+            break;
+        }
+        vec_axpy_k<<<gridn(nnz), kT, 0, ctx.stream()>>>(nnz, y.get(), resid.get(), delta);
+        ctx.note_launch();
+    }
+    stats.matvec_count = op.application_count();
+    stats.predicted_ranks = predictor.history;
+    if (truth_ml && truth_mr && r_true > 0) {
+        // ||U S V^T - ML MR^T||_F / ||ML MR^T||_F via one GEMM with K = rank + r_true
+        const Index r = sol.uv.rank();
+        DMat left(ctx, m, r + r_true, false), right(ctx, n, r + r_true, false);
+        if (r > 0) {
+            DBuf<double> sd(ctx, static_cast<size_t>(r));
+            ctx.write(sd.get(), sol.uv.sigma.data(), r);
+            scale_columns(ctx, left.view().left(r), sol.uv.u(), sd.get());
+            copy(ctx, right.view().left(r), sol.uv.v());
+        }
+        upload(ctx, left.view().cols_range(r, r_true), truth_ml, m);
+        copy(ctx, left.view().cols_range(r, r_true), left.view().cols_range(r, r_true), -1.0);
+        upload(ctx, right.view().cols_range(r, r_true), truth_mr, n);
+        DMat full(ctx, m, n, false);
+        gemm(ctx, false, true, m, n, r + r_true, 1.0, left.data(), left.ld, right.data(), right.ld, 0.0, full.data(),
+             full.ld);
+        const double num = frob(ctx, full.view());
+        gemm(ctx, false, true, m, n, r_true, -1.0, left.data() + r * left.ld, left.ld, right.data() + r * right.ld,
+             right.ld, 0.0, full.data(), full.ld);
+        stats.rel_err = num / frob(ctx, full.view());
+    }
+    stats.wall_time_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return sol;
+}
+
+}  // namespace blws

@@ -1,0 +1,481 @@
+// Level-1 / small dense / GEMV / sparse kernels of the BLWS hot path.
+#include <algorithm>
+#include <cmath>
+
+#include "ops.cuh"
+
+namespace blws {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+inline unsigned grid_for(long total, int threads = kThreads, long cap = 4096) {
+    return static_cast<unsigned>(std::max<long>(1, std::min<long>(cap, (total + threads - 1) / threads)));
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+/// Block-wide sum; result valid in thread 0. blockDim.x multiple of 32, <= 1024.
+__device__ double block_sum(double v) {
+    __shared__ double sh[32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    v = warp_sum(v);
+    __syncthreads();
+    if (lane == 0) sh[wid] = v;
+    __syncthreads();
+    const int nw = (blockDim.x + 31) >> 5;
+    v = threadIdx.x < nw ? sh[threadIdx.x] : 0.0;
+    if (wid == 0) v = warp_sum(v);
+    return v;
+}
+
+__global__ void fill_k(double* x, long rows, long cols, long ld, double v) {
+    const long total = rows * cols;
+    for (long idx = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<long>(gridDim.x) * blockDim.x)
+        x[idx % rows + (idx / rows) * ld] = v;
+}
+
+__global__ void copy_k(double* d, long ldd, const double* s, long lds, long rows, long cols, double alpha) {
+    const long total = rows * cols;
+    for (long idx = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<long>(gridDim.x) * blockDim.x) {
+        const long i = idx % rows, j = idx / rows;
+        d[i + j * ldd] = alpha == 1.0 ? s[i + j * lds] : alpha * s[i + j * lds];
+    }
+}
+
+__global__ void axpy_k(double* y, long ldy, const double* x, long ldx, long rows, long cols, double alpha) {
+    const long total = rows * cols;
+    for (long idx = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<long>(gridDim.x) * blockDim.x) {
+        const long i = idx % rows, j = idx / rows;
+        y[i + j * ldy] += alpha * x[i + j * ldx];
+    }
+}
+
+__global__ void sumsq_partial_k(const double* x, long rows, long cols, long ld, int minus_identity,
+                                double* partial) {
+    const long total = rows * cols;
+    double s = 0.0;
+    for (long idx = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<long>(gridDim.x) * blockDim.x) {
+        const long i = idx % rows, j = idx / rows;
+        double v = x[i + j * ld];
+        if (minus_identity && i == j) v -= 1.0;
+        s += v * v;
+    }
+    s = block_sum(s);
+    if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+__global__ void reduce_k(const double* partial, long count, double* out) {
+    double s = 0.0;
+    for (long i = threadIdx.x; i < count; i += blockDim.x) s += partial[i];
+    s = block_sum(s);
+    if (threadIdx.x == 0) out[0] = s;
+}
+
+__global__ void symmetrize_k(double* d, long ldd, const double* s, long lds, long n) {
+    const long total = n * n;
+    for (long idx = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<long>(gridDim.x) * blockDim.x) {
+        const long i = idx % n, j = idx / n;
+        d[i + j * ldd] = 0.5 * (s[i + j * lds] + s[j + i * lds]);
+    }
+}
+
+__global__ void place_k(double* d, long ldd, const double* s, long lds, long rows, long cols, int transpose) {
+    const long total = rows * cols;
+    for (long idx = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<long>(gridDim.x) * blockDim.x) {
+        const long i = idx % rows, j = idx / rows;
+        if (transpose)
+            d[j + i * ldd] = s[i + j * lds];
+        else
+            d[i + j * ldd] = s[i + j * lds];
+    }
+}
+
+__global__ void scale_cols_k(double* d, long ldd, const double* s, long lds, long rows, long cols,
+                             const double* sc) {
+    const long total = rows * cols;
+    for (long idx = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<long>(gridDim.x) * blockDim.x) {
+        const long i = idx % rows, j = idx / rows;
+        d[i + j * ldd] = s[i + j * lds] * sc[j];
+    }
+}
+
+__global__ void gather_cols_k(double* d, long ldd, const double* s, long lds, long rows, long cols, const int* ix) {
+    const long total = rows * cols;
+    for (long idx = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<long>(gridDim.x) * blockDim.x) {
+        const long i = idx % rows, j = idx / rows;
+        d[i + j * ldd] = s[i + static_cast<long>(ix[j]) * lds];
+    }
+}
+
+// Right-looking upper Cholesky, one CTA, G in global memory (L1/L2 resident).
+__global__ void __launch_bounds__(1024) potrf_k(double* g, long n, long ld, int* status, double* diag) {
+    __shared__ double rowj[2048];
+    __shared__ int fail;
+    if (threadIdx.x == 0) fail = 0;
+    __syncthreads();
+    for (long j = 0; j < n; ++j) {
+        const double piv = g[j + j * ld];
+        if (!(piv > 0.0) || !isfinite(piv)) {
+            if (threadIdx.x == 0) fail = static_cast<int>(j + 1);
+            break;
+        }
+        const double rjj = sqrt(piv);
+        __syncthreads();
+        // row j of R (columns k > j); stage in shared when it fits
+        for (long k = j + 1 + threadIdx.x; k < n; k += blockDim.x) {
+            const double r = g[j + k * ld] / rjj;
+            g[j + k * ld] = r;
+            if (k - j - 1 < 2048) rowj[k - j - 1] = r;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) g[j + j * ld] = rjj;
+        // trailing update of the upper triangle: G[i,k] -= R[j,i] R[j,k], j < i <= k
+        const long w = n - j - 1;
+        const long total = w * (w + 1) / 2;
+        for (long idx = threadIdx.x; idx < total; idx += blockDim.x) {
+            // map idx -> (ii, kk) with 0 <= ii <= kk < w, column-major over kk
+            long kk = static_cast<long>((sqrt(8.0 * static_cast<double>(idx) + 1.0) - 1.0) * 0.5);
+            while (kk * (kk + 1) / 2 > idx) --kk;
+            while ((kk + 1) * (kk + 2) / 2 <= idx) ++kk;
+            const long ii = idx - kk * (kk + 1) / 2;
+            const long i = j + 1 + ii, k = j + 1 + kk;
+            const double ri = ii < 2048 ? rowj[ii] : g[j + i * ld];
+            const double rk = kk < 2048 ? rowj[kk] : g[j + k * ld];
+            g[i + k * ld] -= ri * rk;
+        }
+        __syncthreads();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) status[0] = fail;
+    if (fail) return;
+    // zero the strict lower triangle; min / max of diag(R)
+    for (long idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
+        const long i = idx % n, k = idx / n;
+        if (i > k) g[i + k * ld] = 0.0;
+    }
+    double mn = INFINITY, mx = 0.0;
+    for (long i = threadIdx.x; i < n; i += blockDim.x) {
+        const double d = g[i + i * ld];
+        mn = fmin(mn, d);
+        mx = fmax(mx, d);
+    }
+    __shared__ double smn[32], smx[32];
+    for (int o = 16; o > 0; o >>= 1) {
+        mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        smn[threadIdx.x >> 5] = mn;
+        smx[threadIdx.x >> 5] = mx;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w2 = 1; w2 < static_cast<int>(blockDim.x >> 5); ++w2) {
+            mn = fmin(mn, smn[w2]);
+            mx = fmax(mx, smx[w2]);
+        }
+        diag[0] = mn;
+        diag[1] = mx;
+    }
+}
+
+// Inverse of an upper-triangular matrix: one warp per column, column-oriented
+// back substitution (x = e_j; for i = j..0: x_i /= R_ii; x_{<i} -= R_{<i,i} x_i).
+__global__ void trtri_k(double* out, long ldo, const double* r, long ldr, long n) {
+    const long warps = (static_cast<long>(gridDim.x) * blockDim.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    for (long j = (blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x) >> 5; j < n; j += warps) {
+        double* x = out + j * ldo;
+        for (long i = lane; i < n; i += 32) x[i] = (i == j) ? 1.0 : 0.0;
+        __syncwarp();
+        for (long i = j; i >= 0; --i) {
+            const double xi = x[i] / r[i + i * ldr];
+            __syncwarp();
+            if (lane == 0) x[i] = xi;
+            for (long k = lane; k < i; k += 32) x[k] -= r[k + i * ldr] * xi;
+            __syncwarp();
+        }
+    }
+}
+
+__global__ void add_diag_k(double* g, long ld, long n, const double* s) {
+    const double v = s[0];
+    for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long>(gridDim.x) * blockDim.x)
+        g[i + i * ld] += v;
+}
+
+__global__ void count_diag_k(const double* r, long ld, long n, const double* sumsq, double scale,
+                             std::int64_t* out) {
+    const double tau = scale * sqrt(sumsq[0]);
+    long c = 0;
+    for (long i = threadIdx.x; i < n; i += blockDim.x) c += (r[i + i * ld] > tau) ? 1 : 0;
+    double s = block_sum(static_cast<double>(c));
+    if (threadIdx.x == 0) out[0] = static_cast<std::int64_t>(s + 0.5);
+}
+
+// y_partial[split][i] = sum_{j in split} A[i,j] x[j]
+__global__ void gemv_n_partial(const double* __restrict__ A, long lda, long rows, long cols, long cchunk,
+                               const double* __restrict__ x, double* partial) {
+    const long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
+    const long j0 = blockIdx.y * cchunk, j1 = min(cols, j0 + cchunk);
+    if (i >= rows) return;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    long j = j0;
+    for (; j + 3 < j1; j += 4) {
+        s0 += A[i + j * lda] * x[j];
+        s1 += A[i + (j + 1) * lda] * x[j + 1];
+        s2 += A[i + (j + 2) * lda] * x[j + 2];
+        s3 += A[i + (j + 3) * lda] * x[j + 3];
+    }
+    for (; j < j1; ++j) s0 += A[i + j * lda] * x[j];
+    partial[blockIdx.y * rows + i] = (s0 + s1) + (s2 + s3);
+}
+
+__global__ void gemv_n_finish(const double* partial, int S, long rows, double alpha, double beta, double* y) {
+    for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < rows;
+         i += static_cast<long>(gridDim.x) * blockDim.x) {
+        double s = 0.0;
+        for (int z = 0; z < S; ++z) s += partial[z * rows + i];
+        y[i] = beta == 0.0 ? alpha * s : alpha * s + beta * y[i];
+    }
+}
+
+// partial[split][j] = sum_{i in split} A[i,j] x[i]; one block per (column, split)
+__global__ void gemv_t_partial(const double* __restrict__ A, long lda, long rows, long cols, long rchunk,
+                               const double* __restrict__ x, double* partial) {
+    const long j = blockIdx.x;
+    const long i0 = blockIdx.y * rchunk, i1 = min(rows, i0 + rchunk);
+    const double* a = A + j * lda;
+    double s = 0.0;
+    for (long i = i0 + threadIdx.x; i < i1; i += blockDim.x) s += a[i] * x[i];
+    s = block_sum(s);
+    if (threadIdx.x == 0) partial[blockIdx.y * cols + j] = s;
+}
+
+__global__ void dot_partial_k(long n, const double* x, const double* y, double* partial) {
+    double s = 0.0;
+    for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long>(gridDim.x) * blockDim.x)
+        s += x[i] * y[i];
+    s = block_sum(s);
+    if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+// X (rows x b, col-major, ld) -> XT row-major (rows x b)
+__global__ void to_row_major_k(const double* X, long ld, long rows, long b, double* xt) {
+    const long total = rows * b;
+    for (long idx = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<long>(gridDim.x) * blockDim.x) {
+        const long c = idx / rows, i = idx % rows;
+        xt[i * b + c] = X[i + c * ld];
+    }
+}
+
+// warp per row; lanes over the b output columns (chunks of 128)
+__global__ void csr_spmm_k(long rows, const std::int64_t* __restrict__ rowptr, const std::int32_t* __restrict__ colidx,
+                           const double* __restrict__ val, long b, const double* __restrict__ xt, double* Y,
+                           long ldy) {
+    const long warps = (static_cast<long>(gridDim.x) * blockDim.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    for (long i = (blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x) >> 5; i < rows; i += warps) {
+        const long p0 = rowptr[i], p1 = rowptr[i + 1];
+        for (long c0 = 0; c0 < b; c0 += 128) {
+            double acc[4] = {0.0, 0.0, 0.0, 0.0};
+            for (long p = p0; p < p1; ++p) {
+                const double v = val[p];
+                const double* xr = xt + static_cast<long>(colidx[p]) * b;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const long c = c0 + lane + 32 * q;
+                    if (c < b) acc[q] += v * xr[c];
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const long c = c0 + lane + 32 * q;
+                if (c < b) Y[i + c * ldy] = acc[q];
+            }
+        }
+    }
+}
+
+__global__ void gather_vals_k(long nnz, double* dst, const double* src, const std::int64_t* perm) {
+    for (long p = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; p < nnz;
+         p += static_cast<long>(gridDim.x) * blockDim.x)
+        dst[p] = src[perm[p]];
+}
+
+}  // namespace
+
+#define LAUNCH(ctx, name) \
+    do {                   \
+        (ctx).note_launch(); \
+        (ctx).check_launch(name); \
+    } while (0)
+
+void fill(Context& ctx, View x, double v) {
+    if (x.rows * x.cols == 0) return;
+    fill_k<<<grid_for(x.rows * x.cols), kThreads, 0, ctx.stream()>>>(x.p, x.rows, x.cols, x.ld, v);
+    LAUNCH(ctx, "fill");
+}
+
+void copy(Context& ctx, View d, View s, double alpha) {
+    if (d.rows * d.cols == 0) return;
+    copy_k<<<grid_for(d.rows * d.cols), kThreads, 0, ctx.stream()>>>(d.p, d.ld, s.p, s.ld, d.rows, d.cols, alpha);
+    LAUNCH(ctx, "copy");
+}
+
+void axpy(Context& ctx, View y, View x, double alpha) {
+    if (y.rows * y.cols == 0) return;
+    axpy_k<<<grid_for(y.rows * y.cols), kThreads, 0, ctx.stream()>>>(y.p, y.ld, x.p, x.ld, y.rows, y.cols, alpha);
+    LAUNCH(ctx, "axpy");
+}
+
+static void sumsq_impl(Context& ctx, View x, int minus_identity, double* out) {
+    const unsigned blocks = grid_for(x.rows * x.cols, kThreads, 1024);
+    DBuf<double> part(ctx, blocks);
+    sumsq_partial_k<<<blocks, kThreads, 0, ctx.stream()>>>(x.p, x.rows, x.cols, x.ld, minus_identity, part.get());
+    LAUNCH(ctx, "sumsq_partial");
+    reduce_k<<<1, 1024, 0, ctx.stream()>>>(part.get(), blocks, out);
+    LAUNCH(ctx, "reduce");
+}
+
+void sumsq(Context& ctx, View x, double* out) { sumsq_impl(ctx, x, 0, out); }
+void sumsq_minus_identity(Context& ctx, View x, double* out) { sumsq_impl(ctx, x, 1, out); }
+
+void reduce_partials(Context& ctx, const double* partials, Index count, double* out) {
+    reduce_k<<<1, 1024, 0, ctx.stream()>>>(partials, count, out);
+    LAUNCH(ctx, "reduce");
+}
+
+void symmetrize(Context& ctx, View d, View s) {
+    symmetrize_k<<<grid_for(s.rows * s.rows), kThreads, 0, ctx.stream()>>>(d.p, d.ld, s.p, s.ld, s.rows);
+    LAUNCH(ctx, "symmetrize");
+}
+
+void place_block(Context& ctx, View d, View s, bool transpose) {
+    place_k<<<grid_for(s.rows * s.cols), kThreads, 0, ctx.stream()>>>(d.p, d.ld, s.p, s.ld, s.rows, s.cols,
+                                                                      transpose ? 1 : 0);
+    LAUNCH(ctx, "place_block");
+}
+
+void scale_columns(Context& ctx, View d, View s, const double* sc) {
+    if (s.rows * s.cols == 0) return;
+    scale_cols_k<<<grid_for(s.rows * s.cols), kThreads, 0, ctx.stream()>>>(d.p, d.ld, s.p, s.ld, s.rows, s.cols, sc);
+    LAUNCH(ctx, "scale_columns");
+}
+
+void gather_columns(Context& ctx, View d, View s, const int* ix) {
+    if (d.rows * d.cols == 0) return;
+    gather_cols_k<<<grid_for(d.rows * d.cols), kThreads, 0, ctx.stream()>>>(d.p, d.ld, s.p, s.ld, d.rows, d.cols,
+                                                                            ix);
+    LAUNCH(ctx, "gather_columns");
+}
+
+void potrf_upper(Context& ctx, View g, int* status, double* diag) {
+    potrf_k<<<1, 1024, 0, ctx.stream()>>>(g.p, g.rows, g.ld, status, diag);
+    LAUNCH(ctx, "potrf");
+}
+
+void trtri_upper(Context& ctx, View out, View r) {
+    const long n = r.rows;
+    const unsigned blocks = static_cast<unsigned>(std::max<long>(1, (n * 32 + kThreads - 1) / kThreads));
+    trtri_k<<<blocks, kThreads, 0, ctx.stream()>>>(out.p, out.ld, r.p, r.ld, n);
+    LAUNCH(ctx, "trtri");
+}
+
+void trmm_upper(Context& ctx, View c, View a, View b) {
+    gemm(ctx, false, false, a.rows, b.cols, a.cols, 1.0, a.p, a.ld, b.p, b.ld, 0.0, c.p, c.ld);
+}
+
+void add_diagonal(Context& ctx, View g, const double* s) {
+    add_diag_k<<<grid_for(g.rows), kThreads, 0, ctx.stream()>>>(g.p, g.ld, g.rows, s);
+    LAUNCH(ctx, "add_diagonal");
+}
+
+void count_diag_above(Context& ctx, View r, const double* ss, double scale, std::int64_t* out) {
+    count_diag_k<<<1, 256, 0, ctx.stream()>>>(r.p, r.ld, r.rows, ss, scale, out);
+    LAUNCH(ctx, "count_diag");
+}
+
+void gemv(Context& ctx, bool trans, Index rows, Index cols, double alpha, const double* A, Index lda,
+          const double* x, double beta, double* y) {
+    const int sms = ctx.sm_count();
+    if (!trans) {
+        if (rows <= 0) return;
+        const long rb = (rows + kThreads - 1) / kThreads;
+        long S = std::max<long>(1, std::min<long>((8L * sms + rb - 1) / rb, std::max<long>(1, cols / 64)));
+        const long cchunk = (cols + S - 1) / S;
+        S = std::max<long>(1, (cols + cchunk - 1) / cchunk);
+        DBuf<double> part(ctx, static_cast<size_t>(S * rows));
+        if (cols > 0) {
+            gemv_n_partial<<<dim3(static_cast<unsigned>(rb), static_cast<unsigned>(S)), kThreads, 0, ctx.stream()>>>(
+                A, lda, rows, cols, cchunk, x, part.get());
+            LAUNCH(ctx, "gemv_n_partial");
+        } else {
+            S = 0;
+        }
+        gemv_n_finish<<<grid_for(rows), kThreads, 0, ctx.stream()>>>(part.get(), static_cast<int>(S), rows, alpha, beta,
+                                                                     y);
+        LAUNCH(ctx, "gemv_n_finish");
+    } else {
+        if (cols <= 0) return;
+        long S = std::max<long>(1, std::min<long>((8L * sms + cols - 1) / cols, std::max<long>(1, rows / 1024)));
+        const long rchunk = (rows + S - 1) / S;
+        S = std::max<long>(1, (rows + rchunk - 1) / rchunk);
+        DBuf<double> part(ctx, static_cast<size_t>(S * cols));
+        if (rows > 0) {
+            gemv_t_partial<<<dim3(static_cast<unsigned>(cols), static_cast<unsigned>(S)), 128, 0, ctx.stream()>>>(
+                A, lda, rows, cols, rchunk, x, part.get());
+            LAUNCH(ctx, "gemv_t_partial");
+        } else {
+            S = 0;
+        }
+        gemv_n_finish<<<grid_for(cols), kThreads, 0, ctx.stream()>>>(part.get(), static_cast<int>(S), cols, alpha, beta,
+                                                                     y);
+        LAUNCH(ctx, "gemv_t_finish");
+    }
+}
+
+void dot(Context& ctx, Index n, const double* x, const double* y, double* out) {
+    const unsigned blocks = grid_for(n, kThreads, 512);
+    DBuf<double> part(ctx, blocks);
+    dot_partial_k<<<blocks, kThreads, 0, ctx.stream()>>>(n, x, y, part.get());
+    LAUNCH(ctx, "dot_partial");
+    reduce_k<<<1, 1024, 0, ctx.stream()>>>(part.get(), blocks, out);
+    LAUNCH(ctx, "reduce");
+}
+
+void csr_spmm(Context& ctx, Index rows, const std::int64_t* rowptr, const std::int32_t* colidx, const double* val,
+              Index ncols, Index b, const double* X, Index ldx, double* Y, Index ldy, double* xt) {
+    if (rows <= 0 || b <= 0) return;
+    to_row_major_k<<<grid_for(ncols * b), kThreads, 0, ctx.stream()>>>(X, ldx, ncols, b, xt);
+    LAUNCH(ctx, "to_row_major");
+    const long warps_needed = rows;
+    const unsigned blocks = static_cast<unsigned>(std::min<long>(8L * 1024, (warps_needed * 32 + kThreads - 1) / kThreads));
+    csr_spmm_k<<<blocks, kThreads, 0, ctx.stream()>>>(rows, rowptr, colidx, val, b, xt, Y, ldy);
+    LAUNCH(ctx, "csr_spmm");
+}
+
+void gather_values(Context& ctx, Index nnz, double* dst, const double* src, const std::int64_t* perm) {
+    if (nnz <= 0) return;
+    gather_vals_k<<<grid_for(nnz), kThreads, 0, ctx.stream()>>>(nnz, dst, src, perm);
+    LAUNCH(ctx, "gather_values");
+}
+
+}  // namespace blws

@@ -1,0 +1,75 @@
+// Host-callable launchers for every device kernel of the BLWS hot path.
+// Each launcher enqueues on ctx.stream() and counts its launches.
+#pragma once
+#include "common.cuh"
+
+namespace blws {
+
+// ------------------------------------------------------------------ GEMM (K1, K2, K5)
+/// C = alpha * op(A) * op(B) + beta * C, column-major fp64, DMMA tensor cores.
+/// op(A) is M x K, op(B) is K x N. Split-K with a deterministic reduction
+/// when the output tile grid alone cannot fill the SMs.
+void gemm(Context& ctx, bool ta, bool tb, Index M, Index N, Index K, double alpha, const double* A, Index lda,
+          const double* B, Index ldb, double beta, double* C, Index ldc);
+
+// ------------------------------------------------------------------ level-1 / small
+void fill(Context& ctx, View x, double v);
+void copy(Context& ctx, View dst, View src, double alpha = 1.0);  // dst = alpha * src
+void axpy(Context& ctx, View y, View x, double alpha);            // y += alpha * x
+/// out[0] = sum of squares of x (deterministic two-pass reduction).
+void sumsq(Context& ctx, View x, double* out);
+/// out[0] = sum of squares of (X - I) for a square X.
+void sumsq_minus_identity(Context& ctx, View x, double* out);
+/// dst = 0.5 * (src + src^T), square.
+void symmetrize(Context& ctx, View dst, View src);
+/// Scatter a b x b block (or its transpose) into a larger matrix.
+void place_block(Context& ctx, View dst, View src, bool transpose);
+/// dst(:, j) = src(:, j) * s[j]   (s on device)
+void scale_columns(Context& ctx, View dst, View src, const double* s);
+/// Gather selected columns: dst(:, j) = src(:, idx[j]) (idx on device).
+void gather_columns(Context& ctx, View dst, View src, const int* idx);
+
+// ------------------------------------------------------------------ small dense (K3, K4)
+/// In-place upper Cholesky of the leading n x n of G (G = R^T R, R upper).
+/// status[0] = 0 on success, j+1 if pivot j was not positive or not finite.
+/// min_diag/max_diag of R written to status-adjacent doubles diag[0..1].
+void potrf_upper(Context& ctx, View g, int* status, double* diag);
+/// R^{-1} of an upper-triangular n x n R (out may not alias r).
+void trtri_upper(Context& ctx, View out, View r);
+/// C = A * B for upper-triangular n x n A, B (C upper triangular).
+void trmm_upper(Context& ctx, View c, View a, View b);
+/// G += s * I
+void add_diagonal(Context& ctx, View g, const double* s_dev);
+/// count of diag(R) > tau (tau = scale * sqrt(sumsq[0])) -> out[0]
+void count_diag_above(Context& ctx, View r, const double* sumsq_dev, double scale, std::int64_t* out);
+
+/// Symmetric EVD (Jacobi). values descending, vectors columns (n x n).
+/// Returns sweeps used (host value, requires a sync).
+int sym_evd_jacobi(Context& ctx, View t, double* values, View vectors);
+/// Top `want` eigenpairs of the symmetric tridiagonal (d, e): values
+/// descending, vectors n x want. Bisection + inverse iteration with cluster
+/// reorthogonalisation.
+void tridiag_eig_top(Context& ctx, Index n, const double* d, const double* e, Index want, double* values,
+                     View vectors);
+
+// ------------------------------------------------------------------ GEMV (K10)
+/// y = alpha * op(A) x + beta * y for column-major A (rows x cols).
+void gemv(Context& ctx, bool trans, Index rows, Index cols, double alpha, const double* A, Index lda,
+          const double* x, double beta, double* y);
+/// out = dot(x, y) (device scalar).
+void dot(Context& ctx, Index n, const double* x, const double* y, double* out);
+
+// ------------------------------------------------------------------ sparse (K8, K9)
+/// Y (rows x b) = S * X where S is CSR (rowptr, colidx, val); X col-major.
+/// xt is scratch of cols(S) * b doubles (row-major copy of X).
+void csr_spmm(Context& ctx, Index rows, const std::int64_t* rowptr, const std::int32_t* colidx,
+              const double* val, Index ncols, Index b, const double* X, Index ldx, double* Y, Index ldy,
+              double* xt);
+void gather_values(Context& ctx, Index nnz, double* dst, const double* src, const std::int64_t* perm);
+
+// ------------------------------------------------------------------ misc
+/// FP64 peak microbenchmark in TFLOP/s (mode 0 DMMA tensor pipe, 1 DFMA).
+double fp64_peak_tflops(Context& ctx, int mode);
+void reduce_partials(Context& ctx, const double* partials, Index count, double* out);
+
+}  // namespace blws

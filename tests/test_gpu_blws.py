@@ -1,0 +1,197 @@
+"""GPU parity of the BLWS hot path (blws_svd, block Lanczos, cold Lanczos
+reseed, svt) against the CPU oracle on identical seeded inputs.
+
+Restates proj/tests/test_block_lanczos.cpp, test_lanczos.cpp and
+test_svt.cpp with the device path under test, plus the BASELINE parity
+contract: singular values of each partial SVD to 1e-10 relative, subspaces
+by principal angle.
+"""
+import numpy as np
+import pytest
+
+from conftest import principal_angle
+
+pytestmark = pytest.mark.gpu
+
+
+def exact_warm(O, w, r):
+    u, s, v = O.full_svd_small(w)
+    return u[:, :r].copy(order="F"), v[:, :r].copy(order="F"), s[:r].copy()
+
+
+def test_counter_semantics(G, O):
+    w = O.Rng(37).gaussian_matrix(6, 4)
+    op = G.DenseOperator(w)
+    assert op.application_count() == 0
+    x = O.Rng(1).gaussian_matrix(6, 3)
+    y = O.Rng(2).gaussian_matrix(4, 3)
+    top, bot = op.apply_pair_block(x, y)
+    assert op.application_count() == 3
+    assert np.allclose(top, w @ y, atol=1e-13) and np.allclose(bot, w.T @ x, atol=1e-13)
+
+
+def test_block_lanczos_matches_oracle(G, O):
+    rng = O.Rng(43)
+    m, n, r = 100, 80, 6
+    w = rng.gaussian_matrix(m, n)
+    u, v, s = exact_warm(O, w, r)
+    pu = u + 1e-3 * rng.gaussian_matrix(m, r)
+    pv = v + 1e-3 * rng.gaussian_matrix(n, r)
+    x1 = O.thin_qr(np.vstack([pu, pv]) / np.sqrt(2)).q
+    opo = O.AugmentedOperator(O.DenseOperator(w))
+    q_ref, t_ref, built_ref, term_ref = O.block_lanczos_procedure(opo, x1, 2)
+    q, t, built, term = G.block_lanczos_procedure(G.DenseOperator(w), x1, 2)
+    assert built == built_ref and term == term_ref
+    cols = q.shape[1]
+    assert np.linalg.norm(q.T @ q - np.eye(cols)) <= 1e-6  # test_block_lanczos.cpp:255-273
+    # same Krylov basis up to the QR sign convention (both diag(R) >= 0)
+    assert np.abs(q - q_ref).max() <= 1e-9
+    assert np.abs(t - t_ref).max() <= 1e-9 * np.abs(t_ref).max()
+
+
+def test_blws_fixed_point(G, O):
+    # test_block_lanczos.cpp:190-204
+    rng = O.Rng(29)
+    w = rng.gaussian_matrix(30, 20)
+    eu, es, ev = O.full_svd_small(w)
+    u, v, s = eu[:, :4].copy(order="F"), ev[:, :4].copy(order="F"), es[:4].copy()
+    res = G.blws_svd(G.DenseOperator(w), G.WarmStart(u, v, s), 2, 4, G.Rng(29))
+    assert res.warm.rank() == 4 and not res.padded
+    assert np.abs(res.warm.sigma - es[:4]).max() <= 1e-9 * es[0]
+    assert principal_angle(res.warm.u, eu[:, :4]) <= 1e-8
+    assert principal_angle(res.warm.v, ev[:, :4]) <= 1e-8
+
+
+def test_blws_diag(G, O):
+    w = np.diag([9.0, 4.0, 1.0])
+    res = G.blws_svd(G.DenseOperator(w), G.WarmStart(np.eye(3)[:, :2], np.eye(3)[:, :2], np.array([9.0, 4.0])), 2,
+                     2, G.Rng(31))
+    assert abs(res.warm.sigma[0] - 9) <= 9e-12 and abs(res.warm.sigma[1] - 4) <= 4e-12
+
+
+def test_blws_drifting_sequence_parity(G, O):
+    # test_block_lanczos.cpp:216-241, compared call by call with the oracle
+    rng = O.Rng(37)
+    m, r = 200, 10
+    u0 = O.thin_qr(rng.gaussian_matrix(m, 15)).q
+    v0 = O.thin_qr(rng.gaussian_matrix(m, 15)).q
+    s0 = 100.0 * 0.7 ** np.arange(15)
+    w0 = (u0 * s0) @ v0.T
+    delta = rng.gaussian_matrix(m, m)
+    delta *= 0.01 * np.linalg.norm(w0) / np.linalg.norm(delta)
+    wu, wv, ws = exact_warm(O, w0, r)
+    warm_g = G.WarmStart(wu, wv, ws)
+    warm_o = O.WarmStart(wu, wv, ws)
+    op_g, op_o = G.DenseOperator(w0), O.DenseOperator(w0)
+    rg, ro = G.Rng(37), O.Rng(37)
+    for i in range(1, 11):
+        wi = w0 + i * 0.01 * delta
+        op_g.assign(wi)
+        op_o.assign(wi)
+        res_g = G.blws_svd(op_g, warm_g, 2, r, rg)
+        res_o = O.blws_svd(op_o, warm_o, 2, r, ro)
+        warm_g, warm_o = res_g.warm, res_o.warm
+        assert (res_g.padded, res_g.k_raised, res_g.terminated_early) == (res_o.padded, res_o.k_raised,
+                                                                          res_o.terminated_early)
+        assert np.abs(warm_g.sigma - warm_o.sigma).max() <= 1e-10 * warm_o.sigma.max()
+        assert principal_angle(warm_g.u, warm_o.u) <= 1e-8
+        assert principal_angle(warm_g.v, warm_o.v) <= 1e-8
+        exact = O.full_svd_small(wi)[1]
+        assert np.abs(warm_g.sigma - exact[:r]).max() / exact[0] <= 1e-4
+    assert op_g.application_count() == op_o.application_count()
+
+
+def test_blws_raises_k_and_pads(G, O):
+    # test_block_lanczos.cpp:275-299
+    rng = O.Rng(47)
+    w = rng.gaussian_matrix(40, 40)
+    u, v, s = exact_warm(O, w, 2)
+    res = G.blws_svd(G.DenseOperator(w), G.WarmStart(u, v, s), 2, 6, G.Rng(47))
+    ref = O.blws_svd(O.DenseOperator(w), O.WarmStart(u, v, s), 2, 6, O.Rng(47))
+    assert res.k_raised and res.warm.rank() == 6
+    assert abs(res.warm.sigma[0] - ref.warm.sigma[0]) <= 1e-10 * ref.warm.sigma[0]
+    rng = O.Rng(53)
+    warm = O.adapt_subspace(None, 3, 8, 8, rng)
+    res = G.blws_svd(G.DenseOperator(np.zeros((8, 8))), G.WarmStart(warm.u, warm.v, warm.sigma), 2, 3, G.Rng(53))
+    assert res.padded and res.warm.rank() == 3
+    assert np.linalg.norm(res.warm.u.T @ res.warm.u - np.eye(3)) <= 1e-10
+    assert np.abs(res.warm.sigma).max() == 0.0
+
+
+def test_adapt_subspace_consumes_same_draws(G, O):
+    rng_o, rng_g = O.Rng(23), G.Rng(23)
+    fresh_o = O.adapt_subspace(None, 4, 30, 20, rng_o)
+    fresh_g = G.adapt_subspace(None, 4, 30, 20, rng_g)
+    assert np.abs(fresh_g.u - fresh_o.u).max() <= 1e-12
+    assert np.abs(fresh_g.v - fresh_o.v).max() <= 1e-12
+    assert rng_o.next_u64() == rng_g.next_u64()
+
+
+def test_blws_counter_budget(G, O):
+    # test_block_lanczos.cpp:243-253
+    rng = O.Rng(41)
+    w = rng.gaussian_matrix(50, 30)
+    warm = O.adapt_subspace(None, 5, 50, 30, rng)
+    op = G.DenseOperator(w)
+    G.blws_svd(op, G.WarmStart(warm.u, warm.v, warm.sigma), 3, 5, G.Rng(41))
+    assert op.application_count() <= 3 * 2 * 5 + 2 * 5
+
+
+def test_lanczos_partial_svd_parity(G, O):
+    # test_lanczos.cpp:157-175, plus call-level parity with the oracle
+    w = O.Rng(41).gaussian_matrix(80, 60)
+    u, s, v, st = G.lanczos_partial_svd(G.DenseOperator(w), 8, tol=1e-9)
+    ru, rs_, rv, rst = O.lanczos_partial_svd(O.DenseOperator(w), 8, tol=1e-9)
+    eu, es, ev = O.full_svd_small(w)
+    assert len(s) == 8
+    assert np.abs(s - es[:8]).max() <= 1e-7 * es[0]
+    assert np.abs(s - rs_).max() <= 1e-10 * rs_[0]
+    assert list(st) == list(rst)
+    assert np.linalg.norm(u.T @ u - np.eye(8)) <= 1e-8
+    assert principal_angle(u, eu[:, :8]) <= 1e-6 and principal_angle(v, ev[:, :8]) <= 1e-6
+
+
+def test_spectral_norm(G, O):
+    w = O.Rng(43).gaussian_matrix(50, 40)
+    got = G.spectral_norm(G.DenseOperator(w))
+    assert abs(got - O.full_svd_small(w)[1][0]) <= 1e-5 * got
+    assert abs(got - O.spectral_norm(O.DenseOperator(w))) <= 1e-12 * got
+
+
+def test_lanczos_restarts_on_degenerate_spectrum(G, O):
+    # rank-deficient W: the augmented Krylov space exhausts -> restarts
+    w = np.zeros((12, 10))
+    w[0, 0], w[1, 1] = 3.0, 1.0
+    u, s, v, st = G.lanczos_partial_svd(G.DenseOperator(w), 4)
+    ru, rs_, rv, rst = O.lanczos_partial_svd(O.DenseOperator(w), 4)
+    assert list(st) == list(rst)
+    assert np.abs(np.sort(s)[::-1][: len(rs_)] - rs_).max() <= 1e-10 * 3
+
+
+def test_svt_blws_backend_grows_rank(G, O):
+    # test_svt.cpp:127-153, compared with the oracle call by call
+    rng = O.Rng(19)
+    m = 100
+    base = rng.gaussian_matrix(m, 30) @ rng.gaussian_matrix(m, 30).T
+    drift = rng.gaussian_matrix(m, m)
+    drift *= 1e-3 * np.linalg.norm(base) / np.linalg.norm(drift)
+    final_w = base + 4.0 * drift
+    s_exact = O.full_svd_small(final_w)[1]
+    eps = 0.5 * (s_exact[9] + s_exact[10])
+    bg, bo = G.SvdBackend.blws(seed=101), O.SvdBackend.blws(seed=101)
+    pg, po = G.RankPredictor(4, 3, m), O.RankPredictor(4, 3, m)
+    opg, opo = G.DenseOperator(base), O.DenseOperator(base)
+    for i in range(5):
+        wi = base + i * drift
+        opg.assign(wi)
+        opo.assign(wi)
+        rg = G.svt(opg, eps, bg, pg)
+        ro = O.svt(opo, eps, bo, po)
+        assert rg.achieved_rank == ro.achieved_rank
+        assert np.abs(rg.sigma - ro.sigma).max() <= 1e-9 * ro.sigma.max()
+    assert pg.history == po.history and pg.r == po.r
+    u, s, v = O.full_svd_small(final_w)
+    exact = (u[:, :10] * (s[:10] - eps)) @ v[:, :10].T
+    assert np.linalg.norm(rg.dense() - exact) <= 1e-5 * np.linalg.norm(exact)
+    assert rg.achieved_rank == 10
+    assert opg.application_count() == opo.application_count()

@@ -1,0 +1,130 @@
+"""GPU parity of the dense building blocks against the CPU oracle / numpy.
+
+Each test restates a reference test (proj/tests/test_dense_core.cpp,
+test_lanczos.cpp) with the device path under test; tolerances are the
+reference's unless stated.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def gpu(G):
+    import torch
+
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    return G
+
+
+@pytest.mark.parametrize("ta,tb", [(False, False), (True, False), (False, True), (True, True)])
+@pytest.mark.parametrize("m,n,k", [(64, 64, 16), (257, 33, 1001), (1000, 100, 4000), (7, 5, 3), (100, 100, 20000)])
+def test_dgemm_matches_numpy(gpu, ta, tb, m, n, k):
+    import torch
+
+    rs = np.random.default_rng(m * 7 + n * 3 + k)
+    A = rs.standard_normal((k, m) if ta else (m, k))
+    B = rs.standard_normal((n, k) if tb else (k, n))
+    C0 = rs.standard_normal((m, n))
+    ref = 1.5 * ((A.T if ta else A) @ (B.T if tb else B)) - 0.5 * C0
+    dev = torch.device("cuda:0")
+    # column-major = transpose of a contiguous row-major tensor
+    At = torch.tensor(A.T.copy(), device=dev)
+    Bt = torch.tensor(B.T.copy(), device=dev)
+    Ct = torch.tensor(C0.T.copy(), device=dev)
+    gpu.api.dgemm(ta, tb, m, n, k, 1.5, At, A.shape[0], Bt, B.shape[0], -0.5, Ct, m)
+    torch.cuda.synchronize()
+    got = Ct.cpu().numpy().T
+    assert np.abs(got - ref).max() <= 1e-12 * max(1.0, np.abs(ref).max()) * np.sqrt(k)
+
+
+def test_thin_qr_known_answers(gpu, O):
+    q, r, rank = gpu.thin_qr(np.array([[3.0], [4.0]]))
+    assert abs(q[0, 0] - 0.6) <= 1e-14 and abs(q[1, 0] - 0.8) <= 1e-14 and abs(r[0, 0] - 5.0) <= 1e-14
+    assert rank == 1
+    g = O.Rng(11).gaussian_matrix(12, 4)
+    qq = O.thin_qr(g).q
+    q2, r2, rk = gpu.thin_qr(qq)
+    assert np.linalg.norm(q2 - qq) <= 1e-12 and np.linalg.norm(r2 - np.eye(4)) <= 1e-12 and rk == 4
+
+
+@pytest.mark.parametrize("m,b", [(5, 1), (20, 4), (50, 10), (200, 30), (8000, 100), (4000, 205)])
+def test_thin_qr_recomposition_and_oracle(gpu, O, m, b):
+    a = O.Rng(17 + m).gaussian_matrix(m, b)
+    q, r, rank = gpu.thin_qr(a)
+    assert np.linalg.norm(a - q @ r) <= 1e-12 * np.linalg.norm(a)
+    assert np.linalg.norm(q.T @ q - np.eye(b)) <= 1e-12
+    assert np.all(np.diag(r) >= 0) and rank == b
+    assert np.allclose(np.tril(r, -1), 0.0)
+    ref = O.thin_qr(a)
+    assert np.abs(q - ref.q).max() <= 1e-10
+    assert np.abs(r - ref.r).max() <= 1e-10 * np.abs(ref.r).max()
+
+
+def test_thin_qr_rank_deficiency(gpu, O):
+    col = O.Rng(3).gaussian_vector(10)
+    m = np.stack([col, 2.0 * col], axis=1)
+    assert gpu.thin_qr(m)[2] == 1
+    assert O.thin_qr(m).rank == 1
+    with pytest.raises(ValueError):
+        gpu.thin_qr(np.zeros((2, 5)))
+    with pytest.raises(ValueError):
+        gpu.thin_qr(np.array([[1.0], [np.nan]]))
+
+
+def test_thin_qr_ill_conditioned_uses_shifted_cholqr(gpu, O):
+    rs = np.random.default_rng(5)
+    u, _ = np.linalg.qr(rs.standard_normal((3000, 40)))
+    v, _ = np.linalg.qr(rs.standard_normal((40, 40)))
+    a = (u * np.logspace(0, -11, 40)) @ v.T
+    q, r, rank = gpu.thin_qr(a)
+    assert np.linalg.norm(q.T @ q - np.eye(40)) <= 1e-12
+    assert np.linalg.norm(a - q @ r) <= 1e-12 * np.linalg.norm(a)
+    assert rank == O.thin_qr(a).rank
+
+
+def test_sym_evd_known_answers(gpu):
+    vals, vecs = gpu.sym_evd_small(np.diag([3.0, 1.0, 2.0]))
+    assert np.allclose(vals, [3, 2, 1])
+    assert np.allclose(np.abs(vecs).max(axis=0), 1.0, atol=1e-12)
+    vals, vecs = gpu.sym_evd_small(np.array([[0.0, 1.0], [1.0, 0.0]]))
+    assert abs(vals[0] - 1) <= 1e-14 and abs(vals[1] + 1) <= 1e-14
+    assert abs(abs(vecs[0, 0] * vecs[1, 0]) - 0.5) <= 1e-12
+    assert abs(vecs[0, 1] * vecs[1, 1] + 0.5) <= 1e-12
+    with pytest.raises(ValueError):
+        gpu.sym_evd_small(np.array([[0.0, 1.0], [5.0, 0.0]]))
+
+
+@pytest.mark.parametrize("n", [12, 61, 110, 200, 222, 260])
+def test_sym_evd_matches_oracle(gpu, O, n):
+    g = O.Rng(23 + n).gaussian_matrix(n, n)
+    t = 0.5 * (g + g.T)
+    vals, vecs = gpu.sym_evd_small(t)
+    ref_vals, _ = O.sym_evd_small(t)
+    tn = np.linalg.norm(t)
+    assert np.abs(vals - ref_vals).max() <= 1e-12 * tn
+    assert np.linalg.norm(t @ vecs - vecs * vals) <= 1e-10 * tn
+    assert np.linalg.norm(vecs.T @ vecs - np.eye(n)) <= 1e-10
+
+
+def test_tridiagonal_top_matches_oracle(gpu, O):
+    rs = np.random.default_rng(9)
+    for n, want in [(10, 3), (60, 20), (500, 40)]:
+        d = rs.standard_normal(n)
+        e = np.abs(rs.standard_normal(n - 1))
+        vals, vecs = gpu.sym_evd_tridiagonal_top(d, e, want)
+        rv, rvec = O.sym_evd_tridiagonal(d, e)
+        assert np.abs(vals - rv[:want]).max() <= 1e-13 * np.abs(rv).max()
+        t = np.diag(d) + np.diag(e, 1) + np.diag(e, -1)
+        assert np.linalg.norm(t @ vecs - vecs * vals) <= 1e-11 * np.abs(rv).max()
+        assert np.linalg.norm(vecs.T @ vecs - np.eye(want)) <= 1e-10
+
+
+def test_tridiagonal_degenerate_clusters(gpu):
+    # identity blocks decoupled by zero couplings (Lanczos restarts on I)
+    d = np.ones(9)
+    e = np.zeros(8)
+    vals, vecs = gpu.sym_evd_tridiagonal_top(d, e, 3)
+    assert np.allclose(vals, 1.0, atol=1e-14)
+    assert np.linalg.norm(vecs.T @ vecs - np.eye(3)) <= 1e-10

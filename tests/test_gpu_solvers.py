@@ -1,0 +1,72 @@
+"""GPU parity of the RPCA / MC solvers against the CPU oracle on identical
+seeded inputs (BASELINE.json parity contract: iterations +-1, same recovered
+rank, final A and E to 1e-6 relative Frobenius; test_solvers.cpp bounds)."""
+import numpy as np
+import pytest
+
+from paper_1012_0365_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def _rpca_instance(O, m, rank, frac, seed):
+    return synth.rpca_lowrank_sparse(m, rank, int(round(frac * m * m)), seed, O.Rng, O.sample_distinct)
+
+
+@pytest.mark.parametrize("m,rank,frac,seed", [(80, 8, 0.10, 21), (200, 10, 0.05, 1)])
+def test_rpca_parity(G, O, m, rank, frac, seed):
+    d, a0, _, _ = _rpca_instance(O, m, rank, frac, seed)
+    bseed = seed ^ 0x5BDBEEF
+    a_g, e_g, st_g, nnz_g = G.rpca_adm(d, G.SvdBackend.blws(seed=bseed), truth=a0)
+    a_o, e_o, st_o, nnz_o = O.rpca_adm(d, O.SvdBackend.blws(seed=bseed), truth=a0)
+    assert st_g.converged and st_o.converged
+    assert abs(st_g.iterations - st_o.iterations) <= 1
+    assert st_g.rank_hat == st_o.rank_hat
+    assert np.linalg.norm(a_g - a_o) <= 1e-6 * np.linalg.norm(a_o)
+    assert np.linalg.norm(e_g - e_o) <= 1e-6 * np.linalg.norm(e_o)
+    assert abs(st_g.e_l0 - st_o.e_l0) <= max(2, 1e-3 * st_o.e_l0)
+    n = min(st_g.iterations, st_o.iterations)
+    assert st_g.predicted_ranks[:n] == st_o.predicted_ranks[:n]
+    assert st_g.matvec_history[:n] == st_o.matvec_history[:n]
+    assert st_g.matvec_init == st_o.matvec_init
+    assert st_g.matvec_init + sum(st_g.matvec_history) == st_g.matvec_count
+
+
+def test_rpca_clean_rank_one(G, O):
+    rng = O.Rng(3)
+    a, b = rng.gaussian_vector(40), rng.gaussian_vector(40)
+    d = np.outer(a, b)
+    a_g, e_g, st, _ = G.rpca_adm(d, G.SvdBackend.blws(seed=6))
+    assert st.converged and st.rank_hat == 1 and st.e_l0 == 0
+    assert np.linalg.norm(a_g - d) <= 1e-6 * np.linalg.norm(d)
+
+
+def test_rpca_capped(G, O):
+    d, _, _, _ = _rpca_instance(O, 50, 5, 0.1, 9)
+    _, _, st, _ = G.rpca_adm(d, G.SvdBackend.blws(seed=3), max_iter=2)
+    assert not st.converged and st.iterations == 2
+
+
+def test_rpca_rejects_non_finite(G):
+    d = np.ones((6, 6))
+    d[2, 3] = np.nan
+    with pytest.raises(ValueError):
+        G.rpca_adm(d, G.SvdBackend.blws())
+
+
+def test_mc_parity(G, O):
+    colptr, rowidx, vals, ml, mr = synth.mc_lowrank(200, 5, 6000, 13, O.Rng, O.sample_distinct)
+    ug, sg, vg, stg = G.mc_svt(200, 200, colptr, rowidx, vals, G.SvdBackend.blws(seed=8), truth_ml=ml, truth_mr=mr)
+    uo, so, vo, sto = O.mc_svt(200, 200, colptr, rowidx, vals, O.SvdBackend.blws(seed=8), truth_ml=ml, truth_mr=mr)
+    assert stg.converged and sto.converged
+    assert abs(stg.iterations - sto.iterations) <= 1
+    assert stg.rank_hat == sto.rank_hat
+    assert stg.rel_err <= 2e-4
+    ag, ao = (ug * sg) @ vg.T, (uo * so) @ vo.T
+    assert np.linalg.norm(ag - ao) <= 1e-6 * np.linalg.norm(ao)
+
+
+def test_mc_rejects_empty(G):
+    with pytest.raises(ValueError):
+        G.mc_svt(10, 10, np.zeros(11, dtype=np.int64), np.zeros(0, dtype=np.int32), np.zeros(0),
+                 G.SvdBackend.blws())
