@@ -402,7 +402,7 @@ int blws_sym_evd(blws_context* ctx, int64_t n, const double* t, double* values, 
         upload(c, a.view(), t, n);
         blws::symmetrize(c, s.view(), a.view());
         DBuf<double> vals(c, static_cast<size_t>(n));
-        sym_evd_jacobi(c, s.view(), vals.get(), vec.view());
+        sym_evd_top(c, s.view(), n, vals.get(), vec.view());
         c.read(vals.get(), values, n);
         download(c, vec.view(), vectors, n);
     });

@@ -1,0 +1,247 @@
+// Symmetric EVD of the projected block-tridiagonal T (K4), top `want` pairs.
+//
+// The reference diagonalises T = BlockTridiagonal::embed() completely with
+// Eigen's SelfAdjointEigenSolver (block_lanczos.hpp:144 -> small_dense.hpp:36)
+// and then keeps at most r leading positive pairs (block_lanczos.hpp:235-248).
+// Here only the top `want` (= r) pairs are produced:
+//   1. sytrd_k: Householder tridiagonalisation (LAPACK dsytd2, lower), one CTA,
+//      the lower triangle packed in shared memory (global for large n);
+//   2. tridiag_eig_top: bisection + inverse iteration on (d, e) (tridiag.cu);
+//   3. ormtr_k: back-transformation Z = H_0 ... H_{n-3} Y, one warp per
+//      eigenvector, no inter-warp synchronisation.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "ops.cuh"
+
+namespace blws {
+namespace {
+
+constexpr int kThreads = 512;
+constexpr int kWarps = kThreads / 32;
+constexpr int kMaxRowsPerLane = 8;  // n <= 256 on this path (32 * 8 trailing rows per warp)
+constexpr long kSmemBudget = 220 * 1024;
+
+__device__ __forceinline__ long loff(long j, long n) { return j * n - j * (j - 1) / 2; }  // start of column j
+__device__ __forceinline__ long lidx(long i, long j, long n) {                              // (i >= j)
+    return loff(j, n) + (i - j);
+}
+
+__device__ double block_sum_1024(double v, double* red) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __syncthreads();
+    if (lane == 0) red[wid] = v;
+    __syncthreads();
+    double s = 0.0;
+    const int nw = blockDim.x >> 5;
+    for (int w = 0; w < nw; ++w) s += red[w];
+    return s;
+}
+
+// In: T (n x n, ld) symmetric. Out: d (n), e (n-1), packed lower with the
+// reflectors below the diagonal (v[0] = 1 implicit) in `lp`, tau (n).
+__global__ void __launch_bounds__(kThreads) sytrd_k(const double* __restrict__ t, long ld, int n, int on_chip,
+                                                    double* lp, double* d, double* e, double* tau) {
+    extern __shared__ __align__(16) double sm[];
+    double* v = sm;               // n
+    double* p = v + n;            // n
+    double* pcol = p + n;         // n
+    double* red = pcol + n;       // 32
+    double* pw = red + 32;        // kWarps * n private partials (n <= 256 only)
+    double* a = on_chip ? pw + (n <= 32 * kMaxRowsPerLane ? kWarps * n : 0) : lp;
+    const long np = static_cast<long>(n) * (n + 1) / 2;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    // load the lower triangle, column by column (warp per column)
+    for (int j = wid; j < n; j += nw)
+        for (int i = j + lane; i < n; i += 32) a[lidx(i, j, n)] = 0.5 * (t[i + j * ld] + t[j + i * ld]);
+    __syncthreads();
+    for (int k = 0; k < n - 2; ++k) {
+        const int w = n - k - 1;  // trailing order, rows k+1 .. n-1
+        double* x = a + lidx(k + 1, k, n);
+        double s = 0.0;
+        for (int i = 1 + threadIdx.x; i < w; i += blockDim.x) s += x[i] * x[i];
+        const double sigma2 = block_sum_1024(s, red);
+        const double alpha = x[0];
+        double tk = 0.0, beta = alpha;
+        if (sigma2 > 0.0) {
+            beta = -copysign(sqrt(alpha * alpha + sigma2), alpha);
+            tk = (beta - alpha) / beta;
+            const double scl = 1.0 / (alpha - beta);
+            for (int i = threadIdx.x; i < w; i += blockDim.x) v[i] = i == 0 ? 1.0 : x[i] * scl;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            e[k] = beta;
+            tau[k] = tk;
+            d[k] = a[lidx(k, k, n)];
+        }
+        if (tk == 0.0) {
+            // H = I: store a zero reflector, nothing to update
+            for (int i = threadIdx.x; i < w; i += blockDim.x) x[i] = 0.0;
+            __syncthreads();
+            continue;
+        }
+        // p = tau * A22 v from column reads only (conflict-free): warp `wid`
+        // owns columns j = wid, wid+nw, ...; per column it forms the dot of the
+        // strictly-lower part with v (-> pcol[j]) and accumulates L(:,j) v_j into
+        // a private per-lane register vector (rows i = lane + 32 t).
+        if (w > 32 * kMaxRowsPerLane) {
+            // large orders: warp per row, row part strided (global-memory path)
+            for (int i = wid; i < w; i += nw) {
+                const int gi = k + 1 + i;
+                double acc = 0.0;
+                for (int j = lane; j < w; j += 32) {
+                    const int gj = k + 1 + j;
+                    const double aij = gi >= gj ? a[lidx(gi, gj, n)] : a[lidx(gj, gi, n)];
+                    acc += aij * v[j];
+                }
+                for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                if (lane == 0) p[i] = tk * acc;
+            }
+        } else {
+            double acc[kMaxRowsPerLane];
+#pragma unroll
+            for (int q = 0; q < kMaxRowsPerLane; ++q) acc[q] = 0.0;
+            for (int j = wid; j < w; j += nw) {
+                const double* col = a + lidx(k + 1 + j, k + 1 + j, n) - j;  // col[i] = A(k+1+i, k+1+j), i >= j
+                const double vj = v[j];
+                double dotp = 0.0;
+#pragma unroll
+                for (int q = 0; q < kMaxRowsPerLane; ++q) {
+                    const int i = lane + 32 * q;
+                    if (i >= j && i < w) {
+                        const double lij = col[i];
+                        acc[q] += lij * vj;
+                        if (i > j) dotp += lij * v[i];
+                    }
+                }
+                for (int o = 16; o > 0; o >>= 1) dotp += __shfl_xor_sync(0xffffffffu, dotp, o);
+                if (lane == 0) pcol[j] = dotp;
+            }
+#pragma unroll
+            for (int q = 0; q < kMaxRowsPerLane; ++q) {
+                const int i = lane + 32 * q;
+                if (i < w) pw[wid * n + i] = acc[q];
+            }
+            __syncthreads();
+            for (int i = threadIdx.x; i < w; i += blockDim.x) {
+                double sacc = pcol[i];
+                for (int ww = 0; ww < nw; ++ww) sacc += pw[ww * n + i];
+                p[i] = tk * sacc;
+            }
+        }
+        __syncthreads();
+        double pv = 0.0;
+        for (int i = threadIdx.x; i < w; i += blockDim.x) pv += p[i] * v[i];
+        const double K = 0.5 * tk * block_sum_1024(pv, red);
+        for (int i = threadIdx.x; i < w; i += blockDim.x) p[i] -= K * v[i];  // p <- w
+        __syncthreads();
+        // A22 -= v w^T + w v^T (lower), warp per column
+        for (int j = wid; j < w; j += nw) {
+            const int gj = k + 1 + j;
+            const double vj = v[j], wj = p[j];
+            double* col = a + lidx(gj, gj, n) - j;  // so col[i] = A(k+1+i, gj) for i >= j
+            for (int i = j + lane; i < w; i += 32) col[i] -= v[i] * wj + p[i] * vj;
+        }
+        __syncthreads();
+        // keep the reflector below the diagonal of column k
+        for (int i = threadIdx.x; i < w; i += blockDim.x) x[i] = v[i];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        if (n >= 2) {
+            d[n - 2] = a[lidx(n - 2, n - 2, n)];
+            e[n - 2] = a[lidx(n - 1, n - 2, n)];
+            tau[n - 2] = 0.0;
+        }
+        d[n - 1] = a[lidx(n - 1, n - 1, n)];
+        tau[n - 1] = 0.0;
+    }
+    if (on_chip)
+        for (long idx = threadIdx.x; idx < np; idx += blockDim.x) lp[idx] = a[idx];
+}
+
+// Z = H_0 H_1 ... H_{n-3} Y, column j of Y per warp; H_k = I - tau_k v_k v_k^T
+// acting on rows k+1..n-1 with v_k stored in packed column k (v[0] = 1).
+// Reflectors are staged through shared memory in chunks shared by the CTA.
+constexpr int kOrmWarps = 8;
+constexpr int kOrmChunk = 8;
+__global__ void __launch_bounds__(kOrmWarps * 32) ormtr_k(const double* __restrict__ lp, const double* __restrict__ tau,
+                                                          int n, int want, double* z, long ldz) {
+    extern __shared__ __align__(16) double sm[];
+    double* vs = sm;                           // kOrmChunk * n
+    double* zs = sm + kOrmChunk * n;           // kOrmWarps * n
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const long j = static_cast<long>(blockIdx.x) * kOrmWarps + warp;
+    const bool active = j < want;
+    double* zc = zs + warp * n;
+    if (active)
+        for (int i = lane; i < n; i += 32) zc[i] = z[i + j * ldz];
+    for (int k0 = n - 3; k0 >= 0; k0 -= kOrmChunk) {
+        const int k1 = max(0, k0 - kOrmChunk + 1);  // chunk covers k = k0 .. k1 (descending)
+        __syncthreads();
+        for (int kk = k1; kk <= k0; ++kk) {
+            const int w = n - kk - 1;
+            const double* src = lp + lidx(kk + 1, kk, n);
+            double* dst = vs + (k0 - kk) * n;
+            for (int i = threadIdx.x; i < w; i += blockDim.x) dst[i] = i == 0 ? 1.0 : src[i];
+        }
+        __syncthreads();
+        if (!active) continue;
+        for (int kk = k0; kk >= k1; --kk) {
+            const double tk = tau[kk];
+            if (tk == 0.0) continue;
+            const double* vk = vs + (k0 - kk) * n;
+            const int w = n - kk - 1;
+            double s = 0.0;
+            for (int i = lane; i < w; i += 32) s += vk[i] * zc[kk + 1 + i];
+            for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+            const double f = tk * s;
+            for (int i = lane; i < w; i += 32) zc[kk + 1 + i] -= f * vk[i];
+            __syncwarp();
+        }
+    }
+    if (active)
+        for (int i = lane; i < n; i += 32) z[i + j * ldz] = zc[i];
+}
+
+}  // namespace
+
+void sym_evd_top(Context& ctx, View t, Index want, double* values, View vectors) {
+    const int n = static_cast<int>(t.rows);
+    if (n <= 0 || want <= 0) return;
+    if (n == 1) {
+        BLWS_CUDA(cudaMemcpyAsync(values, t.p, sizeof(double), cudaMemcpyDeviceToDevice, ctx.stream()));
+        fill(ctx, vectors.left(1), 1.0);
+        return;
+    }
+    const long np = static_cast<long>(n) * (n + 1) / 2;
+    const long head = (3L * n + 32 + (n <= 32 * kMaxRowsPerLane ? static_cast<long>(kWarps) * n : 0)) * 8;
+    const bool on_chip = head + np * 8 <= kSmemBudget;
+    DBuf<double> lp(ctx, static_cast<size_t>(np)), d(ctx, static_cast<size_t>(n)), e(ctx, static_cast<size_t>(n)),
+        tau(ctx, static_cast<size_t>(n));
+    static bool cfg = false;
+    if (!cfg) {
+        BLWS_CUDA(cudaFuncSetAttribute(sytrd_k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget));
+        cfg = true;
+    }
+    const int smem = static_cast<int>(head + (on_chip ? np * 8 : 0));
+    sytrd_k<<<1, kThreads, smem, ctx.stream()>>>(t.p, t.ld, n, on_chip ? 1 : 0, lp.get(), d.get(), e.get(), tau.get());
+    ctx.note_launch();
+    ctx.check_launch("sytrd_k");
+    tridiag_eig_top(ctx, n, d.get(), e.get(), want, values, vectors);
+    static bool cfg2 = false;
+    if (!cfg2) {
+        BLWS_CUDA(cudaFuncSetAttribute(ormtr_k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget));
+        cfg2 = true;
+    }
+    const int smem2 = (kOrmChunk + kOrmWarps) * n * 8;
+    ormtr_k<<<static_cast<unsigned>((want + kOrmWarps - 1) / kOrmWarps), kOrmWarps * 32, smem2, ctx.stream()>>>(
+        lp.get(), tau.get(), n, static_cast<int>(want), vectors.p, vectors.ld);
+    ctx.note_launch();
+    ctx.check_launch("ormtr_k");
+}
+
+}  // namespace blws

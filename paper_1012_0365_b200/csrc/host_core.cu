@@ -547,16 +547,18 @@ BlwsResult blws_svd(LinearOperator& w, const DWarm& warm, Index k, Index r, Rng&
             place_block(ctx, t.view().sub(l * bs, l * bs + bs, bs, bs), fac.b[l].view(), true);
         }
     }
-    DBuf<double> vals(ctx, static_cast<size_t>(d));
-    DMat vecs(ctx, d, d, false);
-    sym_evd_jacobi(ctx, t.view(), vals.get(), vecs.view());
-    std::vector<double> hv(static_cast<size_t>(d));
-    ctx.read(vals.get(), hv.data(), d);
+    // only the leading min(r, d) pairs can be kept (block_lanczos.hpp:235-238)
+    const Index want = std::min(r, d);
+    DBuf<double> vals(ctx, static_cast<size_t>(want));
+    DMat vecs(ctx, d, want, false);
+    sym_evd_top(ctx, t.view(), want, vals.get(), vecs.view());
+    std::vector<double> hv(static_cast<size_t>(want));
+    ctx.read(vals.get(), hv.data(), want);
     for (double v : hv)
         if (!std::isfinite(v)) throw NumericalError("sym_evd_small: failed to converge");
 
     // keep the strictly positive part (block_lanczos.hpp:233-238); avail = d >= r
-    const Index avail = std::min(k_eff * bs, d);
+    const Index avail = std::min(k_eff * bs, want);
     const double floor = d > 0 ? 1e-12 * std::fabs(hv[0]) : 0.0;
     Index keep = 0;
     while (keep < avail && keep < r && hv[static_cast<size_t>(keep)] > floor) ++keep;

@@ -44,7 +44,7 @@ __global__ void __launch_bounds__(kJacobiThreads) jacobi_k(const double* __restr
     double* rt = rs + half;
     int* rp = reinterpret_cast<int*>(rt + half);
     int* rq = rp + half;
-    double* a = on_chip ? reinterpret_cast<double*>(rq + half + (half & 1)) : gpacked;
+    double* a = on_chip ? reinterpret_cast<double*>(rq + half) : gpacked;  // 32*half bytes: 8-aligned
     __shared__ double red[32];
     __shared__ int flag;
 

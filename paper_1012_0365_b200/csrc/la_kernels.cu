@@ -121,57 +121,59 @@ __global__ void gather_cols_k(double* d, long ldd, const double* s, long lds, lo
     }
 }
 
-// Right-looking upper Cholesky, one CTA, G in global memory (L1/L2 resident).
+// Right-looking upper Cholesky, one CTA. G is staged in shared memory when it
+// fits (n <= 160), else updated in place in global memory (L1/L2 resident).
+constexpr long kCholSmem = 160 * 160;
 __global__ void __launch_bounds__(1024) potrf_k(double* g, long n, long ld, int* status, double* diag) {
-    __shared__ double rowj[2048];
+    extern __shared__ __align__(16) double sm[];
+    double* rj = sm;  // row j of R (n doubles)
+    const bool on_chip = n * n <= kCholSmem;
+    double* a = on_chip ? sm + n : g;
+    const long la = on_chip ? n : ld;
     __shared__ int fail;
     if (threadIdx.x == 0) fail = 0;
+    if (on_chip)
+        for (long idx = threadIdx.x; idx < n * n; idx += blockDim.x) a[idx] = g[idx % n + (idx / n) * ld];
     __syncthreads();
     for (long j = 0; j < n; ++j) {
-        const double piv = g[j + j * ld];
+        const double piv = a[j + j * la];
         if (!(piv > 0.0) || !isfinite(piv)) {
             if (threadIdx.x == 0) fail = static_cast<int>(j + 1);
             break;
         }
         const double rjj = sqrt(piv);
         __syncthreads();
-        // row j of R (columns k > j); stage in shared when it fits
         for (long k = j + 1 + threadIdx.x; k < n; k += blockDim.x) {
-            const double r = g[j + k * ld] / rjj;
-            g[j + k * ld] = r;
-            if (k - j - 1 < 2048) rowj[k - j - 1] = r;
+            const double r = a[j + k * la] / rjj;
+            a[j + k * la] = r;
+            rj[k] = r;
         }
+        if (threadIdx.x == 0) a[j + j * la] = rjj;
         __syncthreads();
-        if (threadIdx.x == 0) g[j + j * ld] = rjj;
-        // trailing update of the upper triangle: G[i,k] -= R[j,i] R[j,k], j < i <= k
-        const long w = n - j - 1;
-        const long total = w * (w + 1) / 2;
-        for (long idx = threadIdx.x; idx < total; idx += blockDim.x) {
-            // map idx -> (ii, kk) with 0 <= ii <= kk < w, column-major over kk
-            long kk = static_cast<long>((sqrt(8.0 * static_cast<double>(idx) + 1.0) - 1.0) * 0.5);
-            while (kk * (kk + 1) / 2 > idx) --kk;
-            while ((kk + 1) * (kk + 2) / 2 <= idx) ++kk;
-            const long ii = idx - kk * (kk + 1) / 2;
-            const long i = j + 1 + ii, k = j + 1 + kk;
-            const double ri = ii < 2048 ? rowj[ii] : g[j + i * ld];
-            const double rk = kk < 2048 ? rowj[kk] : g[j + k * ld];
-            g[i + k * ld] -= ri * rk;
+        // trailing update of the upper triangle, warp per column k, lanes over i <= k
+        {
+            const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+            const int jj = static_cast<int>(j), nn = static_cast<int>(n);
+            for (int k = jj + 1 + wid; k < nn; k += nw) {
+                const double rk = rj[k];
+                double* col = a + static_cast<long>(k) * la;
+                for (int i = jj + 1 + lane; i <= k; i += 32) col[i] -= rj[i] * rk;
+            }
         }
         __syncthreads();
     }
     __syncthreads();
     if (threadIdx.x == 0) status[0] = fail;
     if (fail) return;
-    // zero the strict lower triangle; min / max of diag(R)
+    double mn = INFINITY, mx = 0.0;
     for (long idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
         const long i = idx % n, k = idx / n;
-        if (i > k) g[i + k * ld] = 0.0;
-    }
-    double mn = INFINITY, mx = 0.0;
-    for (long i = threadIdx.x; i < n; i += blockDim.x) {
-        const double d = g[i + i * ld];
-        mn = fmin(mn, d);
-        mx = fmax(mx, d);
+        const double v = i > k ? 0.0 : a[i + k * la];
+        g[i + k * ld] = v;
+        if (i == k) {
+            mn = fmin(mn, v);
+            mx = fmax(mx, v);
+        }
     }
     __shared__ double smn[32], smx[32];
     for (int o = 16; o > 0; o >>= 1) {
@@ -193,22 +195,41 @@ __global__ void __launch_bounds__(1024) potrf_k(double* g, long n, long ld, int*
     }
 }
 
-// Inverse of an upper-triangular matrix: one warp per column, column-oriented
-// back substitution (x = e_j; for i = j..0: x_i /= R_ii; x_{<i} -= R_{<i,i} x_i).
+// Inverse of an upper-triangular R: R staged in shared memory per CTA (when it
+// fits), one warp per column, column-oriented back substitution on a
+// per-warp shared vector (x = e_j; for i = j..0: x_i /= R_ii; x_{<i} -= R_{<i,i} x_i).
+constexpr long kTrtriSmem = 150 * 150;
+constexpr int kTrtriWarps = 8;
 __global__ void trtri_k(double* out, long ldo, const double* r, long ldr, long n) {
-    const long warps = (static_cast<long>(gridDim.x) * blockDim.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    for (long j = (blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x) >> 5; j < n; j += warps) {
-        double* x = out + j * ldo;
-        for (long i = lane; i < n; i += 32) x[i] = (i == j) ? 1.0 : 0.0;
+    extern __shared__ __align__(16) double sm[];
+    const bool on_chip = n * n <= kTrtriSmem;
+    double* xs = sm;  // kTrtriWarps * n
+    const double* R = r;
+    long lr = ldr;
+    if (on_chip) {
+        double* rs = sm + kTrtriWarps * n;
+        for (long idx = threadIdx.x; idx < n * n; idx += blockDim.x) rs[idx] = r[idx % n + (idx / n) * ldr];
+        R = rs;
+        lr = n;
+        __syncthreads();
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double* x = xs + warp * n;
+    const int nn = static_cast<int>(n), l = static_cast<int>(lr);
+    for (int j = blockIdx.x * kTrtriWarps + warp; j < nn; j += gridDim.x * kTrtriWarps) {
+        for (int i = lane; i <= j; i += 32) x[i] = (i == j) ? 1.0 : 0.0;
         __syncwarp();
-        for (long i = j; i >= 0; --i) {
-            const double xi = x[i] / r[i + i * ldr];
+        for (int i = j; i >= 0; --i) {
+            const double xi = x[i] / R[i + i * l];
+            const double* rc = R + i * l;
+            for (int k = lane; k < i; k += 32) x[k] -= rc[k] * xi;
             __syncwarp();
             if (lane == 0) x[i] = xi;
-            for (long k = lane; k < i; k += 32) x[k] -= r[k + i * ldr] * xi;
             __syncwarp();
         }
+        double* o = out + static_cast<long>(j) * ldo;
+        for (int i = lane; i < nn; i += 32) o[i] = i <= j ? x[i] : 0.0;
+        __syncwarp();
     }
 }
 
@@ -388,14 +409,27 @@ void gather_columns(Context& ctx, View d, View s, const int* ix) {
 }
 
 void potrf_upper(Context& ctx, View g, int* status, double* diag) {
-    potrf_k<<<1, 1024, 0, ctx.stream()>>>(g.p, g.rows, g.ld, status, diag);
+    static bool cfg = false;
+    if (!cfg) {
+        BLWS_CUDA(cudaFuncSetAttribute(potrf_k, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+        cfg = true;
+    }
+    const long n = g.rows;
+    const size_t smem = static_cast<size_t>((n + (n * n <= kCholSmem ? n * n : 0)) * 8);
+    potrf_k<<<1, 1024, smem, ctx.stream()>>>(g.p, n, g.ld, status, diag);
     LAUNCH(ctx, "potrf");
 }
 
 void trtri_upper(Context& ctx, View out, View r) {
+    static bool cfg = false;
+    if (!cfg) {
+        BLWS_CUDA(cudaFuncSetAttribute(trtri_k, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+        cfg = true;
+    }
     const long n = r.rows;
-    const unsigned blocks = static_cast<unsigned>(std::max<long>(1, (n * 32 + kThreads - 1) / kThreads));
-    trtri_k<<<blocks, kThreads, 0, ctx.stream()>>>(out.p, out.ld, r.p, r.ld, n);
+    const size_t smem = static_cast<size_t>((kTrtriWarps * n + (n * n <= kTrtriSmem ? n * n : 0)) * 8);
+    const unsigned blocks = static_cast<unsigned>(std::max<long>(1, std::min<long>(32, (n + kTrtriWarps - 1) / kTrtriWarps)));
+    trtri_k<<<blocks, kTrtriWarps * 32, smem, ctx.stream()>>>(out.p, out.ld, r.p, r.ld, n);
     LAUNCH(ctx, "trtri");
 }
 

@@ -46,6 +46,9 @@ void count_diag_above(Context& ctx, View r, const double* sumsq_dev, double scal
 /// Symmetric EVD (Jacobi). values descending, vectors columns (n x n).
 /// Returns sweeps used (host value, requires a sync).
 int sym_evd_jacobi(Context& ctx, View t, double* values, View vectors);
+/// Top `want` eigenpairs (descending) of a dense symmetric n x n T:
+/// Householder tridiagonalisation + bisection / inverse iteration + back-transform.
+void sym_evd_top(Context& ctx, View t, Index want, double* values, View vectors);
 /// Top `want` eigenpairs of the symmetric tridiagonal (d, e): values
 /// descending, vectors n x want. Bisection + inverse iteration with cluster
 /// reorthogonalisation.

@@ -20,6 +20,11 @@
 namespace blws {
 namespace {
 
+// Eigenvalues closer than this (relative to ||T||_1) are inverse-iterated
+// together with modified Gram-Schmidt (LAPACK dstein uses 1e-3; outside a
+// cluster the loss of orthogonality is <= eps ||T|| / gap <= 2e-11).
+constexpr double kClusterTol = 1e-5;
+
 __device__ __forceinline__ int sturm_count(const double* d, const double* e2, int n, double x, double pivmin) {
     double q = d[0] - x;
     if (fabs(q) <= pivmin) q = -pivmin;
@@ -79,7 +84,7 @@ __global__ void inverse_iteration_k(const double* __restrict__ d, const double* 
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const double eps = 2.220446049250313e-16;
     const double eps3 = eps * onenrm;
-    const double ortol = 1e-3 * onenrm;
+    const double ortol = kClusterTol * onenrm;
     double* u0 = scratch + static_cast<long>(gw) * 6 * n;
     double* u1 = u0 + n;
     double* u2 = u1 + n;
@@ -234,7 +239,7 @@ void tridiag_eig_top(Context& ctx, Index n_, const double* d, const double* e, I
     ctx.read(values, hv.data(), want);
     std::vector<int> cs;
     cs.push_back(0);
-    const double ortol = 1e-3 * onenrm;
+    const double ortol = kClusterTol * onenrm;
     for (int j = 1; j < want; ++j)
         if (hv[j - 1] - hv[j] > ortol) cs.push_back(j);
     cs.push_back(want);

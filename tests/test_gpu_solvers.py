@@ -55,7 +55,8 @@ def test_rpca_rejects_non_finite(G):
 
 
 def test_mc_parity(G, O):
-    colptr, rowidx, vals, ml, mr = synth.mc_lowrank(200, 5, 6000, 13, O.Rng, O.sample_distinct)
+    # gen_mc(200, 5, 6.0, 13): s = round(6 * 5 * (2*200 - 5)) = 11850 (test_solvers.cpp:110-137)
+    colptr, rowidx, vals, ml, mr = synth.mc_lowrank(200, 5, 11850, 13, O.Rng, O.sample_distinct)
     ug, sg, vg, stg = G.mc_svt(200, 200, colptr, rowidx, vals, G.SvdBackend.blws(seed=8), truth_ml=ml, truth_mr=mr)
     uo, so, vo, sto = O.mc_svt(200, 200, colptr, rowidx, vals, O.SvdBackend.blws(seed=8), truth_ml=ml, truth_mr=mr)
     assert stg.converged and sto.converged

@@ -1,0 +1,30 @@
+"""Run the C2 partial SVT a few times (for ncu launch lists / quick timing)."""
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench  # noqa: E402
+import paper_1012_0365_b200 as B  # noqa: E402
+
+
+def main(calls=2):
+    import torch
+
+    W, U, V, s, eps = bench.make_instance(B.Rng)
+    ctx = B.Context(0)
+    Wd = torch.from_numpy(np.ascontiguousarray(W.T)).cuda()
+    op = B.DenseOperator(Wd, ctx=ctx, device=True, shape=(bench.M, bench.N), ld=bench.M)
+    warm = B.DeviceWarmStart.from_host(U, V, s, ctx)
+    for i in range(calls):
+        t = time.perf_counter()
+        res = B.blws_svd(op, warm, 2, bench.R, B.Rng(1), keep_device=True)
+        ctx.synchronize()
+        print(f"call {i}: {1e3 * (time.perf_counter() - t):.2f} ms, launches {ctx.launches}, "
+              f"achieved {int(np.sum(res.warm.sigma() > eps))}", flush=True)
+
+
+if __name__ == "__main__":
+    main(int(sys.argv[1]) if len(sys.argv) > 1 else 2)
