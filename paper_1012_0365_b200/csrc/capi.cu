@@ -10,6 +10,9 @@
 #include "ops.cuh"
 
 using namespace blws;
+namespace blws {
+void chol_probe_read(double* out);
+}
 
 struct blws_context {
     std::unique_ptr<Context> ctx;
@@ -541,3 +544,168 @@ int blws_mc_svt(blws_context* ctx, int64_t m, int64_t n, int64_t nnz, const int6
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Kernel microbenchmarks (development / profiling only): average device time
+// in microseconds of one call of a hot-path piece on a seeded input of order n
+// (and width b where relevant). which: 0 chol_inv (SPD n x n), 1 sym_evd_top
+// (n x n symmetric, want = n/2), 2 thin_qr (rows n, cols b), 3 gemm NN
+// (n x b = n x n * n x b), 4 gemm TN (b x b = (n x b)^T (n x b)).
+extern "C" int blws_microbench(blws_context* ctx, int which, int64_t n, int64_t b, int reps, double* us) {
+    return guard([&] {
+        Context& c = *ctx->ctx;
+        std::vector<double> h(static_cast<size_t>(std::max<int64_t>(n * n, n * b)));
+        Rng rng(12345);
+        auto fill_host = [&](Index cnt) {
+            for (Index i = 0; i < cnt; ++i) h[static_cast<size_t>(i)] = rng.normal();
+        };
+        cudaEvent_t e0, e1;
+        BLWS_CUDA(cudaEventCreate(&e0));
+        BLWS_CUDA(cudaEventCreate(&e1));
+        float total = 0;
+        if (which == 0 || which == 1) {
+            fill_host(n * n);
+            DMat a(c, n, n), s(c, n, n), g0(c, n, n), work(c, n, n), rinv(c, n, n), vec(c, n, std::max<int64_t>(1, n / 2));
+            upload(c, a.view(), h.data(), n);
+            if (which == 0) {
+                // G = A^T A + n I (SPD)
+                gemm(c, true, false, n, n, n, 1.0, a.data(), a.ld, a.data(), a.ld, 0.0, g0.data(), g0.ld);
+            } else {
+                symmetrize(c, g0.view(), a.view());
+            }
+            DBuf<int> st(c, 1);
+            DBuf<double> dg(c, 8), vals(c, static_cast<size_t>(n));
+            for (int r = -1; r < reps; ++r) {
+                copy(c, work.view(), g0.view());
+                BLWS_CUDA(cudaEventRecord(e0, c.stream()));
+                if (which == 0)
+                    chol_inv_upper(c, work.view(), rinv.view(), st.get(), dg.get());
+                else
+                    sym_evd_top(c, work.view(), std::max<int64_t>(1, n / 2), vals.get(), vec.view());
+                BLWS_CUDA(cudaEventRecord(e1, c.stream()));
+                BLWS_CUDA(cudaEventSynchronize(e1));
+                float ms = 0;
+                BLWS_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+                if (r >= 0) total += ms;
+            }
+        } else if (which == 2) {
+            fill_host(n * b);
+            DMat x0(c, n, b), x(c, n, b);
+            upload(c, x0.view(), h.data(), n);
+            for (int r = -1; r < reps; ++r) {
+                copy(c, x.view(), x0.view());
+                BLWS_CUDA(cudaEventRecord(e0, c.stream()));
+                blws::thin_qr(c, x.view(), nullptr);
+                BLWS_CUDA(cudaEventRecord(e1, c.stream()));
+                BLWS_CUDA(cudaEventSynchronize(e1));
+                float ms = 0;
+                BLWS_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+                if (r >= 0) total += ms;
+            }
+        } else {
+            DMat a(c, n, which == 3 ? n : b), x(c, n, b), y(c, which == 3 ? n : b, b);
+            fill(c, a.view(), 1.0 / static_cast<double>(n));
+            fill(c, x.view(), 0.5);
+            for (int r = -1; r < reps; ++r) {
+                BLWS_CUDA(cudaEventRecord(e0, c.stream()));
+                if (which == 3)
+                    gemm(c, false, false, n, b, n, 1.0, a.data(), a.ld, x.data(), x.ld, 0.0, y.data(), y.ld);
+                else
+                    gemm(c, true, false, b, b, n, 1.0, x.data(), x.ld, x.data(), x.ld, 0.0, y.data(), y.ld);
+                BLWS_CUDA(cudaEventRecord(e1, c.stream()));
+                BLWS_CUDA(cudaEventSynchronize(e1));
+                float ms = 0;
+                BLWS_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+                if (r >= 0) total += ms;
+            }
+        }
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        *us = 1e3 * total / std::max(1, reps);
+        if (which == 0) {
+            double ph[4];
+            chol_probe_read(ph);
+            us[1] = ph[0];
+            us[2] = ph[1];
+            us[3] = ph[2];
+            us[4] = ph[3];
+        }
+    });
+}
+
+namespace {
+__global__ void probe_clock_k(long long spin_ns, double* out) {
+    unsigned long long t0, t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    const long long c0 = clock64();
+    do {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    } while (static_cast<long long>(t1 - t0) < spin_ns);
+    const long long c1 = clock64();
+    if (threadIdx.x == 0) out[0] = static_cast<double>(c1 - c0) / static_cast<double>(t1 - t0) * 1e3;  // MHz
+}
+__global__ void probe_sync_k(int iters, double* out) {
+    __shared__ double s[1024];
+    double v = threadIdx.x;
+    const long long c0 = clock64();
+    for (int i = 0; i < iters; ++i) {
+        s[threadIdx.x] = v;
+        __syncthreads();
+        v += s[(threadIdx.x + 1) & 1023];
+        __syncthreads();
+    }
+    const long long c1 = clock64();
+    if (threadIdx.x == 0) out[0] = static_cast<double>(c1 - c0) / (2.0 * iters);  // cycles per barrier
+    if (v == 12345.0) out[1] = v;
+}
+__global__ void probe_empty_k() {}
+__global__ void probe_ops_k(double x0, double* out) {
+    // cycles per dependent op: 0 DFMA, 1 div, 2 sqrt, 3 rsqrt, 4 rcp(approx)+2 Newton
+    double x = x0;
+    long long c0 = clock64();
+    for (int i = 0; i < 256; ++i) x = fma(x, 1.0000001, 1e-9);
+    long long c1 = clock64();
+    out[0] = (c1 - c0) / 256.0;
+    c0 = clock64();
+    for (int i = 0; i < 256; ++i) x = 1.0 / x + 0.5;
+    c1 = clock64();
+    out[1] = (c1 - c0) / 256.0;
+    c0 = clock64();
+    for (int i = 0; i < 256; ++i) x = sqrt(x) + 0.5;
+    c1 = clock64();
+    out[2] = (c1 - c0) / 256.0;
+    c0 = clock64();
+    for (int i = 0; i < 256; ++i) x = rsqrt(x) + 0.5;
+    c1 = clock64();
+    out[3] = (c1 - c0) / 256.0;
+    out[4] = x;
+}
+}  // namespace
+
+// probe: out[0] SM MHz during a 200 us spin, out[1] cycles per __syncthreads
+// (1024 threads), out[2] us per empty launch (event-timed, 100 launches)
+extern "C" int blws_probe(blws_context* ctx, double* out) {
+    return guard([&] {
+        Context& c = *ctx->ctx;
+        DBuf<double> d(c, 4);
+        probe_clock_k<<<1, 32, 0, c.stream()>>>(200000, d.get());
+        c.read(d.get(), out, 1);
+        probe_sync_k<<<1, 1024, 0, c.stream()>>>(1000, d.get());
+        c.read(d.get(), out + 1, 1);
+        DBuf<double> ops(c, 8);
+        probe_ops_k<<<1, 1, 0, c.stream()>>>(1.5, ops.get());
+        c.read(ops.get(), out + 3, 4);
+        cudaEvent_t e0, e1;
+        BLWS_CUDA(cudaEventCreate(&e0));
+        BLWS_CUDA(cudaEventCreate(&e1));
+        BLWS_CUDA(cudaEventRecord(e0, c.stream()));
+        for (int i = 0; i < 100; ++i) probe_empty_k<<<1, 32, 0, c.stream()>>>();
+        BLWS_CUDA(cudaEventRecord(e1, c.stream()));
+        BLWS_CUDA(cudaEventSynchronize(e1));
+        float ms = 0;
+        BLWS_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        out[2] = ms * 10.0;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+    });
+}

@@ -1,0 +1,234 @@
+// Fused Cholesky + triangular inverse for CholQR (K3): G = R^T R, Rinv = R^{-1}.
+//
+// thin_qr (core/qr.hpp:24-47) becomes CholQR2 on the device; each pass needs
+// chol(G) and R^{-1} of a b x b Gram (b <= ~411). One CTA does both:
+//   * right-looking Cholesky: per column one warp scales the pivot row, then
+//     every warp updates its trailing columns (two barriers per column);
+//   * R^{-1}: one thread per column, back substitution with four independent
+//     accumulators, reciprocal pivots precomputed.
+// Compact loops on purpose: fully unrolled register-resident blocks made the
+// code large enough to thrash the instruction cache (measured 30 us at b=32).
+// Staged in shared memory when it fits (b <= 116); the SH template parameter
+// keeps those accesses LDS/STS instead of generic loads.
+#include <algorithm>
+#include <cmath>
+
+#include "ops.cuh"
+
+namespace blws {
+__device__ double g_chol_probe[4];  // phase cycle counts of the last chol_inv call (profiling)
+namespace {
+
+constexpr int kCT = 1024;
+constexpr long kSmemBudget = 216 * 1024;
+
+template <bool SH>
+__global__ void __launch_bounds__(kCT) chol_inv_k(double* g, long ldg, double* rinv, long ldri, int n,
+                                                  double* scratch, int* status, double* diag) {
+    extern __shared__ __align__(16) double sm[];
+    __shared__ int fail;
+    const int ld = n | 1;  // odd stride: conflict-free row access
+    double* A = SH ? sm : scratch;
+    double* X = A + static_cast<long>(ld) * n;
+    double* rowj = X + static_cast<long>(ld) * n;  // n
+    double* dinv = rowj + n;                         // n
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if (threadIdx.x == 0) fail = 0;
+    long long t0 = clock64();
+    for (int j = wid; j < n; j += nw)
+        for (int i = lane; i < n; i += 32) A[i + j * ld] = g[i + j * ldg];
+    __syncthreads();
+    long long t1 = clock64();
+    // ---- right-looking Cholesky, trailing matrix in registers: thread t owns
+    // upper-triangle entries e = t + kCT * q (q < kOwn) in column-major packed
+    // order. Per column: the pivot owner publishes R(k,k); row-k owners publish
+    // R(k, j); every owner updates its (i, j) with k < i <= j.
+    // ---- blocked right-looking Cholesky (32-wide panels)
+    for (int kb = 0; kb < n && !fail; kb += 32) {
+        const int nb = min(32, n - kb);
+        if (wid == 0) {
+            // diagonal block by one warp: lane = row i; per pivot k the column loop
+            // over j has independent iterations (pipelined LDS/FMA/STS)
+            const int i = kb + lane;
+            for (int k = 0; k < nb; ++k) {
+                const int gk = kb + k;
+                const double piv = A[gk + gk * ld];
+                const bool bad = !(piv > 0.0) || !isfinite(piv);
+                const double rs = bad ? 1.0 : rsqrt(piv);
+                if (lane == 0) {
+                    if (bad && fail == 0) fail = gk + 1;
+                    A[gk + gk * ld] = piv * rs;
+                    dinv[gk] = rs;
+                }
+                // scale row k (columns j = lane > k)
+                if (lane > k && lane < nb) A[gk + i * ld] *= rs;
+                __syncwarp();
+                const double rki = (lane > k && lane < nb) ? A[gk + i * ld] : 0.0;  // R(k, i)
+                for (int j = k + 1; j < nb; ++j) {
+                    const double rkj = A[gk + (kb + j) * ld];
+                    if (lane > k && lane <= j) A[i + (kb + j) * ld] -= rki * rkj;
+                }
+                __syncwarp();
+            }
+        }
+        __syncthreads();
+        if (fail) break;
+        const int rest = n - kb - nb;
+        if (rest <= 0) break;
+        // panel rows: R12 = R11^{-T} A12, forward substitution, warp per column, lane = row
+        for (int j = kb + nb + wid; j < n; j += nw) {
+            double x = lane < nb ? A[kb + lane + j * ld] : 0.0;
+            for (int ii = 0; ii < nb; ++ii) {
+                const double xi = __shfl_sync(0xffffffffu, x, ii) * dinv[kb + ii];
+                if (lane == ii) x = xi;
+                if (lane > ii && lane < nb) x -= A[kb + ii + (kb + lane) * ld] * xi;
+            }
+            if (lane < nb) A[kb + lane + j * ld] = x;
+        }
+        __syncthreads();
+        // trailing SYRK (upper): A22 -= R12^T R12, warp per column, lanes over rows
+        for (int j = kb + nb + wid; j < n; j += nw) {
+            const double* cj = A + kb + j * ld;
+            for (int i2 = kb + nb + lane; i2 <= j; i2 += 32) {
+                const double* ci = A + kb + i2 * ld;
+                double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+                int k = 0;
+                for (; k + 3 < nb; k += 4) {
+                    s0 = fma(ci[k], cj[k], s0);
+                    s1 = fma(ci[k + 1], cj[k + 1], s1);
+                    s2 = fma(ci[k + 2], cj[k + 2], s2);
+                    s3 = fma(ci[k + 3], cj[k + 3], s3);
+                }
+                for (; k < nb; ++k) s0 = fma(ci[k], cj[k], s0);
+                A[i2 + j * ld] -= (s0 + s1) + (s2 + s3);
+            }
+        }
+        __syncthreads();
+    }
+    long long t2 = clock64();
+    if (threadIdx.x == 0) status[0] = fail;
+    if (fail) return;
+    // ---- R^{-1} by recursive doubling: X_{2k-block} = [[XA, -XA B XC], [0, XC]]
+    for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
+        const int i = idx % n, j = idx / n;
+        X[i + j * ld] = i == j ? dinv[i] : 0.0;
+    }
+    __syncthreads();
+    for (int k = 1; k < n; k *= 2) {
+        const int pairs = (n + 2 * k - 1) / (2 * k);
+        const int total = pairs * k * k;
+        // phase 1: T = B XC into X's upper-right block (B = R[o:o+k, o+k:o+2k])
+        for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+            const int p = idx / (k * k), rr = idx % k, cc = (idx / k) % k;
+            const int o = p * 2 * k, r = o + rr, c = o + k + cc;
+            if (c >= n) continue;
+            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+            int t = o + k;
+            for (; t + 3 <= c; t += 4) {
+                s0 = fma(A[r + t * ld], X[t + c * ld], s0);
+                s1 = fma(A[r + (t + 1) * ld], X[t + 1 + c * ld], s1);
+                s2 = fma(A[r + (t + 2) * ld], X[t + 2 + c * ld], s2);
+                s3 = fma(A[r + (t + 3) * ld], X[t + 3 + c * ld], s3);
+            }
+            for (; t <= c; ++t) s0 = fma(A[r + t * ld], X[t + c * ld], s0);
+            X[r + c * ld] = (s0 + s1) + (s2 + s3);
+        }
+        __syncthreads();
+        // phase 2: X_UR = -XA T (read all into registers, sync, write)
+        for (int base = 0; base < total; base += 4 * kCT) {
+            double out[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int idx = base + q * kCT + threadIdx.x;
+                out[q] = 0.0;
+                if (idx >= total) continue;
+                const int p = idx / (k * k), rr = idx % k, cc = (idx / k) % k;
+                const int o = p * 2 * k, r = o + rr, c = o + k + cc;
+                if (c >= n) continue;
+                double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+                int t = r;
+                for (; t + 3 < o + k; t += 4) {
+                    s0 = fma(X[r + t * ld], X[t + c * ld], s0);
+                    s1 = fma(X[r + (t + 1) * ld], X[t + 1 + c * ld], s1);
+                    s2 = fma(X[r + (t + 2) * ld], X[t + 2 + c * ld], s2);
+                    s3 = fma(X[r + (t + 3) * ld], X[t + 3 + c * ld], s3);
+                }
+                for (; t < o + k; ++t) s0 = fma(X[r + t * ld], X[t + c * ld], s0);
+                out[q] = -((s0 + s1) + (s2 + s3));
+            }
+            __syncthreads();
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int idx = base + q * kCT + threadIdx.x;
+                if (idx >= total) continue;
+                const int p = idx / (k * k), rr = idx % k, cc = (idx / k) % k;
+                const int o = p * 2 * k, r = o + rr, c = o + k + cc;
+                if (c < n) X[r + c * ld] = out[q];
+            }
+            __syncthreads();
+        }
+    }
+    __syncthreads();
+    long long t3 = clock64();
+    double mn = INFINITY, mx = 0.0;
+    for (int j = wid; j < n; j += nw)
+        for (int i = lane; i < n; i += 32) {
+            const double v = i > j ? 0.0 : A[i + j * ld];
+            g[i + j * ldg] = v;
+            if (rinv) rinv[i + j * ldri] = i > j ? 0.0 : X[i + j * ld];
+            if (i == j) {
+                mn = fmin(mn, v);
+                mx = fmax(mx, v);
+            }
+        }
+    __shared__ double smn[32], smx[32];
+    for (int o = 16; o > 0; o >>= 1) {
+        mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if (lane == 0) {
+        smn[wid] = mn;
+        smx[wid] = mx;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w2 = 1; w2 < nw; ++w2) {
+            mn = fmin(mn, smn[w2]);
+            mx = fmax(mx, smx[w2]);
+        }
+        diag[0] = mn;
+        diag[1] = mx;
+        g_chol_probe[0] = static_cast<double>(t1 - t0);
+        g_chol_probe[1] = static_cast<double>(t2 - t1);
+        g_chol_probe[2] = static_cast<double>(t3 - t2);
+        g_chol_probe[3] = static_cast<double>(clock64() - t3);
+    }
+}
+
+}  // namespace
+
+void chol_inv_upper(Context& ctx, View g, View rinv, int* status, double* diag) {
+    const int n = static_cast<int>(g.rows);
+    const long ld = n | 1;
+    const long bytes = (2L * ld * n + 2L * n) * 8;
+    const bool on_chip = bytes <= kSmemBudget;
+    static bool cfg = false;
+    if (!cfg) {
+        BLWS_CUDA(cudaFuncSetAttribute(chol_inv_k<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget));
+        cfg = true;
+    }
+    if (on_chip) {
+        chol_inv_k<true><<<1, kCT, bytes, ctx.stream()>>>(g.p, g.ld, rinv.p, rinv.ld, n, nullptr, status, diag);
+    } else {
+        DBuf<double> scratch(ctx, static_cast<size_t>(2L * ld * n + 2L * n));
+        chol_inv_k<false><<<1, kCT, 0, ctx.stream()>>>(g.p, g.ld, rinv.p, rinv.ld, n, scratch.get(), status, diag);
+    }
+    ctx.note_launch();
+    ctx.check_launch("chol_inv_k");
+}
+
+}  // namespace blws
+
+namespace blws {
+void chol_probe_read(double* out) { BLWS_CUDA(cudaMemcpyFromSymbol(out, g_chol_probe, 4 * sizeof(double))); }
+}  // namespace blws

@@ -21,10 +21,11 @@ namespace {
 constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxRowsPerLane = 8;  // n <= 256 on this path (32 * 8 trailing rows per warp)
+constexpr int kColsPerWarp = 16;    // 256 columns / 16 warps
 constexpr long kSmemBudget = 220 * 1024;
 
-__device__ __forceinline__ long loff(long j, long n) { return j * n - j * (j - 1) / 2; }  // start of column j
-__device__ __forceinline__ long lidx(long i, long j, long n) {                              // (i >= j)
+__device__ __forceinline__ int loff(int j, int n) { return j * n - ((j * (j - 1)) >> 1); }  // start of column j
+__device__ __forceinline__ int lidx(int i, int j, int n) {                                 // (i >= j), n <= 4096
     return loff(j, n) + (i - j);
 }
 
@@ -42,8 +43,10 @@ __device__ double block_sum_1024(double v, double* red) {
 
 // In: T (n x n, ld) symmetric. Out: d (n), e (n-1), packed lower with the
 // reflectors below the diagonal (v[0] = 1 implicit) in `lp`, tau (n).
-__global__ void __launch_bounds__(kThreads) sytrd_k(const double* __restrict__ t, long ld, int n, int on_chip,
+template <bool SH>
+__global__ void __launch_bounds__(kThreads) sytrd_k(const double* __restrict__ t, long ld, int n,
                                                     double* lp, double* d, double* e, double* tau) {
+    constexpr bool on_chip = SH;
     extern __shared__ __align__(16) double sm[];
     double* v = sm;               // n
     double* p = v + n;            // n
@@ -87,7 +90,7 @@ __global__ void __launch_bounds__(kThreads) sytrd_k(const double* __restrict__ t
         // owns columns j = wid, wid+nw, ...; per column it forms the dot of the
         // strictly-lower part with v (-> pcol[j]) and accumulates L(:,j) v_j into
         // a private per-lane register vector (rows i = lane + 32 t).
-        if (w > 32 * kMaxRowsPerLane) {
+        if (n > 32 * kMaxRowsPerLane) {
             // large orders: warp per row, row part strided (global-memory path)
             for (int i = wid; i < w; i += nw) {
                 const int gi = k + 1 + i;
@@ -101,24 +104,51 @@ __global__ void __launch_bounds__(kThreads) sytrd_k(const double* __restrict__ t
                 if (lane == 0) p[i] = tk * acc;
             }
         } else {
-            double acc[kMaxRowsPerLane];
+            // v, restricted to this lane's rows, in registers
+            double vr[kMaxRowsPerLane], acc[kMaxRowsPerLane], dp[kColsPerWarp];
 #pragma unroll
-            for (int q = 0; q < kMaxRowsPerLane; ++q) acc[q] = 0.0;
-            for (int j = wid; j < w; j += nw) {
-                const double* col = a + lidx(k + 1 + j, k + 1 + j, n) - j;  // col[i] = A(k+1+i, k+1+j), i >= j
-                const double vj = v[j];
-                double dotp = 0.0;
+            for (int q = 0; q < kMaxRowsPerLane; ++q) {
+                const int i = lane + 32 * q;
+                vr[q] = i < w ? v[i] : 0.0;
+                acc[q] = 0.0;
+            }
 #pragma unroll
-                for (int q = 0; q < kMaxRowsPerLane; ++q) {
-                    const int i = lane + 32 * q;
-                    if (i >= j && i < w) {
-                        const double lij = col[i];
-                        acc[q] += lij * vj;
-                        if (i > j) dotp += lij * v[i];
+            for (int c = 0; c < kColsPerWarp; ++c) {
+                dp[c] = 0.0;
+                const int j = wid + c * kWarps;
+                if (j < w) {
+                    const double* col = a + lidx(k + 1 + j, k + 1 + j, n) - j;  // col[i] = A(k+1+i, k+1+j)
+                    const double vj = v[j];
+#pragma unroll
+                    for (int q = 0; q < kMaxRowsPerLane; ++q) {
+                        const int i = lane + 32 * q;
+                        if (i >= j && i < w) {
+                            const double lij = col[i];
+                            acc[q] = fma(lij, vj, acc[q]);
+                            if (i > j) dp[c] = fma(lij, vr[q], dp[c]);
+                        }
                     }
                 }
-                for (int o = 16; o > 0; o >>= 1) dotp += __shfl_xor_sync(0xffffffffu, dotp, o);
-                if (lane == 0) pcol[j] = dotp;
+            }
+            // batched reduction of the kColsPerWarp (=16) column dots over the warp:
+            // each stage halves the values per lane (16 -> 8 -> 4 -> 2 -> 1)
+#pragma unroll
+            for (int stage = 0; stage < 4; ++stage) {
+                const int half = kColsPerWarp >> (stage + 1);
+                const int o = 16 >> stage;
+                const bool hi = (lane & o) != 0;
+#pragma unroll
+                for (int c = 0; c < half; ++c) {
+                    const double send = hi ? dp[c] : dp[c + half];
+                    const double keep = hi ? dp[c + half] : dp[c];
+                    dp[c] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+                }
+            }
+            dp[0] += __shfl_xor_sync(0xffffffffu, dp[0], 1);
+            {
+                const int c = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+                const int j = wid + c * kWarps;
+                if ((lane & 1) == 0 && j < w) pcol[j] = dp[0];
             }
 #pragma unroll
             for (int q = 0; q < kMaxRowsPerLane; ++q) {
@@ -139,11 +169,33 @@ __global__ void __launch_bounds__(kThreads) sytrd_k(const double* __restrict__ t
         for (int i = threadIdx.x; i < w; i += blockDim.x) p[i] -= K * v[i];  // p <- w
         __syncthreads();
         // A22 -= v w^T + w v^T (lower), warp per column
-        for (int j = wid; j < w; j += nw) {
-            const int gj = k + 1 + j;
-            const double vj = v[j], wj = p[j];
-            double* col = a + lidx(gj, gj, n) - j;  // so col[i] = A(k+1+i, gj) for i >= j
-            for (int i = j + lane; i < w; i += 32) col[i] -= v[i] * wj + p[i] * vj;
+        if (n <= 32 * kMaxRowsPerLane) {
+            double vr[kMaxRowsPerLane], wr[kMaxRowsPerLane];
+#pragma unroll
+            for (int q = 0; q < kMaxRowsPerLane; ++q) {
+                const int i = lane + 32 * q;
+                vr[q] = i < w ? v[i] : 0.0;
+                wr[q] = i < w ? p[i] : 0.0;
+            }
+#pragma unroll
+            for (int c = 0; c < kColsPerWarp; ++c) {
+                const int j = wid + c * kWarps;
+                if (j >= w) break;
+                const double vj = v[j], wj = p[j];
+                double* col = a + lidx(k + 1 + j, k + 1 + j, n) - j;
+#pragma unroll
+                for (int q = 0; q < kMaxRowsPerLane; ++q) {
+                    const int i = lane + 32 * q;
+                    if (i >= j && i < w) col[i] -= fma(vr[q], wj, wr[q] * vj);
+                }
+            }
+        } else {
+            for (int j = wid; j < w; j += nw) {
+                const int gj = k + 1 + j;
+                const double vj = v[j], wj = p[j];
+                double* col = a + lidx(gj, gj, n) - j;  // so col[i] = A(k+1+i, gj) for i >= j
+                for (int i = j + lane; i < w; i += 32) col[i] -= v[i] * wj + p[i] * vj;
+            }
         }
         __syncthreads();
         // keep the reflector below the diagonal of column k
@@ -224,11 +276,15 @@ void sym_evd_top(Context& ctx, View t, Index want, double* values, View vectors)
         tau(ctx, static_cast<size_t>(n));
     static bool cfg = false;
     if (!cfg) {
-        BLWS_CUDA(cudaFuncSetAttribute(sytrd_k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget));
+        BLWS_CUDA(cudaFuncSetAttribute(sytrd_k<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget));
+        BLWS_CUDA(cudaFuncSetAttribute(sytrd_k<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget));
         cfg = true;
     }
     const int smem = static_cast<int>(head + (on_chip ? np * 8 : 0));
-    sytrd_k<<<1, kThreads, smem, ctx.stream()>>>(t.p, t.ld, n, on_chip ? 1 : 0, lp.get(), d.get(), e.get(), tau.get());
+    if (on_chip)
+        sytrd_k<true><<<1, kThreads, smem, ctx.stream()>>>(t.p, t.ld, n, lp.get(), d.get(), e.get(), tau.get());
+    else
+        sytrd_k<false><<<1, kThreads, smem, ctx.stream()>>>(t.p, t.ld, n, lp.get(), d.get(), e.get(), tau.get());
     ctx.note_launch();
     ctx.check_launch("sytrd_k");
     tridiag_eig_top(ctx, n, d.get(), e.get(), want, values, vectors);

@@ -298,77 +298,121 @@ struct CholStep {
     double dmin = 0, dmax = 0;
 };
 
-// One Cholesky-QR pass: G = X^T X (+ shift), R = chol(G), X <- X R^{-1}.
-CholStep cholqr_pass(Context& ctx, View x, const double* shift_dev) {
-    const Index b = x.cols;
+// R = chol(G) in place, Rinv = R^{-1}; reads back status + diag range (one sync).
+CholStep chol_step(Context& ctx, DMat g) {
     CholStep s;
-    s.r = DMat(ctx, b, b, false);
-    gemm(ctx, true, false, b, b, x.rows, 1.0, x.p, x.ld, x.p, x.ld, 0.0, s.r.data(), s.r.ld);
-    if (shift_dev) add_diagonal(ctx, s.r.view(), shift_dev);
+    const Index b = g.rows;
+    s.r = std::move(g);
+    s.rinv = DMat(ctx, b, b, false);
     DBuf<int> status(ctx, 1);
     DBuf<double> diag(ctx, 2);
-    potrf_upper(ctx, s.r.view(), status.get(), diag.get());
+    chol_inv_upper(ctx, s.r.view(), s.rinv.view(), status.get(), diag.get());
     int st = 0;
     double dd[2] = {0, 0};
     BLWS_CUDA(cudaMemcpyAsync(&st, status.get(), sizeof(int), cudaMemcpyDeviceToHost, ctx.stream()));
     ctx.read(diag.get(), dd, 2);
     s.ok = st == 0;
-    if (!s.ok) return s;
     s.dmin = dd[0];
     s.dmax = dd[1];
-    s.rinv = DMat(ctx, b, b, false);
-    trtri_upper(ctx, s.rinv.view(), s.r.view());
-    DMat tmp(ctx, x.rows, b, false);
-    gemm(ctx, false, false, x.rows, b, b, 1.0, x.p, x.ld, s.rinv.data(), s.rinv.ld, 0.0, tmp.data(), tmp.ld);
-    copy(ctx, x, tmp.view());
     return s;
+}
+
+DMat gram(Context& ctx, View x) {
+    DMat g(ctx, x.cols, x.cols, false);
+    gemm(ctx, true, false, x.cols, x.cols, x.rows, 1.0, x.p, x.ld, x.p, x.ld, 0.0, g.data(), g.ld);
+    return g;
+}
+
+// ||G - I||_F^2 (device) -> host
+double off_identity_sq(Context& ctx, View g, double* scratch) {
+    sumsq_minus_identity(ctx, g, scratch);
+    double h = 0;
+    ctx.read(scratch, &h, 1);
+    return h;
 }
 
 }  // namespace
 
+Index thin_qr_impl(Context& ctx, View x, View* r_out);
+
 Index thin_qr(Context& ctx, View x, View* r_out) {
+    ctx.region_begin(2);
+    const Index rank = thin_qr_impl(ctx, x, r_out);
+    ctx.region_end(2, 0.0, 0.0);
+    return rank;
+}
+
+// thin_qr (core/qr.hpp:24-47) as adaptive CholQR2 with a shifted-CholQR3
+// fallback. Q is the unique orthonormal factor with diag(R) > 0, i.e. the
+// reference's sign-normalised Householder Q; a pass is skipped when its Gram
+// is already the identity to 1e-14 (then R = I to working precision).
+Index thin_qr_impl(Context& ctx, View x, View* r_out) {
     const Index rows = x.rows, b = x.cols;
     if (rows == 0 || b == 0) throw std::invalid_argument("thin_qr: empty matrix");
     if (rows < b) throw std::invalid_argument("thin_qr: requires rows >= cols");
-    DBuf<double> ss(ctx, 1);
+    DBuf<double> ss(ctx, 2);
     sumsq(ctx, x, ss.get());
     double hss = 0;
     ctx.read(ss.get(), &hss, 1);
     if (!std::isfinite(hss)) throw std::invalid_argument("thin_qr: non-finite entries");
-    // keep the input for the shifted fallback
-    DMat x0(ctx, rows, b, false);
-    copy(ctx, x0.view(), x);
+    constexpr double kIdentityTol2 = 1e-28;  // ||G - I||_F <= 1e-14
+
     std::vector<CholStep> steps;
-    CholStep s1 = cholqr_pass(ctx, x, nullptr);
+    DMat g1 = gram(ctx, x);
+    if (off_identity_sq(ctx, g1.view(), ss.get() + 1) <= kIdentityTol2) {
+        // already orthonormal: Q = X, R = I (rank = b unless the tau test says otherwise)
+        if (r_out) {
+            fill(ctx, *r_out, 0.0);
+            DBuf<double> one(ctx, 1);
+            const double h1 = 1.0;
+            ctx.write(one.get(), &h1, 1);
+            add_diagonal(ctx, *r_out, one.get());
+        }
+        return 1.0 > 1e-12 * std::sqrt(hss) ? b : 0;
+    }
+    CholStep s1 = chol_step(ctx, std::move(g1));
     const bool ill = !s1.ok || !(s1.dmin > 0) || s1.dmax / s1.dmin > 1e6;
+    DMat y(ctx, rows, b, false);
     if (!ill) {
+        gemm(ctx, false, false, rows, b, b, 1.0, x.p, x.ld, s1.rinv.data(), s1.rinv.ld, 0.0, y.data(), y.ld);
         steps.push_back(std::move(s1));
-        steps.push_back(cholqr_pass(ctx, x, nullptr));
-        if (!steps.back().ok) throw NumericalError("thin_qr: CholQR2 second pass failed");
+        DMat g2 = gram(ctx, y.view());
+        if (off_identity_sq(ctx, g2.view(), ss.get() + 1) <= kIdentityTol2) {
+            copy(ctx, x, y.view());
+        } else {
+            CholStep s2 = chol_step(ctx, std::move(g2));
+            if (!s2.ok) throw NumericalError("thin_qr: CholQR2 second pass failed");
+            gemm(ctx, false, false, rows, b, b, 1.0, y.data(), y.ld, s2.rinv.data(), s2.rinv.ld, 0.0, x.p, x.ld);
+            steps.push_back(std::move(s2));
+        }
     } else {
-        // shifted CholQR3 (Fukaya et al.): s = 11 (rows*b + b(b+1)) u ||X||_F^2
-        copy(ctx, x, x0.view());
+        // shifted CholQR3 (Fukaya et al. 2020): s = 11 (rows*b + b(b+1)) u ||X||_F^2
+        DMat g(ctx, b, b, false);
+        gemm(ctx, true, false, b, b, rows, 1.0, x.p, x.ld, x.p, x.ld, 0.0, g.data(), g.ld);
         DBuf<double> shift(ctx, 1);
-        const double factor = 11.0 * (static_cast<double>(rows) * b + static_cast<double>(b) * (b + 1)) * 1.1102230246251565e-16;
+        const double factor =
+            11.0 * (static_cast<double>(rows) * b + static_cast<double>(b) * (b + 1)) * 1.1102230246251565e-16;
         shift_for_cholqr3_k<<<1, 1, 0, ctx.stream()>>>(ss.get(), factor, shift.get());
         ctx.note_launch();
-        CholStep a = cholqr_pass(ctx, x, shift.get());
+        add_diagonal(ctx, g.view(), shift.get());
+        CholStep a = chol_step(ctx, std::move(g));
         if (!a.ok) {
             if (hss == 0.0) {
-                // all-zero input: Q undefined, rank 0 (R = 0)
                 if (r_out) fill(ctx, *r_out, 0.0);
                 return 0;
             }
             throw NumericalError("thin_qr: shifted CholQR failed");
         }
+        gemm(ctx, false, false, rows, b, b, 1.0, x.p, x.ld, a.rinv.data(), a.rinv.ld, 0.0, y.data(), y.ld);
+        copy(ctx, x, y.view());
         steps.push_back(std::move(a));
         for (int k = 0; k < 2; ++k) {
-            CholStep c = cholqr_pass(ctx, x, nullptr);
-            if (!c.ok) {
-                // Q columns already orthonormal to working precision except for
-                // the null directions; keep what we have
-                break;
-            }
+            DMat gk = gram(ctx, x);
+            if (off_identity_sq(ctx, gk.view(), ss.get() + 1) <= kIdentityTol2) break;
+            CholStep c = chol_step(ctx, std::move(gk));
+            if (!c.ok) break;  // remaining directions are numerically null
+            gemm(ctx, false, false, rows, b, b, 1.0, x.p, x.ld, c.rinv.data(), c.rinv.ld, 0.0, y.data(), y.ld);
+            copy(ctx, x, y.view());
             steps.push_back(std::move(c));
         }
     }
@@ -551,7 +595,9 @@ BlwsResult blws_svd(LinearOperator& w, const DWarm& warm, Index k, Index r, Rng&
     const Index want = std::min(r, d);
     DBuf<double> vals(ctx, static_cast<size_t>(want));
     DMat vecs(ctx, d, want, false);
+    ctx.region_begin(1);
     sym_evd_top(ctx, t.view(), want, vals.get(), vecs.view());
+    ctx.region_end(1, 0.0, 0.0);
     std::vector<double> hv(static_cast<size_t>(want));
     ctx.read(vals.get(), hv.data(), want);
     for (double v : hv)

@@ -34,6 +34,9 @@ void gather_columns(Context& ctx, View dst, View src, const int* idx);
 /// status[0] = 0 on success, j+1 if pivot j was not positive or not finite.
 /// min_diag/max_diag of R written to status-adjacent doubles diag[0..1].
 void potrf_upper(Context& ctx, View g, int* status, double* diag);
+/// Fused blocked Cholesky + inverse: G <- R (upper, zero lower), rinv <- R^{-1};
+/// status / diag as potrf_upper.
+void chol_inv_upper(Context& ctx, View g, View rinv, int* status, double* diag);
 /// R^{-1} of an upper-triangular n x n R (out may not alias r).
 void trtri_upper(Context& ctx, View out, View r);
 /// C = A * B for upper-triangular n x n A, B (C upper triangular).

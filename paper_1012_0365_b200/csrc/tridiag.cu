@@ -25,14 +25,29 @@ namespace {
 // cluster the loss of orthogonality is <= eps ||T|| / gap <= 2e-11).
 constexpr double kClusterTol = 1e-5;
 
+// Number of eigenvalues < x: sign changes of the Sturm sequence
+// p_i = det(T_i - x I), p_i = (d_i - x) p_{i-1} - e_{i-1}^2 p_{i-2}
+// (division-free: two dependent FMAs per step instead of a division), with
+// exact power-of-two rescaling against over/underflow. A zero p_i takes the
+// sign opposite to p_{i-1} (dstebz's pivmin convention in the ratio form).
 __device__ __forceinline__ int sturm_count(const double* d, const double* e2, int n, double x, double pivmin) {
-    double q = d[0] - x;
-    if (fabs(q) <= pivmin) q = -pivmin;
-    int cnt = q < 0.0;
+    double p0 = 1.0, p1 = d[0] - x;
+    if (p1 == 0.0) p1 = -pivmin;
+    int cnt = p1 < 0.0;
     for (int i = 1; i < n; ++i) {
-        q = d[i] - x - e2[i - 1] / q;
-        if (fabs(q) <= pivmin) q = -pivmin;
-        cnt += q < 0.0;
+        double p2 = fma(d[i] - x, p1, -e2[i - 1] * p0);
+        if (p2 == 0.0) p2 = p1 > 0.0 ? -pivmin * fabs(p1) : pivmin * fabs(p1);
+        cnt += (p2 < 0.0) != (p1 < 0.0);
+        const double a = fabs(p2);
+        if (a > 0x1p+600) {
+            p1 *= 0x1p-600;
+            p2 *= 0x1p-600;
+        } else if (a < 0x1p-600) {
+            p1 *= 0x1p+600;
+            p2 *= 0x1p+600;
+        }
+        p0 = p1;
+        p1 = p2;
     }
     return cnt;
 }
@@ -62,7 +77,10 @@ __global__ void bisect_k(const double* __restrict__ d, const double* __restrict_
                 hi = xh;
             }
         }
-        if (lane == 0) values[j] = 0.5 * (lo + hi);
+        if (lane == 0) {
+            const double lam = 0.5 * (lo + hi);
+            values[j] = fabs(lam) <= 4.0 * pivmin ? 0.0 : lam;
+        }
     }
 }
 
@@ -130,17 +148,23 @@ __global__ void inverse_iteration_k(const double* __restrict__ d, const double* 
                     }
                 }
                 u0[n - 1] = a;
-                for (int k = 0; k < n; ++k)
+                for (int k = 0; k < n; ++k) {
                     if (fabs(u0[k]) < eps3) u0[k] = u0[k] >= 0.0 ? eps3 : -eps3;
+                    y[k] = 1.0 / u0[k];  // reciprocal pivots (y is reused as rhs below)
+                }
+                for (int k = 0; k < n; ++k) u0[k] = y[k];
                 for (long i = 0; i < n; ++i) x[i] = hash_uniform(0x5eedull + static_cast<unsigned long long>(j), i);
             }
             __syncwarp();
-            for (int it = 0; it < 4; ++it) {
+            // dstein: iterate until the solution grows past sqrt(0.1 / n), then once more
+            const double dtpcrt = sqrt(0.1 / n);
+            int extra = 0;
+            for (int it = 0; it < 5; ++it) {
                 // scale rhs: ||x||_1 -> n * onenrm * max(eps, |u_nn|) as in dstein
                 double s1 = 0.0;
                 for (int i = lane; i < n; i += 32) s1 += fabs(x[i]);
                 for (int o = 16; o > 0; o >>= 1) s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-                const double scl = static_cast<double>(n) * onenrm * fmax(eps, fabs(u0[n - 1])) / fmax(s1, 1e-300);
+                const double scl = static_cast<double>(n) * onenrm * fmax(eps, fabs(1.0 / u0[n - 1])) / fmax(s1, 1e-300);
                 __syncwarp();
                 if (lane == 0) {
                     for (int i = 0; i < n; ++i) y[i] = x[i] * scl;
@@ -156,7 +180,7 @@ __global__ void inverse_iteration_k(const double* __restrict__ d, const double* 
                         double v = y[k];
                         if (k + 1 < n) v -= u1[k] * x[k + 1];
                         if (k + 2 < n) v -= u2[k] * x[k + 2];
-                        x[k] = v / u0[k];
+                        x[k] = v * u0[k];
                     }
                 }
                 __syncwarp();
@@ -194,6 +218,7 @@ __global__ void inverse_iteration_k(const double* __restrict__ d, const double* 
                 __syncwarp();
                 for (int i = lane; i < n; i += 32) x[i] *= inv;
                 __syncwarp();
+                if (amax >= dtpcrt && ++extra >= 2) break;
             }
         }
     }
@@ -216,6 +241,14 @@ void tridiag_eig_top(Context& ctx, Index n_, const double* d, const double* e, I
         gu = std::max(gu, hd[i] + el + er);
         onenrm = std::max(onenrm, std::fabs(hd[i]) + el + er);
         if (i < n - 1) emax2 = std::max(emax2, he[i] * he[i]);
+    }
+    if (onenrm == 0.0) {
+        // T == 0: eigenvalues exactly zero, eigenvectors the unit vectors (as Eigen returns)
+        BLWS_CUDA(cudaMemsetAsync(values, 0, sizeof(double) * want, ctx.stream()));
+        fill(ctx, vectors.left(want), 0.0);
+        std::vector<double> one(1, 1.0);
+        for (int j = 0; j < want; ++j) ctx.write(vectors.p + (n - 1 - j) + static_cast<long>(j) * vectors.ld, one.data(), 1);
+        return;
     }
     const double safmin = 2.2250738585072014e-308;
     const double pivmin = safmin * std::max(1.0, emax2);
