@@ -312,12 +312,13 @@ def block_lanczos_procedure(op: LinearOperator, x1, k: int):
     x1 = F(x1)
     b = x1.shape[1]
     q = np.empty((op.rows(), k * b), order="F")
-    t = np.zeros((k * b, k * b), order="F")
+    t = np.zeros((k * b) ** 2)
     built = i64(0)
     term = C.c_int(0)
     _check(lib().orc_block_lanczos(op._h, b, _ptr(x1), k, _ptr(q), _ptr(t), C.byref(built), C.byref(term)))
     nb = built.value * b
-    return q[:, :nb].copy(order="F"), t[:nb, :nb].copy(order="F"), built.value, bool(term.value)
+    tt = t[: nb * nb].reshape((nb, nb), order="F")
+    return q[:, :nb].copy(order="F"), tt.copy(order="F"), built.value, bool(term.value)
 
 
 def bl_evd(op: LinearOperator, x1, k: int, r: int):

@@ -1,0 +1,217 @@
+"""Pins the CPU oracle against the reference's own known answers and
+property tests (CPU only; no GPU).
+
+Restates /root/reference/proj/tests/test_dense_core.cpp and
+tests/oracles.hpp (the independent cyclic-Jacobi oracle) plus the C++
+standard's mt19937_64 known answer that makes core/rng.hpp bit-portable.
+"""
+import numpy as np
+import pytest
+
+
+def jacobi_evd(a):
+    """tests/oracles.hpp:28-78: cyclic Jacobi, sweeps until off <= 1e-15 ||A||."""
+    a = np.array(a, dtype=float)
+    n = a.shape[0]
+    v = np.eye(n)
+    scale = max(np.linalg.norm(a), 1e-300)
+    for _ in range(100):
+        off = np.sum(np.triu(a, 1) ** 2)
+        if np.sqrt(2 * off) <= 1e-15 * scale:
+            break
+        for p in range(n):
+            for q in range(p + 1, n):
+                if abs(a[p, q]) <= 1e-300:
+                    continue
+                theta = (a[q, q] - a[p, p]) / (2 * a[p, q])
+                t = (1.0 if theta >= 0 else -1.0) / (abs(theta) + np.sqrt(theta * theta + 1.0))
+                c = 1.0 / np.sqrt(t * t + 1.0)
+                s = t * c
+                ap, aq = a[:, p].copy(), a[:, q].copy()
+                a[:, p], a[:, q] = c * ap - s * aq, s * ap + c * aq
+                ap, aq = a[p, :].copy(), a[q, :].copy()
+                a[p, :], a[q, :] = c * ap - s * aq, s * ap + c * aq
+                vp, vq = v[:, p].copy(), v[:, q].copy()
+                v[:, p], v[:, q] = c * vp - s * vq, s * vp + c * vq
+    order = np.argsort(-np.diag(a), kind="stable")
+    return np.diag(a)[order], v[:, order]
+
+
+def random_symmetric(n, rng):
+    g = rng.gaussian_matrix(n, n)
+    return 0.5 * (g + g.T)
+
+
+def test_mt19937_64_known_answer(O):
+    r = O.Rng(5489)
+    for _ in range(9999):
+        r.next_u64()
+    assert r.next_u64() == 9981545732273789042
+
+
+def test_rng_streams(O):
+    a, b = O.Rng(7), O.Rng(7)
+    assert [a.next_u64() for _ in range(5)] == [b.next_u64() for _ in range(5)]
+    s1, s2 = O.Rng(7).split(1), O.Rng(7).split(2)
+    assert s1.next_u64() != s2.next_u64()
+    u = O.Rng(3)
+    xs = [u.uniform() for _ in range(1000)]
+    assert min(xs) >= 0.0 and max(xs) < 1.0
+    assert all(0 <= O.Rng(5).uniform_index(7) < 7 for _ in range(10))
+    g = O.Rng(11).gaussian_matrix(200, 50)
+    assert abs(g.mean()) < 0.02 and abs(g.std() - 1) < 0.02
+    v = O.Rng(2).unit_vector(33)
+    assert abs(np.linalg.norm(v) - 1) <= 1e-15
+
+
+def test_thin_qr_reproduces_orthonormal(O):
+    # test_dense_core.cpp:37-45
+    m = O.thin_qr(O.Rng(11).gaussian_matrix(12, 4)).q
+    qr = O.thin_qr(m)
+    assert np.linalg.norm(qr.q - m) <= 1e-12
+    assert np.linalg.norm(qr.r - np.eye(4)) <= 1e-12
+    assert qr.rank == 4
+
+
+def test_thin_qr_single_column(O):
+    # test_dense_core.cpp:47-54
+    qr = O.thin_qr(np.array([[3.0], [4.0]]))
+    assert abs(qr.q[0, 0] - 0.6) <= 1e-14 and abs(qr.q[1, 0] - 0.8) <= 1e-14
+    assert abs(qr.r[0, 0] - 5.0) <= 1e-14
+
+
+@pytest.mark.parametrize("m,b", [(5, 1), (20, 4), (50, 10), (200, 30)])
+def test_thin_qr_recomposition(O, m, b):
+    # test_dense_core.cpp:56-66 (one Rng(17) stream across the sizes in the reference)
+    a = O.Rng(17 + m).gaussian_matrix(m, b)
+    qr = O.thin_qr(a)
+    assert np.linalg.norm(a - qr.q @ qr.r) <= 1e-12 * np.linalg.norm(a)
+    assert np.linalg.norm(qr.q.T @ qr.q - np.eye(b)) <= 1e-12
+    assert np.all(np.diag(qr.r) >= 0) and qr.rank == b
+
+
+def test_thin_qr_rank_and_validation(O):
+    # test_dense_core.cpp:68-83
+    col = O.Rng(3).gaussian_vector(10)
+    assert O.thin_qr(np.stack([col, 2 * col], axis=1)).rank == 1
+    with pytest.raises(ValueError):
+        O.thin_qr(np.zeros((0, 0)))
+    with pytest.raises(ValueError):
+        O.thin_qr(np.zeros((2, 5)))
+    with pytest.raises(ValueError):
+        O.thin_qr(np.array([[1.0], [np.nan]]))
+
+
+def test_sym_evd_small_known_answers(O):
+    # test_dense_core.cpp:85-107
+    vals, vecs = O.sym_evd_small(np.diag([3.0, 1.0, 2.0]))
+    assert np.allclose(vals, [3, 2, 1])
+    assert np.allclose(np.abs(vecs).max(axis=0), 1.0, atol=1e-12)
+    vals, vecs = O.sym_evd_small(np.array([[0.0, 1.0], [1.0, 0.0]]))
+    assert abs(vals[0] - 1) <= 1e-14 and abs(vals[1] + 1) <= 1e-14
+    assert abs(abs(vecs[0, 0] * vecs[1, 0]) - 0.5) <= 1e-12
+    assert abs(vecs[0, 1] * vecs[1, 1] + 0.5) <= 1e-12
+
+
+def test_sym_evd_small_vs_jacobi_oracle(O):
+    # test_dense_core.cpp:109-121
+    rng = O.Rng(23)
+    for _ in range(5):
+        t = random_symmetric(12, rng)
+        vals, vecs = O.sym_evd_small(t)
+        ref, _ = jacobi_evd(t)
+        tn = np.linalg.norm(t)
+        assert np.abs(vals - ref).max() <= 1e-9 * tn
+        assert np.linalg.norm(t @ vecs - vecs * vals) <= 1e-10 * tn
+        assert np.linalg.norm(vecs.T @ vecs - np.eye(12)) <= 1e-10
+
+
+def test_sym_evd_small_validation(O):
+    # test_dense_core.cpp:123-131
+    with pytest.raises(ValueError):
+        O.sym_evd_small(np.ones((3, 4)))
+    with pytest.raises(ValueError):
+        O.sym_evd_small(np.array([[0.0, 1.0], [5.0, 0.0]]))
+    with pytest.raises(ValueError):
+        O.sym_evd_small(np.array([[np.inf, 0.0], [0.0, 0.0]]))
+
+
+def test_full_svd_small(O):
+    # test_dense_core.cpp:133-152
+    u, s, v = O.full_svd_small(np.diag([2.0, 5.0]))
+    assert abs(s[0] - 5) <= 1e-14 and abs(s[1] - 2) <= 1e-14
+    assert np.abs(O.full_svd_small(np.zeros((4, 3)))[1]).max() == 0.0
+    m = O.Rng(29).gaussian_matrix(10, 7)
+    u, s, v = O.full_svd_small(m)
+    gv, _ = O.sym_evd_small(m.T @ m)
+    assert np.allclose(s, np.sqrt(np.maximum(gv, 0)), rtol=1e-8)
+    assert np.linalg.norm(m - (u * s) @ v.T) <= 1e-10 * np.linalg.norm(m)
+
+
+def test_augmented_spectrum_identity(O):
+    # test_dense_core.cpp:154-192 (100 random rectangular matrices)
+    rng = O.Rng(31)
+    for _ in range(100):
+        m = 2 + rng.uniform_index(8)
+        n = 2 + rng.uniform_index(8)
+        w = rng.gaussian_matrix(m, n)
+        s = O.full_svd_small(w)[1]
+        aug = np.zeros((m + n, m + n))
+        aug[:m, m:] = w
+        aug[m:, :m] = w.T
+        vals, _ = O.sym_evd_small(aug)
+        exp = np.zeros(m + n)
+        p = min(m, n)
+        exp[:p] = s
+        exp[m + n - p:] = -s[::-1]
+        exp = np.sort(exp)[::-1]
+        assert np.abs(vals - exp).max() <= 1e-10 * max(1.0, s[0])
+
+
+def test_application_counters(O):
+    # test_dense_core.cpp:194-214
+    rng = O.Rng(37)
+    op = O.DenseOperator(rng.gaussian_matrix(6, 4))
+    assert op.application_count() == 0
+    op.apply_block(rng.gaussian_matrix(4, 3))
+    assert op.application_count() == 3
+    op.apply_pair_block(rng.gaussian_matrix(6, 1), rng.gaussian_matrix(4, 1))
+    assert op.application_count() == 4
+    aug = O.AugmentedOperator(op)
+    aug.apply_block(rng.gaussian_matrix(10, 5))
+    assert op.application_count() == 9  # exactly one paired W apply per augmented column
+    assert aug.application_count() == 5
+
+
+def test_adjoint_consistency(O):
+    # test_dense_core.cpp:216-234
+    rng = O.Rng(41)
+    wd = rng.gaussian_matrix(9, 5)
+    for op in (O.DenseOperator(wd), O.AugmentedOperator(O.DenseOperator(wd))):
+        x = rng.gaussian_matrix(op.cols(), 1)
+        y = rng.gaussian_matrix(op.rows(), 1)
+        lhs = float((op.apply_block(x).T @ y)[0, 0])
+        # adjoint via the transposed product (dense / augmented operators are self-dual here)
+        if isinstance(op, O.DenseOperator):
+            rhs = float((x.T @ (wd.T @ y))[0, 0])
+        else:
+            rhs = float((x.T @ op.apply_block(y))[0, 0])
+        assert abs(lhs - rhs) <= 1e-12 * (abs(lhs) + abs(rhs) + 1e-300)
+
+
+def test_sparse_operator(O):
+    # CSC SpMM vs dense, assign_values validation (test_dense_core.cpp:236-254)
+    rng = np.random.default_rng(0)
+    d = rng.standard_normal((9, 5)) * (rng.random((9, 5)) < 0.5)
+    colptr = np.concatenate([[0], np.cumsum((d != 0).sum(axis=0))])
+    rows = np.concatenate([np.nonzero(d[:, j])[0] for j in range(5)]).astype(np.int32)
+    vals = np.concatenate([d[np.nonzero(d[:, j])[0], j] for j in range(5)])
+    op = O.SparseOperator(9, 5, colptr, rows, vals)
+    x = rng.standard_normal((5, 3))
+    assert np.allclose(op.apply_block(x), d @ x, atol=1e-13)
+    top, bot = op.apply_pair_block(rng.standard_normal((9, 2)), x[:, :2])
+    assert np.allclose(top, d @ x[:, :2], atol=1e-13)
+    with pytest.raises(ValueError):
+        op.assign_values(np.zeros(len(vals) - 1))
+    with pytest.raises(ValueError):
+        O.DenseOperator(np.array([[0.0, np.nan]]))
