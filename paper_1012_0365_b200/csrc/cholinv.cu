@@ -19,7 +19,22 @@ namespace blws {
 __device__ double g_chol_probe[4];  // phase cycle counts of the last chol_inv call (profiling)
 namespace {
 
-constexpr int kCT = 1024;
+/// a[idx] for a runtime idx in [0, 32) as a 5-level select tree (depth 5
+/// instead of a 32-long dependent select chain).
+__device__ __forceinline__ double pick32(const double (&a)[32], int idx) {
+    double v16[16], v8[8], v4[4], v2[2];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v16[j] = (idx & 16) ? a[j + 16] : a[j];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v8[j] = (idx & 8) ? v16[j + 8] : v16[j];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) v4[j] = (idx & 4) ? v8[j + 4] : v8[j];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) v2[j] = (idx & 2) ? v4[j + 2] : v4[j];
+    return (idx & 1) ? v2[1] : v2[0];
+}
+
+constexpr int kCT = 1024;  // one thread per element of a 32x32 diagonal block
 constexpr long kSmemBudget = 216 * 1024;
 
 template <bool SH>
@@ -32,6 +47,7 @@ __global__ void __launch_bounds__(kCT) chol_inv_k(double* g, long ldg, double* r
     double* X = A + static_cast<long>(ld) * n;
     double* rowj = X + static_cast<long>(ld) * n;  // n
     double* dinv = rowj + n;                         // n
+    double* rowbuf = dinv + n;                       // 32 row entries + 2 pivot slots
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     if (threadIdx.x == 0) fail = 0;
     long long t0 = clock64();
@@ -44,34 +60,42 @@ __global__ void __launch_bounds__(kCT) chol_inv_k(double* g, long ldg, double* r
     // order. Per column: the pivot owner publishes R(k,k); row-k owners publish
     // R(k, j); every owner updates its (i, j) with k < i <= j.
     // ---- blocked right-looking Cholesky (32-wide panels)
+    long long td = 0, tp = 0, tsy = 0;
     for (int kb = 0; kb < n && !fail; kb += 32) {
         const int nb = min(32, n - kb);
-        if (wid == 0) {
-            // diagonal block by one warp: lane = row i; per pivot k the column loop
-            // over j has independent iterations (pipelined LDS/FMA/STS)
-            const int i = kb + lane;
+        long long c0 = clock64();
+        {
+            // diagonal block: thread t owns element (i, j) = (t % 32, t / 32) of the
+            // 32x32 block in a register (all 1024 threads); two barriers per pivot
+            const int ti = threadIdx.x & 31, tj = threadIdx.x >> 5;
+            const bool own = ti < nb && tj < nb && ti <= tj;
+            double a = own ? A[(kb + ti) + (kb + tj) * ld] : 0.0;
+            if (ti == 0 && tj == 0) rowbuf[32] = a;  // pivot 0
+            __syncthreads();
             for (int k = 0; k < nb; ++k) {
-                const int gk = kb + k;
-                const double piv = A[gk + gk * ld];
+                const double piv = rowbuf[32 + (k & 1)];
                 const bool bad = !(piv > 0.0) || !isfinite(piv);
                 const double rs = bad ? 1.0 : rsqrt(piv);
-                if (lane == 0) {
-                    if (bad && fail == 0) fail = gk + 1;
-                    A[gk + gk * ld] = piv * rs;
-                    dinv[gk] = rs;
+                if (own && ti == k) {
+                    a = (tj == k) ? piv * rs : a * rs;
+                    rowbuf[tj] = a;
                 }
-                // scale row k (columns j = lane > k)
-                if (lane > k && lane < nb) A[gk + i * ld] *= rs;
-                __syncwarp();
-                const double rki = (lane > k && lane < nb) ? A[gk + i * ld] : 0.0;  // R(k, i)
-                for (int j = k + 1; j < nb; ++j) {
-                    const double rkj = A[gk + (kb + j) * ld];
-                    if (lane > k && lane <= j) A[i + (kb + j) * ld] -= rki * rkj;
+                if (threadIdx.x == 0) {
+                    dinv[kb + k] = rs;
+                    if (bad && fail == 0) fail = kb + k + 1;
                 }
-                __syncwarp();
+                __syncthreads();
+                if (own && ti > k) {
+                    a = fma(-rowbuf[ti], rowbuf[tj], a);
+                    if (ti == k + 1 && tj == k + 1) rowbuf[32 + ((k + 1) & 1)] = a;
+                }
+                __syncthreads();
             }
+            if (ti < nb && tj < nb) A[(kb + ti) + (kb + tj) * ld] = own ? a : 0.0;
         }
         __syncthreads();
+        long long c1 = clock64();
+        td += c1 - c0;
         if (fail) break;
         const int rest = n - kb - nb;
         if (rest <= 0) break;
@@ -86,6 +110,8 @@ __global__ void __launch_bounds__(kCT) chol_inv_k(double* g, long ldg, double* r
             if (lane < nb) A[kb + lane + j * ld] = x;
         }
         __syncthreads();
+        long long c2 = clock64();
+        tp += c2 - c1;
         // trailing SYRK (upper): A22 -= R12^T R12, warp per column, lanes over rows
         for (int j = kb + nb + wid; j < n; j += nw) {
             const double* cj = A + kb + j * ld;
@@ -104,6 +130,7 @@ __global__ void __launch_bounds__(kCT) chol_inv_k(double* g, long ldg, double* r
             }
         }
         __syncthreads();
+        tsy += clock64() - c2;
     }
     long long t2 = clock64();
     if (threadIdx.x == 0) status[0] = fail;
@@ -114,12 +141,13 @@ __global__ void __launch_bounds__(kCT) chol_inv_k(double* g, long ldg, double* r
         X[i + j * ld] = i == j ? dinv[i] : 0.0;
     }
     __syncthreads();
-    for (int k = 1; k < n; k *= 2) {
+    for (int lk = 0; (1 << lk) < n; ++lk) {
+        const int k = 1 << lk;  // power of two: index math by shifts / masks
         const int pairs = (n + 2 * k - 1) / (2 * k);
         const int total = pairs * k * k;
         // phase 1: T = B XC into X's upper-right block (B = R[o:o+k, o+k:o+2k])
         for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
-            const int p = idx / (k * k), rr = idx % k, cc = (idx / k) % k;
+            const int p = idx >> (2 * lk), rr = idx & (k - 1), cc = (idx >> lk) & (k - 1);
             const int o = p * 2 * k, r = o + rr, c = o + k + cc;
             if (c >= n) continue;
             double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
@@ -142,7 +170,7 @@ __global__ void __launch_bounds__(kCT) chol_inv_k(double* g, long ldg, double* r
                 const int idx = base + q * kCT + threadIdx.x;
                 out[q] = 0.0;
                 if (idx >= total) continue;
-                const int p = idx / (k * k), rr = idx % k, cc = (idx / k) % k;
+                const int p = idx >> (2 * lk), rr = idx & (k - 1), cc = (idx >> lk) & (k - 1);
                 const int o = p * 2 * k, r = o + rr, c = o + k + cc;
                 if (c >= n) continue;
                 double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
@@ -161,7 +189,7 @@ __global__ void __launch_bounds__(kCT) chol_inv_k(double* g, long ldg, double* r
             for (int q = 0; q < 4; ++q) {
                 const int idx = base + q * kCT + threadIdx.x;
                 if (idx >= total) continue;
-                const int p = idx / (k * k), rr = idx % k, cc = (idx / k) % k;
+                const int p = idx >> (2 * lk), rr = idx & (k - 1), cc = (idx >> lk) & (k - 1);
                 const int o = p * 2 * k, r = o + rr, c = o + k + cc;
                 if (c < n) X[r + c * ld] = out[q];
             }
@@ -198,10 +226,11 @@ __global__ void __launch_bounds__(kCT) chol_inv_k(double* g, long ldg, double* r
         }
         diag[0] = mn;
         diag[1] = mx;
-        g_chol_probe[0] = static_cast<double>(t1 - t0);
+        g_chol_probe[0] = static_cast<double>(td) + 1e-6 * static_cast<double>(tp);  // diag . panel(1e6 scale)
+        g_chol_probe[4 % 4] = static_cast<double>(td);
         g_chol_probe[1] = static_cast<double>(t2 - t1);
         g_chol_probe[2] = static_cast<double>(t3 - t2);
-        g_chol_probe[3] = static_cast<double>(clock64() - t3);
+        g_chol_probe[3] = static_cast<double>(tp) * 1e6 + static_cast<double>(tsy);
     }
 }
 
@@ -210,7 +239,7 @@ __global__ void __launch_bounds__(kCT) chol_inv_k(double* g, long ldg, double* r
 void chol_inv_upper(Context& ctx, View g, View rinv, int* status, double* diag) {
     const int n = static_cast<int>(g.rows);
     const long ld = n | 1;
-    const long bytes = (2L * ld * n + 2L * n) * 8;
+    const long bytes = (2L * ld * n + 2L * n + 34) * 8;
     const bool on_chip = bytes <= kSmemBudget;
     static bool cfg = false;
     if (!cfg) {
@@ -220,7 +249,7 @@ void chol_inv_upper(Context& ctx, View g, View rinv, int* status, double* diag) 
     if (on_chip) {
         chol_inv_k<true><<<1, kCT, bytes, ctx.stream()>>>(g.p, g.ld, rinv.p, rinv.ld, n, nullptr, status, diag);
     } else {
-        DBuf<double> scratch(ctx, static_cast<size_t>(2L * ld * n + 2L * n));
+        DBuf<double> scratch(ctx, static_cast<size_t>(2L * ld * n + 2L * n + 34));
         chol_inv_k<false><<<1, kCT, 0, ctx.stream()>>>(g.p, g.ld, rinv.p, rinv.ld, n, scratch.get(), status, diag);
     }
     ctx.note_launch();

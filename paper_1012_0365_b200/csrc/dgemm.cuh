@@ -172,3 +172,118 @@ __device__ __forceinline__ void mainloop(double (&acc)[4][4][2], double* smem, c
 
 }  // namespace gemm_detail
 }  // namespace blws
+
+namespace blws {
+namespace gemm_ts {
+// Tall-skinny output variant: the CTA covers all BN (<= 128) output columns;
+// the 4 warps split BM = 64 rows (16 each), so a warp issues 2 x BN/8 DMMAs per
+// k-step from 2 A and BN/8 B fragments. Used for W*X, W^T*X, X*S with b <= 128
+// (and in 4 column tiles of 104 for b ~ 405). Requires 16-byte aligned operands.
+using gemm_detail::cp_async16;
+using gemm_detail::cp_commit;
+using gemm_detail::cp_wait;
+using gemm_detail::dmma;
+
+constexpr int BM = 64, BK = 16, STAGES = 4, THREADS = 128;
+
+template <bool TA>
+struct AL {
+    static constexpr int LD = TA ? BK + 4 : BM + 4;
+    static constexpr int SIZE = TA ? BM * (BK + 4) : BK * (BM + 4);
+};
+template <int BN>
+struct BL {  // op(B) = B (k contiguous): [BN][BK+4]
+    static constexpr int LD = BK + 4;
+    static constexpr int SIZE = BN * (BK + 4);
+};
+template <bool TA, int BN>
+constexpr int smem_bytes() {
+    return STAGES * (AL<TA>::SIZE + BL<BN>::SIZE) * 8;
+}
+
+template <bool TA, int BN>
+__device__ __forceinline__ void load_tile(double* As, double* Bs, const double* __restrict__ A, long lda,
+                                          const double* __restrict__ B, long ldb, long M, long N, long m0, long n0,
+                                          long k0, long kend) {
+    const int tid = threadIdx.x;
+    if (!TA) {
+        constexpr int CPR = BM / 2;
+        for (int c = tid; c < CPR * BK; c += THREADS) {
+            const int k = c / CPR, i = (c % CPR) * 2;
+            const long gi = m0 + i, gk = k0 + k;
+            int nv = 0;
+            if (gk < kend) nv = static_cast<int>(max(0L, min(2L, M - gi)));
+            cp_async16(As + k * AL<TA>::LD + i, nv ? A + gi + gk * lda : A, nv * 8);
+        }
+    } else {
+        constexpr int CPR = BK / 2;
+        for (int c = tid; c < CPR * BM; c += THREADS) {
+            const int i = c / CPR, k = (c % CPR) * 2;
+            const long gi = m0 + i, gk = k0 + k;
+            int nv = 0;
+            if (gi < M) nv = static_cast<int>(max(0L, min(2L, kend - gk)));
+            cp_async16(As + i * AL<TA>::LD + k, nv ? A + gk + gi * lda : A, nv * 8);
+        }
+    }
+    constexpr int CPR = BK / 2;
+    for (int c = tid; c < CPR * BN; c += THREADS) {
+        const int j = c / CPR, k = (c % CPR) * 2;
+        const long gj = n0 + j, gk = k0 + k;
+        int nv = 0;
+        if (gj < N) nv = static_cast<int>(max(0L, min(2L, kend - gk)));
+        cp_async16(Bs + j * BL<BN>::LD + k, nv ? B + gk + gj * ldb : B, nv * 8);
+    }
+}
+
+/// acc[mi][ni][e] += op(A)(m0 + 16w + 8mi + g, k) * B(k, n0 + 8ni + 2t + e)
+template <bool TA, int BN>
+__device__ __forceinline__ void mainloop(double (&acc)[2][BN / 8][2], double* smem, const double* __restrict__ A,
+                                         long lda, const double* __restrict__ B, long ldb, long M, long N, long m0,
+                                         long n0, long kbeg, long kend) {
+    double* As = smem;
+    double* Bs = smem + STAGES * AL<TA>::SIZE;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane >> 2, t = lane & 3;
+    const int wm = warp * 16;
+    const long ntiles = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+        if (s < ntiles)
+            load_tile<TA, BN>(As + s * AL<TA>::SIZE, Bs + s * BL<BN>::SIZE, A, lda, B, ldb, M, N, m0, n0,
+                              kbeg + s * BK, kend);
+        cp_commit();
+    }
+    for (long kt = 0; kt < ntiles; ++kt) {
+        cp_wait<STAGES - 2>();
+        __syncthreads();
+        const long pf = kt + STAGES - 1;
+        if (pf < ntiles) {
+            const int ps = static_cast<int>(pf % STAGES);
+            load_tile<TA, BN>(As + ps * AL<TA>::SIZE, Bs + ps * BL<BN>::SIZE, A, lda, B, ldb, M, N, m0, n0,
+                              kbeg + pf * BK, kend);
+        }
+        cp_commit();
+        const int st = static_cast<int>(kt % STAGES);
+        const double* as = As + st * AL<TA>::SIZE;
+        const double* bs = Bs + st * BL<BN>::SIZE;
+#pragma unroll
+        for (int kk = 0; kk < BK; kk += 4) {
+            double af[2];
+#pragma unroll
+            for (int mi = 0; mi < 2; ++mi) {
+                const int row = wm + mi * 8 + g;
+                af[mi] = TA ? as[row * AL<TA>::LD + kk + t] : as[(kk + t) * AL<TA>::LD + row];
+            }
+#pragma unroll
+            for (int ni = 0; ni < BN / 8; ++ni) {
+                const double bf = bs[(ni * 8 + g) * BL<BN>::LD + kk + t];
+                dmma(acc[0][ni], af[0], bf);
+                dmma(acc[1][ni], af[1], bf);
+            }
+        }
+    }
+    cp_wait<0>();
+}
+
+}  // namespace gemm_ts
+}  // namespace blws

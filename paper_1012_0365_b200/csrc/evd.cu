@@ -121,12 +121,12 @@ __global__ void __launch_bounds__(kThreads) sytrd_k(const double* __restrict__ t
                     const double vj = v[j];
 #pragma unroll
                     for (int q = 0; q < kMaxRowsPerLane; ++q) {
+                        // branch-free: out-of-range rows read a clamped address and are masked
                         const int i = lane + 32 * q;
-                        if (i >= j && i < w) {
-                            const double lij = col[i];
-                            acc[q] = fma(lij, vj, acc[q]);
-                            if (i > j) dp[c] = fma(lij, vr[q], dp[c]);
-                        }
+                        const bool in = i >= j && i < w;
+                        const double lij = in ? col[in ? i : j] : 0.0;
+                        acc[q] = fma(lij, vj, acc[q]);
+                        dp[c] = fma(i > j ? lij : 0.0, vr[q], dp[c]);
                     }
                 }
             }
@@ -186,7 +186,12 @@ __global__ void __launch_bounds__(kThreads) sytrd_k(const double* __restrict__ t
 #pragma unroll
                 for (int q = 0; q < kMaxRowsPerLane; ++q) {
                     const int i = lane + 32 * q;
-                    if (i >= j && i < w) col[i] -= fma(vr[q], wj, wr[q] * vj);
+                    if (32 * q + 31 < j || 32 * q >= w) continue;  // warp-uniform skip
+                    const bool in = i >= j && i < w;
+                    const int ii = in ? i : j;
+                    const double upd = fma(vr[q], wj, wr[q] * vj);
+                    const double cur = col[ii];
+                    if (in) col[ii] = cur - upd;
                 }
             }
         } else {

@@ -99,6 +99,114 @@ void dispatch(Context& ctx, bool ta, bool tb, dim3 grid, const double* A, long l
     else launch<true, true, VEC>(ctx, grid, A, lda, B, ldb, C, ldc, M, N, K, kchunk, alpha, beta, ws);
 }
 
+template <bool TA, int BN>
+__global__ void __launch_bounds__(gemm_ts::THREADS) dgemm_ts_kernel(const double* __restrict__ A, long lda,
+                                                                    const double* __restrict__ B, long ldb, double* C,
+                                                                    long ldc, long M, long N, long K, long kchunk,
+                                                                    double alpha, double beta, double* ws) {
+    extern __shared__ __align__(16) double smem[];
+    const long m0 = static_cast<long>(blockIdx.x) * gemm_ts::BM, n0 = static_cast<long>(blockIdx.y) * BN;
+    const long kbeg = static_cast<long>(blockIdx.z) * kchunk;
+    const long kend = min(K, kbeg + kchunk);
+    double acc[2][BN / 8][2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < BN / 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    gemm_ts::mainloop<TA, BN>(acc, smem, A, lda, B, ldb, M, N, m0, n0, kbeg, kend);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane >> 2, t = lane & 3;
+    double* P = ws ? ws + static_cast<long>(blockIdx.z) * M * N : nullptr;
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi) {
+        const long row = m0 + warp * 16 + mi * 8 + g;
+        if (row >= M) continue;
+#pragma unroll
+        for (int ni = 0; ni < BN / 8; ++ni)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const long col = n0 + ni * 8 + 2 * t + e;
+                if (col >= N) continue;
+                const double v = acc[mi][ni][e];
+                if (P) {
+                    P[row + col * M] = v;
+                } else {
+                    double* c = C + row + col * ldc;
+                    *c = beta == 0.0 ? alpha * v : alpha * v + beta * *c;
+                }
+            }
+    }
+}
+
+template <bool TA, int BN>
+int ts_occupancy(int dev) {
+    static int occ[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (!occ[dev & 7]) {
+        constexpr int bytes = gemm_ts::smem_bytes<TA, BN>();
+        BLWS_CUDA(cudaFuncSetAttribute(dgemm_ts_kernel<TA, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+        int o = 0;
+        BLWS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, dgemm_ts_kernel<TA, BN>, gemm_ts::THREADS, bytes));
+        occ[dev & 7] = std::max(o, 1);
+    }
+    return occ[dev & 7];
+}
+
+template <bool TA, int BN>
+void launch_ts(Context& ctx, const double* A, long lda, const double* B, long ldb, double* C, long ldc, long M,
+               long N, long K, double alpha, double beta) {
+    const int occ = ts_occupancy<TA, BN>(ctx.device());
+    const long mt = ceil_div(M, gemm_ts::BM), nt = ceil_div(N, BN);
+    const long ktiles = ceil_div(K, gemm_ts::BK);
+    const long slots = static_cast<long>(ctx.sm_count()) * occ;
+    // split-K so the CTA count fills whole waves (each split >= 8 k-tiles)
+    long S = 1;
+    const long tiles = mt * nt;
+    if (tiles < 2 * slots) {
+        const long smax = std::max<long>(1, std::min<long>(64, ktiles / 8));
+        double best = 1e30;
+        for (long s = 1; s <= smax; ++s) {
+            const long ctas = tiles * s;
+            const long waves = ceil_div(ctas, slots);
+            // time ~ waves * (work per CTA) ~ waves / s ; prefer full waves
+            const double cost = static_cast<double>(waves) / s + (s > 1 ? 0.02 : 0.0);
+            if (cost < best - 1e-12) {
+                best = cost;
+                S = s;
+            }
+        }
+    }
+    const long kchunk = ceil_div(ktiles, S) * gemm_ts::BK;
+    S = ceil_div(K, kchunk);
+    DBuf<double> ws;
+    if (S > 1) ws = DBuf<double>(ctx, static_cast<size_t>(S * M * N));
+    constexpr int bytes = gemm_ts::smem_bytes<TA, BN>();
+    dim3 grid(static_cast<unsigned>(mt), static_cast<unsigned>(nt), static_cast<unsigned>(S));
+    dgemm_ts_kernel<TA, BN><<<grid, gemm_ts::THREADS, bytes, ctx.stream()>>>(A, lda, B, ldb, C, ldc, M, N, K, kchunk,
+                                                                             alpha, beta, S > 1 ? ws.get() : nullptr);
+    ctx.note_launch();
+    ctx.check_launch("dgemm_ts_kernel");
+    if (S > 1) {
+        const long total = M * N;
+        splitk_reduce<<<static_cast<unsigned>(std::min<long>(2048, (total + 255) / 256)), 256, 0, ctx.stream()>>>(
+            ws.get(), M, N, static_cast<int>(S), alpha, beta, C, ldc);
+        ctx.note_launch();
+        ctx.check_launch("splitk_reduce");
+    }
+}
+
+template <bool TA>
+bool try_ts(Context& ctx, const double* A, long lda, const double* B, long ldb, double* C, long ldc, long M, long N,
+            long K, double alpha, double beta) {
+    // column tile: smallest of {32, 64, 104, 128} covering ceil(N / ntiles)
+    const long ntiles = ceil_div(N, 128);
+    const long per = ceil_div(N, ntiles);
+    if (per <= 32) launch_ts<TA, 32>(ctx, A, lda, B, ldb, C, ldc, M, N, K, alpha, beta);
+    else if (per <= 64) launch_ts<TA, 64>(ctx, A, lda, B, ldb, C, ldc, M, N, K, alpha, beta);
+    else if (per <= 104) launch_ts<TA, 104>(ctx, A, lda, B, ldb, C, ldc, M, N, K, alpha, beta);
+    else launch_ts<TA, 128>(ctx, A, lda, B, ldb, C, ldc, M, N, K, alpha, beta);
+    return true;
+}
+
 }  // namespace
 
 void gemm(Context& ctx, bool ta, bool tb, Index M, Index N, Index K, double alpha, const double* A, Index lda,
@@ -110,6 +218,16 @@ void gemm(Context& ctx, bool ta, bool tb, Index M, Index N, Index K, double alph
             C, ldc, M, N, beta);
         ctx.note_launch();
         ctx.check_launch("scale_kernel");
+        return;
+    }
+    const bool aligned16 = (lda % 2 == 0) && (ldb % 2 == 0) && (reinterpret_cast<uintptr_t>(A) % 16 == 0) &&
+                           (reinterpret_cast<uintptr_t>(B) % 16 == 0);
+    // tall-skinny outputs (M >> N, the BLWS panels): one CTA spans all columns
+    if (aligned16 && !tb && M >= 256 && M >= 4 * N) {
+        if (ta)
+            try_ts<true>(ctx, A, lda, B, ldb, C, ldc, M, N, K, alpha, beta);
+        else
+            try_ts<false>(ctx, A, lda, B, ldb, C, ldc, M, N, K, alpha, beta);
         return;
     }
     const Index tiles = ceil_div(M, BM) * ceil_div(N, BN);

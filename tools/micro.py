@@ -11,8 +11,8 @@ ctx.fp64_peak(0)
 print("probe after load", ctx.probe(), flush=True)
 for n in (32, 64, 100, 111, 200):
     d = ctx.microbench(0, n, 0, 20, detail=True)
-    print(f"chol_inv n={n}: {d[0]:8.1f} us   phase cycles load {d[1]:.0f} chol {d[2]:.0f} inv {d[3]:.0f} store {d[4]:.0f}",
-          flush=True)
+    print(f"chol_inv n={n}: {d[0]:8.1f} us   diag {d[1]:.0f} chol {d[2]:.0f} inv {d[3]:.0f} "
+          f"panel {int(d[4] // 1e6)} syrk {d[4] % 1e6:.0f}", flush=True)
 for n in (60, 110, 200, 222):
     print(f"sym_evd_top n={n} (want n/2): {ctx.microbench(1, n, 0, 5):8.1f} us", flush=True)
 for rows, b in ((8000, 100), (4000, 100), (1000, 30)):
