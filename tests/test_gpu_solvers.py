@@ -1,6 +1,8 @@
 """GPU parity of the RPCA / MC solvers against the CPU oracle on identical
 seeded inputs (BASELINE.json parity contract: iterations +-1, same recovered
 rank, final A and E to 1e-6 relative Frobenius; test_solvers.cpp bounds)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -71,3 +73,18 @@ def test_mc_rejects_empty(G):
     with pytest.raises(ValueError):
         G.mc_svt(10, 10, np.zeros(11, dtype=np.int64), np.zeros(0, dtype=np.int32), np.zeros(0),
                  G.SvdBackend.blws())
+
+
+@pytest.mark.slow
+def test_rpca_c1_config_parity(G, O):
+    """BASELINE configs[0] (C1): RPCA 500^2, rank 25, 5% corruption, seed 1."""
+    d, a0, _, _ = synth.rpca_lowrank_sparse(500, 25, 12500, 1, O.Rng, O.sample_distinct)
+    bseed = 1 ^ 0x5BDBEEF
+    a_g, e_g, st_g, _ = G.rpca_adm(d, G.SvdBackend.blws(seed=bseed), truth=a0)
+    O.set_threads(os.cpu_count() or 1)
+    a_o, e_o, st_o, _ = O.rpca_adm(d, O.SvdBackend.blws(seed=bseed), truth=a0)
+    assert st_g.converged and st_o.converged
+    assert abs(st_g.iterations - st_o.iterations) <= 1 and st_g.rank_hat == st_o.rank_hat == 25
+    assert np.linalg.norm(a_g - a_o) <= 1e-6 * np.linalg.norm(a_o)
+    assert np.linalg.norm(e_g - e_o) <= 1e-6 * np.linalg.norm(e_o)
+    assert st_g.rel_err <= 1e-5

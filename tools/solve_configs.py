@@ -1,0 +1,74 @@
+"""Solver configs of BASELINE.json on the GPU, with the CPU oracle beside them.
+
+C1: RPCA 500^2, rank 25, 5% corruption, tol 1e-7       (parity + timing)
+C3: RPCA 2000^2, rank 100, 10% corruption, tol 1e-7    (parity + timing)
+C4: MC 10^4^2, rank 50, 10^7 observed, tol 1e-6        (GPU; oracle skipped: its
+    sparse products are naive single-thread loops, hours at this size)
+Prints one JSON line per config.
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_1012_0365_b200 as B  # noqa: E402
+from paper_1012_0365_b200 import synth  # noqa: E402
+
+SEED = 1
+
+
+def rpca(name, m, rank, frac, oracle=True):
+    from oracle import oracle as O
+    d, a0, _, _ = synth.rpca_lowrank_sparse(m, rank, int(round(frac * m * m)), SEED, B.Rng, B.sample_distinct)
+    bseed = SEED ^ 0x5BDBEEF
+    ctx = B.Context(0)
+    B.rpca_adm(d[:64, :64].copy(order="F"), B.SvdBackend.blws(seed=bseed, ctx=ctx))  # warm-up (module load)
+    t = time.perf_counter()
+    a, e, st, _ = B.rpca_adm(d, B.SvdBackend.blws(seed=bseed, ctx=ctx), truth=a0)
+    gpu_s = time.perf_counter() - t
+    line = dict(config=name, m=m, rank=rank, corrupt=frac, gpu_solve_s=gpu_s, iterations=st.iterations,
+                rank_hat=st.rank_hat, rel_err=st.rel_err, e_l0=st.e_l0, matvecs=st.matvec_count,
+                converged=st.converged)
+    if oracle:
+        cores = os.cpu_count() or 1
+        O.set_threads(cores)
+        t = time.perf_counter()
+        ao, eo, so, _ = O.rpca_adm(d, O.SvdBackend.blws(seed=bseed), truth=a0)
+        line.update(cpu_solve_s=time.perf_counter() - t, cpu_cores=cores, cpu_iterations=so.iterations,
+                    cpu_rank_hat=so.rank_hat, cpu_rel_err=so.rel_err,
+                    a_rel_diff=float(np.linalg.norm(a - ao) / np.linalg.norm(ao)),
+                    e_rel_diff=float(np.linalg.norm(e - eo) / np.linalg.norm(eo)),
+                    same_predicted_ranks=st.predicted_ranks[:min(st.iterations, so.iterations)]
+                    == so.predicted_ranks[:min(st.iterations, so.iterations)])
+    print(json.dumps(line), flush=True)
+
+
+def mc(name, m, rank, nobs):
+    colptr, rowidx, vals, ml, mr = synth.mc_lowrank(m, rank, nobs, SEED, B.Rng, B.sample_distinct)
+    ctx = B.Context(0)
+    t = time.perf_counter()
+    u, s, v, st = B.mc_svt(m, m, colptr, rowidx, vals, B.SvdBackend.blws(seed=SEED ^ 0x5BDBEEF, ctx=ctx),
+                           tol_outer=1e-6, truth_ml=ml, truth_mr=mr, cap=512)
+    gpu_s = time.perf_counter() - t
+    print(json.dumps(dict(config=name, m=m, rank=rank, nobs=nobs, gpu_solve_s=gpu_s, iterations=st.iterations,
+                          rank_hat=st.rank_hat, rel_err=st.rel_err, matvecs=st.matvec_count,
+                          converged=st.converged)), flush=True)
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("configs", nargs="*", default=["C1", "C3", "C4"])
+    ap.add_argument("--no-oracle", action="store_true")
+    a = ap.parse_args()
+    for c in a.configs:
+        if c == "C1":
+            rpca("C1", 500, 25, 0.05, not a.no_oracle)
+        elif c == "C3":
+            rpca("C3", 2000, 100, 0.10, not a.no_oracle)
+        elif c == "C4":
+            mc("C4", 10000, 50, 10_000_000)
