@@ -14,22 +14,27 @@ namespace blws {
 void chol_probe_read(double* out);
 }
 
+// Every handle keeps its Context alive (shared ownership): callers may destroy
+// the context handle first (e.g. interpreter shutdown order) without the
+// dependent handles' device buffers freeing through a dangling context.
 struct blws_context {
-    std::unique_ptr<Context> ctx;
+    std::shared_ptr<Context> ctx;
 };
 struct blws_rng {
     Rng rng;
 };
 struct blws_operator {
+    std::shared_ptr<Context> keep;  // declared first: destroyed last
     blws_context* owner;
     std::unique_ptr<LinearOperator> op;
     bool dense = true;
 };
 struct blws_warm_start {
-    blws_context* owner;
+    std::shared_ptr<Context> keep;
     DWarm w;
 };
 struct blws_svd_backend {
+    std::shared_ptr<Context> keep;
     blws_context* owner;
     std::unique_ptr<SvdBackend> b;
 };
@@ -61,7 +66,7 @@ void need(bool c, const char* msg) {
     if (!c) throw std::invalid_argument(msg);
 }
 
-blws_warm_start* wrap(blws_context* owner, DWarm w) { return new blws_warm_start{owner, std::move(w)}; }
+blws_warm_start* wrap(const std::shared_ptr<Context>& keep, DWarm w) { return new blws_warm_start{keep, std::move(w)}; }
 
 void copy_in(Context& ctx, View dst, const double* src, Index ld, int where) {
     if (where == BLWS_HOST)
@@ -109,7 +114,7 @@ int blws_context_create(int device, blws_context** out) {
     return guard([&] {
         need(out != nullptr, "blws_context_create: null out");
         auto c = std::make_unique<blws_context>();
-        c->ctx = std::make_unique<Context>(device);
+        c->ctx = std::make_shared<Context>(device);
         *out = c.release();
     });
 }
@@ -189,6 +194,7 @@ int blws_dense_operator_create(blws_context* ctx, int64_t m, int64_t n, const do
         need(m > 0 && n > 0 && w && ldw >= m, "DenseOperator: bad shape");
         Context& c = *ctx->ctx;
         auto h = std::make_unique<blws_operator>();
+        h->keep = ctx->ctx;
         h->owner = ctx;
         if (where == BLWS_DEVICE && borrow) {
             need(ldw % 2 == 0 && reinterpret_cast<uintptr_t>(w) % 16 == 0,
@@ -222,6 +228,7 @@ int blws_sparse_operator_create(blws_context* ctx, int64_t m, int64_t n, int64_t
     return guard([&] {
         need(m > 0 && n > 0 && nnz >= 0, "SparseOperator: bad shape");
         auto h = std::make_unique<blws_operator>();
+        h->keep = ctx->ctx;
         h->owner = ctx;
         h->dense = false;
         h->op = std::make_unique<SparseOperator>(*ctx->ctx, m, n, nnz, colptr, rowidx, values);
@@ -274,17 +281,17 @@ int blws_warm_start_create(blws_context* ctx, int64_t m, int64_t n, int64_t r, c
             copy_in(c, w.v(), v, ldv, where);
             std::copy(sigma, sigma + r, w.sigma.begin());
         }
-        *out = wrap(ctx, std::move(w));
+        *out = wrap(ctx->ctx, std::move(w));
     });
 }
 int blws_warm_start_copy(const blws_warm_start* src, blws_warm_start** out) {
-    return guard([&] { *out = wrap(src->owner, copy_warm(*src->owner->ctx, src->w, src->w.rank())); });
+    return guard([&] { *out = wrap(src->keep, copy_warm(*src->keep, src->w, src->w.rank())); });
 }
 int64_t blws_warm_start_rank(const blws_warm_start* w) { return w->w.rank(); }
 int blws_warm_start_get(const blws_warm_start* w, double* u, int64_t ldu, double* v, int64_t ldv, double* sigma,
                         int where) {
     return guard([&] {
-        Context& c = *w->owner->ctx;
+        Context& c = *w->keep;
         copy_out(c, w->w.u(), u, ldu, where);
         copy_out(c, w->w.v(), v, ldv, where);
         if (sigma) std::copy(w->w.sigma.begin(), w->w.sigma.end(), sigma);
@@ -302,14 +309,14 @@ int blws_svd(blws_operator* w, const blws_warm_start* warm, int64_t k, int64_t r
         need(w && warm && rng && out, "blws_svd: null argument");
         auto res = blws::blws_svd(*w->op, warm->w, k, r, rng->rng);
         if (flags) *flags = (res.padded ? 1 : 0) | (res.k_raised ? 2 : 0) | (res.terminated_early ? 4 : 0);
-        *out = wrap(w->owner, std::move(res.warm));
+        *out = wrap(w->keep, std::move(res.warm));
     });
 }
 int blws_adapt_subspace(blws_context* ctx, const blws_warm_start* warm, int64_t r_new, int64_t m, int64_t n,
                         blws_rng* rng, blws_warm_start** out) {
     return guard([&] {
         DWarm o = blws::adapt_subspace(*ctx->ctx, warm ? &warm->w : nullptr, r_new, m, n, rng->rng);
-        *out = wrap(ctx, std::move(o));
+        *out = wrap(ctx->ctx, std::move(o));
     });
 }
 int blws_block_lanczos_procedure(blws_operator* w, int64_t b, const double* x1, int64_t k, double* q, double* t,
@@ -361,7 +368,7 @@ int blws_lanczos_partial_svd(blws_operator* w, int64_t r, double tol, int64_t ma
             stats[2] = res.stats.converged;
             stats[3] = res.stats.all_converged ? 1 : 0;
         }
-        *out = wrap(w->owner, std::move(res.uv));
+        *out = wrap(w->keep, std::move(res.uv));
     });
 }
 int blws_spectral_norm(blws_operator* w, double tol, uint64_t seed, double* out) {
@@ -444,7 +451,7 @@ int blws_svd_backend_create(blws_context* ctx, int kind, int64_t block_steps, do
         o.max_k = max_k;
         o.seed_margin = seed_margin;
         o.seed = seed;
-        *out = new blws_svd_backend{ctx, std::make_unique<SvdBackend>(*ctx->ctx, static_cast<SvdBackend::Kind>(kind), o)};
+        *out = new blws_svd_backend{ctx->ctx, ctx, std::make_unique<SvdBackend>(*ctx->ctx, static_cast<SvdBackend::Kind>(kind), o)};
     });
 }
 int blws_svd_backend_destroy(blws_svd_backend* b) {
@@ -453,11 +460,11 @@ int blws_svd_backend_destroy(blws_svd_backend* b) {
 int blws_svd_backend_warm_state(const blws_svd_backend* b, blws_warm_start** out) {
     return guard([&] {
         const auto& w = b->b->warm_state();
-        *out = w ? wrap(b->owner, copy_warm(*b->owner->ctx, *w, w->rank())) : nullptr;
+        *out = w ? wrap(b->keep, copy_warm(*b->keep, *w, w->rank())) : nullptr;
     });
 }
 int blws_svd_backend_set_warm_state(blws_svd_backend* b, const blws_warm_start* w) {
-    return guard([&] { b->b->set_warm(copy_warm(*b->owner->ctx, w->w, w->w.rank())); });
+    return guard([&] { b->b->set_warm(copy_warm(*b->keep, w->w, w->w.rank())); });
 }
 int blws_svt(blws_operator* w, double eps, blws_svd_backend* backend, blws_rank_predictor* pred, int64_t* history,
              int64_t history_cap, int64_t* history_len, blws_warm_start** out, int64_t* achieved_rank,
@@ -472,7 +479,7 @@ int blws_svt(blws_operator* w, double eps, blws_svd_backend* backend, blws_rank_
         if (history && history_len && *history_len < history_cap) history[(*history_len)++] = p.history.back();
         if (achieved_rank) *achieved_rank = res.achieved_rank;
         if (all_above_threshold) *all_above_threshold = res.all_above_threshold ? 1 : 0;
-        if (out) *out = wrap(w->owner, std::move(res.trip));
+        if (out) *out = wrap(w->keep, std::move(res.trip));
     });
 }
 

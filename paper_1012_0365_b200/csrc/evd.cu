@@ -121,12 +121,12 @@ __global__ void __launch_bounds__(kThreads) sytrd_k(const double* __restrict__ t
                     const double vj = v[j];
 #pragma unroll
                     for (int q = 0; q < kMaxRowsPerLane; ++q) {
-                        // branch-free: out-of-range rows read a clamped address and are masked
                         const int i = lane + 32 * q;
-                        const bool in = i >= j && i < w;
-                        const double lij = in ? col[in ? i : j] : 0.0;
-                        acc[q] = fma(lij, vj, acc[q]);
-                        dp[c] = fma(i > j ? lij : 0.0, vr[q], dp[c]);
+                        if (i >= j && i < w) {
+                            const double lij = col[i];
+                            acc[q] = fma(lij, vj, acc[q]);
+                            if (i > j) dp[c] = fma(lij, vr[q], dp[c]);
+                        }
                     }
                 }
             }
@@ -186,12 +186,7 @@ __global__ void __launch_bounds__(kThreads) sytrd_k(const double* __restrict__ t
 #pragma unroll
                 for (int q = 0; q < kMaxRowsPerLane; ++q) {
                     const int i = lane + 32 * q;
-                    if (32 * q + 31 < j || 32 * q >= w) continue;  // warp-uniform skip
-                    const bool in = i >= j && i < w;
-                    const int ii = in ? i : j;
-                    const double upd = fma(vr[q], wj, wr[q] * vj);
-                    const double cur = col[ii];
-                    if (in) col[ii] = cur - upd;
+                    if (i >= j && i < w) col[i] -= fma(vr[q], wj, wr[q] * vj);
                 }
             }
         } else {
@@ -266,6 +261,8 @@ __global__ void __launch_bounds__(kOrmWarps * 32) ormtr_k(const double* __restri
 
 }  // namespace
 
+bool sytrd_cluster(Context& ctx, View t, double* lp, double* d, double* e, double* tau);
+
 void sym_evd_top(Context& ctx, View t, Index want, double* values, View vectors) {
     const int n = static_cast<int>(t.rows);
     if (n <= 0 || want <= 0) return;
@@ -286,12 +283,14 @@ void sym_evd_top(Context& ctx, View t, Index want, double* values, View vectors)
         cfg = true;
     }
     const int smem = static_cast<int>(head + (on_chip ? np * 8 : 0));
+    if (!sytrd_cluster(ctx, t, lp.get(), d.get(), e.get(), tau.get())) {
     if (on_chip)
         sytrd_k<true><<<1, kThreads, smem, ctx.stream()>>>(t.p, t.ld, n, lp.get(), d.get(), e.get(), tau.get());
     else
         sytrd_k<false><<<1, kThreads, smem, ctx.stream()>>>(t.p, t.ld, n, lp.get(), d.get(), e.get(), tau.get());
     ctx.note_launch();
     ctx.check_launch("sytrd_k");
+    }
     tridiag_eig_top(ctx, n, d.get(), e.get(), want, values, vectors);
     static bool cfg2 = false;
     if (!cfg2) {

@@ -108,6 +108,19 @@ def test_sym_evd_matches_oracle(gpu, O, n):
     assert np.linalg.norm(vecs.T @ vecs - np.eye(n)) <= 1e-10
 
 
+@pytest.mark.parametrize("n", [64, 110, 208, 260])
+def test_sym_evd_cluster_tridiagonalisation(gpu, O, n, monkeypatch):
+    # opt-in cluster-distributed Householder stage (sytrd_cluster.cu)
+    monkeypatch.setenv("BLWS_SYTRD", "cluster")
+    g = O.Rng(41 + n).gaussian_matrix(n, n)
+    t = 0.5 * (g + g.T)
+    vals, vecs = gpu.sym_evd_small(t)
+    ref_vals, _ = O.sym_evd_small(t)
+    tn = np.linalg.norm(t)
+    assert np.abs(vals - ref_vals).max() <= 1e-12 * tn
+    assert np.linalg.norm(t @ vecs - vecs * vals) <= 1e-10 * tn
+
+
 def test_tridiagonal_top_matches_oracle(gpu, O):
     rs = np.random.default_rng(9)
     for n, want in [(10, 3), (60, 20), (500, 40)]:
