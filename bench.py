@@ -260,6 +260,10 @@ def run_gpu(args):
     k1_flops = k1["flops"] / max(1, k1["count"])
     achieved_tf = k1_flops / (k1_avg_ms * 1e-3) / 1e12 if k1_avg_ms > 0 else 0.0
     peak = max(peak_dmma, peak_dfma)
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "r01_k1_traffic.json")
+    if os.path.exists(tp):  # one ncu --set full capture of the same K1 launch group
+        traffic = json.load(open(tp))["dram_bytes_per_launch"]
 
     if rank == 0:
         line = {
@@ -273,7 +277,9 @@ def run_gpu(args):
             "e2e": {"value": e2e_value, "unit": "calls/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
             "roofline": {"bound": "tensor", "achieved": achieved_tf, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved_tf / peak if peak else None, "traffic": None,
+                         "frac": achieved_tf / peak if peak else None, "traffic": traffic,
+                         "traffic_unit": "bytes per K1 launch group (ncu, profiles/r01_k1_traffic.json)",
+                         "algorithmic_bytes_per_launch": 16.0 * M * N,
                          "kernel": "K1 paired W products (dgemm_kernel NN + TN, split-K reduce)",
                          "flops_per_launch": k1_flops, "avg_launch_ms": k1_avg_ms,
                          "peak_source": "measured in this run: DMMA microbenchmark %.2f, DFMA %.2f TFLOP/s; "
