@@ -86,6 +86,13 @@ int blws_dense_operator_create(blws_context* ctx, int64_t m, int64_t n, const do
                                int borrow, blws_operator** out);
 /* DenseOperator::assign (linear_operator.hpp:113-116): replace W, non-finite check. */
 int blws_dense_operator_assign(blws_operator* op, const double* w, int64_t ldw, int where);
+/* Asynchronous host assign (B200 extension of DenseOperator::assign): queues the
+   upload on the context's copy stream behind the kernels already queued and
+   returns at once, so the next W uploads while the current solve runs on another
+   operator. The next call using `op` waits for the copy and performs the
+   reference's non-finite check then (BLWS_EINVAL from that call). `w` (pinned
+   host memory for real overlap) must stay valid and unchanged until then. */
+int blws_dense_operator_assign_async(blws_operator* op, const double* w, int64_t ldw);
 /* SparseOperator (linear_operator.hpp:136-169) from host CSC (Eigen's default order). */
 int blws_sparse_operator_create(blws_context* ctx, int64_t m, int64_t n, int64_t nnz, const int64_t* colptr,
                                 const int32_t* rowidx, const double* values, blws_operator** out);
@@ -112,6 +119,11 @@ int blws_warm_start_get(const blws_warm_start* w, double* u, int64_t ldu, double
 int blws_warm_start_destroy(blws_warm_start* w);
 
 /* --------------------------------------------------------- block lanczos */
+/* Number of blws_svd calls (process-wide) whose deferred single-round-trip
+   path was redone on the exact path because a host test would have branched
+   away from the common case (breakdown, rank loss, ill-conditioned Gram,
+   keep < min(r, d)). BLWS_EXACT=1 in the environment forces the exact path. */
+int64_t blws_svd_deferred_fallbacks(void);
 /* blws_svd (block_lanczos.hpp:204-261). flags: bit0 padded, bit1 k_raised,
  * bit2 terminated_early. *out receives a new warm start of rank r. */
 int blws_svd(blws_operator* w, const blws_warm_start* warm, int64_t k, int64_t r, blws_rng* rng,

@@ -17,6 +17,7 @@ from .api import (  # noqa: F401
     WarmStart,
     adapt_subspace,
     blws_svd,
+    deferred_fallbacks,
     block_lanczos_procedure,
     lanczos_partial_svd,
     mc_svt,

@@ -68,6 +68,7 @@ SIGNATURES = {
     "blws_sample_distinct": (i64, [i64, i64, vp, vp]),
     "blws_dense_operator_create": (ci, [vp, i64, i64, vp, i64, ci, ci, P(vp)]),
     "blws_dense_operator_assign": (ci, [vp, vp, i64, ci]),
+    "blws_dense_operator_assign_async": (ci, [vp, vp, i64]),
     "blws_sparse_operator_create": (ci, [vp, i64, i64, i64, vp, vp, vp, P(vp)]),
     "blws_sparse_operator_assign_values": (ci, [vp, vp, i64, ci]),
     "blws_operator_destroy": (ci, [vp]),
@@ -80,6 +81,7 @@ SIGNATURES = {
     "blws_warm_start_rank": (i64, [vp]),
     "blws_warm_start_get": (ci, [vp, vp, i64, vp, i64, vp, ci]),
     "blws_warm_start_destroy": (ci, [vp]),
+    "blws_svd_deferred_fallbacks": (i64, []),
     "blws_svd": (ci, [vp, vp, i64, i64, vp, P(vp), P(ci)]),
     "blws_adapt_subspace": (ci, [vp, vp, i64, i64, i64, vp, P(vp)]),
     "blws_block_lanczos_procedure": (ci, [vp, i64, vp, i64, vp, vp, P(i64), P(ci)]),
@@ -309,6 +311,12 @@ class DenseOperator(LinearOperator):
     def assign_ptr(self, ptr: int, ld: int, where: int):
         _check(lib().blws_dense_operator_assign(self._h, ptr, ld, where))
 
+    def assign_async(self, ptr: int, ld: int):
+        """Queue a pinned-host upload on the copy stream; the next use waits
+        for it (blws_dense_operator_assign_async). The caller keeps the host
+        buffer alive and unchanged until then."""
+        _check(lib().blws_dense_operator_assign_async(self._h, ptr, ld))
+
     def assign(self, w, device=False, ld=None):
         if device:
             _check(lib().blws_dense_operator_assign(self._h, _ptr(w), ld or self.m, DEVICE))
@@ -372,8 +380,17 @@ class DeviceWarmStart:
         _check(lib().blws_warm_start_copy(self._h, C.byref(h)))
         return DeviceWarmStart(h, self.ctx)
 
-    def to_host(self, m, n):
+    def to_host(self, m, n, out: "WarmStart | None" = None):
+        """Download U, V, sigma; `out` (F-ordered arrays, e.g. views of pinned
+        memory, with at least rank() columns) is filled in place and trimmed."""
         r = self.rank()
+        if out is not None:
+            u, v, s = out.u, out.v, out.sigma
+            if not (u.flags.f_contiguous and v.flags.f_contiguous and u.shape[0] == m and v.shape[0] == n
+                    and u.shape[1] >= r and v.shape[1] >= r and s.shape[0] >= r):
+                raise ValueError("to_host: out arrays must be F-ordered (m, >=r), (n, >=r), (>=r,)")
+            _check(lib().blws_warm_start_get(self._h, _ptr(u), m, _ptr(v), n, _ptr(s), HOST))
+            return WarmStart(u[:, :r], v[:, :r], s[:r])
         u = np.empty((m, r), order="F")
         v = np.empty((n, r), order="F")
         s = np.empty(r)
@@ -409,6 +426,11 @@ def blws_svd(op: LinearOperator, warm, k: int, r: int, rng: Rng, keep_device=Fal
     f = flags.value
     w = out if keep_device else out.to_host(op.rows(), op.cols())
     return BlwsResult(w, bool(f & 1), bool(f & 2), bool(f & 4))
+
+
+def deferred_fallbacks() -> int:
+    """blws_svd calls redone on the exact path (blws_svd_deferred_fallbacks)."""
+    return int(lib().blws_svd_deferred_fallbacks())
 
 
 def adapt_subspace(warm, r_new, m, n, rng: Rng, ctx: Context | None = None) -> WarmStart:

@@ -223,6 +223,13 @@ int blws_dense_operator_assign(blws_operator* op, const double* w, int64_t ldw, 
             d->assign_device(w, ldw);
     });
 }
+int blws_dense_operator_assign_async(blws_operator* op, const double* w, int64_t ldw) {
+    return guard([&] {
+        need(op->dense, "assign_async: not a dense operator");
+        need(w != nullptr, "assign_async: null source");
+        static_cast<DenseOperator*>(op->op.get())->assign_host_async(w, ldw);
+    });
+}
 int blws_sparse_operator_create(blws_context* ctx, int64_t m, int64_t n, int64_t nnz, const int64_t* colptr,
                                 const int32_t* rowidx, const double* values, blws_operator** out) {
     return guard([&] {
@@ -303,6 +310,7 @@ int blws_warm_start_destroy(blws_warm_start* w) {
 }
 
 // ---------------------------------------------------------- block lanczos
+int64_t blws_svd_deferred_fallbacks(void) { return blws::g_blws_deferred_fallbacks; }
 int blws_svd(blws_operator* w, const blws_warm_start* warm, int64_t k, int64_t r, blws_rng* rng,
              blws_warm_start** out, int* flags) {
     return guard([&] {

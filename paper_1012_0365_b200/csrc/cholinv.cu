@@ -39,9 +39,25 @@ constexpr long kSmemBudget = 216 * 1024;
 
 template <bool SH>
 __global__ void __launch_bounds__(kCT) chol_inv_k(double* g, long ldg, double* rinv, long ldri, int n,
-                                                  double* scratch, int* status, double* diag) {
+                                                  double* scratch, int* status, double* diag,
+                                                  const double* skip_offsq, double skip_tol) {
     extern __shared__ __align__(16) double sm[];
     __shared__ int fail;
+    if (skip_offsq && *skip_offsq <= skip_tol) {
+        // device-predicated CholQR pass skip: G == I to tolerance -> R = Rinv = I
+        const int lane0 = threadIdx.x & 31, wid0 = threadIdx.x >> 5, nw0 = blockDim.x >> 5;
+        for (int j = wid0; j < n; j += nw0)
+            for (int i = lane0; i < n; i += 32) {
+                g[i + j * ldg] = i == j ? 1.0 : 0.0;
+                if (rinv) rinv[i + j * ldri] = i == j ? 1.0 : 0.0;
+            }
+        if (threadIdx.x == 0) {
+            status[0] = 0;
+            diag[0] = 1.0;
+            diag[1] = 1.0;
+        }
+        return;
+    }
     const int ld = n | 1;  // odd stride: conflict-free row access
     double* A = SH ? sm : scratch;
     double* X = A + static_cast<long>(ld) * n;
@@ -236,7 +252,8 @@ __global__ void __launch_bounds__(kCT) chol_inv_k(double* g, long ldg, double* r
 
 }  // namespace
 
-void chol_inv_upper(Context& ctx, View g, View rinv, int* status, double* diag) {
+void chol_inv_upper(Context& ctx, View g, View rinv, int* status, double* diag, const double* skip_offsq,
+                    double skip_tol) {
     const int n = static_cast<int>(g.rows);
     const long ld = n | 1;
     const long bytes = (2L * ld * n + 2L * n + 34) * 8;
@@ -247,10 +264,12 @@ void chol_inv_upper(Context& ctx, View g, View rinv, int* status, double* diag) 
         cfg = true;
     }
     if (on_chip) {
-        chol_inv_k<true><<<1, kCT, bytes, ctx.stream()>>>(g.p, g.ld, rinv.p, rinv.ld, n, nullptr, status, diag);
+        chol_inv_k<true><<<1, kCT, bytes, ctx.stream()>>>(g.p, g.ld, rinv.p, rinv.ld, n, nullptr, status, diag,
+                                                         skip_offsq, skip_tol);
     } else {
         DBuf<double> scratch(ctx, static_cast<size_t>(2L * ld * n + 2L * n + 34));
-        chol_inv_k<false><<<1, kCT, 0, ctx.stream()>>>(g.p, g.ld, rinv.p, rinv.ld, n, scratch.get(), status, diag);
+        chol_inv_k<false><<<1, kCT, 0, ctx.stream()>>>(g.p, g.ld, rinv.p, rinv.ld, n, scratch.get(), status,
+                                               diag, skip_offsq, skip_tol);
     }
     ctx.note_launch();
     ctx.check_launch("chol_inv_k");

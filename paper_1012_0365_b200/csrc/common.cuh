@@ -47,6 +47,9 @@ public:
     Context& operator=(const Context&) = delete;
 
     cudaStream_t stream() const { return stream_; }
+    /// Second stream for host->device uploads that overlap queued kernels
+    /// (created on first use; ordered against stream() with events).
+    cudaStream_t copy_stream();
     int device() const { return device_; }
     int sm_count() const { return sms_; }
 
@@ -73,6 +76,7 @@ private:
     int device_ = 0;
     int sms_ = 148;
     cudaStream_t stream_ = nullptr;
+    cudaStream_t copy_stream_ = nullptr;
     void* pinned_ = nullptr;
     size_t pinned_bytes_ = 0;
     std::int64_t launches_ = 0;

@@ -2,6 +2,7 @@
 #include <cstring>
 
 #include "common.cuh"
+#include "ops.cuh"
 
 namespace blws {
 
@@ -62,8 +63,17 @@ void Context::region_reset() {
     }
 }
 
+cudaStream_t Context::copy_stream() {
+    if (!copy_stream_) BLWS_CUDA(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking));
+    return copy_stream_;
+}
+
 Context::~Context() {
     region_reset();
+    if (copy_stream_) {
+        cudaStreamSynchronize(copy_stream_);
+        cudaStreamDestroy(copy_stream_);
+    }
     if (stream_) {
         cudaStreamSynchronize(stream_);
         cudaStreamDestroy(stream_);
@@ -136,7 +146,7 @@ void Context::write(double* dev, const double* host, size_t count) {
 
 DMat::DMat(Context& ctx, Index r, Index c, bool zero) : rows(r), cols(c), ld(std::max<Index>(round_up(r, 2), 2)) {
     buf = DBuf<double>(ctx, static_cast<size_t>(ld * std::max<Index>(c, 1)));
-    if (zero) BLWS_CUDA(cudaMemsetAsync(buf.get(), 0, sizeof(double) * buf.size(), ctx.stream()));
+    if (zero) blws::zero(ctx, buf.get(), sizeof(double) * buf.size());
 }
 
 }  // namespace blws

@@ -62,6 +62,10 @@ public:
         pair_impl(left, right, top, bot);
     }
     std::int64_t application_count() const { return count_; }
+    /// If a deferred input check is pending (async upload), queue it now with
+    /// its verdict (nonzero = non-finite entries) written to the device int
+    /// `*flag`, instead of the synchronous check at the next use.
+    virtual void defer_pending_check(int* flag) { (void)flag; }
 
 protected:
     virtual void pair_block_impl(View left, View right, View top, View bot) = 0;
@@ -79,11 +83,24 @@ public:
     DenseOperator(Context& ctx, Index m, Index n);
     /// Borrow caller memory (ld must be even, 16-byte aligned).
     DenseOperator(Context& ctx, Index m, Index n, double* dev, Index ld);
+    ~DenseOperator() override;
     Index rows() const override { return m_; }
     Index cols() const override { return n_; }
-    View w() const { return View{p_, m_, n_, ld_}; }
+    /// The held matrix; first waits for (and checks) a pending async upload.
+    View w() const {
+        ensure_ready();
+        return View{p_, m_, n_, ld_};
+    }
     /// Host upload with the reference's non-finite check (:113-116).
     void assign_host(const double* w, Index ldw);
+    /// Asynchronous host upload (B200 extension of assign): the copy is queued
+    /// on the context's copy stream behind every kernel already queued on the
+    /// compute stream and returns at once, so it overlaps work in flight on
+    /// another operator; the next use of this operator waits for it and runs
+    /// the non-finite check then. `w` must stay valid (and pinned, for real
+    /// overlap) until that use.
+    void assign_host_async(const double* w, Index ldw);
+    void defer_pending_check(int* flag) override;
     /// Device copy with the non-finite check.
     void assign_device(const double* w, Index ldw);
     /// Non-finite scan of the held matrix (throws std::invalid_argument).
@@ -94,9 +111,12 @@ protected:
     void pair_impl(const double* left, const double* right, double* top, double* bot) override;
 
 private:
+    void ensure_ready() const;
     Index m_, n_, ld_;
     DBuf<double> own_;
     double* p_ = nullptr;
+    mutable bool pending_ = false;
+    cudaEvent_t consumed_ = nullptr, ready_ = nullptr;
 };
 
 /// SparseOperator (linear_operator.hpp:136-169): the pattern in CSR (for W*x)
@@ -161,6 +181,7 @@ struct BlwsResult {
 DWarm adapt_subspace(Context& ctx, const DWarm* warm, Index r_new, Index m, Index n, Rng& rng);
 /// blws_svd (block_lanczos.hpp:204-261).
 BlwsResult blws_svd(LinearOperator& w, const DWarm& warm, Index k, Index r, Rng& rng);
+extern std::int64_t g_blws_deferred_fallbacks;
 
 /// Factorisation for tests: block_lanczos_procedure on the augmented view.
 struct BlockLanczos {

@@ -363,7 +363,7 @@ SolverStats rpca_adm(Context& ctx, Index m, const double* d_in, Index ldd, doubl
     Index last_rank = 0;
     DBuf<int> bad(ctx, 1);
     // first W = D - E + Y/mu (later ones come out of the fused kernel)
-    BLWS_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(int), ctx.stream()));
+    zero(ctx, bad.get(), sizeof(int));
     form_w_k<<<gridn(m * m), kT, 0, ctx.stream()>>>(D.data(), E.data(), Y.data(), Wm.data(), m, ld, mu, bad.get());
     ctx.note_launch();
     using namespace gemm_detail;
@@ -383,7 +383,7 @@ SolverStats rpca_adm(Context& ctx, Index m, const double* d_in, Index ldd, doubl
         DMat us(ctx, m, std::max<Index>(r, 1), false);
         if (r > 0) scale_columns(ctx, us.view().left(r), prox.trip.u(), prox.sigma_dev.get());
         const double mu_next = std::min(opts.rho * mu, mu_max);
-        BLWS_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(int), ctx.stream()));
+        zero(ctx, bad.get(), sizeof(int));
         alm_fused_k<<<grid, THREADS, smem, ctx.stream()>>>(us.data(), us.ld, prox.trip.v().p, prox.trip.uv.ld, m, r,
                                                            D.data(), Y.data(), Wm.data(), E.data(), ld, mu, mu_next,
                                                            lambda / mu, part.get(), bad.get());
@@ -412,7 +412,7 @@ SolverStats rpca_adm(Context& ctx, Index m, const double* d_in, Index ldd, doubl
     }
     {
         DBuf<unsigned long long> cnt(ctx, 2);
-        BLWS_CUDA(cudaMemsetAsync(cnt.get(), 0, 2 * sizeof(unsigned long long), ctx.stream()));
+        zero(ctx, cnt.get(), 2 * sizeof(unsigned long long));
         e_counts_k<<<gridn(m * m, 1024), kT, 0, ctx.stream()>>>(E.data(), m, ld, 1e-8 * dmax, cnt.get());
         ctx.note_launch();
         unsigned long long h[2];

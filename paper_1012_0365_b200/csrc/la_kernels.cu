@@ -41,6 +41,12 @@ __global__ void fill_k(double* x, long rows, long cols, long ld, double v) {
         x[idx % rows + (idx / rows) * ld] = v;
 }
 
+__global__ void zero_k(unsigned* p, size_t words) {
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < words;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x)
+        p[i] = 0u;
+}
+
 __global__ void copy_k(double* d, long ldd, const double* s, long lds, long rows, long cols, double alpha) {
     const long total = rows * cols;
     for (long idx = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; idx < total;
@@ -348,6 +354,14 @@ __global__ void gather_vals_k(long nnz, double* dst, const double* src, const st
         (ctx).note_launch(); \
         (ctx).check_launch(name); \
     } while (0)
+
+void zero(Context& ctx, void* p, size_t bytes) {
+    if (bytes == 0) return;
+    if (bytes % 4) throw std::invalid_argument("zero: size must be a multiple of 4 bytes");
+    const size_t words = bytes / 4;
+    zero_k<<<grid_for(static_cast<Index>(words)), kThreads, 0, ctx.stream()>>>(static_cast<unsigned*>(p), words);
+    LAUNCH(ctx, "zero");
+}
 
 void fill(Context& ctx, View x, double v) {
     if (x.rows * x.cols == 0) return;

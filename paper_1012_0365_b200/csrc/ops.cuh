@@ -14,6 +14,9 @@ void gemm(Context& ctx, bool ta, bool tb, Index M, Index N, Index K, double alph
 
 // ------------------------------------------------------------------ level-1 / small
 void fill(Context& ctx, View x, double v);
+/// Zeroes `bytes` (multiple of 4) with a kernel: a cudaMemsetAsync may be
+/// queued on a copy engine behind a pending host upload.
+void zero(Context& ctx, void* p, size_t bytes);
 void copy(Context& ctx, View dst, View src, double alpha = 1.0);  // dst = alpha * src
 void axpy(Context& ctx, View y, View x, double alpha);            // y += alpha * x
 /// out[0] = sum of squares of x (deterministic two-pass reduction).
@@ -35,8 +38,11 @@ void gather_columns(Context& ctx, View dst, View src, const int* idx);
 /// min_diag/max_diag of R written to status-adjacent doubles diag[0..1].
 void potrf_upper(Context& ctx, View g, int* status, double* diag);
 /// Fused blocked Cholesky + inverse: G <- R (upper, zero lower), rinv <- R^{-1};
-/// status / diag as potrf_upper.
-void chol_inv_upper(Context& ctx, View g, View rinv, int* status, double* diag);
+/// status / diag as potrf_upper. With skip_offsq (device scalar ||G - I||_F^2)
+/// <= skip_tol the kernel writes R = Rinv = I instead (device-predicated CholQR
+/// pass skip, no host round trip).
+void chol_inv_upper(Context& ctx, View g, View rinv, int* status, double* diag, const double* skip_offsq = nullptr,
+                    double skip_tol = 0.0);
 /// R^{-1} of an upper-triangular n x n R (out may not alias r).
 void trtri_upper(Context& ctx, View out, View r);
 /// C = A * B for upper-triangular n x n A, B (C upper triangular).

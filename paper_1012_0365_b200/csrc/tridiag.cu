@@ -30,12 +30,13 @@ constexpr double kClusterTol = 1e-5;
 // (division-free: two dependent FMAs per step instead of a division), with
 // exact power-of-two rescaling against over/underflow. A zero p_i takes the
 // sign opposite to p_{i-1} (dstebz's pivmin convention in the ratio form).
-__device__ __forceinline__ int sturm_count(const double* d, const double* e2, int n, double x, double pivmin) {
+__device__ __forceinline__ int sturm_count(const double* d, const double* e, int n, double x, double pivmin) {
     double p0 = 1.0, p1 = d[0] - x;
     if (p1 == 0.0) p1 = -pivmin;
     int cnt = p1 < 0.0;
     for (int i = 1; i < n; ++i) {
-        double p2 = fma(d[i] - x, p1, -e2[i - 1] * p0);
+        const double e2 = e[i - 1] * e[i - 1];
+        double p2 = fma(d[i] - x, p1, -e2 * p0);
         if (p2 == 0.0) p2 = p1 > 0.0 ? -pivmin * fabs(p1) : pivmin * fabs(p1);
         cnt += (p2 < 0.0) != (p1 < 0.0);
         const double a = fabs(p2);
@@ -52,12 +53,65 @@ __device__ __forceinline__ int sturm_count(const double* d, const double* e2, in
     return cnt;
 }
 
+// Bisection interval, pivmin and ||T||_1 (dstebz's Gershgorin set-up), on the
+// device so the eigensolver needs no host round trip. params: gl, gu, pivmin,
+// onenrm (0 => T == 0).
+constexpr int kBoundsThreads = 512;
+__global__ void __launch_bounds__(kBoundsThreads) tridiag_bounds_k(const double* __restrict__ d,
+                                                                    const double* __restrict__ e, int n,
+                                                                    double* params) {
+    __shared__ double red[4][kBoundsThreads / 32];
+    double gl = INFINITY, gu = -INFINITY, emax2 = 0.0, onenrm = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const double el = i > 0 ? fabs(e[i - 1]) : 0.0, er = i < n - 1 ? fabs(e[i]) : 0.0;
+        gl = fmin(gl, d[i] - el - er);
+        gu = fmax(gu, d[i] + el + er);
+        onenrm = fmax(onenrm, fabs(d[i]) + el + er);
+        if (i < n - 1) emax2 = fmax(emax2, e[i] * e[i]);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        gl = fmin(gl, __shfl_xor_sync(0xffffffffu, gl, o));
+        gu = fmax(gu, __shfl_xor_sync(0xffffffffu, gu, o));
+        onenrm = fmax(onenrm, __shfl_xor_sync(0xffffffffu, onenrm, o));
+        emax2 = fmax(emax2, __shfl_xor_sync(0xffffffffu, emax2, o));
+    }
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) {
+        red[0][wid] = gl;
+        red[1][wid] = gu;
+        red[2][wid] = onenrm;
+        red[3][wid] = emax2;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) {
+            gl = fmin(gl, red[0][w]);
+            gu = fmax(gu, red[1][w]);
+            onenrm = fmax(onenrm, red[2][w]);
+            emax2 = fmax(emax2, red[3][w]);
+        }
+        const double safmin = 2.2250738585072014e-308;
+        const double pivmin = safmin * fmax(1.0, emax2);
+        const double tnorm = fmax(fabs(gl), fabs(gu));
+        params[0] = gl - (2.0 * 2.220446049250313e-16 * tnorm * n + 2.0 * pivmin);
+        params[1] = gu + (2.0 * 2.220446049250313e-16 * tnorm * n + 2.0 * pivmin);
+        params[2] = pivmin;
+        params[3] = onenrm;  // exact zero flags T == 0
+    }
+}
+
 // one warp per wanted eigenvalue; j-th largest = ascending index n-1-j
-__global__ void bisect_k(const double* __restrict__ d, const double* __restrict__ e2, int n, int want, double gl,
-                         double gu, double pivmin, double* values) {
+__global__ void bisect_k(const double* __restrict__ d, const double* __restrict__ e, int n, int want,
+                         const double* __restrict__ params, double* values) {
     const int warps = (gridDim.x * blockDim.x) >> 5;
     const int lane = threadIdx.x & 31;
+    const double gl = params[0], gu = params[1], pivmin = params[2];
+    const bool zero = params[3] == 0.0;
     for (int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < want; j += warps) {
+        if (zero) {  // T == 0: eigenvalues exactly zero
+            if (lane == 0) values[j] = 0.0;
+            continue;
+        }
         const int k = n - 1 - j;  // want lambda_k (ascending): count(lo) <= k < count(hi)
         double lo = gl, hi = gu;
         for (int it = 0; it < 40; ++it) {
@@ -65,7 +119,7 @@ __global__ void bisect_k(const double* __restrict__ d, const double* __restrict_
             const double tol = 2.0 * 2.220446049250313e-16 * fmax(fabs(lo), fabs(hi)) + 2.0 * pivmin;
             if (w <= tol) break;
             const double x = lo + w * static_cast<double>(lane + 1) / 33.0;
-            const int c = sturm_count(d, e2, n, x, pivmin);
+            const int c = sturm_count(d, e, n, x, pivmin);
             const unsigned above = __ballot_sync(0xffffffffu, c >= k + 1);
             if (above == 0u) {
                 lo = __shfl_sync(0xffffffffu, x, 31);
@@ -92,14 +146,23 @@ __device__ __forceinline__ double hash_uniform(unsigned long long seed, long i) 
     return static_cast<double>(z >> 11) * 0x1.0p-53 * 2.0 - 1.0;
 }
 
-// Inverse iteration, one warp per cluster (clusters are contiguous runs of the
-// wanted eigenvalues in descending order: [cstart[c], cstart[c+1])).
+// Inverse iteration, one warp per cluster. Clusters are the maximal runs of the
+// wanted eigenvalues (descending) with consecutive gaps <= ortol; warp s takes
+// the cluster starting at s, if one does (found here, no host round trip).
 __global__ void inverse_iteration_k(const double* __restrict__ d, const double* __restrict__ e, int n,
-                                    const double* __restrict__ values, const int* __restrict__ cstart, int nclusters,
-                                    double onenrm, double* vecs, long ldv, double* scratch) {
+                                    const double* __restrict__ values, int want, const double* __restrict__ params,
+                                    double* vecs, long ldv, double* scratch) {
     const int warps = (gridDim.x * blockDim.x) >> 5;
     const int lane = threadIdx.x & 31;
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const double onenrm_raw = params[3];
+    if (onenrm_raw == 0.0) {
+        // T == 0: the unit vectors e_{n-1-j} (as Eigen returns)
+        for (int j = gw; j < want; j += warps)
+            for (int i = lane; i < n; i += 32) vecs[static_cast<long>(j) * ldv + i] = i == n - 1 - j ? 1.0 : 0.0;
+        return;
+    }
+    const double onenrm = fmax(onenrm_raw, 1e-300);
     const double eps = 2.220446049250313e-16;
     const double eps3 = eps * onenrm;
     const double ortol = kClusterTol * onenrm;
@@ -109,11 +172,14 @@ __global__ void inverse_iteration_k(const double* __restrict__ d, const double* 
     double* lm = u2 + n;
     double* piv = lm + n;
     double* y = piv + n;
-    for (int c = gw; c < nclusters; c += warps) {
+    for (int c0 = gw; c0 < want; c0 += warps) {
+        if (c0 > 0 && !(values[c0 - 1] - values[c0] > ortol)) continue;  // not a cluster start
+        int c1 = c0 + 1;
+        while (c1 < want && !(values[c1 - 1] - values[c1] > ortol)) ++c1;
         double xjm = 0.0;
-        for (int j = cstart[c]; j < cstart[c + 1]; ++j) {
+        for (int j = c0; j < c1; ++j) {
             double xj = values[j];
-            if (j > cstart[c]) {
+            if (j > c0) {
                 // descending order inside the cluster: keep shifts strictly separated
                 const double pertol = 10.0 * fabs(eps * xj);
                 if (xjm - xj < pertol) xj = xjm - pertol;
@@ -185,7 +251,7 @@ __global__ void inverse_iteration_k(const double* __restrict__ d, const double* 
                 }
                 __syncwarp();
                 // MGS against earlier members of the cluster that are within ortol
-                for (int p = cstart[c]; p < j; ++p) {
+                for (int p = c0; p < j; ++p) {
                     if (fabs(values[p] - values[j]) > ortol) continue;
                     const double* xp = vecs + static_cast<long>(p) * ldv;
                     double dp = 0.0;
@@ -230,60 +296,19 @@ void tridiag_eig_top(Context& ctx, Index n_, const double* d, const double* e, I
                      View vectors) {
     const int n = static_cast<int>(n_), want = static_cast<int>(want_);
     if (n <= 0 || want <= 0) return;
-    // host copy of (d, e) for the bounds (n <= 4096: small)
-    std::vector<double> hd(n), he(std::max(n - 1, 1), 0.0);
-    ctx.read(d, hd.data(), n);
-    if (n > 1) ctx.read(e, he.data(), n - 1);
-    double gl = INFINITY, gu = -INFINITY, emax2 = 0.0, onenrm = 0.0;
-    for (int i = 0; i < n; ++i) {
-        const double el = i > 0 ? std::fabs(he[i - 1]) : 0.0, er = i < n - 1 ? std::fabs(he[i]) : 0.0;
-        gl = std::min(gl, hd[i] - el - er);
-        gu = std::max(gu, hd[i] + el + er);
-        onenrm = std::max(onenrm, std::fabs(hd[i]) + el + er);
-        if (i < n - 1) emax2 = std::max(emax2, he[i] * he[i]);
-    }
-    if (onenrm == 0.0) {
-        // T == 0: eigenvalues exactly zero, eigenvectors the unit vectors (as Eigen returns)
-        BLWS_CUDA(cudaMemsetAsync(values, 0, sizeof(double) * want, ctx.stream()));
-        fill(ctx, vectors.left(want), 0.0);
-        std::vector<double> one(1, 1.0);
-        for (int j = 0; j < want; ++j) ctx.write(vectors.p + (n - 1 - j) + static_cast<long>(j) * vectors.ld, one.data(), 1);
-        return;
-    }
-    const double safmin = 2.2250738585072014e-308;
-    const double pivmin = safmin * std::max(1.0, emax2);
-    const double tnorm = std::max(std::fabs(gl), std::fabs(gu));
-    gl -= 2.0 * 2.220446049250313e-16 * tnorm * n + 2.0 * pivmin;
-    gu += 2.0 * 2.220446049250313e-16 * tnorm * n + 2.0 * pivmin;
-    onenrm = std::max(onenrm, 1e-300);
-
-    std::vector<double> he2(std::max(n - 1, 1), 0.0);
-    for (int i = 0; i + 1 < n; ++i) he2[i] = he[i] * he[i];
-    DBuf<double> e2(ctx, static_cast<size_t>(std::max(n - 1, 1)));
-    ctx.write(e2.get(), he2.data(), std::max(n - 1, 1));
-
+    // three launches, no host round trip (the bounds stay on the device)
+    DBuf<double> params(ctx, 4);
+    tridiag_bounds_k<<<1, kBoundsThreads, 0, ctx.stream()>>>(d, e, n, params.get());
+    ctx.note_launch();
+    ctx.check_launch("tridiag_bounds_k");
     const int threads = 256, wpb = threads / 32;
-    bisect_k<<<static_cast<unsigned>((want + wpb - 1) / wpb), threads, 0, ctx.stream()>>>(d, e2.get(), n, want, gl, gu,
-                                                                                          pivmin, values);
+    const int blocks = (want + wpb - 1) / wpb;
+    bisect_k<<<static_cast<unsigned>(blocks), threads, 0, ctx.stream()>>>(d, e, n, want, params.get(), values);
     ctx.note_launch();
     ctx.check_launch("bisect_k");
-
-    std::vector<double> hv(want);
-    ctx.read(values, hv.data(), want);
-    std::vector<int> cs;
-    cs.push_back(0);
-    const double ortol = kClusterTol * onenrm;
-    for (int j = 1; j < want; ++j)
-        if (hv[j - 1] - hv[j] > ortol) cs.push_back(j);
-    cs.push_back(want);
-    const int ncl = static_cast<int>(cs.size()) - 1;
-    DBuf<int> dcs(ctx, cs.size());
-    BLWS_CUDA(cudaMemcpyAsync(dcs.get(), cs.data(), sizeof(int) * cs.size(), cudaMemcpyHostToDevice, ctx.stream()));
-    ctx.sync();
-    const int blocks = (ncl + wpb - 1) / wpb;
     DBuf<double> scratch(ctx, static_cast<size_t>(blocks) * wpb * 6 * n);
     inverse_iteration_k<<<static_cast<unsigned>(blocks), threads, 0, ctx.stream()>>>(
-        d, e, n, values, dcs.get(), ncl, onenrm, vectors.p, vectors.ld, scratch.get());
+        d, e, n, values, want, params.get(), vectors.p, vectors.ld, scratch.get());
     ctx.note_launch();
     ctx.check_launch("inverse_iteration_k");
 }

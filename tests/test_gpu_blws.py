@@ -200,3 +200,93 @@ def test_svt_blws_backend_grows_rank(G, O):
     assert err <= 2e-4 and abs(err - ref_err) <= 1e-8
     assert rg.achieved_rank == 10
     assert opg.application_count() == opo.application_count()
+
+
+def _pinned_colmajor(w):
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(w.T)).pin_memory()  # row-major W^T == column-major W
+
+
+def test_assign_async_matches_sync(G, O):
+    rs = np.random.default_rng(5)
+    m, n = 300, 200
+    w1, w2 = rs.standard_normal((m, n)), rs.standard_normal((m, n))
+    x, y = rs.standard_normal((m, 7)), rs.standard_normal((n, 7))
+    op = G.DenseOperator(w1)
+    h = _pinned_colmajor(w2)
+    op.assign_async(h.data_ptr(), m)
+    top, bot = op.apply_pair_block(x, y)
+    assert np.abs(top - w2 @ y).max() <= 1e-12 and np.abs(bot - w2.T @ x).max() <= 1e-12
+    # the reference's non-finite check (linear_operator.hpp:113-116) fires at the next use
+    w3 = w2.copy()
+    w3[5, 7] = np.nan
+    h3 = _pinned_colmajor(w3)
+    op.assign_async(h3.data_ptr(), m)
+    with pytest.raises(ValueError):
+        op.apply_pair_block(x, y)
+
+
+def test_assign_async_double_buffered_solves(G, O):
+    # the bench's e2e pattern: upload W_{i+1} into the idle operator while W_i solves
+    rs = np.random.default_rng(11)
+    m, n, r = 240, 180, 8
+    ctx = G.Context(0)
+    ws = [O.Rng(100 + i).gaussian_matrix(m, n) for i in range(4)]
+    hs = [_pinned_colmajor(w) for w in ws]
+    ops = [G.DenseOperator(np.zeros((m, n)), ctx=ctx), G.DenseOperator(np.zeros((m, n)), ctx=ctx)]
+    ops[0].assign_async(hs[0].data_ptr(), m)
+    for i, w in enumerate(ws):
+        if i + 1 < len(ws):
+            ops[(i + 1) % 2].assign_async(hs[i + 1].data_ptr(), m)
+        u, v, s = exact_warm(O, w + 1e-3 * rs.standard_normal((m, n)), r)
+        got = G.blws_svd(ops[i % 2], G.WarmStart(u, v, s), 2, r, G.Rng(3))
+        ref = O.blws_svd(O.DenseOperator(w), O.WarmStart(u, v, s), 2, r, O.Rng(3))
+        assert np.abs(got.warm.sigma - ref.warm.sigma).max() <= 1e-10 * ref.warm.sigma.max()
+        assert principal_angle(got.warm.u, ref.warm.u) <= 1e-8
+
+
+def _run_svd(G, w, warm, k, r, seed, monkeypatch, exact):
+    if exact:
+        monkeypatch.setenv("BLWS_EXACT", "1")
+    else:
+        monkeypatch.delenv("BLWS_EXACT", raising=False)
+    return G.blws_svd(G.DenseOperator(w), warm, k, r, G.Rng(seed))
+
+
+@pytest.mark.parametrize("m,n,r,k", [(500, 400, 20, 2), (300, 300, 12, 3), (260, 200, 30, 1), (1200, 900, 64, 2)])
+def test_deferred_path_bitwise_equals_exact_path(G, O, m, n, r, k, monkeypatch):
+    # the single-round-trip path replays the exact path's host tests; where it
+    # is taken its results must be the exact path's, bit for bit
+    rng = O.Rng(m + 7 * n + r)
+    w = rng.gaussian_matrix(m, n) * 1e-3
+    u0, s0, v0 = O.full_svd_small(rng.gaussian_matrix(m, n))
+    w += (u0[:, :2 * r] * (100.0 * 0.9 ** np.arange(2 * r))) @ v0[:, :2 * r].T
+    wu, wv, ws = exact_warm(O, w + 1e-2 * rng.gaussian_matrix(m, n), r)
+    warm = G.WarmStart(wu, wv, ws)
+    f0 = G.deferred_fallbacks()
+    fast = _run_svd(G, w, warm, k, r, 5, monkeypatch, exact=False)
+    assert G.deferred_fallbacks() == f0, "deferred path fell back on a common-case input"
+    ex = _run_svd(G, w, warm, k, r, 5, monkeypatch, exact=True)
+    assert np.array_equal(fast.warm.sigma, ex.warm.sigma)
+    assert np.array_equal(fast.warm.u, ex.warm.u) and np.array_equal(fast.warm.v, ex.warm.v)
+    assert (fast.padded, fast.k_raised, fast.terminated_early) == (ex.padded, ex.k_raised, ex.terminated_early)
+    ref = O.blws_svd(O.DenseOperator(w), O.WarmStart(wu, wv, ws), k, r, O.Rng(5))
+    assert np.abs(fast.warm.sigma - ref.warm.sigma).max() <= 1e-10 * ref.warm.sigma.max()
+
+
+def test_deferred_path_falls_back_on_breakdown(G, O, monkeypatch):
+    # warm start spanning an exact invariant subspace: the Lanczos residual is
+    # ~0 (breakdown, block_lanczos.hpp:103) -> the deferred replay must detect it
+    m, n, r = 200, 150, 8
+    rng = O.Rng(77)
+    u0, _, v0 = O.full_svd_small(rng.gaussian_matrix(m, n))
+    s = 10.0 * 0.8 ** np.arange(r)
+    w = (u0[:, :r] * s) @ v0[:, :r].T
+    warm = G.WarmStart(u0[:, :r].copy(order="F"), v0[:, :r].copy(order="F"), s.copy())
+    f0 = G.deferred_fallbacks()
+    fast = _run_svd(G, w, warm, 2, r, 9, monkeypatch, exact=False)
+    assert G.deferred_fallbacks() == f0 + 1
+    ex = _run_svd(G, w, warm, 2, r, 9, monkeypatch, exact=True)
+    assert fast.terminated_early and ex.terminated_early
+    assert np.array_equal(fast.warm.sigma, ex.warm.sigma) and np.array_equal(fast.warm.u, ex.warm.u)
