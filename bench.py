@@ -185,12 +185,14 @@ def run_gpu(args):
         return res
 
     torch.cuda.synchronize()
+    # profiling on before the warm-ups: the CUDA graph blws_svd captures on its
+    # third call then carries the K1 timing stamps into the timed replays
+    ctx.set_profiling(True)
     for _ in range(args.warmup):
         step()
     ctx.synchronize()
 
     # ---- timed region: device-resident inputs, L2 flushed between steps
-    ctx.set_profiling(True)
     ctx.region_reset()
     launches0 = ctx.launches
     ev = []
@@ -212,6 +214,7 @@ def run_gpu(args):
         ctx.synchronize()
         torch.cuda.synchronize()
     launches = ctx.launches - launches0
+    graphs_used = B.graph_launches()
     step_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = float(sum(step_ms))
     k1 = ctx.region_stats(0)

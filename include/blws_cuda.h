@@ -124,6 +124,12 @@ int blws_warm_start_destroy(blws_warm_start* w);
    away from the common case (breakdown, rank loss, ill-conditioned Gram,
    keep < min(r, d)). BLWS_EXACT=1 in the environment forces the exact path. */
 int64_t blws_svd_deferred_fallbacks(void);
+/* Number of blws_svd calls (process-wide) served by replaying a captured CUDA
+   graph of the deferred launch sequence (cached per operator data and
+   (rank, k, r); captured on the second call with the same key, replayed after).
+   BLWS_GRAPHS=0 disables the graphs; they are also skipped while region
+   profiling is on. */
+int64_t blws_svd_graph_launches(void);
 /* blws_svd (block_lanczos.hpp:204-261). flags: bit0 padded, bit1 k_raised,
  * bit2 terminated_early. *out receives a new warm start of rank r. */
 int blws_svd(blws_operator* w, const blws_warm_start* warm, int64_t k, int64_t r, blws_rng* rng,

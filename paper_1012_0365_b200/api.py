@@ -82,6 +82,7 @@ SIGNATURES = {
     "blws_warm_start_get": (ci, [vp, vp, i64, vp, i64, vp, ci]),
     "blws_warm_start_destroy": (ci, [vp]),
     "blws_svd_deferred_fallbacks": (i64, []),
+    "blws_svd_graph_launches": (i64, []),
     "blws_svd": (ci, [vp, vp, i64, i64, vp, P(vp), P(ci)]),
     "blws_adapt_subspace": (ci, [vp, vp, i64, i64, i64, vp, P(vp)]),
     "blws_block_lanczos_procedure": (ci, [vp, i64, vp, i64, vp, vp, P(i64), P(ci)]),
@@ -431,6 +432,11 @@ def blws_svd(op: LinearOperator, warm, k: int, r: int, rng: Rng, keep_device=Fal
 def deferred_fallbacks() -> int:
     """blws_svd calls redone on the exact path (blws_svd_deferred_fallbacks)."""
     return int(lib().blws_svd_deferred_fallbacks())
+
+
+def graph_launches() -> int:
+    """blws_svd calls served by a captured CUDA graph (blws_svd_graph_launches)."""
+    return int(lib().blws_svd_graph_launches())
 
 
 def adapt_subspace(warm, r_new, m, n, rng: Rng, ctx: Context | None = None) -> WarmStart:

@@ -311,6 +311,7 @@ int blws_warm_start_destroy(blws_warm_start* w) {
 
 // ---------------------------------------------------------- block lanczos
 int64_t blws_svd_deferred_fallbacks(void) { return blws::g_blws_deferred_fallbacks; }
+int64_t blws_svd_graph_launches(void) { return blws::g_blws_graph_launches; }
 int blws_svd(blws_operator* w, const blws_warm_start* warm, int64_t k, int64_t r, blws_rng* rng,
              blws_warm_start** out, int* flags) {
     return guard([&] {

@@ -69,6 +69,17 @@ public:
     /// total ms, count, flops, bytes of region `id` (syncs; resolves events)
     void region_stats(int id, double* ms, std::int64_t* count, double* flops, double* bytes);
     void region_reset();
+    /// Regions inside a graph capture (profiling on at capture) are timed by
+    /// one-thread %globaltimer stamp kernels writing into `stamps` (event
+    /// record nodes cannot be used with cudaEventElapsedTime).
+    struct CapturedRegion {
+        int id, b, e;  // stamp indices
+        double flops, bytes;
+    };
+    void begin_region_capture(std::uint64_t* stamps, int cap);
+    std::vector<CapturedRegion> end_region_capture();
+    /// After a replay has completed: add its region times to the stats.
+    void add_replayed_regions(const std::vector<CapturedRegion>& regions, const std::uint64_t* stamps);
     std::int64_t launches() const { return launches_; }
     void check_launch(const char* what);
 
@@ -87,6 +98,12 @@ private:
         std::int64_t count = 0;
     };
     Region regions_[8];
+    bool capturing_ = false;
+    std::uint64_t* stamps_ = nullptr;
+    int nstamps_ = 0, stamp_cap_ = 0;
+    int open_[8] = {};
+    std::vector<CapturedRegion> captured_;
+    void stamp(int idx);
     void ensure_pinned(size_t bytes);
 };
 

@@ -1,4 +1,5 @@
 // Device context: stream, stream-ordered pool allocator, pinned staging.
+#include <algorithm>
 #include <cstring>
 
 #include "common.cuh"
@@ -18,7 +19,27 @@ Context::Context(int device) : device_(device) {
     ensure_pinned(1 << 20);
 }
 
+namespace {
+__global__ void stamp_k(std::uint64_t* out) {
+    std::uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    *out = t;
+}
+}  // namespace
+
+void Context::stamp(int idx) {
+    if (idx >= stamp_cap_) throw std::logic_error("region stamps exhausted");
+    stamp_k<<<1, 1, 0, stream_>>>(stamps_ + idx);
+    check_launch("stamp_k");
+}
+
 void Context::region_begin(int id) {
+    if (capturing_) {
+        if (!profiling_) return;
+        open_[id] = nstamps_++;
+        stamp(open_[id]);
+        return;
+    }
     if (!profiling_) return;
     cudaEvent_t e;
     BLWS_CUDA(cudaEventCreate(&e));
@@ -27,6 +48,13 @@ void Context::region_begin(int id) {
 }
 
 void Context::region_end(int id, double flops, double bytes) {
+    if (capturing_) {
+        if (!profiling_) return;
+        const int e = nstamps_++;
+        stamp(e);
+        captured_.push_back(CapturedRegion{id, open_[id], e, flops, bytes});
+        return;
+    }
     if (!profiling_) return;
     cudaEvent_t e;
     BLWS_CUDA(cudaEventCreate(&e));
@@ -53,6 +81,37 @@ void Context::region_stats(int id, double* ms, std::int64_t* count, double* flop
     *count = r.count;
     *flops = r.flops;
     *bytes = r.bytes;
+}
+
+void Context::begin_region_capture(std::uint64_t* stamps, int cap) {
+    capturing_ = true;
+    stamps_ = stamps;
+    stamp_cap_ = cap;
+    nstamps_ = 0;
+    captured_.clear();
+}
+
+std::vector<Context::CapturedRegion> Context::end_region_capture() {
+    capturing_ = false;
+    stamps_ = nullptr;
+    stamp_cap_ = 0;
+    return std::move(captured_);
+}
+
+void Context::add_replayed_regions(const std::vector<CapturedRegion>& regions, const std::uint64_t* stamps) {
+    if (!profiling_ || regions.empty()) return;
+    int n = 0;
+    for (const auto& c : regions) n = std::max(n, std::max(c.b, c.e) + 1);
+    std::vector<std::uint64_t> h(static_cast<size_t>(n));
+    BLWS_CUDA(cudaMemcpyAsync(h.data(), stamps, sizeof(std::uint64_t) * n, cudaMemcpyDeviceToHost, stream_));
+    BLWS_CUDA(cudaStreamSynchronize(stream_));
+    for (const auto& c : regions) {
+        Region& r = regions_[c.id];
+        r.ms += 1e-6 * static_cast<double>(h[static_cast<size_t>(c.e)] - h[static_cast<size_t>(c.b)]);
+        r.flops += c.flops;
+        r.bytes += c.bytes;
+        r.count += 1;
+    }
 }
 
 void Context::region_reset() {

@@ -43,6 +43,8 @@ private:
 /// Device-resident W with the reference's application counter
 /// (core/linear_operator.hpp:20-98). Only the paired products the augmented
 /// view needs are exposed (augmented_operator.hpp:39-57).
+struct SvdGraph;  // captured blws_svd launch sequence (host_core.cu)
+
 class LinearOperator {
 public:
     explicit LinearOperator(Context& ctx) : ctx_(ctx) {}
@@ -66,6 +68,10 @@ public:
     /// its verdict (nonzero = non-finite entries) written to the device int
     /// `*flag`, instead of the synchronous check at the next use.
     virtual void defer_pending_check(int* flag) { (void)flag; }
+    /// Identity of the data the kernels read (graph cache key).
+    virtual const void* data_key() const { return this; }
+    void add_applications(std::int64_t n) { count_ += n; }
+    std::vector<std::shared_ptr<SvdGraph>>& svd_graphs() { return svd_graphs_; }
 
 protected:
     virtual void pair_block_impl(View left, View right, View top, View bot) = 0;
@@ -74,6 +80,7 @@ protected:
 
 private:
     std::int64_t count_ = 0;
+    std::vector<std::shared_ptr<SvdGraph>> svd_graphs_;
 };
 
 /// DenseOperator (linear_operator.hpp:102-131): column-major W on the device,
@@ -101,6 +108,7 @@ public:
     /// overlap) until that use.
     void assign_host_async(const double* w, Index ldw);
     void defer_pending_check(int* flag) override;
+    const void* data_key() const override { return p_; }
     /// Device copy with the non-finite check.
     void assign_device(const double* w, Index ldw);
     /// Non-finite scan of the held matrix (throws std::invalid_argument).
@@ -182,6 +190,7 @@ DWarm adapt_subspace(Context& ctx, const DWarm* warm, Index r_new, Index m, Inde
 /// blws_svd (block_lanczos.hpp:204-261).
 BlwsResult blws_svd(LinearOperator& w, const DWarm& warm, Index k, Index r, Rng& rng);
 extern std::int64_t g_blws_deferred_fallbacks;
+extern std::int64_t g_blws_graph_launches;
 
 /// Factorisation for tests: block_lanczos_procedure on the augmented view.
 struct BlockLanczos {

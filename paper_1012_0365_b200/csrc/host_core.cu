@@ -848,38 +848,34 @@ bool force_exact() {
 
 }  // namespace
 
-std::int64_t g_blws_deferred_fallbacks = 0;  // diagnostics (tests)
+namespace {
 
-BlwsResult blws_svd(LinearOperator& w, const DWarm& warm, Index k, Index r, Rng& rng) {
+struct DeferredShape {
+    Index m, n, bs, k, r, k_eff, d, want;
+    bool k_raised;
+};
+
+struct DeferredRecs {
+    QrRec q1{}, qu{}, qv{};
+    LanczosRec lrec;
+    int vslot = -1;
+};
+
+// blws_svd's common case as one launch sequence with no host reads (capturable
+// as a CUDA graph): input the warm panel `src` (ld x bs), output the next warm
+// panel in `next_uv` (ld x want) and the slots.
+DeferredRecs enqueue_deferred(LinearOperator& w, View src, const DeferredShape& sh, Slots& sl, View next_uv) {
     Context& ctx = w.ctx();
-    const Index m = w.rows(), n = w.cols();
-    const Index bs = warm.rank();
-    if (bs < 1 || r < 1 || r > std::min(m, n) || warm.geo.m != m || warm.geo.n != n)
-        return blws_svd_exact(w, warm, k, r, rng);  // throws the reference's errors
-    Index k_eff = k;
-    bool k_raised = false;
-    if (r > k_eff * bs) {
-        k_eff = (r + bs - 1) / bs;
-        k_raised = true;
-    }
-    k_eff = std::max<Index>(std::min(k_eff, (m + n) / bs), 1);
-    const Index d = k_eff * bs, want = std::min(r, d);
-    // keep < r needs the Rng padding: the exact path owns that case
-    if (force_exact() || want < r || k < 1 || k * bs > m + n) return blws_svd_exact(w, warm, k, r, rng);
-
-    const Stack geo{m, n};
-    Slots sl(ctx, 16 * static_cast<int>(k_eff + 3) + static_cast<int>(want) + 8);
-    const int finite_slot = sl.take();
-    w.defer_pending_check(reinterpret_cast<int*>(sl.at(finite_slot)));  // async-assigned W: checked in the same read
-    DMat x1(ctx, geo.ld(), bs, false);
-    copy(ctx, x1.view(), warm.panel());
-    QrRec q1;
+    const Stack geo{sh.m, sh.n};
+    DeferredRecs rec;
+    DMat x1(ctx, geo.ld(), sh.bs, false);
+    copy(ctx, x1.view(), src);
     {
         View xv = x1.view();
-        q1 = thin_qr_deferred(ctx, xv, nullptr, sl);
+        rec.q1 = thin_qr_deferred(ctx, xv, nullptr, sl);
     }
-    LanczosRec lrec;
-    BlockLanczos fac = block_lanczos_deferred(w, x1.view(), k_eff, sl, lrec);
+    BlockLanczos fac = block_lanczos_deferred(w, x1.view(), sh.k_eff, sl, rec.lrec);
+    const Index bs = sh.bs, d = sh.d, want = sh.want;
     DMat t(ctx, d, d, true);
     for (Index l = 0; l < fac.built; ++l) {
         place_block(ctx, t.view().sub(l * bs, l * bs, bs, bs), fac.m[l].view(), false);
@@ -888,43 +884,183 @@ BlwsResult blws_svd(LinearOperator& w, const DWarm& warm, Index k, Index r, Rng&
             place_block(ctx, t.view().sub(l * bs, l * bs + bs, bs, bs), fac.b[l].view(), true);
         }
     }
-    const int vslot = sl.take(static_cast<int>(want));
+    rec.vslot = sl.take(static_cast<int>(want));
     DMat vecs(ctx, d, want, false);
     ctx.region_begin(1);
-    sym_evd_top(ctx, t.view(), want, sl.at(vslot), vecs.view());
+    sym_evd_top(ctx, t.view(), want, sl.at(rec.vslot), vecs.view());
     ctx.region_end(1, 0.0, 0.0);
-    const Index keep = want;  // assumed; verified below
-    DWarm next = make_warm(ctx, m, n, keep);
-    gemm(ctx, false, false, geo.ld(), keep, d, std::sqrt(2.0), fac.q.data(), fac.q.ld, vecs.data(), vecs.ld, 0.0,
-         next.uv.data(), next.uv.ld);
-    QrRec qu, qv;
-    {
-        View u = next.u(), v = next.v();
-        qu = thin_qr_deferred(ctx, u, nullptr, sl);
-        qv = thin_qr_deferred(ctx, v, nullptr, sl);
-    }
-    sl.fetch(ctx);  // the one host round trip
-    if (sl.as_int(finite_slot) != 0) throw std::invalid_argument("DenseOperator: non-finite entries");
+    // keep = want is assumed (verified by finish_deferred); lift + sqrt(2) unpack
+    gemm(ctx, false, false, geo.ld(), want, d, std::sqrt(2.0), fac.q.data(), fac.q.ld, vecs.data(), vecs.ld, 0.0,
+         next_uv.p, next_uv.ld);
+    View u{next_uv.p, sh.m, want, next_uv.ld}, v{next_uv.p + geo.mp(), sh.n, want, next_uv.ld};
+    rec.qu = thin_qr_deferred(ctx, u, nullptr, sl);
+    rec.qv = thin_qr_deferred(ctx, v, nullptr, sl);
+    return rec;
+}
 
-    // replay the exact path's host tests
+// the exact path's host tests on the fetched slots
+bool finish_deferred(const DeferredRecs& rec, const Slots& sl, const DeferredShape& sh) {
     Index rank = 0;
-    bool ok = qr_check(q1, sl, bs, &rank) && lanczos_check(lrec, sl, bs) && qr_check(qu, sl, keep, &rank) &&
-              qr_check(qv, sl, keep, &rank);
-    const double* hv = sl.h.data() + vslot;
-    for (Index i = 0; ok && i < want; ++i) ok = std::isfinite(hv[i]);
-    if (ok) {
-        const double floor = 1e-12 * std::fabs(hv[0]);
-        Index kept = 0;
-        while (kept < want && hv[kept] > floor) ++kept;
-        ok = kept == keep;
+    if (!qr_check(rec.q1, sl, sh.bs, &rank) || !lanczos_check(rec.lrec, sl, sh.bs) ||
+        !qr_check(rec.qu, sl, sh.want, &rank) || !qr_check(rec.qv, sl, sh.want, &rank))
+        return false;
+    const double* hv = sl.h.data() + rec.vslot;
+    for (Index i = 0; i < sh.want; ++i)
+        if (!std::isfinite(hv[i])) return false;
+    const double floor = 1e-12 * std::fabs(hv[0]);
+    Index kept = 0;
+    while (kept < sh.want && hv[kept] > floor) ++kept;
+    return kept == sh.want;
+}
+
+bool graphs_enabled() {
+    const char* e = std::getenv("BLWS_GRAPHS");
+    return !(e && std::string(e) == "0");
+}
+
+}  // namespace
+
+/// A captured deferred blws_svd for one (operator data, bs, k, r): stable input
+/// and output panels around a CUDA graph of the whole launch sequence. The
+/// kernel nodes live in device memory, so there is no per-kernel command fetch
+/// over PCIe (which an async upload saturates) and no per-launch host cost.
+struct SvdGraph {
+    const void* key_data = nullptr;
+    Index bs = 0, k = 0, r = 0;
+    int seen = 0;
+    bool failed = false;
+    cudaGraphExec_t exec = nullptr;
+    std::unique_ptr<Slots> sl;
+    DMat src, next;
+    DeferredRecs rec;
+    int finite_slot = 0;
+    std::int64_t launches = 0, applications = 0;
+    std::vector<Context::CapturedRegion> regions;  // K1 / EVD / thin_qr, timed by stamp nodes
+    DBuf<std::uint64_t> stamps;
+    ~SvdGraph() {
+        if (exec) cudaGraphExecDestroy(exec);
     }
-    if (!ok) {
+};
+
+std::int64_t g_blws_deferred_fallbacks = 0;  // diagnostics (tests)
+std::int64_t g_blws_graph_launches = 0;
+
+BlwsResult blws_svd(LinearOperator& w, const DWarm& warm, Index k, Index r, Rng& rng) {
+    Context& ctx = w.ctx();
+    const Index m = w.rows(), n = w.cols();
+    const Index bs = warm.rank();
+    if (bs < 1 || r < 1 || r > std::min(m, n) || warm.geo.m != m || warm.geo.n != n)
+        return blws_svd_exact(w, warm, k, r, rng);  // throws the reference's errors
+    DeferredShape sh{m, n, bs, k, r, k, 0, 0, false};
+    if (r > sh.k_eff * bs) {
+        sh.k_eff = (r + bs - 1) / bs;
+        sh.k_raised = true;
+    }
+    sh.k_eff = std::max<Index>(std::min(sh.k_eff, (m + n) / bs), 1);
+    sh.d = sh.k_eff * bs;
+    sh.want = std::min(r, sh.d);
+    // keep < r needs the Rng padding: the exact path owns that case
+    if (force_exact() || sh.want < r || k < 1 || k * bs > m + n) return blws_svd_exact(w, warm, k, r, rng);
+    const Stack geo{m, n};
+    const int cap = 16 * static_cast<int>(sh.k_eff + 3) + static_cast<int>(sh.want) + 8;
+
+    // ---- graph plan for this (operator data, shape); eager on first sight
+    SvdGraph* plan = nullptr;
+    if (graphs_enabled()) {
+        for (auto& g : w.svd_graphs())
+            if (g->key_data == w.data_key() && g->bs == bs && g->k == k && g->r == r) plan = g.get();
+        if (!plan) {
+            auto g = std::make_shared<SvdGraph>();
+            g->key_data = w.data_key();
+            g->bs = bs;
+            g->k = k;
+            g->r = r;
+            w.svd_graphs().push_back(g);
+            plan = g.get();
+        }
+        // captured on the third call with this key (one-off shapes stay eager:
+        // capture + instantiate costs tens of ms)
+        if (plan->failed || (!plan->exec && plan->seen++ < 2)) plan = nullptr;
+    }
+
+    std::unique_ptr<Slots> local;
+    Slots* sl = nullptr;
+    DeferredRecs rec;
+    DWarm next;
+    int finite_slot = 0;
+    if (plan) {
+        if (!plan->exec) {
+            // capture once: stable buffers outside the graph, temporaries inside
+            plan->sl = std::make_unique<Slots>(ctx, cap);
+            plan->finite_slot = plan->sl->take();
+            plan->src = DMat(ctx, geo.ld(), bs, false);
+            plan->next = DMat(ctx, geo.ld(), sh.want, true);
+            plan->stamps = DBuf<std::uint64_t>(ctx, 64);
+        }
+        sl = plan->sl.get();
+        finite_slot = plan->finite_slot;
+        // a pending async upload is waited for and checked outside the graph
+        zero(ctx, sl->at(finite_slot), sizeof(double));
+        w.defer_pending_check(reinterpret_cast<int*>(sl->at(finite_slot)));
+        if (!plan->exec) {
+            const std::int64_t l0 = ctx.launches(), a0 = w.application_count();
+            BLWS_CUDA(cudaStreamBeginCapture(ctx.stream(), cudaStreamCaptureModeRelaxed));
+            ctx.begin_region_capture(plan->stamps.get(), 64);
+            cudaGraph_t graph = nullptr;
+            bool captured = true;
+            try {
+                plan->rec = enqueue_deferred(w, plan->src.view(), sh, *plan->sl, plan->next.view());
+            } catch (...) {
+                captured = false;
+            }
+            plan->regions = ctx.end_region_capture();
+            const cudaError_t ce = cudaStreamEndCapture(ctx.stream(), &graph);
+            cudaError_t ie = cudaErrorUnknown;
+            if (captured && ce == cudaSuccess) ie = cudaGraphInstantiate(&plan->exec, graph, 0);
+            if (graph) cudaGraphDestroy(graph);
+            // the capture's host-side counts are re-added per replay
+            plan->launches = ctx.launches() - l0;
+            plan->applications = w.application_count() - a0;
+            ctx.note_launch(-plan->launches);
+            w.add_applications(-plan->applications);
+            if (ie != cudaSuccess) {
+                cudaGetLastError();  // clear a capture error; run eagerly from now on
+                plan->exec = nullptr;
+                plan->failed = true;
+            }
+        }
+    }
+    const bool graphed = plan && plan->exec;
+    if (graphed) {
+        copy(ctx, plan->src.view(), warm.panel());
+        BLWS_CUDA(cudaGraphLaunch(plan->exec, ctx.stream()));
+        ctx.note_launch(plan->launches);
+        w.add_applications(plan->applications);
+        ++g_blws_graph_launches;
+        rec = plan->rec;
+    } else {
+        local = std::make_unique<Slots>(ctx, cap);
+        sl = local.get();
+        finite_slot = sl->take();
+        w.defer_pending_check(reinterpret_cast<int*>(sl->at(finite_slot)));  // async-assigned W
+        next = make_warm(ctx, m, n, sh.want);
+        rec = enqueue_deferred(w, warm.panel(), sh, *sl, next.panel());
+    }
+    sl->fetch(ctx);  // the one host round trip
+    if (graphed) ctx.add_replayed_regions(plan->regions, plan->stamps.get());
+    if (sl->as_int(finite_slot) != 0) throw std::invalid_argument("DenseOperator: non-finite entries");
+    if (!finish_deferred(rec, *sl, sh)) {
         ++g_blws_deferred_fallbacks;
         return blws_svd_exact(w, warm, k, r, rng);
     }
+    if (graphed) {
+        next = make_warm(ctx, m, n, sh.want);
+        copy(ctx, next.panel(), plan->next.view().left(sh.want));
+    }
     BlwsResult out;
-    out.k_raised = k_raised;
-    next.sigma.assign(hv, hv + keep);
+    out.k_raised = sh.k_raised;
+    const double* hv = sl->h.data() + rec.vslot;
+    next.sigma.assign(hv, hv + sh.want);
     out.warm = std::move(next);
     return out;
 }

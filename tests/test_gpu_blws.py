@@ -290,3 +290,31 @@ def test_deferred_path_falls_back_on_breakdown(G, O, monkeypatch):
     ex = _run_svd(G, w, warm, 2, r, 9, monkeypatch, exact=True)
     assert fast.terminated_early and ex.terminated_early
     assert np.array_equal(fast.warm.sigma, ex.warm.sigma) and np.array_equal(fast.warm.u, ex.warm.u)
+
+
+def test_graph_replay_bitwise_equals_eager(G, O, monkeypatch):
+    # calls 1-2 eager, call 3 captures + replays, call 4 replays: all identical,
+    # and identical to the graph-free path (BLWS_GRAPHS=0)
+    m, n, r = 700, 500, 24
+    rng = O.Rng(123)
+    u0, _, v0 = O.full_svd_small(rng.gaussian_matrix(m, n))
+    w = (u0[:, :2 * r] * (50.0 * 0.9 ** np.arange(2 * r))) @ v0[:, :2 * r].T + 1e-3 * rng.gaussian_matrix(m, n)
+    wu, wv, ws = exact_warm(O, w + 1e-2 * rng.gaussian_matrix(m, n), r)
+    monkeypatch.delenv("BLWS_EXACT", raising=False)
+    monkeypatch.delenv("BLWS_GRAPHS", raising=False)
+    op = G.DenseOperator(w)
+    warm = G.DeviceWarmStart.from_host(wu, wv, ws, op.ctx)
+    g0 = G.graph_launches()
+    op.ctx.set_profiling(True)
+    op.ctx.region_reset()
+    outs = [G.blws_svd(op, warm, 2, r, G.Rng(1)) for _ in range(4)]
+    assert G.graph_launches() == g0 + 2
+    assert op.application_count() == 4 * 2 * r  # k = 2 blocks of r columns per call, replays counted
+    k1 = op.ctx.region_stats(0)  # region events are graph nodes: replays are timed too
+    assert k1["count"] == 4 * 2 and k1["ms"] > 0
+    op.ctx.set_profiling(False)
+    monkeypatch.setenv("BLWS_GRAPHS", "0")
+    eager = G.blws_svd(G.DenseOperator(w), warm, 2, r, G.Rng(1))
+    for o in outs:
+        assert np.array_equal(o.warm.sigma, eager.warm.sigma)
+        assert np.array_equal(o.warm.u, eager.warm.u) and np.array_equal(o.warm.v, eager.warm.v)

@@ -21,8 +21,10 @@ def main(steps=10):
     warm = B.DeviceWarmStart.from_host(U, V, s, ctx)
     big_h = torch.empty(128 * 1024 * 1024 // 8, dtype=torch.float64).pin_memory()
     big_d = torch.empty_like(big_h, device="cuda")
+    small_h = torch.empty(8 * 1024 * 1024 // 8, dtype=torch.float64).pin_memory()
+    small_d = torch.empty_like(small_h, device="cuda")
     side = torch.cuda.Stream()
-    for label, bg in (("quiet", False), ("with H2D stream", True), ("quiet", False)):
+    for label, bg in (("quiet", False), ("H2D 128MB target", True), ("H2D 8MB target", "small"), ("quiet", False)):
         for _ in range(2):
             B.blws_svd(op, warm, 2, bench.R, B.Rng(7), keep_device=True)
         ctx.synchronize()
@@ -32,8 +34,12 @@ def main(steps=10):
         for _ in range(steps):
             if bg:
                 with torch.cuda.stream(side):
-                    for _ in range(3):
-                        big_d.copy_(big_h, non_blocking=True)
+                    if bg == "small":
+                        for _ in range(48):
+                            small_d.copy_(small_h, non_blocking=True)
+                    else:
+                        for _ in range(3):
+                            big_d.copy_(big_h, non_blocking=True)
             t = time.perf_counter()
             B.blws_svd(op, warm, 2, bench.R, B.Rng(7), keep_device=True)
             ctx.synchronize()
@@ -41,6 +47,19 @@ def main(steps=10):
             torch.cuda.synchronize()
         st = [ctx.region_stats(i) for i in range(3)]
         ctx.set_profiling(False)
+        # the same with the captured graph (profiling off)
+        gt = []
+        for _ in range(steps):
+            if bg:
+                with torch.cuda.stream(side):
+                    for _ in range(3):
+                        big_d.copy_(big_h, non_blocking=True)
+            t = time.perf_counter()
+            B.blws_svd(op, warm, 2, bench.R, B.Rng(7), keep_device=True)
+            ctx.synchronize()
+            gt.append(time.perf_counter() - t)
+            torch.cuda.synchronize()
+        print(f"{label:18s} graph svd {1e3 * np.median(gt):6.2f} ms", flush=True)
         print(f"{label:18s} svd {1e3 * np.median(times):6.2f} ms  K1 {st[0]['ms'] / steps:6.3f}  "
               f"EVD {st[1]['ms'] / steps:6.3f}  thin_qr {st[2]['ms'] / steps:6.3f} ms/call", flush=True)
 
