@@ -262,6 +262,7 @@ __global__ void __launch_bounds__(kOrmWarps * 32) ormtr_k(const double* __restri
 }  // namespace
 
 bool sytrd_cluster(Context& ctx, View t, double* lp, double* d, double* e, double* tau);
+bool sytrd_fused(Context& ctx, View t, double* lp, double* d, double* e, double* tau);
 
 void sym_evd_top(Context& ctx, View t, Index want, double* values, View vectors) {
     const int n = static_cast<int>(t.rows);
@@ -283,7 +284,8 @@ void sym_evd_top(Context& ctx, View t, Index want, double* values, View vectors)
         cfg = true;
     }
     const int smem = static_cast<int>(head + (on_chip ? np * 8 : 0));
-    if (!sytrd_cluster(ctx, t, lp.get(), d.get(), e.get(), tau.get())) {
+    if (!sytrd_cluster(ctx, t, lp.get(), d.get(), e.get(), tau.get()) &&
+        !sytrd_fused(ctx, t, lp.get(), d.get(), e.get(), tau.get())) {
     if (on_chip)
         sytrd_k<true><<<1, kThreads, smem, ctx.stream()>>>(t.p, t.ld, n, lp.get(), d.get(), e.get(), tau.get());
     else

@@ -1,0 +1,249 @@
+// Householder tridiagonalisation of T (K4, stage 1), LAPACK dsytd2 (lower)
+// semantics, one CTA, for orders n <= 208 (the packed lower triangle on chip).
+//
+// Single-pass formulation: every step reads and writes each trailing element
+// once, and no phase runs on a single warp. Step k (v_k known):
+//   [S]  sweep over columns j >= k+1: apply the pending rank-2 update of step
+//        k-1 to each element, then accumulate p = A22 v_k from the updated
+//        value -- rows in per-lane registers (row i = lane + 32 q), columns as
+//        per-warp dots (column j = wid + 16 c), reduced by a batched transpose;
+//   [P1] one row per thread: p_i = tau_k (column dot + row partials), p^T v;
+//   [P2] w_i = p_i - K v_i; look-ahead: apply update k to column k+1 (element
+//        i per thread) and its sum of squares below the subdiagonal;
+//   [P3] every thread forms beta, tau_{k+1}, v_{k+1} and stores its reflector
+//        element; four block barriers per step.
+// Thread ownership in [S] is static: row i >= column j needs q >= c / 2, so
+// the unrolled loops cover exactly that slot triangle; only the q = c / 2 slot
+// carries a lane predicate. v and w are double-buffered by step parity and zero
+// outside the trailing range (the pending update is a no-op there).
+// Output equals sytrd_k's layout (packed lower + reflectors, d, e, tau).
+#include "ops.cuh"
+
+namespace blws {
+namespace {
+
+constexpr int kFT = 512;  // 16 warps
+constexpr int kFW = kFT / 32;
+
+__device__ __forceinline__ int floff(int j, int n) { return j * n - ((j * (j - 1)) >> 1); }
+
+__device__ __forceinline__ double warp_sum(double x) {
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    return x;
+}
+
+// [P3] shared by the prologue and the loop: from the sum of squares `s2` of
+// column c below the subdiagonal (already updated) and alpha = A(c+1, c), form
+// the reflector; thread i (= row) writes v[i] and the packed reflector.
+__device__ __forceinline__ void form_reflector(double* a, int n, int c, double s2, double xi, double* v, double* d,
+                                               double* e, double* tau, double* tau_out) {
+    const int i = threadIdx.x;
+    double* colc = a + floff(c, n);  // colc[r - c] = A(r, c)
+    const double alpha = colc[1];
+    double tk = 0.0, beta = alpha, scl = 0.0;
+    if (s2 > 0.0) {
+        beta = -copysign(sqrt(fma(alpha, alpha, s2)), alpha);
+        tk = (beta - alpha) / beta;
+        scl = 1.0 / (alpha - beta);
+    }
+    if (i < n) {
+        double vi = 0.0;
+        if (i > c) vi = tk == 0.0 ? 0.0 : (i == c + 1 ? 1.0 : xi * scl);
+        v[i] = vi;
+        if (i > c) colc[i - c] = vi;  // the reflector below the diagonal of column c
+    }
+    if (i == 0) {
+        d[c] = colc[0];
+        e[c] = beta;
+        tau[c] = tk;
+    }
+    *tau_out = tk;
+}
+
+template <int QN>
+__global__ void __launch_bounds__(kFT) sytrd_fused_k(const double* __restrict__ t, long ld, int n, double* lp,
+                                                     double* d, double* e, double* tau) {
+    constexpr int NP = 32 * QN;  // padded vector length (<= kFT)
+    constexpr int CN = 2 * QN;   // column classes per warp
+    extern __shared__ __align__(16) double sm[];
+    double* vb = sm;             // 2 x NP: v_k by parity
+    double* wb = vb + 2 * NP;    // 2 x NP: w_k by parity
+    double* pcol = wb + 2 * NP;  // NP: column-dot part of p, then p
+    double* red = pcol + NP;     // 64
+    double* pw = red + 64;       // kFW x NP: row part of p per warp
+    double* a = pw + kFW * NP;   // packed lower triangle
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int row = threadIdx.x;  // [P] phases: one row per thread
+
+    for (int j = wid; j < n; j += kFW)
+        for (int i = j + lane; i < n; i += 32) a[floff(j, n) + (i - j)] = 0.5 * (t[i + j * ld] + t[j + i * ld]);
+    for (int i = threadIdx.x; i < 4 * NP; i += kFT) vb[i] = 0.0;  // vb and wb
+    __syncthreads();
+    // prologue: reflector of column 0
+    double tk;
+    {
+        const double xi = row < n ? a[row] : 0.0;  // column 0 packed at offset 0
+        double s2 = warp_sum(row >= 2 && row < n ? xi * xi : 0.0);
+        if (lane == 0) red[wid] = s2;
+        __syncthreads();
+        s2 = warp_sum(lane < kFW ? red[lane] : 0.0);
+        form_reflector(a, n, 0, s2, xi, vb, d, e, tau, &tk);
+        __syncthreads();
+    }
+
+    for (int k = 0; k < n - 2; ++k) {
+        const int par = k & 1;
+        const double* v = vb + par * NP;         // v_k
+        const double* vo = vb + (1 - par) * NP;  // v_{k-1}
+        const double* wo = wb + (1 - par) * NP;  // w_{k-1}
+        double* wn = wb + par * NP;              // w_k
+        double* vn = vb + (1 - par) * NP;        // v_{k+1} (overwrites v_{k-1} after [S])
+        // ---- [S] fused sweep: pending update k-1, then p = A22 v_k
+        {
+            double vr[QN], vor[QN], wor[QN], acc[QN], dp[CN];
+#pragma unroll
+            for (int q = 0; q < QN; ++q) {
+                const int i = lane + 32 * q;
+                vr[q] = v[i];
+                vor[q] = vo[i];
+                wor[q] = wo[i];
+                acc[q] = 0.0;
+            }
+#pragma unroll
+            for (int c = 0; c < CN; ++c) {
+                dp[c] = 0.0;
+                const int j = wid + 16 * c;
+                if (j <= k || j >= n) continue;  // warp-uniform
+                const double vj = v[j], voj = vo[j], woj = wo[j];
+                double* col = a + floff(j, n) - j;  // col[i] = A(i, j)
+#pragma unroll
+                for (int q = c / 2; q < QN; ++q) {
+                    const int i = lane + 32 * q;
+                    const bool ok = (q != c / 2 || i >= j) && (q != QN - 1 || i < n);
+                    if (ok) {
+                        const double x = col[i] - fma(vor[q], woj, wor[q] * voj);
+                        col[i] = x;
+                        acc[q] = fma(x, vj, acc[q]);
+                        if (i > j) dp[c] = fma(x, vr[q], dp[c]);
+                    }
+                }
+            }
+            // column dots: batched transpose-reduce of the CN (<= 16) values
+            double r[16];
+#pragma unroll
+            for (int c = 0; c < 16; ++c) r[c] = c < CN ? dp[c] : 0.0;
+#pragma unroll
+            for (int stage = 0; stage < 4; ++stage) {
+                const int half = 8 >> stage, o = 16 >> stage;
+                const bool hi = (lane & o) != 0;
+#pragma unroll
+                for (int c = 0; c < half; ++c) {
+                    const double send = hi ? r[c] : r[c + half];
+                    const double keep = hi ? r[c + half] : r[c];
+                    r[c] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+                }
+            }
+            r[0] += __shfl_xor_sync(0xffffffffu, r[0], 1);
+            const int cc = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+            const int jj = wid + 16 * cc;
+            if ((lane & 1) == 0 && cc < CN && jj > k && jj < n) pcol[jj] = r[0];
+#pragma unroll
+            for (int q = 0; q < QN; ++q) pw[wid * NP + lane + 32 * q] = acc[q];
+        }
+        __syncthreads();
+        // ---- [P1] p_i = tau (column dot + row partials), p^T v
+        double p = 0.0;
+        if (row > k && row < n) {
+            double sacc = pcol[row];
+#pragma unroll
+            for (int ww = 0; ww < kFW; ++ww) sacc += pw[ww * NP + row];
+            p = tk * sacc;
+        }
+        const double vi = row < NP ? v[row] : 0.0;
+        double pv = warp_sum(p * vi);
+        if (lane == 0) red[wid] = pv;
+        if (row < NP) pcol[row] = p;  // pcol now holds p (row k+1 read in [P2])
+        __syncthreads();
+        // ---- [P2] w = p - K v; look-ahead update of column k+1 and its norm
+        const double K = 0.5 * tk * warp_sum(lane < kFW ? red[lane] : 0.0);
+        const double wi = fma(-K, vi, p);
+        if (row < NP) wn[row] = wi;
+        const int c1 = k + 1;
+        const double wc = fma(-K, v[c1], pcol[c1]), vc = v[c1];  // w_{k+1}, v_{k+1} entries of step k
+        double xi = 0.0;
+        if (row >= c1 && row < n) {
+            double* col1 = a + floff(c1, n) - c1;
+            xi = col1[row] - fma(vi, wc, wi * vc);
+            col1[row] = xi;
+        }
+        double s2 = warp_sum(row >= c1 + 2 && row < n ? xi * xi : 0.0);
+        if (lane == 0) red[32 + wid] = s2;  // second half: red[0..] may still be read for K
+        __syncthreads();
+        // ---- [P3] reflector of column k+1 (if any)
+        if (k + 1 < n - 2) {
+            s2 = warp_sum(lane < kFW ? red[32 + lane] : 0.0);
+            form_reflector(a, n, c1, s2, xi, vn, d, e, tau, &tk);
+        }
+        __syncthreads();
+    }
+    // the last update (step n-3) is already applied to column n-2 by the
+    // look-ahead; column n-1 (one element) still needs it
+    if (threadIdx.x == 0 && n >= 2) {
+        const int kl = n - 3;
+        double* c2 = a + floff(n - 2, n);  // c2[0] = A(n-2, n-2), c2[1] = A(n-1, n-2)
+        double* c1 = a + floff(n - 1, n);  // c1[0] = A(n-1, n-1)
+        if (kl >= 0) {
+            const double* vl = vb + (kl & 1) * NP;
+            const double* wl = wb + (kl & 1) * NP;
+            c1[0] -= fma(vl[n - 1], wl[n - 1], wl[n - 1] * vl[n - 1]);
+        }
+        d[n - 2] = c2[0];
+        e[n - 2] = c2[1];
+        tau[n - 2] = 0.0;
+        d[n - 1] = c1[0];
+        tau[n - 1] = 0.0;
+    }
+    __syncthreads();
+    const long np = static_cast<long>(n) * (n + 1) / 2;
+    for (long idx = threadIdx.x; idx < np; idx += kFT) lp[idx] = a[idx];
+}
+
+template <int QN>
+size_t fused_smem(int n) {
+    constexpr int NP = 32 * QN;
+    return (5L * NP + 64 + static_cast<long>(kFW) * NP + static_cast<long>(n) * (n + 1) / 2) * 8;
+}
+
+template <int QN>
+bool launch_fused(Context& ctx, View t, int n, double* lp, double* d, double* e, double* tau) {
+    const size_t bytes = fused_smem<QN>(n);
+    if (bytes > 220u * 1024u) return false;
+    static bool cfg = false;
+    if (!cfg) {
+        BLWS_CUDA(cudaFuncSetAttribute(sytrd_fused_k<QN>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+        cfg = true;
+    }
+    sytrd_fused_k<QN><<<1, kFT, bytes, ctx.stream()>>>(t.p, t.ld, n, lp, d, e, tau);
+    ctx.note_launch();
+    ctx.check_launch("sytrd_fused_k");
+    return true;
+}
+
+}  // namespace
+
+bool sytrd_fused(Context& ctx, View t, double* lp, double* d, double* e, double* tau) {
+    const int n = static_cast<int>(t.rows);
+    if (n < 3) return false;
+    switch ((n + 31) / 32) {
+        case 1: return launch_fused<1>(ctx, t, n, lp, d, e, tau);
+        case 2: return launch_fused<2>(ctx, t, n, lp, d, e, tau);
+        case 3: return launch_fused<3>(ctx, t, n, lp, d, e, tau);
+        case 4: return launch_fused<4>(ctx, t, n, lp, d, e, tau);
+        case 5: return launch_fused<5>(ctx, t, n, lp, d, e, tau);
+        case 6: return launch_fused<6>(ctx, t, n, lp, d, e, tau);
+        case 7: return launch_fused<7>(ctx, t, n, lp, d, e, tau);
+        default: return false;
+    }
+}
+
+}  // namespace blws
