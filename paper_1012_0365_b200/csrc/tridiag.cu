@@ -26,36 +26,43 @@ namespace {
 constexpr double kClusterTol = 1e-5;
 
 // Number of eigenvalues < x: sign changes of the Sturm sequence
-// p_i = det(T_i - x I), p_i = (d_i - x) p_{i-1} - e_{i-1}^2 p_{i-2}
-// (division-free: two dependent FMAs per step instead of a division), with
-// exact power-of-two rescaling against over/underflow. A zero p_i takes the
-// sign opposite to p_{i-1} (dstebz's pivmin convention in the ratio form).
-__device__ __forceinline__ int sturm_count(const double* d, const double* e, int n, double x, double pivmin) {
-    double p0 = 1.0, p1 = d[0] - x;
-    if (p1 == 0.0) p1 = -pivmin;
+// p_i = det(T_i - x I) = (d_i - x) p_{i-1} - e_{i-1}^2 p_{i-2}, evaluated
+// division-free (a dependent FMA per step instead of a ~130-cycle divide) on T
+// scaled by an exact power of two s with ||sT||_1 <= 1, so |p| grows at most
+// 3x per step. Inputs (shared memory): ds = s d, e2s = (s e)^2, or -1 where
+// (s e)^2 < 2^-200, which splits T (the recurrence restarts; an eigenvalue
+// perturbation <= 2^-100 ||T||). A zero p_i becomes -2^-200 p_{i-1} (dstebz's
+// -pivmin pivot, in scaled units). Every 4 steps the pair is renormalised by an
+// exact power of two; per step max(|p_i|, |p_{i+1}|) >= (e^2 / 4) max(|p_{i-1}|,
+// |p_i|) >= 2^-202 of it, so nothing reaches the subnormal range in between.
+__device__ __forceinline__ int sturm_count(const double* ds, const double* e2s, int n, double xs) {
+    constexpr double kRepl = 0x1p-200;
+    double p0 = 1.0, p1 = ds[0] - xs;
+    p1 = p1 == 0.0 ? -kRepl : p1;
     int cnt = p1 < 0.0;
+#pragma unroll 4
     for (int i = 1; i < n; ++i) {
-        const double e2 = e[i - 1] * e[i - 1];
-        double p2 = fma(d[i] - x, p1, -e2 * p0);
-        if (p2 == 0.0) p2 = p1 > 0.0 ? -pivmin * fabs(p1) : pivmin * fabs(p1);
-        cnt += (p2 < 0.0) != (p1 < 0.0);
-        const double a = fabs(p2);
-        if (a > 0x1p+600) {
-            p1 *= 0x1p-600;
-            p2 *= 0x1p-600;
-        } else if (a < 0x1p-600) {
-            p1 *= 0x1p+600;
-            p2 *= 0x1p+600;
-        }
-        p0 = p1;
+        const double e2 = e2s[i - 1];
+        const double p1s = e2 < 0.0 ? 1.0 : p1;
+        double p2 = fma(ds[i] - xs, p1s, -fmax(e2, 0.0) * p0);
+        p2 = p2 == 0.0 ? -kRepl * p1s : p2;
+        cnt += (p2 < 0.0) != (p1s < 0.0);
+        p0 = p1s;
         p1 = p2;
+        if ((i & 3) == 0) {
+            // renormalise (p0, p1) so the larger magnitude is in [1, 2)
+            const int ex = (__double2hiint(fmax(fabs(p0), fabs(p1))) >> 20) & 0x7ff;
+            const double sc = __hiloint2double((2046 - ex) << 20, 0);  // 2^(1023 - ex)
+            p0 *= sc;
+            p1 *= sc;
+        }
     }
     return cnt;
 }
 
 // Bisection interval, pivmin and ||T||_1 (dstebz's Gershgorin set-up), on the
 // device so the eigensolver needs no host round trip. params: gl, gu, pivmin,
-// onenrm (0 => T == 0).
+// onenrm (0 => T == 0), the power-of-two scale 2^-E >= 1 / ||T||_1.
 constexpr int kBoundsThreads = 512;
 __global__ void __launch_bounds__(kBoundsThreads) tridiag_bounds_k(const double* __restrict__ d,
                                                                     const double* __restrict__ e, int n,
@@ -97,6 +104,9 @@ __global__ void __launch_bounds__(kBoundsThreads) tridiag_bounds_k(const double*
         params[1] = gu + (2.0 * 2.220446049250313e-16 * tnorm * n + 2.0 * pivmin);
         params[2] = pivmin;
         params[3] = onenrm;  // exact zero flags T == 0
+        int ex = 0;
+        frexp(onenrm, &ex);  // onenrm < 2^ex
+        params[4] = onenrm > 0.0 ? ldexp(1.0, -ex) : 1.0;
     }
 }
 
@@ -105,8 +115,20 @@ __global__ void bisect_k(const double* __restrict__ d, const double* __restrict_
                          const double* __restrict__ params, double* values) {
     const int warps = (gridDim.x * blockDim.x) >> 5;
     const int lane = threadIdx.x & 31;
-    const double gl = params[0], gu = params[1], pivmin = params[2];
+    const double gl = params[0], gu = params[1], pivmin = params[2], scale = params[4];
     const bool zero = params[3] == 0.0;
+    extern __shared__ __align__(16) double tsm[];
+    double* ds = tsm;      // n: s d
+    double* e2s = tsm + n;  // n: (s e)^2, -1 marks a split
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        ds[i] = d[i] * scale;
+        if (i < n - 1) {
+            const double es = e[i] * scale;
+            const double e2 = es * es;
+            e2s[i] = e2 < 0x1p-200 ? -1.0 : e2;
+        }
+    }
+    __syncthreads();
     for (int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < want; j += warps) {
         if (zero) {  // T == 0: eigenvalues exactly zero
             if (lane == 0) values[j] = 0.0;
@@ -119,7 +141,7 @@ __global__ void bisect_k(const double* __restrict__ d, const double* __restrict_
             const double tol = 2.0 * 2.220446049250313e-16 * fmax(fabs(lo), fabs(hi)) + 2.0 * pivmin;
             if (w <= tol) break;
             const double x = lo + w * static_cast<double>(lane + 1) / 33.0;
-            const int c = sturm_count(d, e, n, x, pivmin);
+            const int c = sturm_count(ds, e2s, n, x * scale);
             const unsigned above = __ballot_sync(0xffffffffu, c >= k + 1);
             if (above == 0u) {
                 lo = __shfl_sync(0xffffffffu, x, 31);
@@ -149,12 +171,18 @@ __device__ __forceinline__ double hash_uniform(unsigned long long seed, long i) 
 // Inverse iteration, one warp per cluster. Clusters are the maximal runs of the
 // wanted eigenvalues (descending) with consecutive gaps <= ortol; warp s takes
 // the cluster starting at s, if one does (found here, no host round trip).
-__global__ void inverse_iteration_k(const double* __restrict__ d, const double* __restrict__ e, int n,
-                                    const double* __restrict__ values, int want, const double* __restrict__ params,
-                                    double* vecs, long ldv, double* scratch) {
-    const int warps = (gridDim.x * blockDim.x) >> 5;
+// One warp per block: the LU of T - lambda I, the right-hand side, the iterate
+// and (d, e) live in shared memory (9 n doubles); the serial recurrences carry
+// their state in registers (lane 0), loads are independent of the chain.
+constexpr int kInvitMaxN = 2048;
+__global__ void __launch_bounds__(32) inverse_iteration_k(const double* __restrict__ d_g,
+                                                           const double* __restrict__ e_g, int n,
+                                                           const double* __restrict__ values, int want,
+                                                           const double* __restrict__ params, double* vecs, long ldv) {
+    extern __shared__ __align__(16) double ism[];
+    const int warps = gridDim.x;
     const int lane = threadIdx.x & 31;
-    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int gw = blockIdx.x;
     const double onenrm_raw = params[3];
     if (onenrm_raw == 0.0) {
         // T == 0: the unit vectors e_{n-1-j} (as Eigen returns)
@@ -162,16 +190,24 @@ __global__ void inverse_iteration_k(const double* __restrict__ d, const double* 
             for (int i = lane; i < n; i += 32) vecs[static_cast<long>(j) * ldv + i] = i == n - 1 - j ? 1.0 : 0.0;
         return;
     }
-    const double onenrm = fmax(onenrm_raw, 1e-300);
-    const double eps = 2.220446049250313e-16;
-    const double eps3 = eps * onenrm;
-    const double ortol = kClusterTol * onenrm;
-    double* u0 = scratch + static_cast<long>(gw) * 6 * n;
+    double* d = ism;
+    double* e = d + n;   // e[n-1] = 0
+    double* u0 = e + n;  // reciprocal pivots
     double* u1 = u0 + n;
     double* u2 = u1 + n;
     double* lm = u2 + n;
     double* piv = lm + n;
     double* y = piv + n;
+    double* x = y + n;
+    for (int i = lane; i < n; i += 32) {
+        d[i] = d_g[i];
+        e[i] = i < n - 1 ? e_g[i] : 0.0;
+    }
+    __syncwarp();
+    const double onenrm = fmax(onenrm_raw, 1e-300);
+    const double eps = 2.220446049250313e-16;
+    const double eps3 = eps * onenrm;
+    const double ortol = kClusterTol * onenrm;
     for (int c0 = gw; c0 < want; c0 += warps) {
         if (c0 > 0 && !(values[c0 - 1] - values[c0] > ortol)) continue;  // not a cluster start
         int c1 = c0 + 1;
@@ -185,41 +221,31 @@ __global__ void inverse_iteration_k(const double* __restrict__ d, const double* 
                 if (xjm - xj < pertol) xj = xjm - pertol;
             }
             xjm = xj;
-            double* x = vecs + static_cast<long>(j) * ldv;
+            double* xg = vecs + static_cast<long>(j) * ldv;
+            for (int i = lane; i < n; i += 32) x[i] = hash_uniform(0x5eedull + static_cast<unsigned long long>(j), i);
             if (lane == 0) {
-                // LU of T - xj I with partial pivoting
-                double a = d[0] - xj, b = n > 1 ? e[0] : 0.0;
+                // LU of T - xj I with partial pivoting (dstein's dlagtf), reciprocal pivots
+                double a = d[0] - xj, b = e[0];
                 for (int k = 0; k < n - 1; ++k) {
                     const double ck = e[k];
                     const double an = d[k + 1] - xj;
-                    const double bn = k + 1 < n - 1 ? e[k + 1] : 0.0;
-                    if (fabs(a) >= fabs(ck)) {
-                        const double l = a != 0.0 ? ck / a : 0.0;
-                        u0[k] = a;
-                        u1[k] = b;
-                        u2[k] = 0.0;
-                        lm[k] = l;
-                        piv[k] = 0.0;
-                        a = an - l * b;
-                        b = bn;
-                    } else {
-                        const double l = a / ck;
-                        u0[k] = ck;
-                        u1[k] = an;
-                        u2[k] = bn;
-                        lm[k] = l;
-                        piv[k] = 1.0;
-                        a = b - l * an;
-                        b = -l * bn;
-                    }
+                    const double bn = e[k + 1];
+                    const bool sw = !(fabs(a) >= fabs(ck));
+                    const double num = sw ? a : ck, den = sw ? ck : a;
+                    const double l = den != 0.0 ? num / den : 0.0;
+                    const double pv = sw ? ck : a;
+                    u0[k] = fabs(pv) < eps3 ? (pv >= 0.0 ? 1.0 / eps3 : -1.0 / eps3) : 1.0 / pv;
+                    u1[k] = sw ? an : b;
+                    u2[k] = sw ? bn : 0.0;
+                    lm[k] = l;
+                    piv[k] = sw ? 1.0 : 0.0;
+                    const double na = sw ? fma(-l, an, b) : fma(-l, b, an);
+                    b = sw ? -l * bn : bn;
+                    a = na;
                 }
-                u0[n - 1] = a;
-                for (int k = 0; k < n; ++k) {
-                    if (fabs(u0[k]) < eps3) u0[k] = u0[k] >= 0.0 ? eps3 : -eps3;
-                    y[k] = 1.0 / u0[k];  // reciprocal pivots (y is reused as rhs below)
-                }
-                for (int k = 0; k < n; ++k) u0[k] = y[k];
-                for (long i = 0; i < n; ++i) x[i] = hash_uniform(0x5eedull + static_cast<unsigned long long>(j), i);
+                u0[n - 1] = fabs(a) < eps3 ? (a >= 0.0 ? 1.0 / eps3 : -1.0 / eps3) : 1.0 / a;
+                u1[n - 1] = 0.0;  // read (times zero) by the back substitution
+                u2[n - 1] = 0.0;
             }
             __syncwarp();
             // dstein: iterate until the solution grows past sqrt(0.1 / n), then once more
@@ -231,22 +257,26 @@ __global__ void inverse_iteration_k(const double* __restrict__ d, const double* 
                 for (int i = lane; i < n; i += 32) s1 += fabs(x[i]);
                 for (int o = 16; o > 0; o >>= 1) s1 += __shfl_xor_sync(0xffffffffu, s1, o);
                 const double scl = static_cast<double>(n) * onenrm * fmax(eps, fabs(1.0 / u0[n - 1])) / fmax(s1, 1e-300);
+                for (int i = lane; i < n; i += 32) y[i] = x[i] * scl;
                 __syncwarp();
                 if (lane == 0) {
-                    for (int i = 0; i < n; ++i) y[i] = x[i] * scl;
+                    // forward: L^{-1} P y, state in registers
+                    double cur = y[0];
                     for (int k = 0; k < n - 1; ++k) {
-                        if (piv[k] != 0.0) {
-                            const double tmp = y[k];
-                            y[k] = y[k + 1];
-                            y[k + 1] = tmp;
-                        }
-                        y[k + 1] -= lm[k] * y[k];
+                        double nxt = y[k + 1];
+                        const bool sw = piv[k] != 0.0;
+                        const double lo = sw ? nxt : cur, hi = sw ? cur : nxt;
+                        y[k] = lo;
+                        cur = fma(-lm[k], lo, hi);
                     }
+                    y[n - 1] = cur;
+                    // backward: U^{-1}
+                    double x1 = 0.0, x2 = 0.0;  // x[k+1], x[k+2]
                     for (int k = n - 1; k >= 0; --k) {
-                        double v = y[k];
-                        if (k + 1 < n) v -= u1[k] * x[k + 1];
-                        if (k + 2 < n) v -= u2[k] * x[k + 2];
-                        x[k] = v * u0[k];
+                        const double v = fma(-u2[k], x2, fma(-u1[k], x1, y[k])) * u0[k];
+                        x[k] = v;
+                        x2 = x1;
+                        x1 = v;
                     }
                 }
                 __syncwarp();
@@ -286,6 +316,8 @@ __global__ void inverse_iteration_k(const double* __restrict__ d, const double* 
                 __syncwarp();
                 if (amax >= dtpcrt && ++extra >= 2) break;
             }
+            for (int i = lane; i < n; i += 32) xg[i] = x[i];
+            __syncwarp();
         }
     }
 }
@@ -297,18 +329,32 @@ void tridiag_eig_top(Context& ctx, Index n_, const double* d, const double* e, I
     const int n = static_cast<int>(n_), want = static_cast<int>(want_);
     if (n <= 0 || want <= 0) return;
     // three launches, no host round trip (the bounds stay on the device)
-    DBuf<double> params(ctx, 4);
+    DBuf<double> params(ctx, 5);
     tridiag_bounds_k<<<1, kBoundsThreads, 0, ctx.stream()>>>(d, e, n, params.get());
     ctx.note_launch();
     ctx.check_launch("tridiag_bounds_k");
-    const int threads = 256, wpb = threads / 32;
-    const int blocks = (want + wpb - 1) / wpb;
-    bisect_k<<<static_cast<unsigned>(blocks), threads, 0, ctx.stream()>>>(d, e, n, want, params.get(), values);
+    // bisection: one warp per eigenvalue and per block (latency-bound chains,
+    // spread over the SMs instead of sharing schedulers)
+    static bool cfg = false;
+    if (!cfg) {
+        BLWS_CUDA(cudaFuncSetAttribute(bisect_k, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+        cfg = true;
+    }
+    if (n > 4096) throw std::invalid_argument("tridiag_eig_top: order > 4096");
+    bisect_k<<<static_cast<unsigned>(want), 32, 2 * n * sizeof(double), ctx.stream()>>>(d, e, n, want, params.get(),
+                                                                                         values);
     ctx.note_launch();
     ctx.check_launch("bisect_k");
-    DBuf<double> scratch(ctx, static_cast<size_t>(blocks) * wpb * 6 * n);
-    inverse_iteration_k<<<static_cast<unsigned>(blocks), threads, 0, ctx.stream()>>>(
-        d, e, n, values, want, params.get(), vectors.p, vectors.ld, scratch.get());
+    // inverse iteration: one warp per candidate cluster start, one warp per block
+    if (n > kInvitMaxN) throw std::invalid_argument("tridiag_eig_top: order > 2048");
+    static bool cfg2 = false;
+    if (!cfg2) {
+        BLWS_CUDA(cudaFuncSetAttribute(inverse_iteration_k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       9 * kInvitMaxN * static_cast<int>(sizeof(double))));
+        cfg2 = true;
+    }
+    inverse_iteration_k<<<static_cast<unsigned>(want), 32, 9 * n * sizeof(double), ctx.stream()>>>(
+        d, e, n, values, want, params.get(), vectors.p, vectors.ld);
     ctx.note_launch();
     ctx.check_launch("inverse_iteration_k");
 }
