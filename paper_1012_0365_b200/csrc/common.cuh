@@ -46,7 +46,12 @@ public:
     Context(const Context&) = delete;
     Context& operator=(const Context&) = delete;
 
-    cudaStream_t stream() const { return stream_; }
+    /// The stream work is enqueued on: the main stream, or the auxiliary one
+    /// inside an AuxScope.
+    cudaStream_t stream() const { return cur_ ? cur_ : stream_; }
+    /// Fork/join onto a second compute stream (see AuxScope).
+    void fork_aux();
+    void join_aux();
     /// Second stream for host->device uploads that overlap queued kernels
     /// (created on first use; ordered against stream() with events).
     cudaStream_t copy_stream();
@@ -88,6 +93,8 @@ private:
     int sms_ = 148;
     cudaStream_t stream_ = nullptr;
     cudaStream_t copy_stream_ = nullptr;
+    cudaStream_t aux_ = nullptr, cur_ = nullptr;
+    cudaEvent_t fork_ev_ = nullptr, join_ev_ = nullptr;
     void* pinned_ = nullptr;
     size_t pinned_bytes_ = 0;
     std::int64_t launches_ = 0;
@@ -108,6 +115,22 @@ private:
 };
 
 /// Owning device buffer of doubles (or raw bytes), freed stream-ordered.
+/// Work enqueued while an AuxScope lives runs on the context's auxiliary stream,
+/// ordered after everything already queued on the main stream; the scope's end
+/// makes the main stream wait for it. Independent branches (the two products of
+/// a paired apply, the QRs of U and V) overlap; under graph capture they become
+/// parallel branches of the graph.
+class AuxScope {
+public:
+    explicit AuxScope(Context& ctx) : ctx_(ctx) { ctx_.fork_aux(); }
+    ~AuxScope() { ctx_.join_aux(); }
+    AuxScope(const AuxScope&) = delete;
+    AuxScope& operator=(const AuxScope&) = delete;
+
+private:
+    Context& ctx_;
+};
+
 template <typename T>
 class DBuf {
 public:

@@ -29,7 +29,7 @@ __global__ void stamp_k(std::uint64_t* out) {
 
 void Context::stamp(int idx) {
     if (idx >= stamp_cap_) throw std::logic_error("region stamps exhausted");
-    stamp_k<<<1, 1, 0, stream_>>>(stamps_ + idx);
+    stamp_k<<<1, 1, 0, stream()>>>(stamps_ + idx);
     check_launch("stamp_k");
 }
 
@@ -43,7 +43,7 @@ void Context::region_begin(int id) {
     if (!profiling_) return;
     cudaEvent_t e;
     BLWS_CUDA(cudaEventCreate(&e));
-    BLWS_CUDA(cudaEventRecord(e, stream_));
+    BLWS_CUDA(cudaEventRecord(e, stream()));
     regions_[id].begin.push_back(e);
 }
 
@@ -58,7 +58,7 @@ void Context::region_end(int id, double flops, double bytes) {
     if (!profiling_) return;
     cudaEvent_t e;
     BLWS_CUDA(cudaEventCreate(&e));
-    BLWS_CUDA(cudaEventRecord(e, stream_));
+    BLWS_CUDA(cudaEventRecord(e, stream()));
     regions_[id].end.push_back(e);
     regions_[id].flops += flops;
     regions_[id].bytes += bytes;
@@ -122,6 +122,26 @@ void Context::region_reset() {
     }
 }
 
+void Context::fork_aux() {
+    if (cur_) throw std::logic_error("fork_aux: nested fork");
+    if (!aux_) {
+        BLWS_CUDA(cudaStreamCreateWithFlags(&aux_, cudaStreamNonBlocking));
+        BLWS_CUDA(cudaEventCreateWithFlags(&fork_ev_, cudaEventDisableTiming));
+        BLWS_CUDA(cudaEventCreateWithFlags(&join_ev_, cudaEventDisableTiming));
+    }
+    BLWS_CUDA(cudaEventRecord(fork_ev_, stream_));
+    BLWS_CUDA(cudaStreamWaitEvent(aux_, fork_ev_, 0));
+    cur_ = aux_;
+}
+
+void Context::join_aux() {
+    if (!cur_) return;
+    cur_ = nullptr;
+    // no throw from a destructor path: record the failure for the next check
+    if (cudaEventRecord(join_ev_, aux_) != cudaSuccess || cudaStreamWaitEvent(stream_, join_ev_, 0) != cudaSuccess)
+        return;
+}
+
 cudaStream_t Context::copy_stream() {
     if (!copy_stream_) BLWS_CUDA(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking));
     return copy_stream_;
@@ -132,6 +152,12 @@ Context::~Context() {
     if (copy_stream_) {
         cudaStreamSynchronize(copy_stream_);
         cudaStreamDestroy(copy_stream_);
+    }
+    if (aux_) {
+        cudaStreamSynchronize(aux_);
+        cudaStreamDestroy(aux_);
+        cudaEventDestroy(fork_ev_);
+        cudaEventDestroy(join_ev_);
     }
     if (stream_) {
         cudaStreamSynchronize(stream_);
@@ -152,11 +178,11 @@ void Context::ensure_pinned(size_t bytes) {
 
 void* Context::alloc(size_t bytes) {
     void* p = nullptr;
-    BLWS_CUDA(cudaMallocAsync(&p, bytes, stream_));
+    BLWS_CUDA(cudaMallocAsync(&p, bytes, stream()));
     return p;
 }
 
-void Context::free(void* p) { cudaFreeAsync(p, stream_); }
+void Context::free(void* p) { cudaFreeAsync(p, stream()); }
 
 void Context::sync() { BLWS_CUDA(cudaStreamSynchronize(stream_)); }
 

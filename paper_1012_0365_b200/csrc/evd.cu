@@ -259,6 +259,85 @@ __global__ void __launch_bounds__(kOrmWarps * 32) ormtr_k(const double* __restri
         for (int i = lane; i < n; i += 32) z[i + j * ldz] = zc[i];
 }
 
+// Z = H_0 ... H_{n-3} Y with every reflector resident in shared memory (the
+// packed lower triangle, n <= 208) and each eigenvector in registers of one
+// warp (row i = lane + 32 q): no block barrier after the load, one warp
+// reduction per reflector. 4 warps per block (one per scheduler).
+constexpr int kOrmFullWarps = 4;
+template <int QN>
+__global__ void __launch_bounds__(kOrmFullWarps * 32) ormtr_full_k(const double* __restrict__ lp,
+                                                                    const double* __restrict__ tau, int n, int want,
+                                                                    double* z, long ldz) {
+    extern __shared__ __align__(16) double sm[];
+    double* ts = sm;      // n
+    double* a = sm + n;   // packed lower triangle with the reflectors
+    const long np = static_cast<long>(n) * (n + 1) / 2;
+    for (long idx = threadIdx.x; idx < np; idx += blockDim.x) a[idx] = lp[idx];
+    for (int i = threadIdx.x; i < n; i += blockDim.x) ts[i] = tau[i];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const long j = static_cast<long>(blockIdx.x) * kOrmFullWarps + warp;
+    if (j >= want) return;
+    double zr[QN];
+#pragma unroll
+    for (int q = 0; q < QN; ++q) {
+        const int i = lane + 32 * q;
+        zr[q] = i < n ? z[i + j * ldz] : 0.0;
+    }
+    for (int k = n - 3; k >= 0; --k) {
+        const double tk = ts[k];
+        if (tk == 0.0) continue;
+        const double* col = a + lidx(k, k, n) - k;  // col[i] = reflector entry of row i (i > k)
+        double s = 0.0;
+#pragma unroll
+        for (int q = 0; q < QN; ++q) {
+            const int i = lane + 32 * q;
+            if (i > k && i < n) s = fma(col[i], zr[q], s);
+        }
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        const double f = tk * s;
+#pragma unroll
+        for (int q = 0; q < QN; ++q) {
+            const int i = lane + 32 * q;
+            if (i > k && i < n) zr[q] = fma(-f, col[i], zr[q]);
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < QN; ++q) {
+        const int i = lane + 32 * q;
+        if (i < n) z[i + j * ldz] = zr[q];
+    }
+}
+
+template <int QN>
+bool launch_ormtr_full(Context& ctx, const double* lp, const double* tau, int n, int want, View z) {
+    const size_t bytes = (static_cast<size_t>(n) + static_cast<size_t>(n) * (n + 1) / 2) * sizeof(double);
+    if (bytes > 220u * 1024u) return false;
+    static bool cfg = false;
+    if (!cfg) {
+        BLWS_CUDA(cudaFuncSetAttribute(ormtr_full_k<QN>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+        cfg = true;
+    }
+    ormtr_full_k<QN><<<static_cast<unsigned>((want + kOrmFullWarps - 1) / kOrmFullWarps), kOrmFullWarps * 32, bytes,
+                       ctx.stream()>>>(lp, tau, n, want, z.p, z.ld);
+    ctx.note_launch();
+    ctx.check_launch("ormtr_full_k");
+    return true;
+}
+
+bool ormtr_full(Context& ctx, const double* lp, const double* tau, int n, int want, View z) {
+    switch ((n + 31) / 32) {
+        case 1: return launch_ormtr_full<1>(ctx, lp, tau, n, want, z);
+        case 2: return launch_ormtr_full<2>(ctx, lp, tau, n, want, z);
+        case 3: return launch_ormtr_full<3>(ctx, lp, tau, n, want, z);
+        case 4: return launch_ormtr_full<4>(ctx, lp, tau, n, want, z);
+        case 5: return launch_ormtr_full<5>(ctx, lp, tau, n, want, z);
+        case 6: return launch_ormtr_full<6>(ctx, lp, tau, n, want, z);
+        case 7: return launch_ormtr_full<7>(ctx, lp, tau, n, want, z);
+        default: return false;
+    }
+}
+
 }  // namespace
 
 bool sytrd_cluster(Context& ctx, View t, double* lp, double* d, double* e, double* tau);
@@ -299,6 +378,7 @@ void sym_evd_top(Context& ctx, View t, Index want, double* values, View vectors)
         BLWS_CUDA(cudaFuncSetAttribute(ormtr_k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget));
         cfg2 = true;
     }
+    if (ormtr_full(ctx, lp.get(), tau.get(), n, static_cast<int>(want), vectors)) return;
     const int smem2 = (kOrmChunk + kOrmWarps) * n * 8;
     ormtr_k<<<static_cast<unsigned>((want + kOrmWarps - 1) / kOrmWarps), kOrmWarps * 32, smem2, ctx.stream()>>>(
         lp.get(), tau.get(), n, static_cast<int>(want), vectors.p, vectors.ld);

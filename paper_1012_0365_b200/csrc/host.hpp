@@ -152,7 +152,7 @@ private:
     DBuf<std::int64_t> rowptr_, colptr_, perm_;  // perm: csr position -> csc position
     DBuf<std::int32_t> colidx_, rowidx_, colof_;
     DBuf<double> val_csr_, val_csc_;
-    DBuf<double> scratch_;
+    DBuf<double> scratch_, scratch2_;
 };
 
 // ------------------------------------------------------------ warm start

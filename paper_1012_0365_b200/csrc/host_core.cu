@@ -238,8 +238,11 @@ void DenseOperator::pair_block_impl(View left, View right, View top, View bot) {
     const Index b = right.cols;
     // K1: region 0 times the paired product (both GEMMs incl. split-K reduce)
     ctx_.region_begin(0);
+    {
+        AuxScope aux(ctx_);  // W^T U on the auxiliary stream, overlapping W V
+        gemm(ctx_, true, false, n_, b, m_, 1.0, p_, ld_, left.p, left.ld, 0.0, bot.p, bot.ld);
+    }
     gemm(ctx_, false, false, m_, b, n_, 1.0, p_, ld_, right.p, right.ld, 0.0, top.p, top.ld);
-    gemm(ctx_, true, false, n_, b, m_, 1.0, p_, ld_, left.p, left.ld, 0.0, bot.p, bot.ld);
     ctx_.region_end(0, 4.0 * static_cast<double>(m_) * n_ * b, 16.0 * static_cast<double>(m_) * n_);
 }
 
@@ -305,9 +308,13 @@ void SparseOperator::pair_block_impl(View left, View right, View top, View bot) 
     const Index b = right.cols;
     const size_t need = static_cast<size_t>(std::max(m_, n_) * b);
     if (scratch_.size() < need) scratch_ = DBuf<double>(ctx_, need);
+    if (scratch2_.size() < need) scratch2_ = DBuf<double>(ctx_, need);
+    {
+        AuxScope aux(ctx_);  // W^T x on the auxiliary stream, overlapping W x
+        csr_spmm(ctx_, n_, colptr_.get(), rowidx_.get(), val_csc_.get(), m_, b, left.p, left.ld, bot.p, bot.ld,
+                 scratch2_.get());
+    }
     csr_spmm(ctx_, m_, rowptr_.get(), colidx_.get(), val_csr_.get(), n_, b, right.p, right.ld, top.p, top.ld,
-             scratch_.get());
-    csr_spmm(ctx_, n_, colptr_.get(), rowidx_.get(), val_csc_.get(), m_, b, left.p, left.ld, bot.p, bot.ld,
              scratch_.get());
 }
 
@@ -893,8 +900,11 @@ DeferredRecs enqueue_deferred(LinearOperator& w, View src, const DeferredShape& 
     gemm(ctx, false, false, geo.ld(), want, d, std::sqrt(2.0), fac.q.data(), fac.q.ld, vecs.data(), vecs.ld, 0.0,
          next_uv.p, next_uv.ld);
     View u{next_uv.p, sh.m, want, next_uv.ld}, v{next_uv.p + geo.mp(), sh.n, want, next_uv.ld};
+    {
+        AuxScope aux(ctx);  // the two QRs are independent
+        rec.qv = thin_qr_deferred(ctx, v, nullptr, sl);
+    }
     rec.qu = thin_qr_deferred(ctx, u, nullptr, sl);
-    rec.qv = thin_qr_deferred(ctx, v, nullptr, sl);
     return rec;
 }
 

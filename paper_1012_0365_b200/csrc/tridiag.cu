@@ -111,15 +111,16 @@ __global__ void __launch_bounds__(kBoundsThreads) tridiag_bounds_k(const double*
 }
 
 // one warp per wanted eigenvalue; j-th largest = ascending index n-1-j
+template <bool SH>
 __global__ void bisect_k(const double* __restrict__ d, const double* __restrict__ e, int n, int want,
-                         const double* __restrict__ params, double* values) {
+                         const double* __restrict__ params, double* values, double* gscratch) {
     const int warps = (gridDim.x * blockDim.x) >> 5;
     const int lane = threadIdx.x & 31;
     const double gl = params[0], gu = params[1], pivmin = params[2], scale = params[4];
     const bool zero = params[3] == 0.0;
     extern __shared__ __align__(16) double tsm[];
-    double* ds = tsm;      // n: s d
-    double* e2s = tsm + n;  // n: (s e)^2, -1 marks a split
+    double* ds = SH ? tsm : gscratch + 2L * n * blockIdx.x;  // n: s d
+    double* e2s = ds + n;                                    // n: (s e)^2, -1 marks a split
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
         ds[i] = d[i] * scale;
         if (i < n - 1) {
@@ -174,11 +175,13 @@ __device__ __forceinline__ double hash_uniform(unsigned long long seed, long i) 
 // One warp per block: the LU of T - lambda I, the right-hand side, the iterate
 // and (d, e) live in shared memory (9 n doubles); the serial recurrences carry
 // their state in registers (lane 0), loads are independent of the chain.
-constexpr int kInvitMaxN = 2048;
+constexpr int kInvitMaxN = 2048;  // shared-memory path; larger orders use global scratch
+template <bool SH>
 __global__ void __launch_bounds__(32) inverse_iteration_k(const double* __restrict__ d_g,
                                                            const double* __restrict__ e_g, int n,
                                                            const double* __restrict__ values, int want,
-                                                           const double* __restrict__ params, double* vecs, long ldv) {
+                                                           const double* __restrict__ params, double* vecs, long ldv,
+                                                           double* gscratch) {
     extern __shared__ __align__(16) double ism[];
     const int warps = gridDim.x;
     const int lane = threadIdx.x & 31;
@@ -190,7 +193,7 @@ __global__ void __launch_bounds__(32) inverse_iteration_k(const double* __restri
             for (int i = lane; i < n; i += 32) vecs[static_cast<long>(j) * ldv + i] = i == n - 1 - j ? 1.0 : 0.0;
         return;
     }
-    double* d = ism;
+    double* d = SH ? ism : gscratch + 9L * n * blockIdx.x;
     double* e = d + n;   // e[n-1] = 0
     double* u0 = e + n;  // reciprocal pivots
     double* u1 = u0 + n;
@@ -337,24 +340,29 @@ void tridiag_eig_top(Context& ctx, Index n_, const double* d, const double* e, I
     // spread over the SMs instead of sharing schedulers)
     static bool cfg = false;
     if (!cfg) {
-        BLWS_CUDA(cudaFuncSetAttribute(bisect_k, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+        BLWS_CUDA(cudaFuncSetAttribute(bisect_k<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+        BLWS_CUDA(cudaFuncSetAttribute(inverse_iteration_k<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       9 * kInvitMaxN * static_cast<int>(sizeof(double))));
         cfg = true;
     }
-    if (n > 4096) throw std::invalid_argument("tridiag_eig_top: order > 4096");
-    bisect_k<<<static_cast<unsigned>(want), 32, 2 * n * sizeof(double), ctx.stream()>>>(d, e, n, want, params.get(),
-                                                                                         values);
+    const bool small = n <= kInvitMaxN;  // both kernels stage their vectors in shared memory
+    DBuf<double> gscratch;
+    if (!small) gscratch = DBuf<double>(ctx, static_cast<size_t>(want) * 9 * n);
+    if (small)
+        bisect_k<true><<<static_cast<unsigned>(want), 32, 2 * n * sizeof(double), ctx.stream()>>>(
+            d, e, n, want, params.get(), values, nullptr);
+    else
+        bisect_k<false><<<static_cast<unsigned>(want), 32, 0, ctx.stream()>>>(d, e, n, want, params.get(), values,
+                                                                             gscratch.get());
     ctx.note_launch();
     ctx.check_launch("bisect_k");
     // inverse iteration: one warp per candidate cluster start, one warp per block
-    if (n > kInvitMaxN) throw std::invalid_argument("tridiag_eig_top: order > 2048");
-    static bool cfg2 = false;
-    if (!cfg2) {
-        BLWS_CUDA(cudaFuncSetAttribute(inverse_iteration_k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       9 * kInvitMaxN * static_cast<int>(sizeof(double))));
-        cfg2 = true;
-    }
-    inverse_iteration_k<<<static_cast<unsigned>(want), 32, 9 * n * sizeof(double), ctx.stream()>>>(
-        d, e, n, values, want, params.get(), vectors.p, vectors.ld);
+    if (small)
+        inverse_iteration_k<true><<<static_cast<unsigned>(want), 32, 9 * n * sizeof(double), ctx.stream()>>>(
+            d, e, n, values, want, params.get(), vectors.p, vectors.ld, nullptr);
+    else
+        inverse_iteration_k<false><<<static_cast<unsigned>(want), 32, 0, ctx.stream()>>>(
+            d, e, n, values, want, params.get(), vectors.p, vectors.ld, gscratch.get());
     ctx.note_launch();
     ctx.check_launch("inverse_iteration_k");
 }

@@ -123,7 +123,7 @@ def test_sym_evd_cluster_tridiagonalisation(gpu, O, n, monkeypatch):
 
 def test_tridiagonal_top_matches_oracle(gpu, O):
     rs = np.random.default_rng(9)
-    for n, want in [(10, 3), (60, 20), (500, 40)]:
+    for n, want in [(10, 3), (60, 20), (500, 40), (2600, 12)]:  # > 2048: global-memory path
         d = rs.standard_normal(n)
         e = np.abs(rs.standard_normal(n - 1))
         vals, vecs = gpu.sym_evd_tridiagonal_top(d, e, want)
