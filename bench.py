@@ -61,28 +61,51 @@ def make_instance(rng_cls):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks / throttle reasons sampled during the timed region, in-process
+    through NVML (spawning nvidia-smi during the region stalled GPU work
+    submission: single 2x-long steps); nvidia-smi is the fallback."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    # NVML clock-event reason bits: hw_slowdown, hw_thermal_slowdown, sw_thermal_slowdown, sw_power_cap
+    BITS = (0x8, 0x40, 0x20, 0x4)
 
     def __init__(self, index=0):
-        self.index = index
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+        ids = [v for v in vis.split(",") if v.strip()]
+        self.index = int(ids[index]) if index < len(ids) and ids[index].strip().isdigit() else index
         self.samples = []
         self._stop = threading.Event()
         self._t = None
+        self._nvml = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nvml = (pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.index))
+        except Exception:
+            self._nvml = None
+
+    def _sample(self):
+        if self._nvml:
+            nv, h = self._nvml
+            sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            reasons = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+            return [str(sm), str(mx)] + ["Active" if reasons & b else "Not Active" for b in self.BITS]
+        out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+        return [p.strip() for p in out.stdout.strip().split(",")]
 
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                parts = [p.strip() for p in out.stdout.strip().split(",")]
+                parts = self._sample()
                 if len(parts) >= 6:
                     self.samples.append(parts)
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.01 if self._nvml else 0.5)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -101,7 +124,7 @@ class ClockSampler:
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons}
+                "reasons": reasons, "samples": len(self.samples), "via": "nvml" if self._nvml else "nvidia-smi"}
 
 
 def cpu_baseline(W, U, V, s, steps=None, budget_s=20.0):
@@ -303,6 +326,8 @@ def run_gpu(args):
                     "pinned_h2d_GBps": h2d_gbps,
                     "overlap": "W of step i+1 uploads on the copy stream during step i (assign_async, 2 operators)"},
             "gpu_launches": launches,
+            "step_ms": {"min": float(np.min(step_ms)), "median": float(np.median(step_ms)),
+                        "max": float(np.max(step_ms))},
             "roofline": {"bound": "tensor", "achieved": achieved_tf, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved_tf / peak if peak else None, "traffic": traffic,
                          "traffic_unit": "bytes per K1 launch group (ncu, profiles/r01_k1_traffic.json)",

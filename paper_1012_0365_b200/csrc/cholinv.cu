@@ -1,4 +1,7 @@
 // Fused Cholesky + triangular inverse for CholQR (K3): G = R^T R, Rinv = R^{-1}.
+// With skip_rel > 0 a Gram that is a scaled identity to ||G - cI||_F <=
+// skip_rel c (c = tr(G) / n) returns R = sqrt(c) I, Rinv = I / sqrt(c) instead
+// (the CholQR pass skip, decided on the device); tr(G) is optionally written out.
 //
 // thin_qr (core/qr.hpp:24-47) becomes CholQR2 on the device; each pass needs
 // chol(G) and R^{-1} of a b x b Gram (b <= ~411). One CTA does both:
@@ -37,27 +40,25 @@ __device__ __forceinline__ double pick32(const double (&a)[32], int idx) {
 constexpr int kCT = 1024;  // one thread per element of a 32x32 diagonal block
 constexpr long kSmemBudget = 216 * 1024;
 
+// block-wide sum (all threads get the result); red: 32 doubles
+__device__ __forceinline__ double chol_block_sum(double v, double* red) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __syncthreads();
+    if (lane == 0) red[wid] = v;
+    __syncthreads();
+    double s = lane < nw ? red[lane] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    return s;
+}
+
 template <bool SH>
 __global__ void __launch_bounds__(kCT) chol_inv_k(double* g, long ldg, double* rinv, long ldri, int n,
-                                                  double* scratch, int* status, double* diag,
-                                                  const double* skip_offsq, double skip_tol) {
+                                                  double* scratch, int* status, double* diag, double skip_rel,
+                                                  double* trace_out) {
     extern __shared__ __align__(16) double sm[];
     __shared__ int fail;
-    if (skip_offsq && *skip_offsq <= skip_tol) {
-        // device-predicated CholQR pass skip: G == I to tolerance -> R = Rinv = I
-        const int lane0 = threadIdx.x & 31, wid0 = threadIdx.x >> 5, nw0 = blockDim.x >> 5;
-        for (int j = wid0; j < n; j += nw0)
-            for (int i = lane0; i < n; i += 32) {
-                g[i + j * ldg] = i == j ? 1.0 : 0.0;
-                if (rinv) rinv[i + j * ldri] = i == j ? 1.0 : 0.0;
-            }
-        if (threadIdx.x == 0) {
-            status[0] = 0;
-            diag[0] = 1.0;
-            diag[1] = 1.0;
-        }
-        return;
-    }
+    __shared__ double red[32];
     const int ld = n | 1;  // odd stride: conflict-free row access
     double* A = SH ? sm : scratch;
     double* X = A + static_cast<long>(ld) * n;
@@ -70,6 +71,36 @@ __global__ void __launch_bounds__(kCT) chol_inv_k(double* g, long ldg, double* r
     for (int j = wid; j < n; j += nw)
         for (int i = lane; i < n; i += 32) A[i + j * ld] = g[i + j * ldg];
     __syncthreads();
+    // trace (= ||X||_F^2 for a Gram) and the scaled-identity test of the CholQR
+    // pass skip: ||G - c I||_F <= skip_rel c with c = tr(G) / n gives R = sqrt(c) I
+    double tr = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) tr += A[i + i * ld];
+    tr = chol_block_sum(tr, red);
+    if (trace_out && threadIdx.x == 0) *trace_out = tr;
+    if (skip_rel > 0.0 && tr > 0.0 && isfinite(tr)) {
+        const double c = tr / n;
+        double off = 0.0;
+        for (int j = wid; j < n; j += nw)
+            for (int i = lane; i < n; i += 32) {
+                const double x = A[i + j * ld] - (i == j ? c : 0.0);
+                off = fma(x, x, off);
+            }
+        off = chol_block_sum(off, red);
+        if (off <= skip_rel * skip_rel * c * c) {
+            const double rc = sqrt(c), ric = 1.0 / rc;
+            for (int j = wid; j < n; j += nw)
+                for (int i = lane; i < n; i += 32) {
+                    g[i + j * ldg] = i == j ? rc : 0.0;
+                    if (rinv) rinv[i + j * ldri] = i == j ? ric : 0.0;
+                }
+            if (threadIdx.x == 0) {
+                status[0] = 0;
+                diag[0] = rc;
+                diag[1] = rc;
+            }
+            return;
+        }
+    }
     long long t1 = clock64();
     // ---- right-looking Cholesky, trailing matrix in registers: thread t owns
     // upper-triangle entries e = t + kCT * q (q < kOwn) in column-major packed
@@ -252,8 +283,8 @@ __global__ void __launch_bounds__(kCT) chol_inv_k(double* g, long ldg, double* r
 
 }  // namespace
 
-void chol_inv_upper(Context& ctx, View g, View rinv, int* status, double* diag, const double* skip_offsq,
-                    double skip_tol) {
+void chol_inv_upper(Context& ctx, View g, View rinv, int* status, double* diag, double skip_rel,
+                    double* trace_out) {
     const int n = static_cast<int>(g.rows);
     const long ld = n | 1;
     const long bytes = (2L * ld * n + 2L * n + 34) * 8;
@@ -265,11 +296,11 @@ void chol_inv_upper(Context& ctx, View g, View rinv, int* status, double* diag, 
     }
     if (on_chip) {
         chol_inv_k<true><<<1, kCT, bytes, ctx.stream()>>>(g.p, g.ld, rinv.p, rinv.ld, n, nullptr, status, diag,
-                                                         skip_offsq, skip_tol);
+                                                         skip_rel, trace_out);
     } else {
         DBuf<double> scratch(ctx, static_cast<size_t>(2L * ld * n + 2L * n + 34));
         chol_inv_k<false><<<1, kCT, 0, ctx.stream()>>>(g.p, g.ld, rinv.p, rinv.ld, n, scratch.get(), status,
-                                               diag, skip_offsq, skip_tol);
+                                               diag, skip_rel, trace_out);
     }
     ctx.note_launch();
     ctx.check_launch("chol_inv_k");

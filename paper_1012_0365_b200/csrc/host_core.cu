@@ -1,6 +1,7 @@
 // Operators, CholQR thin_qr, block Lanczos / BLWS and the cold Lanczos reseed.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -354,22 +355,28 @@ struct CholStep {
     double dmin = 0, dmax = 0;
 };
 
-// R = chol(G) in place, Rinv = R^{-1}; reads back status + diag range (one sync).
-CholStep chol_step(Context& ctx, DMat g) {
+constexpr double kSkipRel = 1e-14;  // CholQR pass skip: ||G - cI||_F <= 1e-14 c (cholinv.cu)
+
+// R = chol(G) in place (or sqrt(c) I for a scaled-identity Gram), Rinv = R^{-1};
+// reads back status, diag range and tr(G) (one sync). `trace_dev`, if set,
+// receives tr(G) on the device too (the rank threshold reads it there).
+CholStep chol_step(Context& ctx, DMat g, double* trace_dev = nullptr, double* trace_host = nullptr) {
     CholStep s;
     const Index b = g.rows;
     s.r = std::move(g);
     s.rinv = DMat(ctx, b, b, false);
     DBuf<int> status(ctx, 1);
-    DBuf<double> diag(ctx, 2);
-    chol_inv_upper(ctx, s.r.view(), s.rinv.view(), status.get(), diag.get());
+    DBuf<double> diag(ctx, 3);
+    chol_inv_upper(ctx, s.r.view(), s.rinv.view(), status.get(), diag.get(), kSkipRel, diag.get() + 2);
+    if (trace_dev) copy(ctx, View{trace_dev, 1, 1, 2}, View{diag.get() + 2, 1, 1, 2});
     int st = 0;
-    double dd[2] = {0, 0};
+    double dd[3] = {0, 0, 0};
     BLWS_CUDA(cudaMemcpyAsync(&st, status.get(), sizeof(int), cudaMemcpyDeviceToHost, ctx.stream()));
-    ctx.read(diag.get(), dd, 2);
+    ctx.read(diag.get(), dd, 3);
     s.ok = st == 0;
     s.dmin = dd[0];
     s.dmax = dd[1];
+    if (trace_host) *trace_host = dd[2];
     return s;
 }
 
@@ -377,14 +384,6 @@ DMat gram(Context& ctx, View x) {
     DMat g(ctx, x.cols, x.cols, false);
     gemm(ctx, true, false, x.cols, x.cols, x.rows, 1.0, x.p, x.ld, x.p, x.ld, 0.0, g.data(), g.ld);
     return g;
-}
-
-// ||G - I||_F^2 (device) -> host
-double off_identity_sq(Context& ctx, View g, double* scratch) {
-    sumsq_minus_identity(ctx, g, scratch);
-    double h = 0;
-    ctx.read(scratch, &h, 1);
-    return h;
 }
 
 }  // namespace
@@ -398,48 +397,29 @@ Index thin_qr(Context& ctx, View x, View* r_out) {
     return rank;
 }
 
-// thin_qr (core/qr.hpp:24-47) as adaptive CholQR2 with a shifted-CholQR3
-// fallback. Q is the unique orthonormal factor with diag(R) > 0, i.e. the
-// reference's sign-normalised Householder Q; a pass is skipped when its Gram
-// is already the identity to 1e-14 (then R = I to working precision).
+// thin_qr (core/qr.hpp:24-47) as CholQR2 with a shifted-CholQR3 fallback. Q is
+// the unique orthonormal factor with diag(R) > 0, i.e. the reference's
+// sign-normalised Householder Q. A pass whose Gram is a scaled identity
+// (||G - cI||_F <= 1e-14 c) is skipped on the device (R = sqrt(c) I), so the
+// launch sequence is fixed -- the same one thin_qr_deferred() issues.
 Index thin_qr_impl(Context& ctx, View x, View* r_out) {
     const Index rows = x.rows, b = x.cols;
     if (rows == 0 || b == 0) throw std::invalid_argument("thin_qr: empty matrix");
     if (rows < b) throw std::invalid_argument("thin_qr: requires rows >= cols");
-    DBuf<double> ss(ctx, 2);
-    sumsq(ctx, x, ss.get());
-    double hss = 0;
-    ctx.read(ss.get(), &hss, 1);
-    if (!std::isfinite(hss)) throw std::invalid_argument("thin_qr: non-finite entries");
-    constexpr double kIdentityTol2 = 1e-28;  // ||G - I||_F <= 1e-14
-
+    DBuf<double> ss(ctx, 2);  // ss[0] = ||X||_F^2 = tr(X^T X)
     std::vector<CholStep> steps;
-    DMat g1 = gram(ctx, x);
-    if (off_identity_sq(ctx, g1.view(), ss.get() + 1) <= kIdentityTol2) {
-        // already orthonormal: Q = X, R = I (rank = b unless the tau test says otherwise)
-        if (r_out) {
-            fill(ctx, *r_out, 0.0);
-            DBuf<double> one(ctx, 1);
-            fill(ctx, View{one.get(), 1, 1, 2}, 1.0);  // on the device: no H2D behind a pending upload
-            add_diagonal(ctx, *r_out, one.get());
-        }
-        return 1.0 > 1e-12 * std::sqrt(hss) ? b : 0;
-    }
-    CholStep s1 = chol_step(ctx, std::move(g1));
+    double hss = 0;
+    CholStep s1 = chol_step(ctx, gram(ctx, x), ss.get(), &hss);
+    if (!std::isfinite(hss)) throw std::invalid_argument("thin_qr: non-finite entries");
     const bool ill = !s1.ok || !(s1.dmin > 0) || s1.dmax / s1.dmin > 1e6;
     DMat y(ctx, rows, b, false);
     if (!ill) {
         gemm(ctx, false, false, rows, b, b, 1.0, x.p, x.ld, s1.rinv.data(), s1.rinv.ld, 0.0, y.data(), y.ld);
         steps.push_back(std::move(s1));
-        DMat g2 = gram(ctx, y.view());
-        if (off_identity_sq(ctx, g2.view(), ss.get() + 1) <= kIdentityTol2) {
-            copy(ctx, x, y.view());
-        } else {
-            CholStep s2 = chol_step(ctx, std::move(g2));
-            if (!s2.ok) throw NumericalError("thin_qr: CholQR2 second pass failed");
-            gemm(ctx, false, false, rows, b, b, 1.0, y.data(), y.ld, s2.rinv.data(), s2.rinv.ld, 0.0, x.p, x.ld);
-            steps.push_back(std::move(s2));
-        }
+        CholStep s2 = chol_step(ctx, gram(ctx, y.view()));
+        if (!s2.ok) throw NumericalError("thin_qr: CholQR2 second pass failed");
+        gemm(ctx, false, false, rows, b, b, 1.0, y.data(), y.ld, s2.rinv.data(), s2.rinv.ld, 0.0, x.p, x.ld);
+        steps.push_back(std::move(s2));
     } else {
         // shifted CholQR3 (Fukaya et al. 2020): s = 11 (rows*b + b(b+1)) u ||X||_F^2
         DMat g(ctx, b, b, false);
@@ -462,9 +442,7 @@ Index thin_qr_impl(Context& ctx, View x, View* r_out) {
         copy(ctx, x, y.view());
         steps.push_back(std::move(a));
         for (int k = 0; k < 2; ++k) {
-            DMat gk = gram(ctx, x);
-            if (off_identity_sq(ctx, gk.view(), ss.get() + 1) <= kIdentityTol2) break;
-            CholStep c = chol_step(ctx, std::move(gk));
+            CholStep c = chol_step(ctx, gram(ctx, x));
             if (!c.ok) break;  // remaining directions are numerically null
             gemm(ctx, false, false, rows, b, b, 1.0, x.p, x.ld, c.rinv.data(), c.rinv.ld, 0.0, y.data(), y.ld);
             copy(ctx, x, y.view());
@@ -698,8 +676,6 @@ static BlwsResult blws_svd_exact(LinearOperator& w, const DWarm& warm, Index k, 
 // the device-predicated pass skip yields R = Rinv = I and X I == X exactly.
 namespace {
 
-constexpr double kIdentityTol2 = 1e-28;  // ||G - I||_F <= 1e-14 (thin_qr_impl)
-
 struct Slots {
     DBuf<double> buf;
     int used = 0, cap = 0;
@@ -732,28 +708,25 @@ struct Slots {
 };
 
 struct QrRec {
-    int hss, off1, st1, dg1, off2, st2, dg2, rank;
+    int hss, st1, dg1, st2, dg2, rank;
 };
 
-// thin_qr_impl's common case as a fixed launch sequence: both CholQR passes
-// always launched, each skipped on the device when its Gram is the identity.
+// thin_qr_impl's common case as a fixed launch sequence (both CholQR passes,
+// each skipped on the device for a scaled-identity Gram).
 QrRec thin_qr_deferred(Context& ctx, View x, View* r_out, Slots& sl) {
     const Index rows = x.rows, b = x.cols;
-    QrRec q{sl.take(), sl.take(), sl.take(), sl.take(2), sl.take(), sl.take(), sl.take(2), sl.take()};
+    QrRec q{sl.take(), sl.take(), sl.take(3), sl.take(), sl.take(3), sl.take()};
     ctx.region_begin(2);
-    sumsq(ctx, x, sl.at(q.hss));
     DMat r1 = gram(ctx, x);
-    sumsq_minus_identity(ctx, r1.view(), sl.at(q.off1));
     DMat ri1(ctx, b, b, false);
-    chol_inv_upper(ctx, r1.view(), ri1.view(), reinterpret_cast<int*>(sl.at(q.st1)), sl.at(q.dg1), sl.at(q.off1),
-                   kIdentityTol2);
+    chol_inv_upper(ctx, r1.view(), ri1.view(), reinterpret_cast<int*>(sl.at(q.st1)), sl.at(q.dg1), kSkipRel,
+                   sl.at(q.hss));
     DMat y(ctx, rows, b, false);
     gemm(ctx, false, false, rows, b, b, 1.0, x.p, x.ld, ri1.data(), ri1.ld, 0.0, y.data(), y.ld);
     DMat r2 = gram(ctx, y.view());
-    sumsq_minus_identity(ctx, r2.view(), sl.at(q.off2));
     DMat ri2(ctx, b, b, false);
-    chol_inv_upper(ctx, r2.view(), ri2.view(), reinterpret_cast<int*>(sl.at(q.st2)), sl.at(q.dg2), sl.at(q.off2),
-                   kIdentityTol2);
+    chol_inv_upper(ctx, r2.view(), ri2.view(), reinterpret_cast<int*>(sl.at(q.st2)), sl.at(q.dg2), kSkipRel,
+                   sl.at(q.dg2 + 2));
     gemm(ctx, false, false, rows, b, b, 1.0, y.data(), y.ld, ri2.data(), ri2.ld, 0.0, x.p, x.ld);
     DMat r(ctx, b, b, false);
     gemm(ctx, false, false, b, b, b, 1.0, r2.data(), r2.ld, r1.data(), r1.ld, 0.0, r.data(), r.ld);
@@ -766,15 +739,11 @@ QrRec thin_qr_deferred(Context& ctx, View x, View* r_out, Slots& sl) {
 // thin_qr_impl's host tests on the deferred values; false = it would have
 // taken another branch (shifted CholQR3, a failed pass, non-finite input).
 bool qr_check(const QrRec& q, const Slots& sl, Index b, Index* rank) {
-    const double hss = sl.val(q.hss);
-    if (!std::isfinite(hss)) return false;
-    if (sl.val(q.off1) <= kIdentityTol2) {
-        *rank = 1.0 > 1e-12 * std::sqrt(hss) ? b : 0;
-        return true;
-    }
+    (void)b;
+    if (!std::isfinite(sl.val(q.hss))) return false;
     const double dmin = sl.val(q.dg1), dmax = sl.val(q.dg1 + 1);
     if (sl.as_int(q.st1) != 0 || !(dmin > 0) || dmax / dmin > 1e6) return false;
-    if (!(sl.val(q.off2) <= kIdentityTol2) && sl.as_int(q.st2) != 0) return false;
+    if (sl.as_int(q.st2) != 0) return false;
     *rank = sl.as_i64(q.rank);
     return true;
 }

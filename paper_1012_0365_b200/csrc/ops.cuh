@@ -38,11 +38,11 @@ void gather_columns(Context& ctx, View dst, View src, const int* idx);
 /// min_diag/max_diag of R written to status-adjacent doubles diag[0..1].
 void potrf_upper(Context& ctx, View g, int* status, double* diag);
 /// Fused blocked Cholesky + inverse: G <- R (upper, zero lower), rinv <- R^{-1};
-/// status / diag as potrf_upper. With skip_offsq (device scalar ||G - I||_F^2)
-/// <= skip_tol the kernel writes R = Rinv = I instead (device-predicated CholQR
-/// pass skip, no host round trip).
-void chol_inv_upper(Context& ctx, View g, View rinv, int* status, double* diag, const double* skip_offsq = nullptr,
-                    double skip_tol = 0.0);
+/// status / diag as potrf_upper. With skip_rel > 0 a Gram with ||G - cI||_F <=
+/// skip_rel c (c = tr(G) / n) yields R = sqrt(c) I, Rinv = I / sqrt(c) without
+/// factorising (device-predicated CholQR pass skip); tr(G) -> *trace_out if set.
+void chol_inv_upper(Context& ctx, View g, View rinv, int* status, double* diag, double skip_rel = 0.0,
+                    double* trace_out = nullptr);
 /// R^{-1} of an upper-triangular n x n R (out may not alias r).
 void trtri_upper(Context& ctx, View out, View r);
 /// C = A * B for upper-triangular n x n A, B (C upper triangular).
