@@ -19,6 +19,23 @@
 // Output equals sytrd_k's layout (packed lower + reflectors, d, e, tau).
 #include "ops.cuh"
 
+#ifdef SYTRD_PROBE  // per-phase cycle accounting (tools/probes/sytrd_probe.cu only)
+__device__ unsigned long long g_sytrd_phase[8];
+__device__ unsigned int g_sytrd_sweep[256];  // sweep cycles per step (thread 0)
+#define PHASE_MARK(id)                                                       \
+    do {                                                                     \
+        if (threadIdx.x == 0) {                                              \
+            const long long t_ = clock64();                                  \
+            s_phase[id] += static_cast<unsigned long long>(t_ - tp_);        \
+            tp_ = t_;                                                        \
+        }                                                                    \
+    } while (0)
+#else
+#define PHASE_MARK(id) \
+    do {               \
+    } while (0)
+#endif
+
 namespace blws {
 namespace {
 
@@ -74,6 +91,12 @@ __global__ void __launch_bounds__(kFT) sytrd_fused_k(const double* __restrict__ 
     double* a = pw + kFW * NP;   // packed lower triangle
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int row = threadIdx.x;  // [P] phases: one row per thread
+#ifdef SYTRD_PROBE
+    __shared__ unsigned long long s_phase[8];
+    __shared__ unsigned s_sweep[256];
+    if (threadIdx.x < 8) s_phase[threadIdx.x] = 0;
+    long long tp_ = clock64();
+#endif
 
     for (int j = wid; j < n; j += kFW)
         for (int i = j + lane; i < n; i += 32) a[floff(j, n) + (i - j)] = 0.5 * (t[i + j * ld] + t[j + i * ld]);
@@ -91,6 +114,7 @@ __global__ void __launch_bounds__(kFT) sytrd_fused_k(const double* __restrict__ 
         __syncthreads();
     }
 
+    PHASE_MARK(0);
     for (int k = 0; k < n - 2; ++k) {
         const int par = k & 1;
         const double* v = vb + par * NP;         // v_k
@@ -116,16 +140,30 @@ __global__ void __launch_bounds__(kFT) sytrd_fused_k(const double* __restrict__ 
                 if (j <= k || j >= n) continue;  // warp-uniform
                 const double vj = v[j], voj = vo[j], woj = wo[j];
                 double* col = a + floff(j, n) - j;  // col[i] = A(i, j)
+                // all loads of the column first (independent; a store of one slot
+                // would otherwise order the next slot's load behind it), then the
+                // arithmetic, then the stores
+                double xs[QN];
 #pragma unroll
                 for (int q = c / 2; q < QN; ++q) {
                     const int i = lane + 32 * q;
                     const bool ok = (q != c / 2 || i >= j) && (q != QN - 1 || i < n);
-                    if (ok) {
-                        const double x = col[i] - fma(vor[q], woj, wor[q] * voj);
-                        col[i] = x;
-                        acc[q] = fma(x, vj, acc[q]);
-                        if (i > j) dp[c] = fma(x, vr[q], dp[c]);
-                    }
+                    xs[q] = ok ? col[i] : 0.0;
+                }
+#pragma unroll
+                for (int q = c / 2; q < QN; ++q) {
+                    const int i = lane + 32 * q;
+                    const bool ok = (q != c / 2 || i >= j) && (q != QN - 1 || i < n);
+                    const double x = ok ? xs[q] - fma(vor[q], woj, wor[q] * voj) : 0.0;
+                    xs[q] = x;
+                    acc[q] = fma(x, vj, acc[q]);
+                    if (i > j) dp[c] = fma(x, vr[q], dp[c]);
+                }
+#pragma unroll
+                for (int q = c / 2; q < QN; ++q) {
+                    const int i = lane + 32 * q;
+                    const bool ok = (q != c / 2 || i >= j) && (q != QN - 1 || i < n);
+                    if (ok) col[i] = xs[q];
                 }
             }
             // column dots: batched transpose-reduce of the CN (<= 16) values
@@ -150,7 +188,12 @@ __global__ void __launch_bounds__(kFT) sytrd_fused_k(const double* __restrict__ 
 #pragma unroll
             for (int q = 0; q < QN; ++q) pw[wid * NP + lane + 32 * q] = acc[q];
         }
+#ifdef SYTRD_PROBE
+        if (threadIdx.x == 0 && k < 256) s_sweep[k] = static_cast<unsigned>(clock64() - tp_);
+#endif
+        PHASE_MARK(1);
         __syncthreads();
+        PHASE_MARK(2);
         // ---- [P1] p_i = tau (column dot + row partials), p^T v
         double p = 0.0;
         if (row > k && row < n) {
@@ -163,7 +206,9 @@ __global__ void __launch_bounds__(kFT) sytrd_fused_k(const double* __restrict__ 
         double pv = warp_sum(p * vi);
         if (lane == 0) red[wid] = pv;
         if (row < NP) pcol[row] = p;  // pcol now holds p (row k+1 read in [P2])
+        PHASE_MARK(3);
         __syncthreads();
+        PHASE_MARK(4);
         // ---- [P2] w = p - K v; look-ahead update of column k+1 and its norm
         const double K = 0.5 * tk * warp_sum(lane < kFW ? red[lane] : 0.0);
         const double wi = fma(-K, vi, p);
@@ -178,13 +223,16 @@ __global__ void __launch_bounds__(kFT) sytrd_fused_k(const double* __restrict__ 
         }
         double s2 = warp_sum(row >= c1 + 2 && row < n ? xi * xi : 0.0);
         if (lane == 0) red[32 + wid] = s2;  // second half: red[0..] may still be read for K
+        PHASE_MARK(5);
         __syncthreads();
         // ---- [P3] reflector of column k+1 (if any)
         if (k + 1 < n - 2) {
             s2 = warp_sum(lane < kFW ? red[32 + lane] : 0.0);
             form_reflector(a, n, c1, s2, xi, vn, d, e, tau, &tk);
         }
+        PHASE_MARK(6);
         __syncthreads();
+        PHASE_MARK(7);
     }
     // the last update (step n-3) is already applied to column n-2 by the
     // look-ahead; column n-1 (one element) still needs it
@@ -206,6 +254,10 @@ __global__ void __launch_bounds__(kFT) sytrd_fused_k(const double* __restrict__ 
     __syncthreads();
     const long np = static_cast<long>(n) * (n + 1) / 2;
     for (long idx = threadIdx.x; idx < np; idx += kFT) lp[idx] = a[idx];
+#ifdef SYTRD_PROBE
+    if (threadIdx.x < 8) g_sytrd_phase[threadIdx.x] = s_phase[threadIdx.x];
+    for (int i = threadIdx.x; i < 256; i += kFT) g_sytrd_sweep[i] = s_sweep[i];
+#endif
 }
 
 template <int QN>
