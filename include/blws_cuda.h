@@ -84,6 +84,20 @@ int64_t blws_sample_distinct(int64_t n, int64_t s, blws_rng* rng, int64_t* out);
  * 16-byte aligned), borrow=0 copies. */
 int blws_dense_operator_create(blws_context* ctx, int64_t m, int64_t n, const double* w, int64_t ldw, int where,
                                int borrow, blws_operator** out);
+/* ---- row-sharded multi-GPU path (no reference counterpart: the
+   reference is single-process). One process per GPU; each holds a row panel
+   of W (rows [row0, row0 + m_local) of m_total) and the matching rows of U,
+   with V replicated. blws_svd then allreduces every reduction over panel rows
+   (Grams, norms, M = Q^T Z, W^T U) over NCCL; T, its EVD and every host
+   decision are computed from identical allreduced values on all ranks. */
+/* A fresh NCCL unique id (128 bytes): made on one rank, broadcast to the others. */
+int blws_nccl_unique_id(uint8_t* out128);
+/* Collective over all ranks: attach an NCCL communicator to the context. */
+int blws_context_init_comm(blws_context* ctx, int nranks, int rank, const uint8_t* id128);
+int blws_context_comm_info(const blws_context* ctx, int* nranks, int* rank);
+/* Mark a dense operator holding m_local = rows() rows as rows [row0, row0 +
+   m_local) of an m_total x n matrix distributed over the context's ranks. */
+int blws_dense_operator_set_row_shard(blws_operator* op, int64_t m_total, int64_t row0);
 /* DenseOperator::assign (linear_operator.hpp:113-116): replace W, non-finite check. */
 int blws_dense_operator_assign(blws_operator* op, const double* w, int64_t ldw, int where);
 /* Asynchronous host assign (B200 extension of DenseOperator::assign): queues the

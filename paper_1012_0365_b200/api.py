@@ -69,6 +69,10 @@ SIGNATURES = {
     "blws_dense_operator_create": (ci, [vp, i64, i64, vp, i64, ci, ci, P(vp)]),
     "blws_dense_operator_assign": (ci, [vp, vp, i64, ci]),
     "blws_dense_operator_assign_async": (ci, [vp, vp, i64]),
+    "blws_nccl_unique_id": (ci, [vp]),
+    "blws_context_init_comm": (ci, [vp, ci, ci, vp]),
+    "blws_context_comm_info": (ci, [vp, P(ci), P(ci)]),
+    "blws_dense_operator_set_row_shard": (ci, [vp, i64, i64]),
     "blws_sparse_operator_create": (ci, [vp, i64, i64, i64, vp, vp, vp, P(vp)]),
     "blws_sparse_operator_assign_values": (ci, [vp, vp, i64, ci]),
     "blws_operator_destroy": (ci, [vp]),
@@ -176,6 +180,16 @@ class Context:
     def launches(self) -> int:
         return int(lib().blws_context_launches(self._h))
 
+    def init_comm(self, nranks: int, rank: int, unique_id: bytes):
+        """Attach an NCCL communicator (collective over all ranks; see dist.init_comm)."""
+        buf = (C.c_uint8 * 128).from_buffer_copy(bytes(unique_id))
+        _check(lib().blws_context_init_comm(self._h, int(nranks), int(rank), C.cast(buf, vp)))
+
+    def comm_info(self):
+        nr, rk = ci(0), ci(0)
+        _check(lib().blws_context_comm_info(self._h, C.byref(nr), C.byref(rk)))
+        return nr.value, rk.value
+
     def set_profiling(self, on: bool):
         _check(lib().blws_context_set_profiling(self._h, 1 if on else 0))
 
@@ -256,6 +270,13 @@ class Rng:
         return np.array([self.uniform(lo, hi) for _ in range(n)])
 
 
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id (blws_nccl_unique_id)."""
+    buf = (C.c_uint8 * 128)()
+    _check(lib().blws_nccl_unique_id(C.cast(buf, vp)))
+    return bytes(buf)
+
+
 def sample_distinct(n: int, s: int, rng: Rng) -> np.ndarray:
     out = np.empty(s, dtype=np.int64)
     got = lib().blws_sample_distinct(n, s, rng._h, _ptr(out))
@@ -311,6 +332,11 @@ class DenseOperator(LinearOperator):
 
     def assign_ptr(self, ptr: int, ld: int, where: int):
         _check(lib().blws_dense_operator_assign(self._h, ptr, ld, where))
+
+    def set_row_shard(self, m_total: int, row0: int):
+        """This operator's rows are rows [row0, row0 + rows()) of an m_total x n
+        matrix distributed over the context's ranks (blws_dense_operator_set_row_shard)."""
+        _check(lib().blws_dense_operator_set_row_shard(self._h, int(m_total), int(row0)))
 
     def assign_async(self, ptr: int, ld: int):
         """Queue a pinned-host upload on the copy stream; the next use waits

@@ -53,6 +53,9 @@ int guard(F&& f) {
     } catch (const CudaError& e) {
         g_err = e.what();
         return BLWS_CUDA_ERROR;
+    } catch (const CommError& e) {
+        g_err = e.what();
+        return BLWS_NCCL_ERROR;
     } catch (const std::bad_alloc& e) {
         g_err = std::string("allocation failed: ") + e.what();
         return BLWS_CUDA_ERROR;
@@ -221,6 +224,31 @@ int blws_dense_operator_assign(blws_operator* op, const double* w, int64_t ldw, 
             d->assign_host(w, ldw);
         else
             d->assign_device(w, ldw);
+    });
+}
+int blws_nccl_unique_id(uint8_t* out128) {
+    return guard([&] {
+        need(out128 != nullptr, "nccl_unique_id: null output");
+        comm_unique_id(out128);
+    });
+}
+int blws_context_init_comm(blws_context* ctx, int nranks, int rank, const uint8_t* id128) {
+    return guard([&] {
+        need(ctx && id128, "init_comm: null argument");
+        ctx->ctx->init_comm(nranks, rank, id128);
+    });
+}
+int blws_context_comm_info(const blws_context* ctx, int* nranks, int* rank) {
+    return guard([&] {
+        need(ctx != nullptr, "comm_info: null context");
+        if (nranks) *nranks = ctx->ctx->nranks();
+        if (rank) *rank = ctx->ctx->rank();
+    });
+}
+int blws_dense_operator_set_row_shard(blws_operator* op, int64_t m_total, int64_t row0) {
+    return guard([&] {
+        need(op && op->dense, "set_row_shard: not a dense operator");
+        op->op->set_row_shard(m_total, row0);
     });
 }
 int blws_dense_operator_assign_async(blws_operator* op, const double* w, int64_t ldw) {

@@ -1,0 +1,93 @@
+// Collectives for the row-sharded path: NCCL, loaded with
+// dlopen on first use so the library itself has no hard NCCL dependency (one
+// process per GPU; torch's bundled libnccl.so.2 is picked up when torch is
+// already loaded, else the system one).
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "common.cuh"
+
+namespace blws {
+namespace {
+
+struct NcclApi {
+    ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                               cudaStream_t) = nullptr;
+    ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+    const char* (*error_string)(ncclResult_t) = nullptr;
+};
+
+const NcclApi& nccl() {
+    static NcclApi api;
+    static std::once_flag once;
+    static std::string err;
+    std::call_once(once, [] {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            err = std::string("NCCL not found: ") + dlerror();
+            return;
+        }
+        api.get_unique_id = reinterpret_cast<decltype(api.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+        api.comm_init_rank = reinterpret_cast<decltype(api.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+        api.all_reduce = reinterpret_cast<decltype(api.all_reduce)>(dlsym(h, "ncclAllReduce"));
+        api.comm_destroy = reinterpret_cast<decltype(api.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+        api.error_string = reinterpret_cast<decltype(api.error_string)>(dlsym(h, "ncclGetErrorString"));
+        if (!api.get_unique_id || !api.comm_init_rank || !api.all_reduce || !api.comm_destroy)
+            err = "NCCL: missing symbols";
+    });
+    if (!err.empty()) throw CommError(err);
+    return api;
+}
+
+void check(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess) {
+        const char* s = nccl().error_string ? nccl().error_string(r) : "unknown";
+        throw CommError(std::string(what) + ": " + s);
+    }
+}
+
+}  // namespace
+
+void comm_unique_id(void* out128) {
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    ncclUniqueId id;
+    check(nccl().get_unique_id(&id), "ncclGetUniqueId");
+    std::memcpy(out128, &id, sizeof(id));
+}
+
+void Context::init_comm(int nranks, int rank, const void* id128) {
+    if (nranks < 1 || rank < 0 || rank >= nranks) throw std::invalid_argument("init_comm: bad rank / size");
+    if (comm_) throw std::invalid_argument("init_comm: communicator already set");
+    ncclUniqueId id;
+    std::memcpy(&id, id128, sizeof(id));
+    BLWS_CUDA(cudaSetDevice(device_));
+    ncclComm_t c = nullptr;
+    check(nccl().comm_init_rank(&c, nranks, id, rank), "ncclCommInitRank");
+    comm_ = c;
+    nranks_ = nranks;
+    rank_ = rank;
+}
+
+void Context::allreduce_sum(double* p, size_t count) {
+    if (!comm_ || count == 0) return;
+    check(nccl().all_reduce(p, p, count, ncclDouble, ncclSum, static_cast<ncclComm_t>(comm_), stream()),
+          "ncclAllReduce");
+}
+
+void Context::destroy_comm() noexcept {
+    if (!comm_) return;
+    try {
+        nccl().comm_destroy(static_cast<ncclComm_t>(comm_));
+    } catch (...) {
+    }
+    comm_ = nullptr;
+}
+
+}  // namespace blws

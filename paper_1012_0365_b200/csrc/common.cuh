@@ -24,6 +24,12 @@ struct CudaError : std::runtime_error {
 struct NumericalError : std::runtime_error {
     using std::runtime_error::runtime_error;
 };
+struct CommError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+/// A fresh NCCL unique id (128 bytes) for init_comm on every rank.
+void comm_unique_id(void* out128);
 
 #define BLWS_CUDA(call)                                                                         \
     do {                                                                                        \
@@ -49,6 +55,14 @@ public:
     /// The stream work is enqueued on: the main stream, or the auxiliary one
     /// inside an AuxScope.
     cudaStream_t stream() const { return cur_ ? cur_ : stream_; }
+    /// Row-sharded path: an NCCL communicator over `nranks`
+    /// processes (one GPU each); allreduce_sum is a no-op without one.
+    void init_comm(int nranks, int rank, const void* id128);
+    void allreduce_sum(double* p, size_t count);
+    int nranks() const { return nranks_; }
+    int rank() const { return rank_; }
+    bool distributed() const { return comm_ != nullptr && nranks_ > 1; }
+    bool has_comm() const { return comm_ != nullptr; }
     /// Fork/join onto a second compute stream (see AuxScope).
     void fork_aux();
     void join_aux();
@@ -94,6 +108,9 @@ private:
     cudaStream_t stream_ = nullptr;
     cudaStream_t copy_stream_ = nullptr;
     cudaStream_t aux_ = nullptr, cur_ = nullptr;
+    void* comm_ = nullptr;
+    int nranks_ = 1, rank_ = 0;
+    void destroy_comm() noexcept;
     cudaEvent_t fork_ev_ = nullptr, join_ev_ = nullptr;
     void* pinned_ = nullptr;
     size_t pinned_bytes_ = 0;

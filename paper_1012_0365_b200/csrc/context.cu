@@ -149,6 +149,7 @@ cudaStream_t Context::copy_stream() {
 
 Context::~Context() {
     region_reset();
+    destroy_comm();
     if (copy_stream_) {
         cudaStreamSynchronize(copy_stream_);
         cudaStreamDestroy(copy_stream_);

@@ -45,6 +45,20 @@ private:
 /// view needs are exposed (augmented_operator.hpp:39-57).
 struct SvdGraph;  // captured blws_svd launch sequence (host_core.cu)
 
+/// Rows [0, sharded) of a panel are this rank's share of a row-sharded
+/// operator: a reduction over the panel's rows allreduces their
+/// contribution over the context's communicator and adds the replicated rows'
+/// locally. sharded = 0: an ordinary (replicated) panel.
+struct RowSplit {
+    Index sharded = 0;
+};
+
+/// Row-shard geometry of a distributed operator: this rank holds rows
+/// [row0, row0 + rows()) of an m_total x n matrix.
+struct RowShard {
+    Index m_total = 0, row0 = 0;
+};
+
 class LinearOperator {
 public:
     explicit LinearOperator(Context& ctx) : ctx_(ctx) {}
@@ -71,6 +85,12 @@ public:
     /// Identity of the data the kernels read (graph cache key).
     virtual const void* data_key() const { return this; }
     void add_applications(std::int64_t n) { count_ += n; }
+    /// Row-sharded operator: the local rows [row0, row0 + rows()) of m_total.
+    void set_row_shard(Index m_total, Index row0);
+    bool row_sharded() const { return shard_.m_total > 0; }
+    const RowShard& shard() const { return shard_; }
+    /// The split of a stacked panel of this operator (top rows sharded).
+    RowSplit panel_split() const;
     std::vector<std::shared_ptr<SvdGraph>>& svd_graphs() { return svd_graphs_; }
 
 protected:
@@ -80,6 +100,7 @@ protected:
 
 private:
     std::int64_t count_ = 0;
+    RowShard shard_;
     std::vector<std::shared_ptr<SvdGraph>> svd_graphs_;
 };
 
@@ -174,7 +195,7 @@ DWarm copy_warm(Context& ctx, const DWarm& w, Index cols);
 /// thin_qr (core/qr.hpp:24-47) as CholQR2 (shifted CholQR3 fallback) in place:
 /// X <- Q, R (b x b, optional) upper with positive diagonal; returns the rank,
 /// counted as diag(R) > 1e-12 ||X||_F.
-Index thin_qr(Context& ctx, View x, View* r_out);
+Index thin_qr(Context& ctx, View x, View* r_out, RowSplit split = {});
 
 /// Upload / download a host column-major block into a device view.
 void upload(Context& ctx, View dst, const double* host, Index ldh);
@@ -186,7 +207,10 @@ struct BlwsResult {
     bool padded = false, k_raised = false, terminated_early = false;
 };
 /// adapt_subspace (block_lanczos.hpp:157-187).
-DWarm adapt_subspace(Context& ctx, const DWarm* warm, Index r_new, Index m, Index n, Rng& rng);
+/// With `shard`, m is the local row count and the Gaussian padding of U is
+/// drawn for all m_total rows (the reference's draw order) and sliced.
+DWarm adapt_subspace(Context& ctx, const DWarm* warm, Index r_new, Index m, Index n, Rng& rng,
+                     const RowShard* shard = nullptr);
 /// blws_svd (block_lanczos.hpp:204-261).
 BlwsResult blws_svd(LinearOperator& w, const DWarm& warm, Index k, Index r, Rng& rng);
 extern std::int64_t g_blws_deferred_fallbacks;

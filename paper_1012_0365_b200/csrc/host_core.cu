@@ -173,6 +173,29 @@ static void check_finite_view(Context& ctx, View v, const char* what) {
     if (h) throw std::invalid_argument(what);
 }
 
+__global__ void flag_to_double_k(const int* f, double* d) { *d = *f != 0 ? 1.0 : 0.0; }
+
+// the async-upload non-finite verdict of this rank -> slot `dst` as 0/1, summed
+// over the ranks, so every rank takes the same branch
+void share_flag(Context& ctx, const int* flag, double* dst) {
+    if (!ctx.has_comm()) return;
+    flag_to_double_k<<<1, 1, 0, ctx.stream()>>>(flag, dst);
+    ctx.note_launch();
+    ctx.allreduce_sum(dst, 1);
+}
+
+// ======================================================== row sharding
+void LinearOperator::set_row_shard(Index m_total, Index row0) {
+    if (m_total < rows() || row0 < 0 || row0 + rows() > m_total)
+        throw std::invalid_argument("set_row_shard: local rows outside [0, m_total)");
+    shard_ = RowShard{m_total, row0};
+}
+
+RowSplit LinearOperator::panel_split() const {
+    // the top of a stacked panel (rows [0, mp), padding row included: it is zero)
+    return RowSplit{row_sharded() && ctx_.has_comm() ? round_up(rows(), 2) : 0};
+}
+
 // ======================================================== DenseOperator
 DenseOperator::DenseOperator(Context& ctx, Index m, Index n)
     : LinearOperator(ctx), m_(m), n_(n), ld_(std::max<Index>(2, round_up(m, 2))) {
@@ -239,11 +262,24 @@ void DenseOperator::pair_block_impl(View left, View right, View top, View bot) {
     const Index b = right.cols;
     // K1: region 0 times the paired product (both GEMMs incl. split-K reduce)
     ctx_.region_begin(0);
-    {
-        AuxScope aux(ctx_);  // W^T U on the auxiliary stream, overlapping W V
-        gemm(ctx_, true, false, n_, b, m_, 1.0, p_, ld_, left.p, left.ld, 0.0, bot.p, bot.ld);
+    if (row_sharded() && ctx_.has_comm()) {
+        // W^T U over the local rows, summed over the ranks (contiguous n x b
+        // buffer for the allreduce), while W V runs on the local rows only
+        DBuf<double> part(ctx_, static_cast<size_t>(n_ * b));
+        {
+            AuxScope aux(ctx_);
+            gemm(ctx_, true, false, n_, b, m_, 1.0, p_, ld_, left.p, left.ld, 0.0, part.get(), n_);
+            ctx_.allreduce_sum(part.get(), static_cast<size_t>(n_ * b));
+            copy(ctx_, bot, View{part.get(), n_, b, n_});
+        }
+        gemm(ctx_, false, false, m_, b, n_, 1.0, p_, ld_, right.p, right.ld, 0.0, top.p, top.ld);
+    } else {
+        {
+            AuxScope aux(ctx_);  // W^T U on the auxiliary stream, overlapping W V
+            gemm(ctx_, true, false, n_, b, m_, 1.0, p_, ld_, left.p, left.ld, 0.0, bot.p, bot.ld);
+        }
+        gemm(ctx_, false, false, m_, b, n_, 1.0, p_, ld_, right.p, right.ld, 0.0, top.p, top.ld);
     }
-    gemm(ctx_, false, false, m_, b, n_, 1.0, p_, ld_, right.p, right.ld, 0.0, top.p, top.ld);
     ctx_.region_end(0, 4.0 * static_cast<double>(m_) * n_ * b, 16.0 * static_cast<double>(m_) * n_);
 }
 
@@ -380,19 +416,52 @@ CholStep chol_step(Context& ctx, DMat g, double* trace_dev = nullptr, double* tr
     return s;
 }
 
-DMat gram(Context& ctx, View x) {
+}  // namespace
+
+// C (a.cols x b.cols, ldc) = A^T B over the rows of two panels of the same row
+// structure; rows [0, split.sharded) are summed over the ranks.
+void panel_tn(Context& ctx, View a, View b, RowSplit split, double* c, Index ldc) {
+    const Index rows = a.rows, s = split.sharded;
+    if (s == 0 || !ctx.has_comm()) {
+        gemm(ctx, true, false, a.cols, b.cols, rows, 1.0, a.p, a.ld, b.p, b.ld, 0.0, c, ldc);
+        return;
+    }
+    gemm(ctx, true, false, a.cols, b.cols, s, 1.0, a.p, a.ld, b.p, b.ld, 0.0, c, ldc);
+    ctx.allreduce_sum(c, static_cast<size_t>(ldc * b.cols));
+    if (rows > s) gemm(ctx, true, false, a.cols, b.cols, rows - s, 1.0, a.p + s, a.ld, b.p + s, b.ld, 1.0, c, ldc);
+}
+
+// ||X||_F^2 of a panel -> out (device scalar), sharded rows summed over the ranks
+void panel_sumsq(Context& ctx, View x, RowSplit split, double* out) {
+    const Index s = split.sharded;
+    if (s == 0 || !ctx.has_comm()) {
+        sumsq(ctx, x, out);
+        return;
+    }
+    sumsq(ctx, View{x.p, s, x.cols, x.ld}, out);
+    ctx.allreduce_sum(out, 1);
+    if (x.rows > s) {
+        DBuf<double> t(ctx, 1);
+        sumsq(ctx, View{x.p + s, x.rows - s, x.cols, x.ld}, t.get());
+        axpy(ctx, View{out, 1, 1, 1}, View{t.get(), 1, 1, 1}, 1.0);
+    }
+}
+
+namespace {
+
+DMat gram(Context& ctx, View x, RowSplit split = {}) {
     DMat g(ctx, x.cols, x.cols, false);
-    gemm(ctx, true, false, x.cols, x.cols, x.rows, 1.0, x.p, x.ld, x.p, x.ld, 0.0, g.data(), g.ld);
+    panel_tn(ctx, x, x, split, g.data(), g.ld);
     return g;
 }
 
 }  // namespace
 
-Index thin_qr_impl(Context& ctx, View x, View* r_out);
+Index thin_qr_impl(Context& ctx, View x, View* r_out, RowSplit split);
 
-Index thin_qr(Context& ctx, View x, View* r_out) {
+Index thin_qr(Context& ctx, View x, View* r_out, RowSplit split) {
     ctx.region_begin(2);
-    const Index rank = thin_qr_impl(ctx, x, r_out);
+    const Index rank = thin_qr_impl(ctx, x, r_out, split);
     ctx.region_end(2, 0.0, 0.0);
     return rank;
 }
@@ -402,28 +471,27 @@ Index thin_qr(Context& ctx, View x, View* r_out) {
 // sign-normalised Householder Q. A pass whose Gram is a scaled identity
 // (||G - cI||_F <= 1e-14 c) is skipped on the device (R = sqrt(c) I), so the
 // launch sequence is fixed -- the same one thin_qr_deferred() issues.
-Index thin_qr_impl(Context& ctx, View x, View* r_out) {
+Index thin_qr_impl(Context& ctx, View x, View* r_out, RowSplit split) {
     const Index rows = x.rows, b = x.cols;
     if (rows == 0 || b == 0) throw std::invalid_argument("thin_qr: empty matrix");
     if (rows < b) throw std::invalid_argument("thin_qr: requires rows >= cols");
     DBuf<double> ss(ctx, 2);  // ss[0] = ||X||_F^2 = tr(X^T X)
     std::vector<CholStep> steps;
     double hss = 0;
-    CholStep s1 = chol_step(ctx, gram(ctx, x), ss.get(), &hss);
+    CholStep s1 = chol_step(ctx, gram(ctx, x, split), ss.get(), &hss);
     if (!std::isfinite(hss)) throw std::invalid_argument("thin_qr: non-finite entries");
     const bool ill = !s1.ok || !(s1.dmin > 0) || s1.dmax / s1.dmin > 1e6;
     DMat y(ctx, rows, b, false);
     if (!ill) {
         gemm(ctx, false, false, rows, b, b, 1.0, x.p, x.ld, s1.rinv.data(), s1.rinv.ld, 0.0, y.data(), y.ld);
         steps.push_back(std::move(s1));
-        CholStep s2 = chol_step(ctx, gram(ctx, y.view()));
+        CholStep s2 = chol_step(ctx, gram(ctx, y.view(), split));
         if (!s2.ok) throw NumericalError("thin_qr: CholQR2 second pass failed");
         gemm(ctx, false, false, rows, b, b, 1.0, y.data(), y.ld, s2.rinv.data(), s2.rinv.ld, 0.0, x.p, x.ld);
         steps.push_back(std::move(s2));
     } else {
         // shifted CholQR3 (Fukaya et al. 2020): s = 11 (rows*b + b(b+1)) u ||X||_F^2
-        DMat g(ctx, b, b, false);
-        gemm(ctx, true, false, b, b, rows, 1.0, x.p, x.ld, x.p, x.ld, 0.0, g.data(), g.ld);
+        DMat g = gram(ctx, x, split);
         DBuf<double> shift(ctx, 1);
         const double factor =
             11.0 * (static_cast<double>(rows) * b + static_cast<double>(b) * (b + 1)) * 1.1102230246251565e-16;
@@ -442,7 +510,7 @@ Index thin_qr_impl(Context& ctx, View x, View* r_out) {
         copy(ctx, x, y.view());
         steps.push_back(std::move(a));
         for (int k = 0; k < 2; ++k) {
-            CholStep c = chol_step(ctx, gram(ctx, x));
+            CholStep c = chol_step(ctx, gram(ctx, x, split));
             if (!c.ok) break;  // remaining directions are numerically null
             gemm(ctx, false, false, rows, b, b, 1.0, x.p, x.ld, c.rinv.data(), c.rinv.ld, 0.0, y.data(), y.ld);
             copy(ctx, x, y.view());
@@ -465,17 +533,23 @@ Index thin_qr_impl(Context& ctx, View x, View* r_out) {
 }
 
 // ======================================================== adapt_subspace
-DWarm adapt_subspace(Context& ctx, const DWarm* warm, Index r_new, Index m, Index n, Rng& rng) {
-    if (r_new < 1 || r_new > std::min(m, n)) throw std::invalid_argument("adapt_subspace: r_new out of range");
+DWarm adapt_subspace(Context& ctx, const DWarm* warm, Index r_new, Index m, Index n, Rng& rng,
+                     const RowShard* shard) {
+    // with a row shard, U's Gaussian columns are drawn for all m_total rows in the
+    // reference's (column-major) order and this rank keeps rows [row0, row0 + m)
+    const bool sh = shard && shard->m_total > 0;
+    const Index mt = sh ? shard->m_total : m, r0 = sh ? shard->row0 : 0;
+    const RowSplit usplit{sh && ctx.has_comm() ? m : 0};
+    if (r_new < 1 || r_new > std::min(mt, n)) throw std::invalid_argument("adapt_subspace: r_new out of range");
     if (!warm || warm->rank() == 0) {
         DWarm out = make_warm(ctx, m, n, r_new);
-        std::vector<double> h(static_cast<size_t>(std::max(m, n) * r_new));
-        rng.gaussian_matrix(m, r_new, h.data(), m);
-        upload(ctx, out.u(), h.data(), m);
+        std::vector<double> h(static_cast<size_t>(std::max(mt, n) * r_new));
+        rng.gaussian_matrix(mt, r_new, h.data(), mt);
+        upload(ctx, out.u(), h.data() + r0, mt);
         rng.gaussian_matrix(n, r_new, h.data(), n);
         upload(ctx, out.v(), h.data(), n);
         View u = out.u(), v = out.v();
-        thin_qr(ctx, u, nullptr);
+        thin_qr(ctx, u, nullptr, usplit);
         thin_qr(ctx, v, nullptr);
         return out;
     }
@@ -485,13 +559,13 @@ DWarm adapt_subspace(Context& ctx, const DWarm* warm, Index r_new, Index m, Inde
     const Index add = r_new - r_old;
     DWarm out = make_warm(ctx, m, n, r_new);
     copy(ctx, out.panel().left(r_old), warm->panel().left(r_old));
-    std::vector<double> h(static_cast<size_t>(std::max(m, n) * add));
-    rng.gaussian_matrix(m, add, h.data(), m);
-    upload(ctx, out.u().cols_range(r_old, add), h.data(), m);
+    std::vector<double> h(static_cast<size_t>(std::max(mt, n) * add));
+    rng.gaussian_matrix(mt, add, h.data(), mt);
+    upload(ctx, out.u().cols_range(r_old, add), h.data() + r0, mt);
     rng.gaussian_matrix(n, add, h.data(), n);
     upload(ctx, out.v().cols_range(r_old, add), h.data(), n);
     View u = out.u(), v = out.v();
-    thin_qr(ctx, u, nullptr);
+    thin_qr(ctx, u, nullptr, usplit);
     thin_qr(ctx, v, nullptr);
     std::copy(warm->sigma.begin(), warm->sigma.end(), out.sigma.begin());
     return out;
@@ -519,14 +593,14 @@ double read_scalar(Context& ctx, const double* d) {
 BlockLanczos block_lanczos_procedure(LinearOperator& w, View x1, Index k) {
     Context& ctx = w.ctx();
     const Stack geo{w.rows(), w.cols()};
-    const Index dim = geo.m + geo.n, bs = x1.cols, ld = geo.ld();
+    const Index dim = (w.row_sharded() ? w.shard().m_total : geo.m) + geo.n, bs = x1.cols, ld = geo.ld();
     if (k < 1) throw std::invalid_argument("block_lanczos_procedure: k must be >= 1");
     if (bs < 1 || x1.rows != ld) throw std::invalid_argument("block_lanczos_procedure: bad initial block");
     if (k * bs > dim) throw std::invalid_argument("block_lanczos_procedure: k*b exceeds dimension");
+    const RowSplit split = w.panel_split();  // row-sharded operator: the top rows are this rank's
     DBuf<double> sc(ctx, 4);
     {
-        DMat g(ctx, bs, bs, false);
-        gemm(ctx, true, false, bs, bs, ld, 1.0, x1.p, x1.ld, x1.p, x1.ld, 0.0, g.data(), g.ld);
+        DMat g = gram(ctx, x1, split);
         sumsq_minus_identity(ctx, g.view(), sc.get());
         if (std::sqrt(read_scalar(ctx, sc.get())) > 1e-8)
             throw std::invalid_argument("block_lanczos_procedure: X1 not orthonormal");
@@ -540,9 +614,9 @@ BlockLanczos block_lanczos_procedure(LinearOperator& w, View x1, Index k) {
     auto block = [&](Index l) { return View{Q.p + l * bs * Q.ld, ld, bs, Q.ld}; };
 
     aug_apply(w, geo, block(0), z.view());
-    sumsq(ctx, z.view(), sc.get());
+    panel_sumsq(ctx, z.view(), split, sc.get());
     double scale = std::sqrt(read_scalar(ctx, sc.get()));
-    gemm(ctx, true, false, bs, bs, ld, 1.0, Q.p, Q.ld, z.data(), z.ld, 0.0, mtmp.data(), mtmp.ld);
+    panel_tn(ctx, block(0), z.view(), split, mtmp.data(), mtmp.ld);
     out.m.emplace_back(ctx, bs, bs, false);
     symmetrize(ctx, out.m.back().view(), mtmp.view());
     out.built = 1;
@@ -556,7 +630,7 @@ BlockLanczos block_lanczos_procedure(LinearOperator& w, View x1, Index k) {
             gemm(ctx, false, true, ld, bs, bs, -1.0, xp.p, xp.ld, out.b.back().data(), out.b.back().ld, 1.0,
                  z.data(), z.ld);
         }
-        sumsq(ctx, z.view(), sc.get());
+        panel_sumsq(ctx, z.view(), split, sc.get());
         const double rn = std::sqrt(read_scalar(ctx, sc.get()));
         if (rn <= 1e-10 * scale) {  // kBlockBreakdownTol (block_lanczos.hpp:64, :103)
             out.terminated_early = true;
@@ -566,7 +640,7 @@ BlockLanczos block_lanczos_procedure(LinearOperator& w, View x1, Index k) {
         copy(ctx, xn, z.view());
         DMat rb(ctx, bs, bs, true);
         View rv = rb.view();
-        const Index rank = thin_qr(ctx, xn, &rv);
+        const Index rank = thin_qr(ctx, xn, &rv, split);
         if (rank < bs) {
             fill(ctx, xn, 0.0);
             out.terminated_early = true;
@@ -575,9 +649,9 @@ BlockLanczos block_lanczos_procedure(LinearOperator& w, View x1, Index k) {
         out.b.push_back(std::move(rb));
         ++out.built;
         aug_apply(w, geo, xn, z.view());
-        sumsq(ctx, z.view(), sc.get());
+        panel_sumsq(ctx, z.view(), split, sc.get());
         scale = std::max(scale, std::sqrt(read_scalar(ctx, sc.get())));
-        gemm(ctx, true, false, bs, bs, ld, 1.0, xn.p, xn.ld, z.data(), z.ld, 0.0, mtmp.data(), mtmp.ld);
+        panel_tn(ctx, xn, z.view(), split, mtmp.data(), mtmp.ld);
         out.m.emplace_back(ctx, bs, bs, false);
         symmetrize(ctx, out.m.back().view(), mtmp.view());
     }
@@ -592,7 +666,8 @@ static BlwsResult blws_svd_exact(LinearOperator& w, const DWarm& warm, Index k, 
     const Index m = w.rows(), n = w.cols();
     const Index bs = warm.rank();
     if (bs < 1) throw std::invalid_argument("blws_svd: empty warm start (seed via adapt_subspace)");
-    if (r < 1 || r > std::min(m, n)) throw std::invalid_argument("blws_svd: bad r");
+    const Index m_all = w.row_sharded() ? w.shard().m_total : m;
+    if (r < 1 || r > std::min(m_all, n)) throw std::invalid_argument("blws_svd: bad r");
     if (warm.geo.m != m || warm.geo.n != n) throw std::invalid_argument("blws_svd: warm start does not match operator");
     BlwsResult out;
     Index k_eff = k;
@@ -600,7 +675,7 @@ static BlwsResult blws_svd_exact(LinearOperator& w, const DWarm& warm, Index k, 
         k_eff = (r + bs - 1) / bs;
         out.k_raised = true;
     }
-    k_eff = std::min(k_eff, (m + n) / bs);
+    k_eff = std::min(k_eff, (m_all + n) / bs);
     k_eff = std::max<Index>(k_eff, 1);
     const Stack geo{m, n};
 
@@ -608,9 +683,11 @@ static BlwsResult blws_svd_exact(LinearOperator& w, const DWarm& warm, Index k, 
     // so the 1/sqrt(2) is folded away.
     DMat x1(ctx, geo.ld(), bs, false);
     copy(ctx, x1.view(), warm.panel());
+    const RowSplit split = w.panel_split();
+    const RowSplit usplit{split.sharded ? m : 0};
     {
         View xv = x1.view();
-        thin_qr(ctx, xv, nullptr);
+        thin_qr(ctx, xv, nullptr, split);
     }
     BlockLanczos fac = block_lanczos_procedure(w, x1.view(), k_eff);
     out.terminated_early = fac.terminated_early;
@@ -650,11 +727,12 @@ static BlwsResult blws_svd_exact(LinearOperator& w, const DWarm& warm, Index k, 
              next.uv.data(), next.uv.ld);
         std::copy(hv.begin(), hv.begin() + keep, next.sigma.begin());
         View u = next.u(), v = next.v();
-        thin_qr(ctx, u, nullptr);
+        thin_qr(ctx, u, nullptr, usplit);
         thin_qr(ctx, v, nullptr);
     }
     if (keep < r) {
-        next = adapt_subspace(ctx, keep > 0 ? &next : nullptr, r, m, n, rng);
+        next = adapt_subspace(ctx, keep > 0 ? &next : nullptr, r, m, n, rng,
+                              w.row_sharded() ? &w.shard() : nullptr);
         out.padded = true;
     }
     out.warm = std::move(next);
@@ -713,17 +791,17 @@ struct QrRec {
 
 // thin_qr_impl's common case as a fixed launch sequence (both CholQR passes,
 // each skipped on the device for a scaled-identity Gram).
-QrRec thin_qr_deferred(Context& ctx, View x, View* r_out, Slots& sl) {
+QrRec thin_qr_deferred(Context& ctx, View x, View* r_out, Slots& sl, RowSplit split) {
     const Index rows = x.rows, b = x.cols;
     QrRec q{sl.take(), sl.take(), sl.take(3), sl.take(), sl.take(3), sl.take()};
     ctx.region_begin(2);
-    DMat r1 = gram(ctx, x);
+    DMat r1 = gram(ctx, x, split);
     DMat ri1(ctx, b, b, false);
     chol_inv_upper(ctx, r1.view(), ri1.view(), reinterpret_cast<int*>(sl.at(q.st1)), sl.at(q.dg1), kSkipRel,
                    sl.at(q.hss));
     DMat y(ctx, rows, b, false);
     gemm(ctx, false, false, rows, b, b, 1.0, x.p, x.ld, ri1.data(), ri1.ld, 0.0, y.data(), y.ld);
-    DMat r2 = gram(ctx, y.view());
+    DMat r2 = gram(ctx, y.view(), split);
     DMat ri2(ctx, b, b, false);
     chol_inv_upper(ctx, r2.view(), ri2.view(), reinterpret_cast<int*>(sl.at(q.st2)), sl.at(q.dg2), kSkipRel,
                    sl.at(q.dg2 + 2));
@@ -761,6 +839,7 @@ BlockLanczos block_lanczos_deferred(LinearOperator& w, View x1, Index k, Slots& 
     Context& ctx = w.ctx();
     const Stack geo{w.rows(), w.cols()};
     const Index bs = x1.cols, ld = geo.ld();
+    const RowSplit split = w.panel_split();
     BlockLanczos out;
     out.q = DMat(ctx, ld, k * bs, true);
     View Q = out.q.view();
@@ -770,8 +849,8 @@ BlockLanczos block_lanczos_deferred(LinearOperator& w, View x1, Index k, Slots& 
     auto block = [&](Index l) { return View{Q.p + l * bs * Q.ld, ld, bs, Q.ld}; };
     aug_apply(w, geo, block(0), z.view());
     rec.scale0 = sl.take();
-    sumsq(ctx, z.view(), sl.at(rec.scale0));
-    gemm(ctx, true, false, bs, bs, ld, 1.0, Q.p, Q.ld, z.data(), z.ld, 0.0, mtmp.data(), mtmp.ld);
+    panel_sumsq(ctx, z.view(), split, sl.at(rec.scale0));
+    panel_tn(ctx, block(0), z.view(), split, mtmp.data(), mtmp.ld);
     out.m.emplace_back(ctx, bs, bs, false);
     symmetrize(ctx, out.m.back().view(), mtmp.view());
     out.built = 1;
@@ -785,18 +864,18 @@ BlockLanczos block_lanczos_deferred(LinearOperator& w, View x1, Index k, Slots& 
                  z.data(), z.ld);
         }
         rec.rn.push_back(sl.take());
-        sumsq(ctx, z.view(), sl.at(rec.rn.back()));
+        panel_sumsq(ctx, z.view(), split, sl.at(rec.rn.back()));
         View xn = block(l);
         copy(ctx, xn, z.view());
         DMat rb(ctx, bs, bs, true);
         View rv = rb.view();
-        rec.qr.push_back(thin_qr_deferred(ctx, xn, &rv, sl));
+        rec.qr.push_back(thin_qr_deferred(ctx, xn, &rv, sl, split));
         out.b.push_back(std::move(rb));
         ++out.built;
         aug_apply(w, geo, xn, z.view());
         rec.scale.push_back(sl.take());
-        sumsq(ctx, z.view(), sl.at(rec.scale.back()));
-        gemm(ctx, true, false, bs, bs, ld, 1.0, xn.p, xn.ld, z.data(), z.ld, 0.0, mtmp.data(), mtmp.ld);
+        panel_sumsq(ctx, z.view(), split, sl.at(rec.scale.back()));
+        panel_tn(ctx, xn, z.view(), split, mtmp.data(), mtmp.ld);
         out.m.emplace_back(ctx, bs, bs, false);
         symmetrize(ctx, out.m.back().view(), mtmp.view());
     }
@@ -844,11 +923,13 @@ DeferredRecs enqueue_deferred(LinearOperator& w, View src, const DeferredShape& 
     Context& ctx = w.ctx();
     const Stack geo{sh.m, sh.n};
     DeferredRecs rec;
+    const RowSplit split = w.panel_split();
+    const RowSplit usplit{split.sharded ? sh.m : 0};
     DMat x1(ctx, geo.ld(), sh.bs, false);
     copy(ctx, x1.view(), src);
     {
         View xv = x1.view();
-        rec.q1 = thin_qr_deferred(ctx, xv, nullptr, sl);
+        rec.q1 = thin_qr_deferred(ctx, xv, nullptr, sl, split);
     }
     BlockLanczos fac = block_lanczos_deferred(w, x1.view(), sh.k_eff, sl, rec.lrec);
     const Index bs = sh.bs, d = sh.d, want = sh.want;
@@ -871,25 +952,50 @@ DeferredRecs enqueue_deferred(LinearOperator& w, View src, const DeferredShape& 
     View u{next_uv.p, sh.m, want, next_uv.ld}, v{next_uv.p + geo.mp(), sh.n, want, next_uv.ld};
     {
         AuxScope aux(ctx);  // the two QRs are independent
-        rec.qv = thin_qr_deferred(ctx, v, nullptr, sl);
+        rec.qv = thin_qr_deferred(ctx, v, nullptr, sl, RowSplit{});
     }
-    rec.qu = thin_qr_deferred(ctx, u, nullptr, sl);
+    rec.qu = thin_qr_deferred(ctx, u, nullptr, sl, usplit);
     return rec;
 }
 
-// the exact path's host tests on the fetched slots
+// the exact path's host tests on the fetched slots (BLWS_DEBUG=1: the failing one on stderr)
 bool finish_deferred(const DeferredRecs& rec, const Slots& sl, const DeferredShape& sh) {
-    Index rank = 0;
-    if (!qr_check(rec.q1, sl, sh.bs, &rank) || !lanczos_check(rec.lrec, sl, sh.bs) ||
-        !qr_check(rec.qu, sl, sh.want, &rank) || !qr_check(rec.qv, sl, sh.want, &rank))
+    const bool dbg = std::getenv("BLWS_DEBUG") != nullptr;
+    auto fail = [&](const char* why) {
+        if (dbg) std::fprintf(stderr, "blws_svd deferred -> exact: %s\n", why);
         return false;
+    };
+    auto qr_dbg = [&](const char* nm, const QrRec& q) {
+        if (dbg)
+            std::fprintf(stderr, "  %s: hss %.3e st %d/%d diag [%.3e, %.3e] rank %lld\n", nm, sl.val(q.hss),
+                         sl.as_int(q.st1), sl.as_int(q.st2), sl.val(q.dg1), sl.val(q.dg1 + 1),
+                         static_cast<long long>(sl.as_i64(q.rank)));
+    };
+    Index rank = 0;
+    if (!qr_check(rec.q1, sl, sh.bs, &rank)) {
+        qr_dbg("x1", rec.q1);
+        return fail("X1 QR");
+    }
+    if (!lanczos_check(rec.lrec, sl, sh.bs)) {
+        for (const auto& q : rec.lrec.qr) qr_dbg("lanczos", q);
+        return fail("block Lanczos breakdown / rank");
+    }
+    if (!qr_check(rec.qu, sl, sh.want, &rank)) {
+        qr_dbg("u", rec.qu);
+        return fail("U QR");
+    }
+    if (!qr_check(rec.qv, sl, sh.want, &rank)) {
+        qr_dbg("v", rec.qv);
+        return fail("V QR");
+    }
     const double* hv = sl.h.data() + rec.vslot;
     for (Index i = 0; i < sh.want; ++i)
-        if (!std::isfinite(hv[i])) return false;
+        if (!std::isfinite(hv[i])) return fail("non-finite Ritz value");
     const double floor = 1e-12 * std::fabs(hv[0]);
     Index kept = 0;
     while (kept < sh.want && hv[kept] > floor) ++kept;
-    return kept == sh.want;
+    if (kept != sh.want) return fail("keep < min(r, d)");
+    return true;
 }
 
 bool graphs_enabled() {
@@ -906,6 +1012,7 @@ bool graphs_enabled() {
 struct SvdGraph {
     const void* key_data = nullptr;
     Index bs = 0, k = 0, r = 0;
+    bool comm = false;  // captured with the allreduces of a row-sharded operator
     int seen = 0;
     bool failed = false;
     cudaGraphExec_t exec = nullptr;
@@ -928,32 +1035,35 @@ BlwsResult blws_svd(LinearOperator& w, const DWarm& warm, Index k, Index r, Rng&
     Context& ctx = w.ctx();
     const Index m = w.rows(), n = w.cols();
     const Index bs = warm.rank();
-    if (bs < 1 || r < 1 || r > std::min(m, n) || warm.geo.m != m || warm.geo.n != n)
+    const Index m_all = w.row_sharded() ? w.shard().m_total : m;  // global rows of a row shard
+    if (bs < 1 || r < 1 || r > std::min(m_all, n) || warm.geo.m != m || warm.geo.n != n)
         return blws_svd_exact(w, warm, k, r, rng);  // throws the reference's errors
     DeferredShape sh{m, n, bs, k, r, k, 0, 0, false};
     if (r > sh.k_eff * bs) {
         sh.k_eff = (r + bs - 1) / bs;
         sh.k_raised = true;
     }
-    sh.k_eff = std::max<Index>(std::min(sh.k_eff, (m + n) / bs), 1);
+    sh.k_eff = std::max<Index>(std::min(sh.k_eff, (m_all + n) / bs), 1);
     sh.d = sh.k_eff * bs;
     sh.want = std::min(r, sh.d);
     // keep < r needs the Rng padding: the exact path owns that case
-    if (force_exact() || sh.want < r || k < 1 || k * bs > m + n) return blws_svd_exact(w, warm, k, r, rng);
+    if (force_exact() || sh.want < r || k < 1 || k * bs > m_all + n) return blws_svd_exact(w, warm, k, r, rng);
     const Stack geo{m, n};
-    const int cap = 16 * static_cast<int>(sh.k_eff + 3) + static_cast<int>(sh.want) + 8;
+    const int cap = 16 * static_cast<int>(sh.k_eff + 3) + static_cast<int>(sh.want) + 9;
 
     // ---- graph plan for this (operator data, shape); eager on first sight
     SvdGraph* plan = nullptr;
     if (graphs_enabled()) {
         for (auto& g : w.svd_graphs())
-            if (g->key_data == w.data_key() && g->bs == bs && g->k == k && g->r == r) plan = g.get();
+            if (g->key_data == w.data_key() && g->bs == bs && g->k == k && g->r == r && g->comm == ctx.has_comm())
+                plan = g.get();
         if (!plan) {
             auto g = std::make_shared<SvdGraph>();
             g->key_data = w.data_key();
             g->bs = bs;
             g->k = k;
             g->r = r;
+            g->comm = ctx.has_comm();
             w.svd_graphs().push_back(g);
             plan = g.get();
         }
@@ -971,7 +1081,7 @@ BlwsResult blws_svd(LinearOperator& w, const DWarm& warm, Index k, Index r, Rng&
         if (!plan->exec) {
             // capture once: stable buffers outside the graph, temporaries inside
             plan->sl = std::make_unique<Slots>(ctx, cap);
-            plan->finite_slot = plan->sl->take();
+            plan->finite_slot = plan->sl->take(2);
             plan->src = DMat(ctx, geo.ld(), bs, false);
             plan->next = DMat(ctx, geo.ld(), sh.want, true);
             plan->stamps = DBuf<std::uint64_t>(ctx, 64);
@@ -979,8 +1089,9 @@ BlwsResult blws_svd(LinearOperator& w, const DWarm& warm, Index k, Index r, Rng&
         sl = plan->sl.get();
         finite_slot = plan->finite_slot;
         // a pending async upload is waited for and checked outside the graph
-        zero(ctx, sl->at(finite_slot), sizeof(double));
+        zero(ctx, sl->at(finite_slot), 2 * sizeof(double));
         w.defer_pending_check(reinterpret_cast<int*>(sl->at(finite_slot)));
+        share_flag(ctx, reinterpret_cast<int*>(sl->at(finite_slot)), sl->at(finite_slot + 1));
         if (!plan->exec) {
             const std::int64_t l0 = ctx.launches(), a0 = w.application_count();
             BLWS_CUDA(cudaStreamBeginCapture(ctx.stream(), cudaStreamCaptureModeRelaxed));
@@ -1020,14 +1131,16 @@ BlwsResult blws_svd(LinearOperator& w, const DWarm& warm, Index k, Index r, Rng&
     } else {
         local = std::make_unique<Slots>(ctx, cap);
         sl = local.get();
-        finite_slot = sl->take();
+        finite_slot = sl->take(2);
         w.defer_pending_check(reinterpret_cast<int*>(sl->at(finite_slot)));  // async-assigned W
+        share_flag(ctx, reinterpret_cast<int*>(sl->at(finite_slot)), sl->at(finite_slot + 1));
         next = make_warm(ctx, m, n, sh.want);
         rec = enqueue_deferred(w, warm.panel(), sh, *sl, next.panel());
     }
     sl->fetch(ctx);  // the one host round trip
     if (graphed) ctx.add_replayed_regions(plan->regions, plan->stamps.get());
-    if (sl->as_int(finite_slot) != 0) throw std::invalid_argument("DenseOperator: non-finite entries");
+    if (ctx.has_comm() ? sl->val(finite_slot + 1) != 0.0 : sl->as_int(finite_slot) != 0)
+        throw std::invalid_argument("DenseOperator: non-finite entries");
     if (!finish_deferred(rec, *sl, sh)) {
         ++g_blws_deferred_fallbacks;
         return blws_svd_exact(w, warm, k, r, rng);
@@ -1054,6 +1167,8 @@ class DeviceLanczos {
 public:
     DeviceLanczos(LinearOperator& w, const std::vector<double>& q1_logical, Index cap)
         : w_(w), ctx_(w.ctx()), geo_{w.rows(), w.cols()}, dim_(geo_.m + geo_.n), ld_(geo_.ld()), cap_(cap) {
+        if (w.row_sharded() && ctx_.has_comm())
+            throw std::invalid_argument("lanczos: row-sharded operators are not supported (blws_svd only)");
         q_ = DMat(ctx_, ld_, cap_, true);
         next_ = DMat(ctx_, ld_, 1, true);
         r_ = DMat(ctx_, ld_, 1, true);

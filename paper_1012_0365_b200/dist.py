@@ -1,0 +1,61 @@
+"""Row-sharded multi-GPU plumbing on torch.distributed.
+
+One process per GPU. W (m_total x n) is split into contiguous row panels;
+rank p holds rows [row0, row0 + rows) of W and of U, V is replicated. The
+device path (csrc/host_core.cu, RowSplit) allreduces every reduction over
+panel rows with NCCL; this module only does the host-side set-up: the row
+partition and the rendezvous of the NCCL unique id (made on rank 0, broadcast
+over the process group -- gloo on CPU, nccl on GPU).
+"""
+from __future__ import annotations
+
+
+def row_partition(m: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous balanced split: (row0, rows) of rank `rank`; the first
+    m % world ranks get one extra row."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("row_partition: bad rank / world")
+    if m < world:
+        raise ValueError("row_partition: fewer rows than ranks")
+    base, extra = divmod(m, world)
+    row0 = rank * base + min(rank, extra)
+    return row0, base + (1 if rank < extra else 0)
+
+
+def broadcast_unique_id(group=None) -> bytes:
+    """Rank 0 makes an NCCL unique id; every rank returns the same 128 bytes."""
+    import torch
+    import torch.distributed as dist
+
+    from . import api
+
+    rank = dist.get_rank(group)
+    backend = dist.get_backend(group)
+    dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
+    buf = torch.zeros(128, dtype=torch.uint8, device=dev)
+    if rank == 0:
+        buf.copy_(torch.frombuffer(bytearray(api.nccl_unique_id()), dtype=torch.uint8))
+    dist.broadcast(buf, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+    return bytes(buf.cpu().numpy().tobytes())
+
+
+def init_comm(ctx, group=None) -> None:
+    """Attach an NCCL communicator over the process group to `ctx` (collective)."""
+    import torch.distributed as dist
+
+    uid = broadcast_unique_id(group)
+    ctx.init_comm(dist.get_world_size(group), dist.get_rank(group), uid)
+
+
+def shard_operator(w_local, m_total: int, row0: int, ctx, device: bool = False, ld=None):
+    """DenseOperator over this rank's row panel (host array or device tensor),
+    marked as rows [row0, row0 + rows) of m_total."""
+    from . import api
+
+    if device:
+        rows, n = w_local.shape[1], w_local.shape[0]  # column-major panel = row-major (n, rows) tensor
+        op = api.DenseOperator(w_local, ctx=ctx, device=True, shape=(rows, n), ld=ld or rows)
+    else:
+        op = api.DenseOperator(w_local, ctx=ctx)
+    op.set_row_shard(m_total, row0)
+    return op
