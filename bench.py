@@ -194,11 +194,26 @@ def run_gpu(args):
     dev = torch.device(f"cuda:{local}")
     ctx = B.Context(local)
     stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
+    sharded = args.mode == "sharded"
 
     W, U, V, s, eps = make_instance(B.Rng)
-    # column-major device copies (a row-major (n, m) tensor is W in column-major)
+    row0, rows = 0, M
+    if sharded:
+        # row-sharded C2: this rank's panel of W and U, V replicated,
+        # every reduction over panel rows allreduced over NCCL
+        from paper_1012_0365_b200 import dist as D
+
+        row0, rows = D.row_partition(M, world, rank)
+        if world > 1:
+            D.init_comm(ctx)
+        else:
+            ctx.init_comm(1, 0, B.api.nccl_unique_id())
+        W, U = np.asfortranarray(W[row0:row0 + rows]), np.asfortranarray(U[row0:row0 + rows])
+    # column-major device copies (a row-major (n, rows) tensor is W in column-major)
     Wd = torch.from_numpy(np.ascontiguousarray(W.T)).to(dev)
-    op = B.DenseOperator(Wd, ctx=ctx, device=True, shape=(M, N), ld=M)
+    op = B.DenseOperator(Wd, ctx=ctx, device=True, shape=(rows, N), ld=rows)
+    if sharded:
+        op.set_row_shard(M, row0)
     warm0 = B.DeviceWarmStart.from_host(U, V, s, ctx)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > L2
 
@@ -252,10 +267,13 @@ def run_gpu(args):
     Uh = torch.from_numpy(np.ascontiguousarray(U.T)).pin_memory().numpy().T
     Vh = torch.from_numpy(np.ascontiguousarray(V.T)).pin_memory().numpy().T
     sh = s.copy()
-    out_h = B.WarmStart(torch.empty((R, M), dtype=torch.float64).pin_memory().numpy().T,
+    out_h = B.WarmStart(torch.empty((R, rows), dtype=torch.float64).pin_memory().numpy().T,
                         torch.empty((R, N), dtype=torch.float64).pin_memory().numpy().T,
                         torch.empty(R, dtype=torch.float64).pin_memory().numpy())
     ops = [B.DenseOperator(W, ctx=ctx), B.DenseOperator(W, ctx=ctx)]
+    if sharded:
+        for o in ops:
+            o.set_row_shard(M, row0)
     # raw pinned H2D bandwidth of the same buffer (context for the e2e number)
     wd_tmp = torch.empty_like(Wh, device=dev)
     wd_tmp.copy_(Wh, non_blocking=True)
@@ -269,19 +287,21 @@ def run_gpu(args):
     ctx.synchronize()
     e2e_steps = max(1, args.steps)
     t0 = time.perf_counter()
-    ops[0].assign_async(Wh.data_ptr(), M)
+    ops[0].assign_async(Wh.data_ptr(), rows)
     for i in range(e2e_steps):
         w_in = B.DeviceWarmStart.from_host(Uh, Vh, sh, ctx)
         # same-direction copies share the DMA queue: queue the next W behind this warm start
         if i + 1 < e2e_steps:
-            ops[(i + 1) % 2].assign_async(Wh.data_ptr(), M)  # next step's W, overlapped
+            ops[(i + 1) % 2].assign_async(Wh.data_ptr(), rows)  # next step's W, overlapped
         r_e2e = B.blws_svd(ops[i % 2], w_in, 2, R, B.Rng(SEED ^ 0x5BDBEEF), keep_device=True)
-        out = r_e2e.warm.to_host(M, N, out=out_h)
+        out = r_e2e.warm.to_host(rows, N, out=out_h)
         _ = int(np.sum(out.sigma > eps))
     ctx.synchronize()
     e2e_s = time.perf_counter() - t0
-    h2d = M * N * 8 + (M + N) * R * 8 + R * 8
-    d2h = (M + N) * R * 8 + R * 8
+    # bytes per step over the whole job (a row shard moves its rows of W and U)
+    reps = 1 if sharded else world
+    h2d = reps * (M * N * 8 + M * R * 8) + world * (N * R * 8 + R * 8)
+    d2h = reps * M * R * 8 + world * (N * R * 8 + R * 8)
 
     # ---- FP64 peak on this GPU (roofline denominator), DMMA and DFMA
     peak_dmma = ctx.fp64_peak(0)
@@ -302,8 +322,9 @@ def run_gpu(args):
     if world > 1:
         torch.distributed.all_reduce(mine, op=torch.distributed.ReduceOp.MAX)
     total_ms, e2e_s = float(mine[0]), float(mine[1])
-    value = world * args.steps / (total_ms / 1e3)
-    e2e_value = world * e2e_steps / e2e_s
+    units = 1 if sharded else world  # a sharded call spans all ranks; replicas each make one
+    value = units * args.steps / (total_ms / 1e3)
+    e2e_value = units * e2e_steps / e2e_s
     k1_avg_ms = k1["ms"] / max(1, k1["count"])
     k1_flops = k1["flops"] / max(1, k1["count"])
     achieved_tf = k1_flops / (k1_avg_ms * 1e-3) / 1e12 if k1_avg_ms > 0 else 0.0
@@ -317,11 +338,13 @@ def run_gpu(args):
         line = {
             "metric": METRIC, "value": value, "unit": "calls/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded, reference RNG recipe)",
             "config": {"workload": "C2 standalone warm-started BLWS partial SVT", "m": M, "n": N, "r": R, "k": 2,
                        "signal_rank": K_SIGNAL, "eps": eps, "achieved_rank": achieved,
-                       "l2": "flushed between steps (256 MB write)", "parallelism": f"replicas x{world}"},
+                       "l2": "flushed between steps (256 MB write)",
+                       "parallelism": f"rowshard x{world} (NCCL allreduce per panel reduction)" if sharded
+                       else f"replicas x{world}"},
             "e2e": {"value": e2e_value, "unit": "calls/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "pinned_h2d_GBps": h2d_gbps,
                     "overlap": "W of step i+1 uploads on the copy stream during step i (assign_async, 2 operators)"},
@@ -358,6 +381,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--mode", default="replicas", choices=["replicas", "sharded"],
+                    help="replicas: N independent C2 calls per step (weak scaling, default); sharded: one C2 "
+                         "call with W row-sharded over the N GPUs (strong scaling)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
