@@ -127,11 +127,21 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples), "via": "nvml" if self._nvml else "nvidia-smi"}
 
 
-def cpu_baseline(W, U, V, s, steps=None, budget_s=20.0):
-    """Oracle blws_svd on the same W (all host cores), bounded sample."""
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_baseline(W, U, V, s, steps=None, budget_s=20.0, threads=None):
+    """Oracle blws_svd on the same W (all host cores unless `threads`), bounded sample."""
     from oracle import oracle as O
 
-    cores = os.cpu_count() or 1
+    cores = threads or os.cpu_count() or 1
     O.set_threads(cores)
     op = O.DenseOperator(W)
     warm = O.WarmStart(U, V, s)
@@ -174,6 +184,7 @@ def run_reference(args):
                        "l2": "W (128 MB) ~ L2 size; CPU run"},
             "impl": "reference",
             "cpu_baseline": {"value": value, "unit": "calls/s", "cores": cores, "kind": "port",
+                             "host": {"nproc": os.cpu_count(), "cpu": cpu_model()},
                              "sample": f"{args.steps} oracle blws_svd calls on the C2 W (OpenBLAS, {cores} threads)"},
             "e2e": {"value": value, "unit": "calls/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -364,10 +375,14 @@ def run_gpu(args):
         }
         if not args.no_cpu:
             times, cores = cpu_baseline(W, U, V, s)
+            t1, _ = cpu_baseline(W, U, V, s, budget_s=10.0, threads=1)
             line["cpu_baseline"] = {"value": len(times) / sum(times), "unit": "calls/s", "cores": cores,
                                     "kind": "port",
                                     "sample": f"{len(times)} oracle blws_svd calls on the same C2 W "
-                                              f"(OpenBLAS, {cores} threads)"}
+                                              f"(OpenBLAS, {cores} threads)",
+                                    "single_thread": {"value": len(t1) / sum(t1), "unit": "calls/s", "cores": 1,
+                                                      "sample": f"{len(t1)} calls, 1 thread"},
+                                    "host": {"nproc": os.cpu_count(), "cpu": cpu_model()}}
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
