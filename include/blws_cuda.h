@@ -72,6 +72,8 @@ int blws_rng_destroy(blws_rng* rng);
 int blws_rng_split(const blws_rng* rng, uint64_t tag, blws_rng** out);       /* rng.hpp:22-24 */
 uint64_t blws_rng_next_u64(blws_rng* rng);                                 /* rng.hpp:26 */
 double blws_rng_uniform(blws_rng* rng, double lo, double hi);              /* rng.hpp:29-32 */
+/* n successive rng.uniform(lo, hi) draws (instance generation, synth.hpp:88-89). */
+int blws_rng_uniform_fill(blws_rng* rng, int64_t n, double lo, double hi, double* out);
 uint64_t blws_rng_uniform_index(blws_rng* rng, uint64_t n);                /* rng.hpp:35-42 */
 double blws_rng_normal(blws_rng* rng);                                     /* rng.hpp:45-60 */
 int blws_rng_gaussian_matrix(blws_rng* rng, int64_t rows, int64_t cols, double* out); /* rng.hpp:63-68 */

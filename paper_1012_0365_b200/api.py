@@ -62,6 +62,7 @@ SIGNATURES = {
     "blws_rng_split": (ci, [vp, u64, P(vp)]),
     "blws_rng_next_u64": (u64, [vp]),
     "blws_rng_uniform": (dbl, [vp, dbl, dbl]),
+    "blws_rng_uniform_fill": (ci, [vp, i64, dbl, dbl, vp]),
     "blws_rng_uniform_index": (u64, [vp, u64]),
     "blws_rng_normal": (dbl, [vp]),
     "blws_rng_gaussian_matrix": (ci, [vp, i64, i64, vp]),
@@ -267,7 +268,9 @@ class Rng:
         return out
 
     def uniform_fill(self, n, lo, hi) -> np.ndarray:
-        return np.array([self.uniform(lo, hi) for _ in range(n)])
+        out = np.empty(int(n))
+        _check(lib().blws_rng_uniform_fill(self._h, int(n), float(lo), float(hi), _ptr(out)))
+        return out
 
 
 def nccl_unique_id() -> bytes:

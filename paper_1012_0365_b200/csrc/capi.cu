@@ -159,6 +159,12 @@ int blws_rng_split(const blws_rng* r, uint64_t tag, blws_rng** out) {
 }
 uint64_t blws_rng_next_u64(blws_rng* r) { return r->rng.next_u64(); }
 double blws_rng_uniform(blws_rng* r, double lo, double hi) { return r->rng.uniform(lo, hi); }
+int blws_rng_uniform_fill(blws_rng* r, int64_t n, double lo, double hi, double* out) {
+    return guard([&] {
+        need(r && (n == 0 || out), "uniform_fill: null argument");
+        for (int64_t i = 0; i < n; ++i) out[i] = r->rng.uniform(lo, hi);
+    });
+}
 uint64_t blws_rng_uniform_index(blws_rng* r, uint64_t n) { return r->rng.uniform_index(n); }
 double blws_rng_normal(blws_rng* r) { return r->rng.normal(); }
 int blws_rng_gaussian_matrix(blws_rng* r, int64_t rows, int64_t cols, double* out) {

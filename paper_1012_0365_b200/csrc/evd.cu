@@ -259,6 +259,30 @@ __global__ void __launch_bounds__(kOrmWarps * 32) ormtr_k(const double* __restri
         for (int i = lane; i < n; i += 32) z[i + j * ldz] = zc[i];
 }
 
+// Z = H_0 ... H_{n-3} Y straight from global memory (large orders, where the
+// shared-memory staging of ormtr_k does not fit): one warp per eigenvector,
+// reflectors and the vector read through L2.
+__global__ void __launch_bounds__(kOrmWarps * 32) ormtr_global_k(const double* __restrict__ lp,
+                                                                 const double* __restrict__ tau, int n, int want,
+                                                                 double* z, long ldz) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const long j = static_cast<long>(blockIdx.x) * kOrmWarps + warp;
+    if (j >= want) return;
+    double* zc = z + j * ldz;
+    for (int k = n - 3; k >= 0; --k) {
+        const double tk = tau[k];
+        if (tk == 0.0) continue;
+        const int w = n - k - 1;
+        const double* vk = lp + lidx(k + 1, k, n);  // vk[0] = 1 (stored)
+        double s = 0.0;
+        for (int i = lane; i < w; i += 32) s = fma(i == 0 ? 1.0 : vk[i], zc[k + 1 + i], s);
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        const double f = tk * s;
+        for (int i = lane; i < w; i += 32) zc[k + 1 + i] -= f * (i == 0 ? 1.0 : vk[i]);
+        __syncwarp();
+    }
+}
+
 // Z = H_0 ... H_{n-3} Y with every reflector resident in shared memory (the
 // packed lower triangle, n <= 208) and each eigenvector in registers of one
 // warp (row i = lane + 32 q): no block barrier after the load, one warp
@@ -380,6 +404,13 @@ void sym_evd_top(Context& ctx, View t, Index want, double* values, View vectors)
     }
     if (ormtr_full(ctx, lp.get(), tau.get(), n, static_cast<int>(want), vectors)) return;
     const int smem2 = (kOrmChunk + kOrmWarps) * n * 8;
+    if (smem2 > kSmemBudget) {
+        ormtr_global_k<<<static_cast<unsigned>((want + kOrmWarps - 1) / kOrmWarps), kOrmWarps * 32, 0,
+                         ctx.stream()>>>(lp.get(), tau.get(), n, static_cast<int>(want), vectors.p, vectors.ld);
+        ctx.note_launch();
+        ctx.check_launch("ormtr_global_k");
+        return;
+    }
     ormtr_k<<<static_cast<unsigned>((want + kOrmWarps - 1) / kOrmWarps), kOrmWarps * 32, smem2, ctx.stream()>>>(
         lp.get(), tau.get(), n, static_cast<int>(want), vectors.p, vectors.ld);
     ctx.note_launch();

@@ -39,6 +39,8 @@ def rpca_lowrank_sparse(m, rank, n_corrupt, seed, rng_cls, sample):
 
 
 def _uniform_bulk(rng, n, lo, hi):
+    if hasattr(rng, "uniform_fill"):
+        return rng.uniform_fill(n, lo, hi)
     return np.array([rng.uniform(lo, hi) for _ in range(n)])
 
 
@@ -73,3 +75,25 @@ def mc_lowrank(m, rank, n_obs, seed, rng_cls, sample):
     np.add.at(colptr, cols + 1, 1)
     colptr = np.cumsum(colptr)
     return colptr, rows.astype(np.int32), vals, ML, MR
+
+
+def rpca_lowrank_sparse_device(m, rank, n_corrupt, seed, rng_cls, sample, device):
+    """C5-scale variant of rpca_lowrank_sparse: the same draws (host Rng, Floyd
+    sample), D = L R^T + E0 formed on the GPU (a 40000^2 D is 12.8 GB).
+    Returns column-major D and A0 as row-major (m, m) torch tensors holding the
+    transposes (i.e. column-major buffers), plus the host positions / values."""
+    import torch
+
+    base = rng_cls(seed)
+    L = base.split(1).gaussian_matrix(m, rank)
+    R = base.split(2).gaussian_matrix(m, rank)
+    pos = sample(m * m, n_corrupt, base.split(4))
+    vals = _uniform_bulk(base.split(5), len(pos), -500.0, 500.0)
+    Ld = torch.from_numpy(np.ascontiguousarray(L)).to(device)
+    Rd = torch.from_numpy(np.ascontiguousarray(R)).to(device)
+    a0t = Rd @ Ld.T  # row-major (m, m) of A0^T = column-major A0
+    dt = a0t.clone()
+    flat = dt.view(-1)  # column-major flat index of (i, j) = i + j m = row-major index of A0^T
+    flat.index_add_(0, torch.from_numpy(np.asarray(pos, dtype=np.int64)).to(device),
+                    torch.from_numpy(np.asarray(vals)).to(device))
+    return dt, a0t, pos, vals
