@@ -122,6 +122,10 @@ int64_t blws_operator_application_count(const blws_operator* op);
 /* LinearOperator::apply_pair_block (:57-61): top = W*right (m x b), bot = W^T*left (n x b); host buffers. */
 int blws_operator_apply_pair_block(blws_operator* op, int64_t b, const double* left, const double* right,
                                    double* top, double* bot);
+/* LinearOperator::apply_pair (:51-54): top = W*right (m), bot = W^T*left (n); one
+   pass over a dense W (K10); counts 1. Host buffers. */
+int blws_operator_apply_pair(blws_operator* op, const double* left, const double* right, double* top,
+                             double* bot);
 
 /* ------------------------------------------------------------- warm start
  * WarmStart (block_lanczos.hpp:45-52): U m x r, V n x r, sigma r. */

@@ -81,6 +81,7 @@ SIGNATURES = {
     "blws_operator_cols": (i64, [vp]),
     "blws_operator_application_count": (i64, [vp]),
     "blws_operator_apply_pair_block": (ci, [vp, i64, vp, vp, vp, vp]),
+    "blws_operator_apply_pair": (ci, [vp, vp, vp, vp, vp]),
     "blws_warm_start_create": (ci, [vp, i64, i64, i64, vp, i64, vp, i64, vp, ci, P(vp)]),
     "blws_warm_start_copy": (ci, [vp, P(vp)]),
     "blws_warm_start_rank": (i64, [vp]),
@@ -303,6 +304,14 @@ class LinearOperator:
 
     def application_count(self) -> int:
         return int(lib().blws_operator_application_count(self._h))
+
+    def apply_pair_vec(self, left, right):
+        """apply_pair (linear_operator.hpp:51-54): (W right, W^T left), counts 1."""
+        left = np.ascontiguousarray(left, dtype=np.float64)
+        right = np.ascontiguousarray(right, dtype=np.float64)
+        top, bot = np.empty(self.rows()), np.empty(self.cols())
+        _check(lib().blws_operator_apply_pair(self._h, _ptr(left), _ptr(right), _ptr(top), _ptr(bot)))
+        return top, bot
 
     def apply_pair_block(self, left, right):
         left, right = F(left), F(right)

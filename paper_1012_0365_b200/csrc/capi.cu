@@ -310,6 +310,22 @@ int blws_operator_apply_pair_block(blws_operator* op, int64_t b, const double* l
     });
 }
 
+int blws_operator_apply_pair(blws_operator* op, const double* left, const double* right, double* top,
+                             double* bot) {
+    return guard([&] {
+        need(op && left && right && top && bot, "apply_pair: null argument");
+        Context& c = op->op->ctx();
+        const Index m = op->op->rows(), n = op->op->cols();
+        DBuf<double> l(c, static_cast<size_t>(m)), r(c, static_cast<size_t>(n)), t(c, static_cast<size_t>(m)),
+            bt(c, static_cast<size_t>(n));
+        upload(c, View{l.get(), m, 1, m}, left, m);
+        upload(c, View{r.get(), n, 1, n}, right, n);
+        op->op->apply_pair(l.get(), r.get(), t.get(), bt.get());
+        download(c, View{t.get(), m, 1, m}, top, m);
+        download(c, View{bt.get(), n, 1, n}, bot, n);
+    });
+}
+
 // ------------------------------------------------------------- warm start
 int blws_warm_start_create(blws_context* ctx, int64_t m, int64_t n, int64_t r, const double* u, int64_t ldu,
                            const double* v, int64_t ldv, const double* sigma, int where, blws_warm_start** out) {

@@ -285,8 +285,7 @@ void DenseOperator::pair_block_impl(View left, View right, View top, View bot) {
 
 void DenseOperator::pair_impl(const double* left, const double* right, double* top, double* bot) {
     ensure_ready();
-    gemv(ctx_, false, m_, n_, 1.0, p_, ld_, right, 0.0, top);
-    gemv(ctx_, true, m_, n_, 1.0, p_, ld_, left, 0.0, bot);
+    pair_gemv(ctx_, m_, n_, p_, ld_, right, left, top, bot);  // one read of W for both products
 }
 
 // ======================================================== SparseOperator

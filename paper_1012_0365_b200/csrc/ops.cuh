@@ -14,6 +14,9 @@ void gemm(Context& ctx, bool ta, bool tb, Index M, Index N, Index K, double alph
 
 // ------------------------------------------------------------------ level-1 / small
 void fill(Context& ctx, View x, double v);
+/// top = W x (m), bot = W^T y (n) in one pass over column-major W (K10).
+void pair_gemv(Context& ctx, Index m, Index n, const double* w, Index ld, const double* x, const double* y,
+               double* top, double* bot);
 /// Zeroes `bytes` (multiple of 4) with a kernel: a cudaMemsetAsync may be
 /// queued on a copy engine behind a pending host upload.
 void zero(Context& ctx, void* p, size_t bytes);

@@ -141,3 +141,16 @@ def test_tridiagonal_degenerate_clusters(gpu):
     vals, vecs = gpu.sym_evd_tridiagonal_top(d, e, 3)
     assert np.allclose(vals, 1.0, atol=1e-14)
     assert np.linalg.norm(vecs.T @ vecs - np.eye(3)) <= 1e-10
+
+
+@pytest.mark.parametrize("m,n", [(1, 1), (37, 1029), (2500, 700), (5000, 3001)])
+def test_pair_gemv_matches_numpy(gpu, m, n):
+    # K10: W x and W^T y from one pass over W (Lanczos step), via the single-vector pair apply
+    rs = np.random.default_rng(m + n)
+    w = rs.standard_normal((m, n))
+    x, y = rs.standard_normal(n), rs.standard_normal(m)
+    op = gpu.DenseOperator(w)
+    top, bot = op.apply_pair_block(y[:, None], x[:, None])  # block path (reference)
+    t1, b1 = op.apply_pair_vec(y, x)
+    assert np.abs(t1 - w @ x).max() <= 1e-12 * np.sqrt(n) * np.abs(w @ x).max()
+    assert np.abs(b1 - w.T @ y).max() <= 1e-12 * np.sqrt(m) * np.abs(w.T @ y).max()
