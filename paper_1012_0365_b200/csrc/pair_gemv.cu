@@ -41,45 +41,50 @@ __global__ void __launch_bounds__(kPgThreads) pair_gemv_k(const double* __restri
         yr[q] = ok[q] ? y[r] : 0.0;
         acc[q] = 0.0;
     }
+    // 16-byte path: lane owns rows (r2, r2 + 1); both must exist (else the scalar path)
+    const long r2 = row0 + 2 * lane;
+    const bool vec2 = (ld % 2 == 0) && ((reinterpret_cast<unsigned long long>(w) & 15) == 0) &&
+                      (row0 + 64 <= m);  // warp-uniform: the warp's 64 rows are all inside
+    const bool ok2 = r2 + 1 < m;
+    const double2 y2 = make_double2(ok2 ? y[r2] : 0.0, ok2 ? y[r2 + 1] : 0.0);
+    if (vec2) {  // the vector path accumulates rows (r2, r2 + 1) instead of (lane, lane + 32)
+        acc[0] = acc[1] = 0.0;
+    }
     int buf = 0;
     for (long jc = j0; jc < j1; jc += 32) {
         double bp[32];
-        if (jc + 32 <= j1) {
-            // full chunk, branch-free: all 32 x kPgRowsPerLane loads can be in flight
-            double v[32][kPgRowsPerLane];
+        if (jc + 32 <= j1 && vec2) {
+            // full chunk, branch-free: each lane loads its 2 adjacent rows as one
+            // 16-byte load, all 32 loads of the chunk in flight before use
+            double2 v[32];
 #pragma unroll
             for (int c = 0; c < 32; ++c) {
                 const double* col = w + (jc + c) * ld;
-#pragma unroll
-                for (int q = 0; q < kPgRowsPerLane; ++q) {
-                    const long r = row0 + lane + 32 * q;
-                    v[c][q] = ok[q] ? __ldg(col + r) : 0.0;
-                }
+                v[c] = ok2 ? __ldg(reinterpret_cast<const double2*>(col + r2)) : make_double2(0.0, 0.0);
             }
 #pragma unroll
             for (int c = 0; c < 32; ++c) {
                 const double xj = __ldg(x + jc + c);
-                bp[c] = 0.0;
-#pragma unroll
-                for (int q = 0; q < kPgRowsPerLane; ++q) {
-                    acc[q] = fma(v[c][q], xj, acc[q]);
-                    bp[c] = fma(v[c][q], yr[q], bp[c]);
-                }
+                acc[0] = fma(v[c].x, xj, acc[0]);
+                acc[1] = fma(v[c].y, xj, acc[1]);
+                bp[c] = fma(v[c].y, y2.y, v[c].x * y2.x);
             }
         } else {
 #pragma unroll
             for (int c = 0; c < 32; ++c) {
                 bp[c] = 0.0;
                 const long j = jc + c;
-                if (j < j1) {  // warp-uniform (tail chunk only)
+                if (j < j1) {  // warp-uniform (tail chunk / unaligned only)
                     const double xj = x[j];
                     const double* col = w + j * ld;
 #pragma unroll
                     for (int q = 0; q < kPgRowsPerLane; ++q) {
-                        const long r = row0 + lane + 32 * q;
-                        const double vv = ok[q] ? col[r] : 0.0;
+                        const long r = vec2 ? r2 + q : row0 + lane + 32 * q;
+                        const bool okr = vec2 ? ok2 : ok[q];
+                        const double yq = vec2 ? (q == 0 ? y2.x : y2.y) : yr[q];
+                        const double vv = okr ? col[r] : 0.0;
                         acc[q] = fma(vv, xj, acc[q]);
-                        bp[c] = fma(vv, yr[q], bp[c]);
+                        bp[c] = fma(vv, yq, bp[c]);
                     }
                 }
             }
@@ -109,8 +114,8 @@ __global__ void __launch_bounds__(kPgThreads) pair_gemv_k(const double* __restri
     }
 #pragma unroll
     for (int q = 0; q < kPgRowsPerLane; ++q) {
-        const long r = row0 + lane + 32 * q;
-        if (ok[q]) ptop[cg * m + r] = acc[q];
+        const long r = vec2 ? r2 + q : row0 + lane + 32 * q;
+        if (vec2 ? ok2 : ok[q]) ptop[cg * m + r] = acc[q];
     }
 }
 
