@@ -15,7 +15,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libblws_cuda.so")
+LIB_PATH = os.environ.get("BLWS_LIB_PATH") or os.path.join(_HERE, "_lib", "libblws_cuda.so")
 
 i64, u64, dbl, vp, ci = C.c_int64, C.c_uint64, C.c_double, C.c_void_p, C.c_int
 P = C.POINTER

@@ -235,6 +235,47 @@ __device__ __forceinline__ void load_tile(double* As, double* Bs, const double* 
     }
 }
 
+// DMMA without `volatile`: register effects only, so the compiler may interleave
+// it with the cp.async prefetch and the fragment loads
+__device__ __forceinline__ void dmma_nv(double (&d)[2], double a, double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+        : "+d"(d[0]), "+d"(d[1])
+        : "d"(a), "d"(b));
+}
+
+// Interior tile (all BM rows of op(A) inside M, the whole BK inside the k range):
+// no clamping; B columns beyond N are zero-filled (their validity is fixed per CTA).
+template <bool TA, int BN>
+__device__ __forceinline__ void load_tile_fast(double* As, double* Bs, const double* __restrict__ A, long lda,
+                                               const double* __restrict__ B, long ldb, long N, long m0, long n0,
+                                               long k0) {
+    const int tid = threadIdx.x;
+    if (!TA) {
+        constexpr int CPR = BM / 2;
+#pragma unroll
+        for (int c = tid; c < CPR * BK; c += THREADS) {
+            const int k = c / CPR, i = (c % CPR) * 2;
+            cp_async16(As + k * AL<TA>::LD + i, A + (m0 + i) + (k0 + k) * lda, 16);
+        }
+    } else {
+        constexpr int CPR = BK / 2;
+#pragma unroll
+        for (int c = tid; c < CPR * BM; c += THREADS) {
+            const int i = c / CPR, k = (c % CPR) * 2;
+            cp_async16(As + i * AL<TA>::LD + k, A + (k0 + k) + (m0 + i) * lda, 16);
+        }
+    }
+    constexpr int CPR = BK / 2;
+#pragma unroll
+    for (int c = tid; c < CPR * BN; c += THREADS) {
+        const int j = c / CPR, k = (c % CPR) * 2;
+        const bool ok = n0 + j < N;
+        cp_async16(Bs + j * BL<BN>::LD + k, ok ? B + (k0 + k) + (n0 + j) * ldb : B, ok ? 16 : 0);
+    }
+}
+
+constexpr bool kPrefetchLate = false;  // measured: issuing the prefetch first is faster for W V
+
 /// acc[mi][ni][e] += op(A)(m0 + 16w + 8mi + g, k) * B(k, n0 + 8ni + 2t + e)
 template <bool TA, int BN>
 __device__ __forceinline__ void mainloop(double (&acc)[2][BN / 8][2], double* smem, const double* __restrict__ A,
@@ -246,26 +287,31 @@ __device__ __forceinline__ void mainloop(double (&acc)[2][BN / 8][2], double* sm
     const int g = lane >> 2, t = lane & 3;
     const int wm = warp * 16;
     const long ntiles = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
+    const bool rows_in = m0 + BM <= M;
+    auto stage_tile = [&](long tile, int slot) {
+        const long k0 = kbeg + tile * BK;
+        if (rows_in && k0 + BK <= kend)
+            load_tile_fast<TA, BN>(As + slot * AL<TA>::SIZE, Bs + slot * BL<BN>::SIZE, A, lda, B, ldb, N, m0, n0, k0);
+        else
+            load_tile<TA, BN>(As + slot * AL<TA>::SIZE, Bs + slot * BL<BN>::SIZE, A, lda, B, ldb, M, N, m0, n0, k0,
+                              kend);
+    };
 #pragma unroll
     for (int s = 0; s < STAGES - 1; ++s) {
-        if (s < ntiles)
-            load_tile<TA, BN>(As + s * AL<TA>::SIZE, Bs + s * BL<BN>::SIZE, A, lda, B, ldb, M, N, m0, n0,
-                              kbeg + s * BK, kend);
+        if (s < ntiles) stage_tile(s, s);
         cp_commit();
     }
     for (long kt = 0; kt < ntiles; ++kt) {
         cp_wait<STAGES - 2>();
         __syncthreads();
-        const long pf = kt + STAGES - 1;
-        if (pf < ntiles) {
-            const int ps = static_cast<int>(pf % STAGES);
-            load_tile<TA, BN>(As + ps * AL<TA>::SIZE, Bs + ps * BL<BN>::SIZE, A, lda, B, ldb, M, N, m0, n0,
-                              kbeg + pf * BK, kend);
-        }
-        cp_commit();
         const int st = static_cast<int>(kt % STAGES);
         const double* as = As + st * AL<TA>::SIZE;
         const double* bs = Bs + st * BL<BN>::SIZE;
+        const long pf = kt + STAGES - 1;
+        if (!kPrefetchLate) {
+            if (pf < ntiles) stage_tile(pf, static_cast<int>(pf % STAGES));
+            cp_commit();
+        }
 #pragma unroll
         for (int kk = 0; kk < BK; kk += 4) {
             double af[2];
@@ -279,6 +325,12 @@ __device__ __forceinline__ void mainloop(double (&acc)[2][BN / 8][2], double* sm
                 const double bf = bs[(ni * 8 + g) * BL<BN>::LD + kk + t];
                 dmma(acc[0][ni], af[0], bf);
                 dmma(acc[1][ni], af[1], bf);
+            }
+            if (kPrefetchLate && kk == 0) {
+                // prefetch after the first k-step, so the copies overlap the math
+                // (the slot written was consumed two iterations ago: safe after the barrier)
+                if (pf < ntiles) stage_tile(pf, static_cast<int>(pf % STAGES));
+                cp_commit();
             }
         }
     }
