@@ -173,6 +173,11 @@ int blws_spectral_norm(blws_operator* w, double tol, uint64_t seed, double* out)
 /* thin_qr (core/qr.hpp:24-47) on the device; host buffers. */
 int blws_thin_qr(blws_context* ctx, int64_t rows, int64_t cols, const double* m, double* q, double* r,
                  int64_t* rank);
+/* full_svd_small (small_dense.hpp:72-87): SVD of a host m x n W (m + n <= 4096)
+   via the top min(m, n) eigenpairs of the symmetric embedding; sigma
+   descending, u (m x p), v (n x p) column-major, p = min(m, n). */
+int blws_full_svd_small(blws_context* ctx, int64_t m, int64_t n, const double* w, double* sigma, double* u,
+                        double* v);
 /* sym_evd_small (core/small_dense.hpp:24-43): values descending. host buffers */
 int blws_sym_evd(blws_context* ctx, int64_t n, const double* t, double* values, double* vectors);
 /* top `want` pairs of sym_evd_tridiagonal (small_dense.hpp:46-62); vectors n x want. host buffers */

@@ -18,6 +18,7 @@ from .api import (  # noqa: F401
     adapt_subspace,
     blws_svd,
     deferred_fallbacks,
+    full_svd_small,
     graph_launches,
     block_lanczos_procedure,
     lanczos_partial_svd,

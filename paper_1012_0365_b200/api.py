@@ -95,6 +95,7 @@ SIGNATURES = {
     "blws_lanczos_partial_svd": (ci, [vp, i64, dbl, i64, u64, P(vp), vp]),
     "blws_spectral_norm": (ci, [vp, dbl, u64, P(dbl)]),
     "blws_thin_qr": (ci, [vp, i64, i64, vp, vp, vp, P(i64)]),
+    "blws_full_svd_small": (ci, [vp, i64, i64, vp, vp, vp, vp]),
     "blws_sym_evd": (ci, [vp, i64, vp, vp, vp]),
     "blws_sym_evd_tridiagonal_top": (ci, [vp, i64, vp, vp, i64, vp, vp]),
     "blws_dgemm": (ci, [vp, ci, ci, i64, i64, i64, dbl, vp, i64, vp, i64, dbl, vp, i64]),
@@ -528,6 +529,19 @@ def thin_qr(m, ctx: Context | None = None):
     rank = i64(0)
     _check(lib().blws_thin_qr(ctx._h, rows, cols, _ptr(m), _ptr(q), _ptr(r), C.byref(rank)))
     return q, r, rank.value
+
+
+def full_svd_small(w, ctx: Context | None = None):
+    """full_svd_small (small_dense.hpp:72-87) on the GPU: (u, sigma, v), descending."""
+    ctx = ctx or default_context()
+    w = F(w)
+    m, n = w.shape
+    p = min(m, n)
+    s = np.empty(p)
+    u = np.empty((m, p), order="F")
+    v = np.empty((n, p), order="F")
+    _check(lib().blws_full_svd_small(ctx._h, m, n, _ptr(w), _ptr(s), _ptr(u), _ptr(v)))
+    return u, s, v
 
 
 def sym_evd_small(t, ctx: Context | None = None):

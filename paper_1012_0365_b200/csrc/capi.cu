@@ -451,6 +451,24 @@ int blws_thin_qr(blws_context* ctx, int64_t rows, int64_t cols, const double* m,
         if (r) download(c, rr.view(), r, cols);
     });
 }
+int blws_full_svd_small(blws_context* ctx, int64_t m, int64_t n, const double* w, double* sigma, double* u,
+                        double* v) {
+    return guard([&] {
+        need(ctx && w && sigma && u && v && m > 0 && n > 0, "full_svd_small: bad argument");
+        for (int64_t i = 0; i < m * n; ++i)
+            if (!std::isfinite(w[i])) throw std::invalid_argument("full_svd_small: non-finite entries");
+        Context& c = *ctx->ctx;
+        const Index p = std::min(m, n);
+        DMat wd(c, m, n), ud(c, m, p), vd(c, n, p);
+        upload(c, wd.view(), w, m);
+        DBuf<double> s(c, static_cast<size_t>(p));
+        full_svd_small(c, wd.view(), s.get(), ud.view(), vd.view());
+        c.read(s.get(), sigma, static_cast<size_t>(p));
+        download(c, ud.view(), u, m);
+        download(c, vd.view(), v, n);
+        c.sync();
+    });
+}
 int blws_sym_evd(blws_context* ctx, int64_t n, const double* t, double* values, double* vectors) {
     return guard([&] {
         need(n > 0, "sym_evd_small: not square");

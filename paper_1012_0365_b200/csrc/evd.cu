@@ -417,4 +417,21 @@ void sym_evd_top(Context& ctx, View t, Index want, double* values, View vectors)
     ctx.check_launch("ormtr_k");
 }
 
+// full_svd_small (small_dense.hpp:72-87) on the device, from the symmetric
+// embedding (theorem 1, block_lanczos.hpp): the top p = min(m, n) eigenpairs of
+// [[0, W], [W^T, 0]] are (sigma_i, [u_i; v_i] / sqrt(2)). Exact to ~eps ||W||
+// for distinct nonzero sigma (a zero or repeated singular value mixes the
+// +/- pairs; the reference's BDCSVD has no such caveat).
+void full_svd_small(Context& ctx, View w, double* sigma, View u, View v) {
+    const Index m = w.rows, n = w.cols, p = std::min(m, n), d = m + n;
+    if (d > 4096) throw std::invalid_argument("full_svd_small: m + n exceeds the small-dense limit (4096)");
+    DMat t(ctx, d, d, true);
+    place_block(ctx, t.view().sub(0, m, m, n), w, false);
+    place_block(ctx, t.view().sub(m, 0, n, m), w, true);
+    DMat vecs(ctx, d, p, false);
+    sym_evd_top(ctx, t.view(), p, sigma, vecs.view());
+    copy(ctx, u, View{vecs.data(), m, p, vecs.ld}, std::sqrt(2.0));
+    copy(ctx, v, View{vecs.data() + m, n, p, vecs.ld}, std::sqrt(2.0));
+}
+
 }  // namespace blws

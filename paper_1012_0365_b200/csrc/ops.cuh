@@ -14,6 +14,9 @@ void gemm(Context& ctx, bool ta, bool tb, Index M, Index N, Index K, double alph
 
 // ------------------------------------------------------------------ level-1 / small
 void fill(Context& ctx, View x, double v);
+/// full_svd_small (small_dense.hpp:72-87) via the symmetric embedding: sigma (p),
+/// u (m x p), v (n x p), p = min(m, n), descending.
+void full_svd_small(Context& ctx, View w, double* sigma, View u, View v);
 /// top = W x (m), bot = W^T y (n) in one pass over column-major W (K10).
 void pair_gemv(Context& ctx, Index m, Index n, const double* w, Index ld, const double* x, const double* y,
                double* top, double* bot);

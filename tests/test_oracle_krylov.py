@@ -329,3 +329,14 @@ def test_acceptance_rpca_m500(O):
     for it in range(st.iterations // 2, st.iterations):
         r = 10 if it == 0 else st.predicted_ranks[it - 1]
         assert st.matvec_history[it] <= 2 * 2 * r + 2 * r
+
+
+def test_reference_gates_on_oracle(O):
+    # bench/checks.hpp:38-139 restated on the oracle (pins the device gate)
+    from paper_1012_0365_b200 import checks
+
+    t1 = checks.theorem1_suite(12, 20240601, mod=O)
+    assert t1.ok() and t1.total == 36, t1.failures
+    px = checks.prox_agreement_suite(2, 7, mod=O, tol=5e-4)
+    assert px.ok(), px.failures
+    assert all(b > 1e-5 for b, _ in px.values)  # the reference's 1e-5 is not reproduced
