@@ -34,6 +34,7 @@ extern "C" {
 #define BLWS_NUMERICAL_FAILURE 2
 #define BLWS_CUDA_ERROR 3
 #define BLWS_NCCL_ERROR 4
+#define BLWS_IO_ERROR 5
 
 #define BLWS_HOST 0
 #define BLWS_DEVICE 1
@@ -264,6 +265,19 @@ int blws_mc_svt(blws_context* ctx, int64_t m, int64_t n, int64_t nnz, const int6
                 const double* truth_ml, const double* truth_mr, int64_t r_true, double* u, double* sigma, double* v,
                 int64_t cap, int64_t* rank, blws_solver_stats* stats, int64_t* predicted_ranks,
                 int64_t* matvec_history, double* residual_history, int64_t hist_cap);
+
+/* ---- Matrix Market I/O (core/matrix_market.hpp:63-168): host files; the
+   reference's std::runtime_error becomes BLWS_IO_ERROR. Dense = "array"
+   column-major (lda), sparse = "coordinate" read into / written from CSC. */
+int blws_mm_write_dense(const char* path, int64_t rows, int64_t cols, const double* a, int64_t lda);
+int blws_mm_write_sparse(const char* path, int64_t rows, int64_t cols, int64_t nnz, const int64_t* colptr,
+                         const int32_t* rowidx, const double* values);
+/* out == NULL: only rows / cols are returned. */
+int blws_mm_read_dense(const char* path, int64_t* rows, int64_t* cols, double* out, int64_t ldo);
+/* colptr == NULL: only rows / cols / nnz are returned (then call again with
+   colptr (cols + 1), rowidx (nnz), values (nnz)). */
+int blws_mm_read_sparse(const char* path, int64_t* rows, int64_t* cols, int64_t* nnz, int64_t* colptr,
+                        int32_t* rowidx, double* values);
 
 #ifdef __cplusplus
 }

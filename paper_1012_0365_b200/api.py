@@ -95,6 +95,10 @@ SIGNATURES = {
     "blws_lanczos_partial_svd": (ci, [vp, i64, dbl, i64, u64, P(vp), vp]),
     "blws_spectral_norm": (ci, [vp, dbl, u64, P(dbl)]),
     "blws_thin_qr": (ci, [vp, i64, i64, vp, vp, vp, P(i64)]),
+    "blws_mm_write_dense": (ci, [C.c_char_p, i64, i64, vp, i64]),
+    "blws_mm_write_sparse": (ci, [C.c_char_p, i64, i64, i64, vp, vp, vp]),
+    "blws_mm_read_dense": (ci, [C.c_char_p, P(i64), P(i64), vp, i64]),
+    "blws_mm_read_sparse": (ci, [C.c_char_p, P(i64), P(i64), P(i64), vp, vp, vp]),
     "blws_full_svd_small": (ci, [vp, i64, i64, vp, vp, vp, vp]),
     "blws_sym_evd": (ci, [vp, i64, vp, vp, vp]),
     "blws_sym_evd_tridiagonal_top": (ci, [vp, i64, vp, vp, i64, vp, vp]),
@@ -140,6 +144,8 @@ def _check(rc):
         raise ValueError(msg)
     if rc == 2:
         raise RuntimeError(msg)
+    if rc == 5:
+        raise OSError(msg)
     raise BlwsError(f"status {rc}: {msg}")
 
 
@@ -529,6 +535,39 @@ def thin_qr(m, ctx: Context | None = None):
     rank = i64(0)
     _check(lib().blws_thin_qr(ctx._h, rows, cols, _ptr(m), _ptr(q), _ptr(r), C.byref(rank)))
     return q, r, rank.value
+
+
+# ------------------------------------------------ Matrix Market (core/matrix_market.hpp)
+def mm_write_dense(path, a):
+    a = F(a)
+    _check(lib().blws_mm_write_dense(os.fsencode(path), a.shape[0], a.shape[1], _ptr(a), a.shape[0]))
+
+
+def mm_write_sparse(path, m, n, colptr, rowidx, vals):
+    colptr = np.ascontiguousarray(colptr, dtype=np.int64)
+    rowidx = np.ascontiguousarray(rowidx, dtype=np.int32)
+    vals = np.ascontiguousarray(vals, dtype=np.float64)
+    _check(lib().blws_mm_write_sparse(os.fsencode(path), m, n, len(vals), _ptr(colptr), _ptr(rowidx), _ptr(vals)))
+
+
+def mm_read_dense(path) -> np.ndarray:
+    r, c = i64(0), i64(0)
+    _check(lib().blws_mm_read_dense(os.fsencode(path), C.byref(r), C.byref(c), None, 0))
+    out = np.empty((r.value, c.value), order="F")
+    _check(lib().blws_mm_read_dense(os.fsencode(path), C.byref(r), C.byref(c), _ptr(out), r.value))
+    return out
+
+
+def mm_read_sparse(path):
+    """-> (rows, cols, colptr int64, rowidx int32, values): CSC, rows ascending."""
+    r, c, nz = i64(0), i64(0), i64(0)
+    _check(lib().blws_mm_read_sparse(os.fsencode(path), C.byref(r), C.byref(c), C.byref(nz), None, None, None))
+    colptr = np.empty(c.value + 1, dtype=np.int64)
+    rowidx = np.empty(nz.value, dtype=np.int32)
+    vals = np.empty(nz.value)
+    _check(lib().blws_mm_read_sparse(os.fsencode(path), C.byref(r), C.byref(c), C.byref(nz), _ptr(colptr),
+                                     _ptr(rowidx), _ptr(vals)))
+    return r.value, c.value, colptr, rowidx, vals
 
 
 def full_svd_small(w, ctx: Context | None = None):

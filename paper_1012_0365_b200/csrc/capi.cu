@@ -7,6 +7,7 @@
 
 #include "../../include/blws_cuda.h"
 #include "host.hpp"
+#include "matrix_market.hpp"
 #include "ops.cuh"
 
 using namespace blws;
@@ -56,6 +57,9 @@ int guard(F&& f) {
     } catch (const CommError& e) {
         g_err = e.what();
         return BLWS_NCCL_ERROR;
+    } catch (const IoError& e) {
+        g_err = e.what();
+        return BLWS_IO_ERROR;
     } catch (const std::bad_alloc& e) {
         g_err = std::string("allocation failed: ") + e.what();
         return BLWS_CUDA_ERROR;
@@ -791,5 +795,53 @@ extern "C" int blws_probe(blws_context* ctx, double* out) {
         out[2] = ms * 10.0;
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
+    });
+}
+
+int blws_mm_write_dense(const char* path, int64_t rows, int64_t cols, const double* a, int64_t lda) {
+    return guard([&] {
+        need(path && a && rows > 0 && cols > 0 && lda >= rows, "mm_write_dense: bad argument");
+        mm_write_dense(path, rows, cols, a, lda);
+    });
+}
+int blws_mm_write_sparse(const char* path, int64_t rows, int64_t cols, int64_t nnz, const int64_t* colptr,
+                         const int32_t* rowidx, const double* values) {
+    return guard([&] {
+        need(path && colptr && rows > 0 && cols > 0 && nnz >= 0, "mm_write_sparse: bad argument");
+        need(nnz == 0 || (rowidx && values), "mm_write_sparse: null entries");
+        mm_write_sparse(path, rows, cols, nnz, colptr, rowidx, values);
+    });
+}
+int blws_mm_read_dense(const char* path, int64_t* rows, int64_t* cols, double* out, int64_t ldo) {
+    return guard([&] {
+        need(path && rows && cols, "mm_read_dense: bad argument");
+        Index r = 0, c = 0;
+        std::vector<double> data;
+        mm_read_dense(path, &r, &c, out ? &data : nullptr);
+        *rows = r;
+        *cols = c;
+        if (!out) return;
+        need(ldo >= r, "mm_read_dense: ldo < rows");
+        for (Index j = 0; j < c; ++j)
+            for (Index i = 0; i < r; ++i) out[i + j * ldo] = data[static_cast<size_t>(i + j * r)];
+    });
+}
+int blws_mm_read_sparse(const char* path, int64_t* rows, int64_t* cols, int64_t* nnz, int64_t* colptr,
+                        int32_t* rowidx, double* values) {
+    return guard([&] {
+        need(path && rows && cols && nnz, "mm_read_sparse: bad argument");
+        Index r = 0, c = 0;
+        std::vector<std::int64_t> cp;
+        std::vector<std::int32_t> ri;
+        std::vector<double> vs;
+        mm_read_sparse(path, &r, &c, &cp, &ri, &vs);
+        *rows = r;
+        *cols = c;
+        *nnz = static_cast<int64_t>(vs.size());
+        if (!colptr) return;
+        need(rowidx && values, "mm_read_sparse: null outputs");
+        std::copy(cp.begin(), cp.end(), colptr);
+        std::copy(ri.begin(), ri.end(), rowidx);
+        std::copy(vs.begin(), vs.end(), values);
     });
 }

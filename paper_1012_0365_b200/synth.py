@@ -97,3 +97,27 @@ def rpca_lowrank_sparse_device(m, rank, n_corrupt, seed, rng_cls, sample, device
     flat.index_add_(0, torch.from_numpy(np.asarray(pos, dtype=np.int64)).to(device),
                     torch.from_numpy(np.asarray(vals)).to(device))
     return dt, a0t, pos, vals
+
+
+def export_rpca_instance(d, a_true, e_true, directory):
+    """export_instance (synth.hpp:152-159): d.mtx, a_true.mtx, e_true.mtx (array format)."""
+    import os
+
+    from . import api
+
+    os.makedirs(directory, exist_ok=True)
+    api.mm_write_dense(os.path.join(directory, "d.mtx"), d)
+    api.mm_write_dense(os.path.join(directory, "a_true.mtx"), a_true)
+    api.mm_write_dense(os.path.join(directory, "e_true.mtx"), e_true)
+
+
+def export_mc_instance(m, n, colptr, rowidx, vals, ml, mr, directory):
+    """export_instance (synth.hpp:161-168): observed.mtx (coordinate), ml.mtx, mr.mtx."""
+    import os
+
+    from . import api
+
+    os.makedirs(directory, exist_ok=True)
+    api.mm_write_sparse(os.path.join(directory, "observed.mtx"), m, n, colptr, rowidx, vals)
+    api.mm_write_dense(os.path.join(directory, "ml.mtx"), ml)
+    api.mm_write_dense(os.path.join(directory, "mr.mtx"), mr)
