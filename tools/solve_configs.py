@@ -20,12 +20,19 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import paper_1012_0365_b200 as B  # noqa: E402
-from paper_1012_0365_b200 import synth  # noqa: E402
+from paper_1012_0365_b200 import report, synth  # noqa: E402
 
 SEED = 1
+ROWS = {}  # config -> [ReportRow] (bench/report.hpp schema)
 
 
-def rpca(name, m, rank, frac, oracle=True):
+def _row(problem, m, method, st, t, r=0, s_dr=0.0, s_m2=0.0):
+    return report.ReportRow(problem=problem, m=m, method=method, rel_err=st.rel_err, rank_hat=st.rank_hat,
+                            e_l0=max(st.e_l0, 0), iters=st.iterations, time_s=t, matvecs=st.matvec_count, r=r,
+                            s_dr=s_dr, s_m2=s_m2, converged=bool(st.converged))
+
+
+def rpca(name, m, rank, frac, oracle=True, baseline=False):
     from oracle import oracle as O
     d, a0, _, _ = synth.rpca_lowrank_sparse(m, rank, int(round(frac * m * m)), SEED, B.Rng, B.sample_distinct)
     bseed = SEED ^ 0x5BDBEEF
@@ -34,6 +41,12 @@ def rpca(name, m, rank, frac, oracle=True):
     t = time.perf_counter()
     a, e, st, _ = B.rpca_adm(d, B.SvdBackend.blws(seed=bseed, ctx=ctx), truth=a0)
     gpu_s = time.perf_counter() - t
+    ROWS.setdefault(name, [])
+    if baseline:  # the paper's ADM row: the same solver with the cold Lanczos backend
+        t = time.perf_counter()
+        _, _, sl, _ = B.rpca_adm(d, B.SvdBackend.lanczos(seed=bseed, ctx=ctx), truth=a0, want_outputs=False)
+        ROWS[name].append(_row(report.RPCA, m, "ADM", sl, time.perf_counter() - t))
+    ROWS[name].append(_row(report.RPCA, m, "BLWS-ADM", st, gpu_s))
     line = dict(config=name, m=m, rank=rank, corrupt=frac, gpu_solve_s=gpu_s, iterations=st.iterations,
                 rank_hat=st.rank_hat, rel_err=st.rel_err, e_l0=st.e_l0, matvecs=st.matvec_count,
                 converged=st.converged)
@@ -51,13 +64,21 @@ def rpca(name, m, rank, frac, oracle=True):
     print(json.dumps(line), flush=True)
 
 
-def mc(name, m, rank, nobs):
+def mc(name, m, rank, nobs, baseline=False):
     colptr, rowidx, vals, ml, mr = synth.mc_lowrank(m, rank, nobs, SEED, B.Rng, B.sample_distinct)
     ctx = B.Context(0)
     t = time.perf_counter()
     u, s, v, st = B.mc_svt(m, m, colptr, rowidx, vals, B.SvdBackend.blws(seed=SEED ^ 0x5BDBEEF, ctx=ctx),
                            tol_outer=1e-6, truth_ml=ml, truth_mr=mr, cap=512)
     gpu_s = time.perf_counter() - t
+    s_dr = nobs / (rank * (2 * m - rank))
+    ROWS.setdefault(name, [])
+    if baseline:
+        t = time.perf_counter()
+        _, _, _, sl = B.mc_svt(m, m, colptr, rowidx, vals, B.SvdBackend.lanczos(seed=SEED ^ 0x5BDBEEF, ctx=ctx),
+                               tol_outer=1e-6, truth_ml=ml, truth_mr=mr, cap=512)
+        ROWS[name].append(_row(report.MC, m, "SVT", sl, time.perf_counter() - t, rank, s_dr, nobs / (m * m)))
+    ROWS[name].append(_row(report.MC, m, "BLWS-SVT", st, gpu_s, rank, s_dr, nobs / (m * m)))
     print(json.dumps(dict(config=name, m=m, rank=rank, nobs=nobs, gpu_solve_s=gpu_s, iterations=st.iterations,
                           rank_hat=st.rank_hat, rel_err=st.rel_err, matvecs=st.matvec_count,
                           converged=st.converged)), flush=True)
@@ -89,15 +110,21 @@ if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("configs", nargs="*", default=["C1", "C3", "C4"])
     ap.add_argument("--no-oracle", action="store_true")
+    ap.add_argument("--baseline", action="store_true", help="also run the Lanczos-backend solver (ADM / SVT rows)")
+    ap.add_argument("--report", choices=["csv", "markdown"], help="emit the bench/report.hpp table(s) at the end")
     a = ap.parse_args()
     for c in a.configs:
         if c == "C1":
-            rpca("C1", 500, 25, 0.05, not a.no_oracle)
+            rpca("C1", 500, 25, 0.05, not a.no_oracle, a.baseline)
         elif c == "C3":
-            rpca("C3", 2000, 100, 0.10, not a.no_oracle)
+            rpca("C3", 2000, 100, 0.10, not a.no_oracle, a.baseline)
         elif c == "C4":
-            mc("C4", 10000, 50, 10_000_000)
+            mc("C4", 10000, 50, 10_000_000, a.baseline)
         elif c == "C5":
             rpca_device("C5", 40000, 400, 0.05)
         elif c == "C5s":  # reduced C5 (same recipe) to check the device path quickly
             rpca_device("C5s", 8000, 80, 0.05)
+    if a.report:
+        for name, rows in ROWS.items():
+            print(f"# {name}")
+            print(report.emit_table(rows, a.report), end="")
