@@ -1011,6 +1011,7 @@ bool graphs_enabled() {
 struct SvdGraph {
     const void* key_data = nullptr;
     Index bs = 0, k = 0, r = 0;
+    std::uint64_t last_use = 0;  // LRU stamp (the cache holds kMaxSvdGraphs plans per operator)
     bool comm = false;  // captured with the allreduces of a row-sharded operator
     int seen = 0;
     bool failed = false;
@@ -1028,6 +1029,8 @@ struct SvdGraph {
 };
 
 std::int64_t g_blws_deferred_fallbacks = 0;  // diagnostics (tests)
+constexpr size_t kMaxSvdGraphs = 4;
+static std::uint64_t g_svd_graph_clock = 0;
 std::int64_t g_blws_graph_launches = 0;
 
 BlwsResult blws_svd(LinearOperator& w, const DWarm& warm, Index k, Index r, Rng& rng) {
@@ -1057,6 +1060,17 @@ BlwsResult blws_svd(LinearOperator& w, const DWarm& warm, Index k, Index r, Rng&
             if (g->key_data == w.data_key() && g->bs == bs && g->k == k && g->r == r && g->comm == ctx.has_comm())
                 plan = g.get();
         if (!plan) {
+            // bounded cache: a solve whose rank keeps changing must not pin one
+            // graph (panels + graph memory pool) per rank it ever visited
+            auto& gs = w.svd_graphs();
+            if (gs.size() >= kMaxSvdGraphs) {
+                auto lru = std::min_element(gs.begin(), gs.end(), [](const std::shared_ptr<SvdGraph>& a,
+                                                                     const std::shared_ptr<SvdGraph>& b) {
+                    return a->last_use < b->last_use;
+                });
+                ctx.sync();  // nothing in flight may still use the evicted graph
+                gs.erase(lru);
+            }
             auto g = std::make_shared<SvdGraph>();
             g->key_data = w.data_key();
             g->bs = bs;
@@ -1066,6 +1080,7 @@ BlwsResult blws_svd(LinearOperator& w, const DWarm& warm, Index k, Index r, Rng&
             w.svd_graphs().push_back(g);
             plan = g.get();
         }
+        plan->last_use = ++g_svd_graph_clock;
         // captured on the third call with this key (one-off shapes stay eager:
         // capture + instantiate costs tens of ms)
         if (plan->failed || (!plan->exec && plan->seen++ < 2)) plan = nullptr;

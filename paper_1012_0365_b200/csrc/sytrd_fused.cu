@@ -7,11 +7,14 @@
 //        k-1 to each element, then accumulate p = A22 v_k from the updated
 //        value -- rows in per-lane registers (row i = lane + 32 q), columns as
 //        per-warp dots (column j = wid + 16 c), reduced by a batched transpose;
-//   [P1] one row per thread: p_i = tau_k (column dot + row partials), p^T v;
-//   [P2] w_i = p_i - K v_i; look-ahead: apply update k to column k+1 (element
-//        i per thread) and its sum of squares below the subdiagonal;
+//        (each warp also reduces its share of v^T A v, so K = tau^2/2 v^T A v
+//        needs no block reduction of its own);
+//   [P]  one row per thread: p_i = tau_k (column dot + row partials), w_i =
+//        p_i - K v_i; look-ahead: apply update k to column k+1 (element i per
+//        thread; w_{k+1} formed by every thread from broadcast reads) and its
+//        sum of squares below the subdiagonal;
 //   [P3] every thread forms beta, tau_{k+1}, v_{k+1} and stores its reflector
-//        element; four block barriers per step.
+//        element; three block barriers per step.
 // Thread ownership in [S] is static: row i >= column j needs q >= c / 2, so
 // the unrolled loops cover exactly that slot triangle; only the q = c / 2 slot
 // carries a lane predicate. v and w are double-buffered by step parity and zero
@@ -56,13 +59,21 @@ __device__ __forceinline__ void form_reflector(double* a, int n, int c, double s
                                                double* e, double* tau, double* tau_out) {
     const int i = threadIdx.x;
     double* colc = a + floff(c, n);  // colc[r - c] = A(r, c)
-    const double alpha = colc[1];
-    double tk = 0.0, beta = alpha, scl = 0.0;
-    if (s2 > 0.0) {
-        beta = -copysign(sqrt(fma(alpha, alpha, s2)), alpha);
-        tk = (beta - alpha) / beta;
-        scl = 1.0 / (alpha - beta);
+    // the scalar chain (sqrt, two divides) once per warp, then broadcast: 512
+    // redundant copies would queue on the slow double-precision units
+    double tk = 0.0, beta = 0.0, scl = 0.0;
+    if ((threadIdx.x & 31) == 0) {
+        const double alpha = colc[1];
+        beta = alpha;
+        if (s2 > 0.0) {
+            beta = -copysign(sqrt(fma(alpha, alpha, s2)), alpha);
+            tk = (beta - alpha) / beta;
+            scl = 1.0 / (alpha - beta);
+        }
     }
+    tk = __shfl_sync(0xffffffffu, tk, 0);
+    beta = __shfl_sync(0xffffffffu, beta, 0);
+    scl = __shfl_sync(0xffffffffu, scl, 0);
     if (i < n) {
         double vi = 0.0;
         if (i > c) vi = tk == 0.0 ? 0.0 : (i == c + 1 ? 1.0 : xi * scl);
@@ -133,6 +144,7 @@ __global__ void __launch_bounds__(kFT) sytrd_fused_k(const double* __restrict__ 
                 wor[q] = wo[i];
                 acc[q] = 0.0;
             }
+            double qv = 0.0;  // this lane's share of v^T A v (A = the updated A22)
 #pragma unroll
             for (int c = 0; c < CN; ++c) {
                 dp[c] = 0.0;
@@ -165,6 +177,7 @@ __global__ void __launch_bounds__(kFT) sytrd_fused_k(const double* __restrict__ 
                     const bool ok = (q != c / 2 || i >= j) && (q != QN - 1 || i < n);
                     if (ok) col[i] = xs[q];
                 }
+                qv = fma(vj, dp[c], qv);  // v^T A v, strictly-lower half through column j
             }
             // column dots: batched transpose-reduce of the CN (<= 16) values
             double r[16];
@@ -187,6 +200,10 @@ __global__ void __launch_bounds__(kFT) sytrd_fused_k(const double* __restrict__ 
             if ((lane & 1) == 0 && cc < CN && jj > k && jj < n) pcol[jj] = r[0];
 #pragma unroll
             for (int q = 0; q < QN; ++q) pw[wid * NP + lane + 32 * q] = acc[q];
+#pragma unroll
+            for (int q = 0; q < QN; ++q) qv = fma(vr[q], acc[q], qv);  // lower half incl. the diagonal
+            qv = warp_sum(qv);
+            if (lane == 0) red[wid] = qv;  // per-warp share: K needs no separate reduction
         }
 #ifdef SYTRD_PROBE
         if (threadIdx.x == 0 && k < 256) s_sweep[k] = static_cast<unsigned>(clock64() - tp_);
@@ -194,7 +211,13 @@ __global__ void __launch_bounds__(kFT) sytrd_fused_k(const double* __restrict__ 
         PHASE_MARK(1);
         __syncthreads();
         PHASE_MARK(2);
-        // ---- [P1] p_i = tau (column dot + row partials), p^T v
+        // ---- [P] K = tau/2 p^T v = tau^2/2 v^T A v (per-warp shares); p_i, w_i;
+        //      look-ahead update of column k+1 (w_{k+1} formed by every thread
+        //      from broadcast reads) and its squared norm below the subdiagonal
+        double vav = 0.0;
+#pragma unroll
+        for (int ww = 0; ww < kFW; ++ww) vav += red[ww];
+        const double K = 0.5 * tk * tk * vav;
         double p = 0.0;
         if (row > k && row < n) {
             double sacc = pcol[row];
@@ -203,18 +226,14 @@ __global__ void __launch_bounds__(kFT) sytrd_fused_k(const double* __restrict__ 
             p = tk * sacc;
         }
         const double vi = row < NP ? v[row] : 0.0;
-        double pv = warp_sum(p * vi);
-        if (lane == 0) red[wid] = pv;
-        if (row < NP) pcol[row] = p;  // pcol now holds p (row k+1 read in [P2])
-        PHASE_MARK(3);
-        __syncthreads();
-        PHASE_MARK(4);
-        // ---- [P2] w = p - K v; look-ahead update of column k+1 and its norm
-        const double K = 0.5 * tk * warp_sum(lane < kFW ? red[lane] : 0.0);
         const double wi = fma(-K, vi, p);
         if (row < NP) wn[row] = wi;
         const int c1 = k + 1;
-        const double wc = fma(-K, v[c1], pcol[c1]), vc = v[c1];  // w_{k+1}, v_{k+1} entries of step k
+        double pc = pcol[c1];
+#pragma unroll
+        for (int ww = 0; ww < kFW; ++ww) pc += pw[ww * NP + c1];
+        const double vc = v[c1];
+        const double wc = fma(-K, vc, tk * pc);  // w_{k+1}, identical in every thread
         double xi = 0.0;
         if (row >= c1 && row < n) {
             double* col1 = a + floff(c1, n) - c1;
@@ -222,7 +241,7 @@ __global__ void __launch_bounds__(kFT) sytrd_fused_k(const double* __restrict__ 
             col1[row] = xi;
         }
         double s2 = warp_sum(row >= c1 + 2 && row < n ? xi * xi : 0.0);
-        if (lane == 0) red[32 + wid] = s2;  // second half: red[0..] may still be read for K
+        if (lane == 0) red[32 + wid] = s2;  // second half: red[0..] holds the v^T A v shares
         PHASE_MARK(5);
         __syncthreads();
         // ---- [P3] reflector of column k+1 (if any)

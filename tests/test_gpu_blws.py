@@ -318,3 +318,28 @@ def test_graph_replay_bitwise_equals_eager(G, O, monkeypatch):
     for o in outs:
         assert np.array_equal(o.warm.sigma, eager.warm.sigma)
         assert np.array_equal(o.warm.u, eager.warm.u) and np.array_equal(o.warm.v, eager.warm.v)
+
+
+def test_graph_cache_is_bounded_and_exact(G, O, monkeypatch):
+    # a solve whose rank keeps changing: more (b, k, r) keys than the cache
+    # holds (4); captures, evictions and replays must all match the eager path
+    m, n = 400, 300
+    rng = O.Rng(321)
+    u0, _, v0 = O.full_svd_small(rng.gaussian_matrix(m, n))
+    w = (u0[:, :40] * (30.0 * 0.9 ** np.arange(40))) @ v0[:, :40].T + 1e-3 * rng.gaussian_matrix(m, n)
+    monkeypatch.delenv("BLWS_EXACT", raising=False)
+    monkeypatch.delenv("BLWS_GRAPHS", raising=False)
+    op = G.DenseOperator(w)
+    g0 = G.graph_launches()
+    outs = {}
+    for r in (8, 10, 12, 14, 16, 18):
+        u, v, s = exact_warm(O, w + 1e-2 * rng.gaussian_matrix(m, n), r)
+        warm = G.DeviceWarmStart.from_host(u, v, s, op.ctx)
+        outs[r] = ([G.blws_svd(op, warm, 2, r, G.Rng(1)) for _ in range(3)], warm)
+    assert G.graph_launches() == g0 + 6  # each key captured (and replayed) on its third call
+    monkeypatch.setenv("BLWS_GRAPHS", "0")
+    plain = G.DenseOperator(w)
+    for r, (res, warm) in outs.items():
+        ref = G.blws_svd(plain, warm, 2, r, G.Rng(1))
+        for o in res:
+            assert np.array_equal(o.warm.sigma, ref.warm.sigma) and np.array_equal(o.warm.u, ref.warm.u)
