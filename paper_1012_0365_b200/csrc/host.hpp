@@ -104,6 +104,9 @@ private:
     std::vector<std::shared_ptr<SvdGraph>> svd_graphs_;
 };
 
+/// Rows of the whole (possibly row-sharded) operator.
+inline Index global_rows(const LinearOperator& w) { return w.row_sharded() ? w.shard().m_total : w.rows(); }
+
 /// DenseOperator (linear_operator.hpp:102-131): column-major W on the device,
 /// either owned or borrowed (a caller-owned device buffer).
 class DenseOperator final : public LinearOperator {

@@ -286,6 +286,7 @@ void DenseOperator::pair_block_impl(View left, View right, View top, View bot) {
 void DenseOperator::pair_impl(const double* left, const double* right, double* top, double* bot) {
     ensure_ready();
     pair_gemv(ctx_, m_, n_, p_, ld_, right, left, top, bot);  // one read of W for both products
+    if (row_sharded() && ctx_.has_comm()) ctx_.allreduce_sum(bot, static_cast<size_t>(n_));  // W^T left over the ranks
 }
 
 // ======================================================== SparseOperator
@@ -444,6 +445,35 @@ void panel_sumsq(Context& ctx, View x, RowSplit split, double* out) {
         sumsq(ctx, View{x.p + s, x.rows - s, x.cols, x.ld}, t.get());
         axpy(ctx, View{out, 1, 1, 1}, View{t.get(), 1, 1, 1}, 1.0);
     }
+}
+
+// x^T y of two panel vectors -> out (device scalar), sharded rows summed over the ranks
+void panel_dot(Context& ctx, Index rows, const double* x, const double* y, RowSplit split, double* out) {
+    const Index s = split.sharded;
+    if (s == 0 || !ctx.has_comm()) {
+        dot(ctx, rows, x, y, out);
+        return;
+    }
+    dot(ctx, s, x, y, out);
+    ctx.allreduce_sum(out, 1);
+    if (rows > s) {
+        DBuf<double> t(ctx, 1);
+        dot(ctx, rows - s, x + s, y + s, t.get());
+        axpy(ctx, View{out, 1, 1, 1}, View{t.get(), 1, 1, 1}, 1.0);
+    }
+}
+
+// coef (cols) = Q^T r over the panel rows, sharded rows summed over the ranks
+void panel_gemv_t(Context& ctx, Index rows, Index cols, const double* q, Index ldq, const double* r, RowSplit split,
+                  double* coef) {
+    const Index s = split.sharded;
+    if (s == 0 || !ctx.has_comm()) {
+        gemv(ctx, true, rows, cols, 1.0, q, ldq, r, 0.0, coef);
+        return;
+    }
+    gemv(ctx, true, s, cols, 1.0, q, ldq, r, 0.0, coef);
+    ctx.allreduce_sum(coef, static_cast<size_t>(cols));
+    if (rows > s) gemv(ctx, true, rows - s, cols, 1.0, q + s, ldq, r + s, 1.0, coef);
 }
 
 namespace {
@@ -1180,9 +1210,9 @@ namespace {
 class DeviceLanczos {
 public:
     DeviceLanczos(LinearOperator& w, const std::vector<double>& q1_logical, Index cap)
-        : w_(w), ctx_(w.ctx()), geo_{w.rows(), w.cols()}, dim_(geo_.m + geo_.n), ld_(geo_.ld()), cap_(cap) {
-        if (w.row_sharded() && ctx_.has_comm())
-            throw std::invalid_argument("lanczos: row-sharded operators are not supported (blws_svd only)");
+        : w_(w), ctx_(w.ctx()), geo_{w.rows(), w.cols()},
+          m_all_(w.row_sharded() ? w.shard().m_total : geo_.m), row0_(w.row_sharded() ? w.shard().row0 : 0),
+          dim_(m_all_ + geo_.n), ld_(geo_.ld()), cap_(cap), split_(w.panel_split()) {
         q_ = DMat(ctx_, ld_, cap_, true);
         next_ = DMat(ctx_, ld_, 1, true);
         r_ = DMat(ctx_, ld_, 1, true);
@@ -1224,7 +1254,7 @@ public:
             set_logical(r_.data(), v);
             reorth(r_.data());
             reorth(r_.data());
-            sumsq(ctx_, r_.view(), ss_.get());
+            panel_sumsq(ctx_, r_.view(), split_, ss_.get());
             double nv2 = 0;
             ctx_.read(ss_.get(), &nv2, 1);
             const double nv = std::sqrt(nv2);
@@ -1251,10 +1281,11 @@ public:
     const double* coup_dev() const { return coup_.get(); }
 
 private:
+    // a logical (m_all + n) vector into this rank's panel layout (its top rows, all bottom rows)
     void set_logical(double* dst, const std::vector<double>& v) {
         std::vector<double> h(static_cast<size_t>(ld_), 0.0);
-        std::copy(v.begin(), v.begin() + geo_.m, h.begin());
-        std::copy(v.begin() + geo_.m, v.end(), h.begin() + geo_.mp());
+        std::copy(v.begin() + row0_, v.begin() + row0_ + geo_.m, h.begin());
+        std::copy(v.begin() + m_all_, v.end(), h.begin() + geo_.mp());
         BLWS_CUDA(cudaMemcpyAsync(dst, h.data(), sizeof(double) * ld_, cudaMemcpyHostToDevice, ctx_.stream()));
         ctx_.sync();
     }
@@ -1262,7 +1293,7 @@ private:
     // r -= Q (Q^T r) over the current basis
     void reorth(double* r) {
         if (cols_ == 0) return;
-        gemv(ctx_, true, ld_, cols_, 1.0, q_.data(), q_.ld, r, 0.0, coef_.get());
+        panel_gemv_t(ctx_, ld_, cols_, q_.data(), q_.ld, r, split_, coef_.get());
         gemv(ctx_, false, ld_, cols_, -1.0, q_.data(), q_.ld, coef_.get(), 1.0, r);
     }
 
@@ -1271,17 +1302,17 @@ private:
         BLWS_CUDA(cudaMemcpyAsync(ql, next_.data(), sizeof(double) * ld_, cudaMemcpyDeviceToDevice, ctx_.stream()));
         // r = A q_l: (W q_bot ; W^T q_top)
         w_.apply_pair(ql, ql + geo_.mp(), r_.data(), r_.data() + geo_.mp());
-        dot(ctx_, ld_, ql, r_.data(), alpha_.get() + l);
+        panel_dot(ctx_, ld_, ql, r_.data(), split_, alpha_.get() + l);
         lanczos_three_term_k<<<gridn(ld_), kT, 0, ctx_.stream()>>>(r_.data(), q_.data(), q_.ld, l, alpha_.get(),
                                                                    coup_.get(), ld_);
         ctx_.note_launch();
         // full reorthogonalisation, twice (lanczos.hpp:123-126); basis includes column l
         const Index c = l + 1;
         for (int pass = 0; pass < 2; ++pass) {
-            gemv(ctx_, true, ld_, c, 1.0, q_.data(), q_.ld, r_.data(), 0.0, coef_.get());
+            panel_gemv_t(ctx_, ld_, c, q_.data(), q_.ld, r_.data(), split_, coef_.get());
             gemv(ctx_, false, ld_, c, -1.0, q_.data(), q_.ld, coef_.get(), 1.0, r_.data());
         }
-        sumsq(ctx_, r_.view(), ss_.get());
+        panel_sumsq(ctx_, r_.view(), split_, ss_.get());
         lanczos_finalize_k<<<gridn(ld_), kT, 0, ctx_.stream()>>>(r_.data(), next_.data(), ld_, l, dim_, ss_.get(),
                                                                  alpha_.get(), lastbeta_.get(), coup_.get(), cap_,
                                                                  state_.get());
@@ -1301,7 +1332,8 @@ private:
     LinearOperator& w_;
     Context& ctx_;
     Stack geo_;
-    Index dim_, ld_, cap_;
+    Index m_all_, row0_, dim_, ld_, cap_;
+    RowSplit split_;
     DMat q_, next_, r_;
     DBuf<double> alpha_, lastbeta_, coup_, state_, coef_, ss_;
     Index cols_ = 0;
@@ -1347,10 +1379,11 @@ Checkpoint ritz_checkpoint(Context& ctx, DeviceLanczos& run, Index r, double tol
 PartialSvd lanczos_partial_svd(LinearOperator& w, Index r, const LanczosOptions& opts) {
     Context& ctx = w.ctx();
     const Index m = w.rows(), n = w.cols();
-    if (r < 1 || r > std::min(m, n)) throw std::invalid_argument("lanczos_partial_svd: bad r");
-    const Index dim = m + n;
+    const Index m_all = w.row_sharded() ? w.shard().m_total : m;  // a row shard: the global rows
+    if (r < 1 || r > std::min(m_all, n)) throw std::invalid_argument("lanczos_partial_svd: bad r");
+    const Index dim = m_all + n;
     Rng seed_rng = Rng(opts.seed).split(13);
-    std::vector<double> top = seed_rng.unit_vector(m);
+    std::vector<double> top = seed_rng.unit_vector(m_all);
     std::vector<double> q1(static_cast<size_t>(dim), 0.0);
     std::copy(top.begin(), top.end(), q1.begin());
 

@@ -26,7 +26,7 @@ SvdBackend::SvdBackend(Context& ctx, Kind k, Options o) : ctx_(ctx), kind_(k), o
 
 // svt.hpp:104-186
 SvdBackend::Triplets SvdBackend::compute(LinearOperator& w, Index r) {
-    const Index p = std::min(w.rows(), w.cols());
+    const Index p = std::min(global_rows(w), w.cols());
     if (r < 1 || r > p) throw std::invalid_argument("SvdBackend: bad r");
     Triplets t;
     if (kind_ == Kind::Lanczos) {
@@ -51,7 +51,9 @@ SvdBackend::Triplets SvdBackend::compute(LinearOperator& w, Index r) {
         lo.seed = rng_.next_u64();
         auto svd = lanczos_partial_svd(w, r_seed, lo);
         DWarm ws = std::move(svd.uv);
-        if (ws.rank() < r_seed) ws = adapt_subspace(ctx_, ws.rank() > 0 ? &ws : nullptr, r_seed, w.rows(), w.cols(), rng_);
+        if (ws.rank() < r_seed)
+            ws = adapt_subspace(ctx_, ws.rank() > 0 ? &ws : nullptr, r_seed, w.rows(), w.cols(), rng_,
+                                w.row_sharded() ? &w.shard() : nullptr);
         warm_ = std::move(ws);
         t.held = &*warm_;
         t.converged = svd.stats.converged;
@@ -60,7 +62,8 @@ SvdBackend::Triplets SvdBackend::compute(LinearOperator& w, Index r) {
     }
     if (r < held) growth_streak_ = 0;
     if (held > r + 2 * opt_.seed_margin)
-        warm_ = adapt_subspace(ctx_, &*warm_, r + opt_.seed_margin, w.rows(), w.cols(), rng_);
+        warm_ = adapt_subspace(ctx_, &*warm_, r + opt_.seed_margin, w.rows(), w.cols(), rng_,
+                               w.row_sharded() ? &w.shard() : nullptr);
     auto res = blws_svd(w, *warm_, opt_.block_steps, warm_->rank(), rng_);
     warm_ = std::move(res.warm);
     t.held = &*warm_;
@@ -72,7 +75,7 @@ SvdBackend::Triplets SvdBackend::compute(LinearOperator& w, Index r) {
 SvtResult svt(LinearOperator& w, double eps, SvdBackend& backend, RankPredictor& predictor) {
     if (eps < 0.0) throw std::invalid_argument("svt: negative threshold");
     Context& ctx = w.ctx();
-    const Index p = std::min(w.rows(), w.cols());
+    const Index p = std::min(global_rows(w), w.cols());
     Index r = std::clamp<Index>(predictor.r, 1, p);
     SvdBackend::Triplets t;
     bool all_above = false;

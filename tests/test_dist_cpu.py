@@ -185,3 +185,52 @@ def test_sharded_blws_decomposition_matches_oracle():
     assert np.allclose(np.abs(u_all), np.abs(ref.warm.u), atol=1e-8)
     # both ranks computed identical replicated parts
     assert np.array_equal(res[0][3], res[1][3]) and np.array_equal(res[0][4], res[1][4])
+
+
+def _lanczos(apply, dot, reorth_coef, q1t, q1b, steps):
+    qt, qb = [q1t], [q1b]
+    alphas, betas = [], []
+    for l in range(steps):
+        zt, zb = apply(qt[-1], qb[-1])
+        a = dot(qt[-1], qb[-1], zt, zb)
+        alphas.append(a)
+        zt, zb = zt - a * qt[-1], zb - a * qb[-1]
+        if l > 0:
+            zt, zb = zt - betas[-1] * qt[-2], zb - betas[-1] * qb[-2]
+        for _ in range(2):  # full CGS2 (lanczos.hpp:123-126)
+            c = reorth_coef(np.array(qt).T, np.array(qb).T, zt, zb)
+            zt, zb = zt - np.array(qt).T @ c, zb - np.array(qb).T @ c
+        b = np.sqrt(dot(zt, zb, zt, zb))
+        betas.append(b)
+        qt.append(zt / b)
+        qb.append(zb / b)
+    return np.array(alphas), np.array(betas)
+
+
+def _worker_lanczos(rank, world):
+    from paper_1012_0365_b200.dist import row_partition
+
+    _, w, _, _, _ = _case()
+    m, n = w.shape
+    row0, rows = row_partition(m, world, rank)
+    wl = w[row0:row0 + rows]
+    q = np.random.default_rng(0).standard_normal(m + n)
+    q /= np.linalg.norm(q)
+    return _lanczos(lambda xt, xb: (wl @ xb, _allreduce(wl.T @ xt)),
+                    lambda at, ab, bt, bb: float(_allreduce(np.array([at @ bt]))[0] + ab @ bb),
+                    lambda qt, qb, zt, zb: _allreduce(qt.T @ zt) + qb.T @ zb,
+                    q[row0:row0 + rows], q[m:], 12)
+
+
+def test_sharded_lanczos_decomposition_matches_unsharded():
+    res = _run(2, _worker_lanczos)
+    assert not any(isinstance(r, str) for r in res), res
+    _, w, _, _, _ = _case()
+    m, n = w.shape
+    q = np.random.default_rng(0).standard_normal(m + n)
+    q /= np.linalg.norm(q)
+    ref = _lanczos(lambda xt, xb: (w @ xb, w.T @ xt), lambda at, ab, bt, bb: at @ bt + ab @ bb,
+                   lambda qt, qb, zt, zb: qt.T @ zt + qb.T @ zb, q[:m], q[m:], 12)
+    for alphas, betas in res:
+        assert np.abs(alphas - ref[0]).max() <= 1e-12 * np.abs(ref[0]).max()
+        assert np.abs(betas - ref[1]).max() <= 1e-12 * ref[1].max()

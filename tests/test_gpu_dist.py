@@ -58,6 +58,29 @@ def test_sharded_operator_guards(G, O):
     op = G.DenseOperator(w, ctx=ctx)
     with pytest.raises(ValueError):
         op.set_row_shard(100, 0)  # fewer global rows than local
-    op.set_row_shard(200, 0)
-    with pytest.raises(ValueError):  # the cold Lanczos reseed is not sharded (yet)
-        G.lanczos_partial_svd(op, 3)
+
+
+def test_sharded_lanczos_and_svt_single_rank(G, O):
+    # the cold Lanczos reseed (lanczos.hpp:85-329) and svt (svt.hpp:216-254)
+    # on a row-sharded operator: dot / norm / Q^T r reductions and the W^T x
+    # half of the paired GEMV go through the allreduce
+    w, u, v, s = _instance(O, m=600, n=450, r=12, seed=5)
+    ctx = G.Context(0)
+    ctx.init_comm(1, 0, G.api.nccl_unique_id())
+    op = G.DenseOperator(w, ctx=ctx)
+    op.set_row_shard(w.shape[0], 0)
+    plain = G.DenseOperator(w)
+    assert abs(G.spectral_norm(op) - G.spectral_norm(plain)) <= 1e-12 * G.spectral_norm(plain)
+    us, ss, vs, _ = G.lanczos_partial_svd(op, 8, tol=1e-10)
+    up, sp, vp, _ = G.lanczos_partial_svd(plain, 8, tol=1e-10)
+    assert np.abs(ss - sp).max() <= 1e-10 * sp[0]
+    assert principal_angle(us, up) <= 1e-8 and principal_angle(vs, vp) <= 1e-8
+    eps = 0.5 * (O.full_svd_small(w)[1][14] + O.full_svd_small(w)[1][15])
+    b1 = G.SvdBackend.blws(seed=3, ctx=ctx)
+    b2 = G.SvdBackend.blws(seed=3)
+    p1, p2 = G.RankPredictor(10, 5, 450), G.RankPredictor(10, 5, 450)
+    for _ in range(4):  # reseed (rank growth), then BLWS steps
+        r1 = G.svt(op, eps, b1, p1)
+        r2 = G.svt(plain, eps, b2, p2)
+        assert r1.achieved_rank == r2.achieved_rank and p1.history == p2.history
+        assert np.abs(r1.sigma - r2.sigma).max() <= 1e-9 * r2.sigma.max()
