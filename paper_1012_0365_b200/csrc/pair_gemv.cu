@@ -140,11 +140,25 @@ void pair_gemv(Context& ctx, Index m, Index n, const double* w, Index ld, const 
                double* top, double* bot) {
     if (m <= 0 || n <= 0) return;
     const long nblocks = (m + kPgRows - 1) / kPgRows;
-    // column groups: enough CTAs for ~4 per SM, each group a multiple of 32 columns
-    const long target = 4L * ctx.sm_count();
-    long groups = std::max<long>(1, std::min<long>((target + nblocks - 1) / nblocks, (n + 31) / 32));
-    const long cpg = ((n + groups - 1) / groups + 31) / 32 * 32;
-    groups = (n + cpg - 1) / cpg;
+    // column groups (multiples of 32 columns): at least ~4 CTAs per SM, and the
+    // count that wastes least of the last wave (one resident CTA per SM at the
+    // register count of the 16-byte path)
+    const long sms = ctx.sm_count();
+    const long gmax = std::max<long>(1, (n + 31) / 32);
+    long groups = 1, cpg = ((n + 31) / 32) * 32;
+    double best = -1.0;
+    for (long g = std::max<long>(1, (4 * sms + nblocks - 1) / nblocks); g <= std::min<long>(gmax, 128); ++g) {
+        const long c = ((n + g - 1) / g + 31) / 32 * 32;
+        const long gg = (n + c - 1) / c;
+        const long ctas = nblocks * gg;
+        const double eff = static_cast<double>(ctas) / static_cast<double>(((ctas + sms - 1) / sms) * sms);
+        if (eff > best + 1e-9) {
+            best = eff;
+            groups = gg;
+            cpg = c;
+        }
+        if (eff > 0.985) break;
+    }
     DBuf<double> ptop(ctx, static_cast<size_t>(groups * m)), pbot(ctx, static_cast<size_t>(nblocks * n));
     pair_gemv_k<<<dim3(static_cast<unsigned>(nblocks), static_cast<unsigned>(groups)), kPgThreads, 0,
                   ctx.stream()>>>(w, ld, m, n, cpg, x, y, ptop.get(), pbot.get());
