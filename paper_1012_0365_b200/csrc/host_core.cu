@@ -184,6 +184,20 @@ void share_flag(Context& ctx, const int* flag, double* dst) {
     ctx.allreduce_sum(dst, 1);
 }
 
+// region timing for whole calls (regions 3: Lanczos reseed, 4: Ritz checkpoint,
+// 5: blws_svd) -- host-side event records, also around graph launches
+struct RegionGuard {
+    Context& ctx;
+    int id;
+    RegionGuard(Context& c, int i) : ctx(c), id(i) { ctx.region_begin(id); }
+    ~RegionGuard() {
+        try {
+            ctx.region_end(id, 0.0, 0.0);
+        } catch (...) {
+        }
+    }
+};
+
 // ======================================================== row sharding
 void LinearOperator::set_row_shard(Index m_total, Index row0) {
     if (m_total < rows() || row0 < 0 || row0 + rows() > m_total)
@@ -1065,6 +1079,7 @@ std::int64_t g_blws_graph_launches = 0;
 
 BlwsResult blws_svd(LinearOperator& w, const DWarm& warm, Index k, Index r, Rng& rng) {
     Context& ctx = w.ctx();
+    RegionGuard region(ctx, 5);
     const Index m = w.rows(), n = w.cols();
     const Index bs = warm.rank();
     const Index m_all = w.row_sharded() ? w.shard().m_total : m;  // global rows of a row shard
@@ -1349,6 +1364,7 @@ struct Checkpoint {
 
 // ritz_checkpoint (lanczos.hpp:191-207), top min(r, cols) pairs
 Checkpoint ritz_checkpoint(Context& ctx, DeviceLanczos& run, Index r, double tol) {
+    RegionGuard region(ctx, 4);
     Checkpoint cp;
     const Index k = run.cols();
     const Index want = std::min(r, k);
@@ -1378,6 +1394,7 @@ Checkpoint ritz_checkpoint(Context& ctx, DeviceLanczos& run, Index r, double tol
 // lanczos.hpp:209-252 (partial_evd_impl) + :289-329 (lanczos_partial_svd)
 PartialSvd lanczos_partial_svd(LinearOperator& w, Index r, const LanczosOptions& opts) {
     Context& ctx = w.ctx();
+    RegionGuard region(ctx, 3);
     const Index m = w.rows(), n = w.cols();
     const Index m_all = w.row_sharded() ? w.shard().m_total : m;  // a row shard: the global rows
     if (r < 1 || r > std::min(m_all, n)) throw std::invalid_argument("lanczos_partial_svd: bad r");

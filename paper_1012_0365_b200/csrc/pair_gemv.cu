@@ -144,10 +144,11 @@ void pair_gemv(Context& ctx, Index m, Index n, const double* w, Index ld, const 
     // count that wastes least of the last wave (one resident CTA per SM at the
     // register count of the 16-byte path)
     const long sms = ctx.sm_count();
-    const long gmax = std::max<long>(1, (n + 31) / 32);
+    const long gmax = std::max<long>(1, std::min<long>((n + 31) / 32, 128));
+    const long gmin = std::min<long>(gmax, std::max<long>(1, (4 * sms + nblocks - 1) / nblocks));
     long groups = 1, cpg = ((n + 31) / 32) * 32;
     double best = -1.0;
-    for (long g = std::max<long>(1, (4 * sms + nblocks - 1) / nblocks); g <= std::min<long>(gmax, 128); ++g) {
+    for (long g = gmin; g <= gmax; ++g) {  // small problems: gmin == gmax (every 32-column chunk its own group)
         const long c = ((n + g - 1) / g + 31) / 32 * 32;
         const long gg = (n + c - 1) / c;
         const long ctas = nblocks * gg;

@@ -1,0 +1,33 @@
+"""Where an RPCA solve spends its time: region timers (K1, EVD, thin_qr, Lanczos
+reseed, Ritz checkpoints, whole blws_svd calls) over one solve."""
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
+import paper_1012_0365_b200 as B  # noqa: E402
+from paper_1012_0365_b200 import synth  # noqa: E402
+
+
+def main(m=2000, rank=100, frac=0.10):
+    d, a0, _, _ = synth.rpca_lowrank_sparse(m, rank, int(round(frac * m * m)), 1, B.Rng, B.sample_distinct)
+    ctx = B.Context(0)
+    B.rpca_adm(d[:64, :64].copy(order="F"), B.SvdBackend.blws(seed=1 ^ 0x5BDBEEF, ctx=ctx))
+    t = time.perf_counter()
+    B.rpca_adm(d, B.SvdBackend.blws(seed=1 ^ 0x5BDBEEF, ctx=ctx), truth=a0, want_outputs=False)
+    print(f"m={m}: profiling off: {time.perf_counter() - t:.3f} s", flush=True)
+    ctx.set_profiling(True)
+    ctx.region_reset()
+    t = time.perf_counter()
+    _, _, st, _ = B.rpca_adm(d, B.SvdBackend.blws(seed=1 ^ 0x5BDBEEF, ctx=ctx), truth=a0, want_outputs=False)
+    tot = time.perf_counter() - t
+    print(f"m={m}: {tot:.3f} s, {st.iterations} iterations, {st.matvec_count} matvecs", flush=True)
+    names = {0: "K1 paired products", 1: "EVD of T", 2: "thin_qr", 3: "Lanczos reseed (whole)", 4: "Ritz checkpoints",
+             5: "blws_svd (whole)"}
+    for i, nm in names.items():
+        r = ctx.region_stats(i)
+        print(f"  {nm:26s} {r['ms']:9.1f} ms over {r['count']:5d}", flush=True)
+
+
+if __name__ == "__main__":
+    main(*(int(x) if i < 2 else float(x) for i, x in enumerate(sys.argv[1:])))
