@@ -1250,9 +1250,13 @@ public:
 
     /// Launch steps until `target` columns; returns after syncing the state.
     void step_to(Index target) {
-        while (cols_ < target) {
-            launch_step(cols_);
-            ++cols_;
+        if (cols_ < target && coop_steps(target)) {
+            cols_ = target;
+        } else {
+            while (cols_ < target) {
+                launch_step(cols_);
+                ++cols_;
+            }
         }
         sync_state();
     }
@@ -1310,6 +1314,24 @@ private:
         if (cols_ == 0) return;
         panel_gemv_t(ctx_, ld_, cols_, q_.data(), q_.ld, r, split_, coef_.get());
         gemv(ctx_, false, ld_, cols_, -1.0, q_.data(), q_.ld, coef_.get(), 1.0, r);
+    }
+
+    // the whole step range in one cooperative launch (dense, unsharded, m <= 4096)
+    bool coop_steps(Index target) {
+        auto* dense = dynamic_cast<DenseOperator*>(&w_);
+        if (!dense || split_.sharded || ctx_.has_comm() || std::getenv("BLWS_NO_COOP")) return false;
+        const View wv = dense->w();
+        double* ql = q_.data() + cols_ * q_.ld;
+        BLWS_CUDA(cudaMemcpyAsync(ql, next_.data(), sizeof(double) * ld_, cudaMemcpyDeviceToDevice, ctx_.stream()));
+        if (!lanczos_coop_steps(ctx_, wv.p, wv.ld, geo_.m, geo_.n, geo_.mp(), q_.data(), q_.ld, r_.data(),
+                                alpha_.get(),
+                                lastbeta_.get(), coup_.get(), state_.get(), coef_.get(), cap_, dim_, cols_, target))
+            return false;
+        w_.add_applications(target - cols_);  // one paired apply per step (linear_operator.hpp:51-54)
+        if (target < cap_)  // the last direction, for a later step_to / the restart logic
+            BLWS_CUDA(cudaMemcpyAsync(next_.data(), q_.data() + target * q_.ld, sizeof(double) * ld_,
+                                      cudaMemcpyDeviceToDevice, ctx_.stream()));
+        return true;
     }
 
     void launch_step(Index l) {

@@ -17,6 +17,13 @@ void fill(Context& ctx, View x, double v);
 /// full_svd_small (small_dense.hpp:72-87) via the symmetric embedding: sigma (p),
 /// u (m x p), v (n x p), p = min(m, n), descending.
 void full_svd_small(Context& ctx, View w, double* sigma, View u, View v);
+/// Lanczos steps l0..l1-1 on the augmented view of a dense W (m <= 4096) in one
+/// cooperative launch (lanczos_coop.cu); false if not applicable. q holds the
+/// basis (column l0 already set); column l+1 receives each next direction.
+bool lanczos_coop_steps(Context& ctx, const double* w, Index ldw, Index m, Index n, Index mp, double* q, Index ldq,
+                        double* r,
+                        double* alpha, double* lastbeta, double* coup, double* state, double* coef, Index cap,
+                        Index dim, Index l0, Index l1);
 /// top = W x (m), bot = W^T y (n) in one pass over column-major W (K10).
 void pair_gemv(Context& ctx, Index m, Index n, const double* w, Index ld, const double* x, const double* y,
                double* top, double* bot);
