@@ -66,6 +66,7 @@ public:
     /// Fork/join onto a second compute stream (see AuxScope).
     void fork_aux();
     void join_aux();
+    void leave_aux() { cur_ = nullptr; }
     /// Second stream for host->device uploads that overlap queued kernels
     /// (created on first use; ordered against stream() with events).
     cudaStream_t copy_stream();
@@ -108,6 +109,7 @@ private:
     cudaStream_t stream_ = nullptr;
     cudaStream_t copy_stream_ = nullptr;
     cudaStream_t aux_ = nullptr, cur_ = nullptr;
+    bool aux_open_ = false;  // forked, not yet joined
     void* comm_ = nullptr;
     int nranks_ = 1, rank_ = 0;
     void destroy_comm() noexcept;
@@ -131,16 +133,18 @@ private:
     void ensure_pinned(size_t bytes);
 };
 
-/// Owning device buffer of doubles (or raw bytes), freed stream-ordered.
-/// Work enqueued while an AuxScope lives runs on the context's auxiliary stream,
-/// ordered after everything already queued on the main stream; the scope's end
-/// makes the main stream wait for it. Independent branches (the two products of
-/// a paired apply, the QRs of U and V) overlap; under graph capture they become
-/// parallel branches of the graph.
+/// Fork/join: work enqueued after construction runs on the context's auxiliary
+/// stream, ordered after everything already queued on the main stream; main()
+/// switches back to the main stream WITHOUT waiting (the second branch), and the
+/// scope's end makes the main stream wait for the auxiliary branch. Independent
+/// branches (the two products of a paired apply, the QRs of U and V) overlap;
+/// under graph capture they become parallel branches of the graph. Buffers the
+/// auxiliary branch uses must outlive the scope (declare them before it).
 class AuxScope {
 public:
     explicit AuxScope(Context& ctx) : ctx_(ctx) { ctx_.fork_aux(); }
     ~AuxScope() { ctx_.join_aux(); }
+    void main() { ctx_.leave_aux(); }
     AuxScope(const AuxScope&) = delete;
     AuxScope& operator=(const AuxScope&) = delete;
 

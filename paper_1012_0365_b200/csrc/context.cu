@@ -123,7 +123,7 @@ void Context::region_reset() {
 }
 
 void Context::fork_aux() {
-    if (cur_) throw std::logic_error("fork_aux: nested fork");
+    if (aux_open_) throw std::logic_error("fork_aux: nested fork");
     if (!aux_) {
         BLWS_CUDA(cudaStreamCreateWithFlags(&aux_, cudaStreamNonBlocking));
         BLWS_CUDA(cudaEventCreateWithFlags(&fork_ev_, cudaEventDisableTiming));
@@ -132,11 +132,13 @@ void Context::fork_aux() {
     BLWS_CUDA(cudaEventRecord(fork_ev_, stream_));
     BLWS_CUDA(cudaStreamWaitEvent(aux_, fork_ev_, 0));
     cur_ = aux_;
+    aux_open_ = true;
 }
 
 void Context::join_aux() {
-    if (!cur_) return;
+    if (!aux_open_) return;
     cur_ = nullptr;
+    aux_open_ = false;
     // no throw from a destructor path: record the failure for the next check
     if (cudaEventRecord(join_ev_, aux_) != cudaSuccess || cudaStreamWaitEvent(stream_, join_ev_, 0) != cudaSuccess)
         return;

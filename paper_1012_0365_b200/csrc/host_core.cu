@@ -280,18 +280,16 @@ void DenseOperator::pair_block_impl(View left, View right, View top, View bot) {
         // W^T U over the local rows, summed over the ranks (contiguous n x b
         // buffer for the allreduce), while W V runs on the local rows only
         DBuf<double> part(ctx_, static_cast<size_t>(n_ * b));
-        {
-            AuxScope aux(ctx_);
-            gemm(ctx_, true, false, n_, b, m_, 1.0, p_, ld_, left.p, left.ld, 0.0, part.get(), n_);
-            ctx_.allreduce_sum(part.get(), static_cast<size_t>(n_ * b));
-            copy(ctx_, bot, View{part.get(), n_, b, n_});
-        }
+        AuxScope aux(ctx_);
+        gemm(ctx_, true, false, n_, b, m_, 1.0, p_, ld_, left.p, left.ld, 0.0, part.get(), n_);
+        ctx_.allreduce_sum(part.get(), static_cast<size_t>(n_ * b));
+        copy(ctx_, bot, View{part.get(), n_, b, n_});
+        aux.main();
         gemm(ctx_, false, false, m_, b, n_, 1.0, p_, ld_, right.p, right.ld, 0.0, top.p, top.ld);
     } else {
-        {
-            AuxScope aux(ctx_);  // W^T U on the auxiliary stream, overlapping W V
-            gemm(ctx_, true, false, n_, b, m_, 1.0, p_, ld_, left.p, left.ld, 0.0, bot.p, bot.ld);
-        }
+        AuxScope aux(ctx_);  // W^T U on the auxiliary stream, overlapping W V
+        gemm(ctx_, true, false, n_, b, m_, 1.0, p_, ld_, left.p, left.ld, 0.0, bot.p, bot.ld);
+        aux.main();
         gemm(ctx_, false, false, m_, b, n_, 1.0, p_, ld_, right.p, right.ld, 0.0, top.p, top.ld);
     }
     ctx_.region_end(0, 4.0 * static_cast<double>(m_) * n_ * b, 16.0 * static_cast<double>(m_) * n_);
@@ -360,11 +358,10 @@ void SparseOperator::pair_block_impl(View left, View right, View top, View bot) 
     const size_t need = static_cast<size_t>(std::max(m_, n_) * b);
     if (scratch_.size() < need) scratch_ = DBuf<double>(ctx_, need);
     if (scratch2_.size() < need) scratch2_ = DBuf<double>(ctx_, need);
-    {
-        AuxScope aux(ctx_);  // W^T x on the auxiliary stream, overlapping W x
-        csr_spmm(ctx_, n_, colptr_.get(), rowidx_.get(), val_csc_.get(), m_, b, left.p, left.ld, bot.p, bot.ld,
-                 scratch2_.get());
-    }
+    AuxScope aux(ctx_);  // W^T x on the auxiliary stream, overlapping W x
+    csr_spmm(ctx_, n_, colptr_.get(), rowidx_.get(), val_csc_.get(), m_, b, left.p, left.ld, bot.p, bot.ld,
+             scratch2_.get());
+    aux.main();
     csr_spmm(ctx_, m_, rowptr_.get(), colidx_.get(), val_csr_.get(), n_, b, right.p, right.ld, top.p, top.ld,
              scratch_.get());
 }
@@ -996,8 +993,9 @@ DeferredRecs enqueue_deferred(LinearOperator& w, View src, const DeferredShape& 
     {
         AuxScope aux(ctx);  // the two QRs are independent
         rec.qv = thin_qr_deferred(ctx, v, nullptr, sl, RowSplit{});
+        aux.main();
+        rec.qu = thin_qr_deferred(ctx, u, nullptr, sl, usplit);
     }
-    rec.qu = thin_qr_deferred(ctx, u, nullptr, sl, usplit);
     return rec;
 }
 
@@ -1323,10 +1321,19 @@ private:
         const View wv = dense->w();
         double* ql = q_.data() + cols_ * q_.ld;
         BLWS_CUDA(cudaMemcpyAsync(ql, next_.data(), sizeof(double) * ld_, cudaMemcpyDeviceToDevice, ctx_.stream()));
-        if (!lanczos_coop_steps(ctx_, wv.p, wv.ld, geo_.m, geo_.n, geo_.mp(), q_.data(), q_.ld, r_.data(),
-                                alpha_.get(),
-                                lastbeta_.get(), coup_.get(), state_.get(), coef_.get(), cap_, dim_, cols_, target))
-            return false;
+        if (geo_.m > 4096) return false;  // large operators: the HBM-bound paired GEMV path
+        static const bool cols_variant = [] {
+            const char* e = std::getenv("BLWS_COOP");
+            return e && std::string(e) == "cols";
+        }();
+        const bool ok =
+            (!cols_variant && lanczos_rows_steps(ctx_, wv.p, wv.ld, geo_.m, geo_.n, geo_.mp(), q_.data(), q_.ld,
+                                                 r_.data(), alpha_.get(), lastbeta_.get(), coup_.get(), state_.get(),
+                                                 coef_.get(), cap_, dim_, cols_, target)) ||
+            lanczos_coop_steps(ctx_, wv.p, wv.ld, geo_.m, geo_.n, geo_.mp(), q_.data(), q_.ld, r_.data(),
+                               alpha_.get(), lastbeta_.get(), coup_.get(), state_.get(), coef_.get(), cap_, dim_,
+                               cols_, target);
+        if (!ok) return false;
         w_.add_applications(target - cols_);  // one paired apply per step (linear_operator.hpp:51-54)
         if (target < cap_)  // the last direction, for a later step_to / the restart logic
             BLWS_CUDA(cudaMemcpyAsync(next_.data(), q_.data() + target * q_.ld, sizeof(double) * ld_,

@@ -242,10 +242,68 @@ __global__ void __launch_bounds__(gemm_detail::THREADS) alm_fused_k(const double
 }
 
 // K9: a_p = sum_c us[i,c] v[j,c] over CSC positions p (solvers.hpp:181-196, :247);
-// resid_p = obs_p - a_p; per-block partial ||resid||^2.
+// resid_p = obs_p - a_p; per-block partial ||resid||^2. A warp takes 32
+// consecutive positions; lanes run over the rank dimension, so every U / V row
+// read is one coalesced segment; a transpose-reduction leaves the full dot of
+// position t on lane t (fixed order).
+template <int SLOTS>
 __global__ void mc_sampled_k(long nnz, const std::int32_t* __restrict__ rowidx, const std::int32_t* __restrict__ colof,
                              const double* __restrict__ ust, const double* __restrict__ vt, long r,
                              const double* __restrict__ obs, double* resid, double* partial) {
+    const int lane = threadIdx.x & 31;
+    const long gw = (blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x) >> 5;
+    const long nw = (static_cast<long>(gridDim.x) * blockDim.x) >> 5;
+    double ss = 0.0;
+    for (long p0 = gw * 32; p0 < nnz; p0 += nw * 32) {  // warp-uniform
+        const long p = p0 + lane;
+        const long myi = p < nnz ? rowidx[p] : 0, myj = p < nnz ? colof[p] : 0;
+        double pd[32];
+#pragma unroll
+        for (int t = 0; t < 32; ++t) {
+            const long i = __shfl_sync(0xffffffffu, myi, t), j = __shfl_sync(0xffffffffu, myj, t);
+            const double* a = ust + i * r;
+            const double* bb = vt + j * r;
+            double d = 0.0;
+#pragma unroll
+            for (int q = 0; q < SLOTS; ++q) {
+                const long c = lane + 32 * q;
+                if (c < r) d = fma(a[c], bb[c], d);
+            }
+            pd[t] = d;
+        }
+#pragma unroll
+        for (int stage = 0; stage < 5; ++stage) {
+            const int half = 16 >> stage, o = 16 >> stage;
+            const bool hi = (lane & o) != 0;
+#pragma unroll
+            for (int t = 0; t < half; ++t) {
+                const double send = hi ? pd[t] : pd[t + half];
+                const double keep = hi ? pd[t + half] : pd[t];
+                pd[t] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+            }
+        }
+        if (p < nnz) {  // lane t holds the dot of position p0 + t
+            const double res = obs[p] - pd[0];
+            resid[p] = res;
+            ss = fma(res, res, ss);
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    __shared__ double sh[32];
+    if (lane == 0) sh[threadIdx.x >> 5] = ss;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) s += sh[w];
+        partial[blockIdx.x] = s;
+    }
+}
+
+// r > 128: thread per position (the old scheme)
+__global__ void mc_sampled_wide_k(long nnz, const std::int32_t* __restrict__ rowidx,
+                                  const std::int32_t* __restrict__ colof, const double* __restrict__ ust,
+                                  const double* __restrict__ vt, long r, const double* __restrict__ obs,
+                                  double* resid, double* partial) {
     double ss = 0.0;
     for (long p = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; p < nnz;
          p += static_cast<long>(gridDim.x) * blockDim.x) {
@@ -489,8 +547,18 @@ McSolution mc_svt(Context& ctx, Index m, Index n, Index nnz, const std::int64_t*
                                                                       vt.get());
             ctx.note_launch(2);
         }
-        mc_sampled_k<<<blocks, kT, 0, ctx.stream()>>>(nnz, op.rowidx_csc(), op.colof_csc(), ust.get(), vt.get(), r,
-                                                      obs.get(), resid.get(), part.get());
+        if (r <= 32)
+            mc_sampled_k<1><<<blocks, kT, 0, ctx.stream()>>>(nnz, op.rowidx_csc(), op.colof_csc(), ust.get(), vt.get(),
+                                                             r, obs.get(), resid.get(), part.get());
+        else if (r <= 64)
+            mc_sampled_k<2><<<blocks, kT, 0, ctx.stream()>>>(nnz, op.rowidx_csc(), op.colof_csc(), ust.get(), vt.get(),
+                                                             r, obs.get(), resid.get(), part.get());
+        else if (r <= 128)
+            mc_sampled_k<4><<<blocks, kT, 0, ctx.stream()>>>(nnz, op.rowidx_csc(), op.colof_csc(), ust.get(), vt.get(),
+                                                             r, obs.get(), resid.get(), part.get());
+        else
+            mc_sampled_wide_k<<<blocks, kT, 0, ctx.stream()>>>(nnz, op.rowidx_csc(), op.colof_csc(), ust.get(),
+                                                               vt.get(), r, obs.get(), resid.get(), part.get());
         ctx.note_launch();
         ctx.check_launch("mc_sampled_k");
         sol.uv = std::move(prox.trip);

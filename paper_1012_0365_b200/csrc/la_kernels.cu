@@ -313,7 +313,11 @@ __global__ void to_row_major_k(const double* X, long ld, long rows, long b, doub
     }
 }
 
-// warp per row; lanes over the b output columns (chunks of 128)
+// K8: warp per row, lanes over the b output columns (SLOTS x 32 >= b). The
+// row's nonzeros are taken 32 at a time: (column, value) pairs loaded coalesced,
+// shuffled out one by one; the X-row gathers of a batch are independent, so
+// several are in flight (two interleaved accumulators per slot, fixed order).
+template <int SLOTS>
 __global__ void csr_spmm_k(long rows, const std::int64_t* __restrict__ rowptr, const std::int32_t* __restrict__ colidx,
                            const double* __restrict__ val, long b, const double* __restrict__ xt, double* Y,
                            long ldy) {
@@ -321,22 +325,78 @@ __global__ void csr_spmm_k(long rows, const std::int64_t* __restrict__ rowptr, c
     const int lane = threadIdx.x & 31;
     for (long i = (blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x) >> 5; i < rows; i += warps) {
         const long p0 = rowptr[i], p1 = rowptr[i + 1];
-        for (long c0 = 0; c0 < b; c0 += 128) {
-            double acc[4] = {0.0, 0.0, 0.0, 0.0};
-            for (long p = p0; p < p1; ++p) {
-                const double v = val[p];
-                const double* xr = xt + static_cast<long>(colidx[p]) * b;
+        double acc[SLOTS][2];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const long c = c0 + lane + 32 * q;
-                    if (c < b) acc[q] += v * xr[c];
+        for (int q = 0; q < SLOTS; ++q) acc[q][0] = acc[q][1] = 0.0;
+        for (long pb = p0; pb < p1; pb += 32) {
+            const long p = pb + lane;
+            const int cj = p < p1 ? colidx[p] : 0;
+            const double vj = p < p1 ? val[p] : 0.0;  // padding entries contribute 0
+#pragma unroll 8
+            for (int t = 0; t < 32; ++t) {
+                const long col = __shfl_sync(0xffffffffu, cj, t);
+                const double v = __shfl_sync(0xffffffffu, vj, t);
+                const double* xr = xt + col * b;
+#pragma unroll
+                for (int q = 0; q < SLOTS; ++q) {
+                    const long c = lane + 32 * q;
+                    if (c < b) acc[q][t & 1] = fma(v, xr[c], acc[q][t & 1]);
                 }
             }
+        }
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const long c = c0 + lane + 32 * q;
-                if (c < b) Y[i + c * ldy] = acc[q];
+        for (int q = 0; q < SLOTS; ++q) {
+            const long c = lane + 32 * q;
+            if (c < b) Y[i + c * ldy] = acc[q][0] + acc[q][1];
+        }
+    }
+}
+
+// narrow blocks (b <= NB <= 8, e.g. the Lanczos vector products): lanes over
+// the row's nonzeros, NB per-lane accumulators, xor-tree warp reductions
+template <int NB>
+__global__ void csr_spmm_narrow_k(long rows, const std::int64_t* __restrict__ rowptr,
+                                  const std::int32_t* __restrict__ colidx, const double* __restrict__ val, long b,
+                                  const double* __restrict__ xt, double* Y, long ldy) {
+    const long warps = (static_cast<long>(gridDim.x) * blockDim.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    for (long i = (blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x) >> 5; i < rows; i += warps) {
+        const long p1 = rowptr[i + 1];
+        double acc[NB];
+#pragma unroll
+        for (int c = 0; c < NB; ++c) acc[c] = 0.0;
+        for (long p = rowptr[i] + lane; p < p1; p += 32) {
+            const double v = val[p];
+            const double* xr = xt + static_cast<long>(colidx[p]) * b;
+#pragma unroll
+            for (int c = 0; c < NB; ++c)
+                if (c < b) acc[c] = fma(v, xr[c], acc[c]);
+        }
+#pragma unroll
+        for (int c = 0; c < NB; ++c) {
+            for (int o = 16; o > 0; o >>= 1) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
+            if (lane == c && c < b) Y[i + c * ldy] = acc[c];
+        }
+    }
+}
+
+// the generic path for wide blocks (b > 128): lanes over chunks of the columns
+__global__ void csr_spmm_wide_k(long rows, const std::int64_t* __restrict__ rowptr,
+                                const std::int32_t* __restrict__ colidx, const double* __restrict__ val, long b,
+                                const double* __restrict__ xt, double* Y, long ldy) {
+    const long warps = (static_cast<long>(gridDim.x) * blockDim.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    for (long i = (blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x) >> 5; i < rows; i += warps) {
+        const long p0 = rowptr[i], p1 = rowptr[i + 1];
+        for (long c = lane; c < b; c += 32) {
+            double a0 = 0.0, a1 = 0.0;
+            long p = p0;
+            for (; p + 1 < p1; p += 2) {
+                a0 = fma(val[p], xt[static_cast<long>(colidx[p]) * b + c], a0);
+                a1 = fma(val[p + 1], xt[static_cast<long>(colidx[p + 1]) * b + c], a1);
             }
+            if (p < p1) a0 = fma(val[p], xt[static_cast<long>(colidx[p]) * b + c], a0);
+            Y[i + c * ldy] = a0 + a1;
         }
     }
 }
@@ -516,7 +576,20 @@ void csr_spmm(Context& ctx, Index rows, const std::int64_t* rowptr, const std::i
     LAUNCH(ctx, "to_row_major");
     const long warps_needed = rows;
     const unsigned blocks = static_cast<unsigned>(std::min<long>(8L * 1024, (warps_needed * 32 + kThreads - 1) / kThreads));
-    csr_spmm_k<<<blocks, kThreads, 0, ctx.stream()>>>(rows, rowptr, colidx, val, b, xt, Y, ldy);
+    if (b == 1)
+        csr_spmm_narrow_k<1><<<blocks, kThreads, 0, ctx.stream()>>>(rows, rowptr, colidx, val, b, xt, Y, ldy);
+    else if (b <= 4)
+        csr_spmm_narrow_k<4><<<blocks, kThreads, 0, ctx.stream()>>>(rows, rowptr, colidx, val, b, xt, Y, ldy);
+    else if (b <= 8)
+        csr_spmm_narrow_k<8><<<blocks, kThreads, 0, ctx.stream()>>>(rows, rowptr, colidx, val, b, xt, Y, ldy);
+    else if (b <= 32)
+        csr_spmm_k<1><<<blocks, kThreads, 0, ctx.stream()>>>(rows, rowptr, colidx, val, b, xt, Y, ldy);
+    else if (b <= 64)
+        csr_spmm_k<2><<<blocks, kThreads, 0, ctx.stream()>>>(rows, rowptr, colidx, val, b, xt, Y, ldy);
+    else if (b <= 128)
+        csr_spmm_k<4><<<blocks, kThreads, 0, ctx.stream()>>>(rows, rowptr, colidx, val, b, xt, Y, ldy);
+    else
+        csr_spmm_wide_k<<<blocks, kThreads, 0, ctx.stream()>>>(rows, rowptr, colidx, val, b, xt, Y, ldy);
     LAUNCH(ctx, "csr_spmm");
 }
 

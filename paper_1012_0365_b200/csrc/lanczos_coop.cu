@@ -46,7 +46,27 @@ struct CoopArgs {
     double* ptop;            // gridDim.x x m
     double* pscal;           // gridDim.x
     long cap, dim, l0, l1;
+#ifdef COOP_PROBE
+    unsigned long long* probe;  // per-phase ns, block 0's view (tools/probes/coop_probe.cu)
+#endif
 };
+
+#ifdef COOP_PROBE
+unsigned long long* g_coop_probe = nullptr;
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define COOP_MARK(k)                                        \
+    if (blockIdx.x == 0 && threadIdx.x == 0) {              \
+        const unsigned long long now_ = gtimer();           \
+        a.probe[k] += now_ - probe_last;                    \
+        probe_last = now_;                                  \
+    }
+#else
+#define COOP_MARK(k)
+#endif
 
 __device__ __forceinline__ double warp_sum(double x) {
     for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
@@ -103,6 +123,9 @@ __global__ void __launch_bounds__(kCoopThreads) lanczos_coop_k(CoopArgs a) {
     int lanes_per_row = 4;  // r -= Q c: lanes per row, a power of two the grid can feed
     while (lanes_per_row < 32 && (gthreads / (2 * lanes_per_row)) >= a.ld) lanes_per_row <<= 1;
     const long j0 = b * cpb, j1 = min(a.n, j0 + cpb);
+#ifdef COOP_PROBE
+    unsigned long long probe_last = gtimer();
+#endif
     for (long l = a.l0; l < a.l1; ++l) {
         const double* ql = a.q + l * a.ldq;
         const double* qtop = ql;
@@ -162,6 +185,7 @@ __global__ void __launch_bounds__(kCoopThreads) lanczos_coop_k(CoopArgs a) {
             }
         }
         grid.sync();
+        COOP_MARK(0)
         // ---- [2] r_top = sum of the block partials (four lanes per row, eight
         //      independent accumulators each, fixed-order quad combine); alpha partials
         double pa = 0.0;
@@ -198,6 +222,7 @@ __global__ void __launch_bounds__(kCoopThreads) lanczos_coop_k(CoopArgs a) {
         pa = block_sum(pa, red);
         if (threadIdx.x == 0) a.pscal[b] = pa;
         grid.sync();
+        COOP_MARK(1)
         // ---- [3] alpha; three-term recurrence
         const double alpha = grid_partials_sum(a.pscal, G, &s_scalar);
         const double beta_prev = l > 0 ? a.coup[l] : 0.0;
@@ -209,6 +234,7 @@ __global__ void __launch_bounds__(kCoopThreads) lanczos_coop_k(CoopArgs a) {
             a.r[i] = v;
         }
         grid.sync();
+        COOP_MARK(2)
         // ---- [4]-[7] full CGS2 against columns 0..l
         const long c = l + 1;
         double pb = 0.0;
@@ -240,6 +266,7 @@ __global__ void __launch_bounds__(kCoopThreads) lanczos_coop_k(CoopArgs a) {
                 }
             }
             grid.sync();
+            COOP_MARK(3 + 2 * pass)
             // r -= Q c: lpr lanes per row (as many as the grid affords, 4..32), each
             // every lpr-th basis column with four independent accumulators; the lane
             // group combines by shuffles in a fixed order
@@ -268,12 +295,16 @@ __global__ void __launch_bounds__(kCoopThreads) lanczos_coop_k(CoopArgs a) {
                     if (pass == 1) pb = fma(v, v, pb);
                 }
             }
-            if (pass == 0) grid.sync();
+            if (pass == 0) {
+                grid.sync();
+                COOP_MARK(4)
+            }
         }
         pb = block_sum(pb, red);
         const double state0 = a.state[0];  // read before this step's latch update
         if (threadIdx.x == 0) a.pscal[b] = pb;
         grid.sync();
+        COOP_MARK(6)
         // ---- [8] beta, breakdown latch, next direction into the basis
         const double rsq = grid_partials_sum(a.pscal, G, &s_scalar);
         const double beta = sqrt(rsq);
@@ -293,6 +324,7 @@ __global__ void __launch_bounds__(kCoopThreads) lanczos_coop_k(CoopArgs a) {
             for (long i = gtid; i < a.ld; i += gthreads) qn[i] = broken ? 0.0 : a.r[i] * inv;
         }
         grid.sync();
+        COOP_MARK(7)
     }
 }
 
@@ -311,6 +343,9 @@ bool launch_coop(Context& ctx, CoopArgs& args) {
     DBuf<double> ptop(ctx, static_cast<size_t>(G * args.m)), pscal(ctx, static_cast<size_t>(G));
     args.ptop = ptop.get();
     args.pscal = pscal.get();
+#ifdef COOP_PROBE
+    args.probe = g_coop_probe;
+#endif
     void* kargs[] = {&args};
     BLWS_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(lanczos_coop_k<R>), dim3(static_cast<unsigned>(G)),
                                           dim3(kCoopThreads), kargs, 0, ctx.stream()));

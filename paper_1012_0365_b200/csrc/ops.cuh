@@ -24,6 +24,11 @@ bool lanczos_coop_steps(Context& ctx, const double* w, Index ldw, Index m, Index
                         double* r,
                         double* alpha, double* lastbeta, double* coup, double* state, double* coef, Index cap,
                         Index dim, Index l0, Index l1);
+// row-owned variant with the basis resident in shared memory (lanczos_rows.cu)
+bool lanczos_rows_steps(Context& ctx, const double* w, Index ldw, Index m, Index n, Index mp, double* q, Index ldq,
+                        double* r,
+                        double* alpha, double* lastbeta, double* coup, double* state, double* coef, Index cap,
+                        Index dim, Index l0, Index l1);
 /// top = W x (m), bot = W^T y (n) in one pass over column-major W (K10).
 void pair_gemv(Context& ctx, Index m, Index n, const double* w, Index ld, const double* x, const double* y,
                double* top, double* bot);

@@ -154,3 +154,28 @@ def test_pair_gemv_matches_numpy(gpu, m, n):
     t1, b1 = op.apply_pair_vec(y, x)
     assert np.abs(t1 - w @ x).max() <= 1e-12 * np.sqrt(n) * np.abs(w @ x).max()
     assert np.abs(b1 - w.T @ y).max() <= 1e-12 * np.sqrt(m) * np.abs(w.T @ y).max()
+
+
+@pytest.mark.parametrize("b", [1, 3, 4, 7, 8, 9, 32, 33, 64, 100, 128, 130])
+def test_sparse_pair_block_matches_numpy(gpu, b):
+    # K8 (csr_spmm_k, one template per 32-column slot count + the wide path):
+    # ragged columns and rows, including empty ones and one dense row
+    rs = np.random.default_rng(b)
+    m, n = 700, 450
+    dense = np.where(rs.random((m, n)) < 0.05, rs.standard_normal((m, n)), 0.0)
+    dense[13, :] = 0.0
+    dense[:, 17] = 0.0
+    dense[200, :] = rs.standard_normal(n)
+    colptr = np.zeros(n + 1, dtype=np.int64)
+    rows, vals = [], []
+    for j in range(n):
+        nz = np.nonzero(dense[:, j])[0]
+        rows.append(nz)
+        vals.append(dense[nz, j])
+        colptr[j + 1] = colptr[j] + len(nz)
+    op = gpu.api.SparseOperator(m, n, colptr, np.concatenate(rows).astype(np.int32), np.concatenate(vals))
+    left, right = rs.standard_normal((m, b)), rs.standard_normal((n, b))
+    top, bot = op.apply_pair_block(left, right)
+    ref_top, ref_bot = dense @ right, dense.T @ left
+    assert np.abs(top - ref_top).max() <= 1e-12 * np.abs(ref_top).max()
+    assert np.abs(bot - ref_bot).max() <= 1e-12 * np.abs(ref_bot).max()

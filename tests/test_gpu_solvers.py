@@ -69,6 +69,18 @@ def test_mc_parity(G, O):
     assert np.linalg.norm(ag - ao) <= 1e-6 * np.linalg.norm(ao)
 
 
+def test_mc_parity_wide_rank(G, O):
+    # rank 40: the sampled-residual kernel (K9) runs its two-slot (r <= 64) variant
+    colptr, rowidx, vals, ml, mr = synth.mc_lowrank(400, 40, 91200, 21, O.Rng, O.sample_distinct)
+    ug, sg, vg, stg = G.mc_svt(400, 400, colptr, rowidx, vals, G.SvdBackend.blws(seed=9), truth_ml=ml, truth_mr=mr)
+    uo, so, vo, sto = O.mc_svt(400, 400, colptr, rowidx, vals, O.SvdBackend.blws(seed=9), truth_ml=ml, truth_mr=mr)
+    assert stg.converged and sto.converged
+    assert abs(stg.iterations - sto.iterations) <= 1
+    assert stg.rank_hat == sto.rank_hat == 40
+    ag, ao = (ug * sg) @ vg.T, (uo * so) @ vo.T
+    assert np.linalg.norm(ag - ao) <= 1e-6 * np.linalg.norm(ao)
+
+
 def test_mc_rejects_empty(G):
     with pytest.raises(ValueError):
         G.mc_svt(10, 10, np.zeros(11, dtype=np.int64), np.zeros(0, dtype=np.int32), np.zeros(0),
