@@ -297,17 +297,22 @@ def run_gpu(args):
     del wd_tmp
     ctx.synchronize()
     e2e_steps = max(1, args.steps)
+
+    def e2e_run(nsteps):
+        ops[0].assign_async(Wh.data_ptr(), rows)  # the first step's upload is not overlapped
+        for i in range(nsteps):
+            w_in = B.DeviceWarmStart.from_host(Uh, Vh, sh, ctx)
+            # same-direction copies share the DMA queue: queue the next W behind this warm start
+            if i + 1 < nsteps:
+                ops[(i + 1) % 2].assign_async(Wh.data_ptr(), rows)  # next step's W, overlapped
+            r_e2e = B.blws_svd(ops[i % 2], w_in, 2, R, B.Rng(SEED ^ 0x5BDBEEF), keep_device=True)
+            out = r_e2e.warm.to_host(rows, N, out=out_h)
+            _ = int(np.sum(out.sigma > eps))
+        ctx.synchronize()
+
+    e2e_run(max(args.warmup, 6))  # untimed: both operators past their graph capture (3rd call each)
     t0 = time.perf_counter()
-    ops[0].assign_async(Wh.data_ptr(), rows)
-    for i in range(e2e_steps):
-        w_in = B.DeviceWarmStart.from_host(Uh, Vh, sh, ctx)
-        # same-direction copies share the DMA queue: queue the next W behind this warm start
-        if i + 1 < e2e_steps:
-            ops[(i + 1) % 2].assign_async(Wh.data_ptr(), rows)  # next step's W, overlapped
-        r_e2e = B.blws_svd(ops[i % 2], w_in, 2, R, B.Rng(SEED ^ 0x5BDBEEF), keep_device=True)
-        out = r_e2e.warm.to_host(rows, N, out=out_h)
-        _ = int(np.sum(out.sigma > eps))
-    ctx.synchronize()
+    e2e_run(e2e_steps)
     e2e_s = time.perf_counter() - t0
     # bytes per step over the whole job (a row shard moves its rows of W and U)
     reps = 1 if sharded else world
