@@ -266,6 +266,26 @@ int blws_mc_svt(blws_context* ctx, int64_t m, int64_t n, int64_t nnz, const int6
                 int64_t cap, int64_t* rank, blws_solver_stats* stats, int64_t* predicted_ranks,
                 int64_t* matvec_history, double* residual_history, int64_t hist_cap);
 
+/* Row-sharded solvers (one process per GPU, the context's NCCL
+ * communicator from blws_context_init_comm; a context without one runs the same
+ * code path on one rank). This rank holds rows [row0, row0 + rows) of the
+ * m x m RPCA problem (d / truth / a_out / e_out are rows x m panels, ldd >=
+ * rows) or of the m x n MC observation (local CSC over n columns, row indices
+ * in [0, rows), nnz local; truth_ml its rows x r_true rows of ML; u comes back
+ * as this rank's rows x cap). Stats and histories are identical on every rank.
+ * Replaces solvers.hpp:72-74 / :202-204 for a row-distributed problem. */
+int blws_rpca_adm_sharded(blws_context* ctx, int64_t m, int64_t rows, int64_t row0, const double* d, int64_t ldd,
+                          int where, double lambda, blws_svd_backend* backend, const blws_rpca_options* opts,
+                          const double* truth, double* a_out, double* e_out, blws_solver_stats* stats,
+                          int64_t* predicted_ranks, int64_t* matvec_history, double* residual_history,
+                          int64_t hist_cap);
+int blws_mc_svt_sharded(blws_context* ctx, int64_t m, int64_t rows, int64_t row0, int64_t n, int64_t nnz,
+                        const int64_t* colptr, const int32_t* rowidx, const double* values, double tau, double delta,
+                        blws_svd_backend* backend, const blws_mc_options* opts, const double* truth_ml,
+                        const double* truth_mr, int64_t r_true, double* u, double* sigma, double* v, int64_t cap,
+                        int64_t* rank, blws_solver_stats* stats, int64_t* predicted_ranks, int64_t* matvec_history,
+                        double* residual_history, int64_t hist_cap);
+
 /* ---- Matrix Market I/O (core/matrix_market.hpp:63-168): host files; the
    reference's std::runtime_error becomes BLWS_IO_ERROR. Dense = "array"
    column-major (lda), sparse = "coordinate" read into / written from CSC. */

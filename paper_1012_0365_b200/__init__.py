@@ -23,7 +23,9 @@ from .api import (  # noqa: F401
     block_lanczos_procedure,
     lanczos_partial_svd,
     mc_svt,
+    mc_svt_sharded,
     rpca_adm,
+    rpca_adm_sharded,
     sample_distinct,
     spectral_norm,
     svt,

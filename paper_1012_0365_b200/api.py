@@ -112,6 +112,10 @@ SIGNATURES = {
                            i64]),
     "blws_mc_svt": (ci, [vp, i64, i64, i64, vp, vp, vp, dbl, dbl, vp, P(McOptionsC), vp, vp, i64, vp, vp, vp, i64,
                          P(i64), P(SolverStatsC), vp, vp, vp, i64]),
+    "blws_rpca_adm_sharded": (ci, [vp, i64, i64, i64, vp, i64, ci, dbl, vp, P(RpcaOptionsC), vp, vp, vp,
+                                   P(SolverStatsC), vp, vp, vp, i64]),
+    "blws_mc_svt_sharded": (ci, [vp, i64, i64, i64, i64, i64, vp, vp, vp, dbl, dbl, vp, P(McOptionsC), vp, vp, i64,
+                                 vp, vp, vp, i64, P(i64), P(SolverStatsC), vp, vp, vp, i64]),
 }
 
 _lib = None
@@ -768,5 +772,62 @@ def mc_svt(m, n, colptr, rowidx, vals, backend: SvdBackend, tau=0.0, delta=0.0, 
     _check(lib().blws_mc_svt(ctx._h, m, n, len(vals), _ptr(colptr), _ptr(rowidx), _ptr(vals), tau, delta, backend._h,
                              C.byref(opts), _ptr(ml), _ptr(mr), r_true, _ptr(u), _ptr(s), _ptr(v), cap, C.byref(rank),
                              C.byref(st), _ptr(ph), _ptr(mh), _ptr(rh), max_iter + 1))
+    k = rank.value
+    return u[:, :k].copy(order="F"), s[:k].copy(), v[:, :k].copy(order="F"), _stats(st, ph, mh, rh)
+
+
+def rpca_adm_sharded(d_rows, m, row0, backend: SvdBackend, lam=0.0, tol_outer=1e-7, max_iter=1000, rho=1.5,
+                     mu_max_factor=1e7, initial_rank=10, rank_increment=5, truth_rows=None, want_outputs=True):
+    """Row-sharded rpca_adm: this rank holds rows [row0, row0 + rows)
+    of the m x m D (host numpy, rows x m); the backend's context carries the
+    communicator (Context.init_comm; without one it runs as a single rank).
+    Returns this rank's rows of A and E and the (rank-identical) stats."""
+    ctx = backend.ctx
+    d = F(d_rows)
+    rows = d.shape[0]
+    if d.shape[1] != m:
+        raise ValueError("rpca_adm_sharded: D rows must have m columns")
+    opts = RpcaOptionsC(tol_outer, max_iter, rho, mu_max_factor, initial_rank, rank_increment)
+    st = SolverStatsC()
+    ph = np.zeros(max_iter + 1, dtype=np.int64)
+    mh = np.zeros(max_iter + 1, dtype=np.int64)
+    rh = np.zeros(max_iter + 1)
+    a = np.empty((rows, m), order="F") if want_outputs else None
+    e = np.empty((rows, m), order="F") if want_outputs else None
+    tr = F(truth_rows) if truth_rows is not None else None
+    _check(lib().blws_rpca_adm_sharded(ctx._h, m, rows, row0, _ptr(d), rows, HOST, lam, backend._h, C.byref(opts),
+                                       _ptr(tr), _ptr(a), _ptr(e), C.byref(st), _ptr(ph), _ptr(mh), _ptr(rh),
+                                       max_iter + 1))
+    return a, e, _stats(st, ph, mh, rh), int(st.e_nnz)
+
+
+def mc_svt_sharded(m, row0, rows, n, colptr, rowidx, vals, backend: SvdBackend, tau=0.0, delta=0.0, tol_outer=1e-4,
+                   max_iter=500, initial_rank=10, rank_increment=5, truth_ml_rows=None, truth_mr=None, cap=None):
+    """Row-sharded mc_svt: this rank's observed rows [row0, row0 + rows) as a
+    local CSC over the n columns (row indices local). Returns this rank's rows
+    of U, sigma, V and the stats (dist.shard_csc builds the local CSC)."""
+    ctx = backend.ctx
+    colptr = np.ascontiguousarray(colptr, dtype=np.int64)
+    rowidx = np.ascontiguousarray(rowidx, dtype=np.int32)
+    vals = np.ascontiguousarray(vals, dtype=np.float64)
+    cap = cap or min(m, n)
+    u = np.empty((rows, cap), order="F")
+    s = np.empty(cap)
+    v = np.empty((n, cap), order="F")
+    rank = i64(0)
+    opts = McOptionsC(tol_outer, max_iter, initial_rank, rank_increment)
+    st = SolverStatsC()
+    ph = np.zeros(max_iter + 1, dtype=np.int64)
+    mh = np.zeros(max_iter + 1, dtype=np.int64)
+    rh = np.zeros(max_iter + 1)
+    r_true = 0
+    ml = mr = None
+    if truth_ml_rows is not None:
+        ml, mr = F(truth_ml_rows), F(truth_mr)
+        r_true = ml.shape[1]
+    _check(lib().blws_mc_svt_sharded(ctx._h, m, rows, row0, n, len(vals), _ptr(colptr), _ptr(rowidx), _ptr(vals),
+                                     tau, delta, backend._h, C.byref(opts), _ptr(ml), _ptr(mr), r_true, _ptr(u),
+                                     _ptr(s), _ptr(v), cap, C.byref(rank), C.byref(st), _ptr(ph), _ptr(mh), _ptr(rh),
+                                     max_iter + 1))
     k = rank.value
     return u[:, :k].copy(order="F"), s[:k].copy(), v[:, :k].copy(order="F"), _stats(st, ph, mh, rh)

@@ -565,43 +565,101 @@ int blws_svt(blws_operator* w, double eps, blws_svd_backend* backend, blws_rank_
 }
 
 // ---------------------------------------------------------------- solvers
+}  // extern "C"
+
+namespace {
+// rpca_adm through the C ABI: the unsharded call has rows = m, shard = null
+void rpca_entry(blws_context* ctx, int64_t m, int64_t rows, const RowShard* shard, const double* d, int64_t ldd,
+                int where, double lambda, blws_svd_backend* backend, const blws_rpca_options* opts,
+                const double* truth, double* a_out, double* e_out, blws_solver_stats* stats,
+                int64_t* predicted_ranks, int64_t* matvec_history, double* residual_history, int64_t hist_cap) {
+    need(m > 0 && rows > 0 && rows <= m && d && ldd >= rows, "rpca_adm: bad D");
+    need(backend != nullptr, "rpca_adm: null backend");
+    Context& c = *ctx->ctx;
+    RpcaOptions o;
+    if (opts) {
+        o.tol_outer = opts->tol_outer;
+        o.max_iter = opts->max_iter;
+        o.rho = opts->rho;
+        o.mu_max_factor = opts->mu_max_factor;
+        o.initial_rank = opts->initial_rank;
+        o.rank_increment = opts->rank_increment;
+    }
+    const Index ld = std::max<Index>(2, round_up(rows, 2));
+    if (where == BLWS_DEVICE && ldd % 2 == 0) {
+        auto s = blws::rpca_adm(c, m, d, ldd, lambda, *backend->b, o, truth, a_out, e_out, shard, rows);
+        put_stats(s, stats, predicted_ranks, matvec_history, residual_history, hist_cap);
+        return;
+    }
+    DMat dd(c, rows, m, false);
+    copy_in(c, dd.view(), d, ldd, where);
+    DMat tr, a, e;
+    if (truth) {
+        tr = DMat(c, rows, m, false);
+        copy_in(c, tr.view(), truth, ldd, where);
+    }
+    if (a_out) a = DMat(c, rows, m, false);
+    if (e_out) e = DMat(c, rows, m, false);
+    auto s = blws::rpca_adm(c, m, dd.data(), ld, lambda, *backend->b, o, truth ? tr.data() : nullptr,
+                            a_out ? a.data() : nullptr, e_out ? e.data() : nullptr, shard, rows);
+    if (a_out) copy_out(c, a.view(), a_out, ldd, where);
+    if (e_out) copy_out(c, e.view(), e_out, ldd, where);
+    c.sync();
+    put_stats(s, stats, predicted_ranks, matvec_history, residual_history, hist_cap);
+}
+
+void mc_entry(blws_context* ctx, int64_t m, int64_t rows, const RowShard* shard, int64_t n, int64_t nnz,
+              const int64_t* colptr, const int32_t* rowidx, const double* values, double tau, double delta,
+              blws_svd_backend* backend, const blws_mc_options* opts, const double* truth_ml, const double* truth_mr,
+              int64_t r_true, double* u, double* sigma, double* v, int64_t cap, int64_t* rank,
+              blws_solver_stats* stats, int64_t* predicted_ranks, int64_t* matvec_history, double* residual_history,
+              int64_t hist_cap) {
+    need(m > 0 && n > 0 && rows > 0 && rows <= m && nnz >= 0 && colptr && (nnz == 0 || (rowidx && values)),
+         "mc_svt: bad observation");
+    need(backend != nullptr, "mc_svt: null backend");
+    for (int64_t p = 0; p < nnz; ++p) need(rowidx[p] >= 0 && rowidx[p] < rows, "mc_svt: row index out of range");
+    Context& c = *ctx->ctx;
+    McOptions o;
+    if (opts) {
+        o.tol_outer = opts->tol_outer;
+        o.max_iter = opts->max_iter;
+        o.initial_rank = opts->initial_rank;
+        o.rank_increment = opts->rank_increment;
+    }
+    auto sol = blws::mc_svt(c, m, n, nnz, colptr, rowidx, values, tau, delta, *backend->b, o, truth_ml, truth_mr,
+                            r_true, shard, rows);
+    const Index k = sol.uv.rank();
+    if (rank) *rank = k;
+    if (k > cap) throw std::invalid_argument("mc_svt: output capacity too small");
+    if (u) download(c, sol.uv.u(), u, rows);
+    if (v) download(c, sol.uv.v(), v, n);
+    if (sigma) std::copy(sol.uv.sigma.begin(), sol.uv.sigma.end(), sigma);
+    put_stats(sol.stats, stats, predicted_ranks, matvec_history, residual_history, hist_cap);
+}
+}  // namespace
+
+extern "C" {
+
 int blws_rpca_adm(blws_context* ctx, int64_t m, const double* d, int64_t ldd, int where, double lambda,
                   blws_svd_backend* backend, const blws_rpca_options* opts, const double* truth, double* a_out,
                   double* e_out, blws_solver_stats* stats, int64_t* predicted_ranks, int64_t* matvec_history,
                   double* residual_history, int64_t hist_cap) {
     return guard([&] {
-        need(m > 0 && d && ldd >= m, "rpca_adm: bad D");
-        Context& c = *ctx->ctx;
-        RpcaOptions o;
-        if (opts) {
-            o.tol_outer = opts->tol_outer;
-            o.max_iter = opts->max_iter;
-            o.rho = opts->rho;
-            o.mu_max_factor = opts->mu_max_factor;
-            o.initial_rank = opts->initial_rank;
-            o.rank_increment = opts->rank_increment;
-        }
-        const Index ld = std::max<Index>(2, round_up(m, 2));
-        if (where == BLWS_DEVICE && ldd % 2 == 0) {
-            auto s = blws::rpca_adm(c, m, d, ldd, lambda, *backend->b, o, truth, a_out, e_out);
-            put_stats(s, stats, predicted_ranks, matvec_history, residual_history, hist_cap);
-            return;
-        }
-        DMat dd(c, m, m, false);
-        copy_in(c, dd.view(), d, ldd, where);
-        DMat tr, a, e;
-        if (truth) {
-            tr = DMat(c, m, m, false);
-            copy_in(c, tr.view(), truth, ldd, where);
-        }
-        if (a_out) a = DMat(c, m, m, false);
-        if (e_out) e = DMat(c, m, m, false);
-        auto s = blws::rpca_adm(c, m, dd.data(), ld, lambda, *backend->b, o, truth ? tr.data() : nullptr,
-                                a_out ? a.data() : nullptr, e_out ? e.data() : nullptr);
-        if (a_out) copy_out(c, a.view(), a_out, ldd, where);
-        if (e_out) copy_out(c, e.view(), e_out, ldd, where);
-        c.sync();
-        put_stats(s, stats, predicted_ranks, matvec_history, residual_history, hist_cap);
+        rpca_entry(ctx, m, m, nullptr, d, ldd, where, lambda, backend, opts, truth, a_out, e_out, stats,
+                   predicted_ranks, matvec_history, residual_history, hist_cap);
+    });
+}
+
+int blws_rpca_adm_sharded(blws_context* ctx, int64_t m, int64_t rows, int64_t row0, const double* d, int64_t ldd,
+                          int where, double lambda, blws_svd_backend* backend, const blws_rpca_options* opts,
+                          const double* truth, double* a_out, double* e_out, blws_solver_stats* stats,
+                          int64_t* predicted_ranks, int64_t* matvec_history, double* residual_history,
+                          int64_t hist_cap) {
+    return guard([&] {
+        need(row0 >= 0 && row0 + rows <= m, "rpca_adm_sharded: rows outside [0, m)");
+        const RowShard sh{m, row0};
+        rpca_entry(ctx, m, rows, &sh, d, ldd, where, lambda, backend, opts, truth, a_out, e_out, stats,
+                   predicted_ranks, matvec_history, residual_history, hist_cap);
     });
 }
 
@@ -611,23 +669,22 @@ int blws_mc_svt(blws_context* ctx, int64_t m, int64_t n, int64_t nnz, const int6
                 int64_t cap, int64_t* rank, blws_solver_stats* stats, int64_t* predicted_ranks,
                 int64_t* matvec_history, double* residual_history, int64_t hist_cap) {
     return guard([&] {
-        Context& c = *ctx->ctx;
-        McOptions o;
-        if (opts) {
-            o.tol_outer = opts->tol_outer;
-            o.max_iter = opts->max_iter;
-            o.initial_rank = opts->initial_rank;
-            o.rank_increment = opts->rank_increment;
-        }
-        auto sol = blws::mc_svt(c, m, n, nnz, colptr, rowidx, values, tau, delta, *backend->b, o, truth_ml, truth_mr,
-                                r_true);
-        const Index k = sol.uv.rank();
-        if (rank) *rank = k;
-        if (k > cap) throw std::invalid_argument("mc_svt: output capacity too small");
-        if (u) download(c, sol.uv.u(), u, m);
-        if (v) download(c, sol.uv.v(), v, n);
-        if (sigma) std::copy(sol.uv.sigma.begin(), sol.uv.sigma.end(), sigma);
-        put_stats(sol.stats, stats, predicted_ranks, matvec_history, residual_history, hist_cap);
+        mc_entry(ctx, m, m, nullptr, n, nnz, colptr, rowidx, values, tau, delta, backend, opts, truth_ml, truth_mr,
+                 r_true, u, sigma, v, cap, rank, stats, predicted_ranks, matvec_history, residual_history, hist_cap);
+    });
+}
+
+int blws_mc_svt_sharded(blws_context* ctx, int64_t m, int64_t rows, int64_t row0, int64_t n, int64_t nnz,
+                        const int64_t* colptr, const int32_t* rowidx, const double* values, double tau, double delta,
+                        blws_svd_backend* backend, const blws_mc_options* opts, const double* truth_ml,
+                        const double* truth_mr, int64_t r_true, double* u, double* sigma, double* v, int64_t cap,
+                        int64_t* rank, blws_solver_stats* stats, int64_t* predicted_ranks, int64_t* matvec_history,
+                        double* residual_history, int64_t hist_cap) {
+    return guard([&] {
+        need(row0 >= 0 && row0 + rows <= m, "mc_svt_sharded: rows outside [0, m)");
+        const RowShard sh{m, row0};
+        mc_entry(ctx, m, rows, &sh, n, nnz, colptr, rowidx, values, tau, delta, backend, opts, truth_ml, truth_mr,
+                 r_true, u, sigma, v, cap, rank, stats, predicted_ranks, matvec_history, residual_history, hist_cap);
     });
 }
 

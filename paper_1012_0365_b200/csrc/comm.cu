@@ -81,6 +81,12 @@ void Context::allreduce_sum(double* p, size_t count) {
           "ncclAllReduce");
 }
 
+void Context::allreduce_max(double* p, size_t count) {
+    if (!comm_ || count == 0) return;
+    check(nccl().all_reduce(p, p, count, ncclDouble, ncclMax, static_cast<ncclComm_t>(comm_), stream()),
+          "ncclAllReduce");
+}
+
 void Context::destroy_comm() noexcept {
     if (!comm_) return;
     try {

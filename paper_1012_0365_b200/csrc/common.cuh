@@ -59,6 +59,7 @@ public:
     /// processes (one GPU each); allreduce_sum is a no-op without one.
     void init_comm(int nranks, int rank, const void* id128);
     void allreduce_sum(double* p, size_t count);
+    void allreduce_max(double* p, size_t count);
     int nranks() const { return nranks_; }
     int rank() const { return rank_; }
     bool distributed() const { return comm_ != nullptr && nranks_ > 1; }

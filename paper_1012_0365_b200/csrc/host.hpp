@@ -318,8 +318,11 @@ struct RpcaOptions {
 };
 /// rpca_adm (solvers.hpp:72-157). d / truth / a_out / e_out are device
 /// pointers with leading dimension ldd (truth, a_out, e_out may be null).
+/// With `shard` (m_total = m), they hold this rank's `rows` rows starting at
+/// shard->row0, and the solve runs row-sharded over the context's communicator.
 SolverStats rpca_adm(Context& ctx, Index m, const double* d, Index ldd, double lambda, SvdBackend& backend,
-                     const RpcaOptions& opts, const double* truth, double* a_out, double* e_out);
+                     const RpcaOptions& opts, const double* truth, double* a_out, double* e_out,
+                     const RowShard* shard = nullptr, Index rows = 0);
 
 struct McOptions {
     double tol_outer = 1e-4;
@@ -330,9 +333,12 @@ struct McSolution {
     DWarm uv;  // sigma = shrunk values
     SolverStats stats;
 };
-/// mc_svt (solvers.hpp:202-270); the observation is host CSC.
+/// mc_svt (solvers.hpp:202-270); the observation is host CSC. With `shard`
+/// (m_total = m), the CSC holds this rank's `rows` rows (row indices local to
+/// the shard, nnz local), truth_ml its rows of ML; U comes back row-sharded.
 McSolution mc_svt(Context& ctx, Index m, Index n, Index nnz, const std::int64_t* colptr, const std::int32_t* rowidx,
                   const double* vals, double tau, double delta, SvdBackend& backend, const McOptions& opts,
-                  const double* truth_ml, const double* truth_mr, Index r_true);
+                  const double* truth_ml, const double* truth_mr, Index r_true, const RowShard* shard = nullptr,
+                  Index rows = 0);
 
 }  // namespace blws

@@ -159,6 +159,11 @@ static void launch_nonfinite(Context& ctx, View v, int* flag) {
     ctx.check_launch("nonfinite");
 }
 
+void nonfinite_count(Context& ctx, View v, int* flag) {
+    zero(ctx, flag, sizeof(int));
+    launch_nonfinite(ctx, v, flag);
+}
+
 static void check_finite_view(Context& ctx, View v, const char* what) {
     DBuf<int> flag(ctx, 1);
     zero(ctx, flag.get(), sizeof(int));
@@ -358,9 +363,20 @@ void SparseOperator::pair_block_impl(View left, View right, View top, View bot) 
     const size_t need = static_cast<size_t>(std::max(m_, n_) * b);
     if (scratch_.size() < need) scratch_ = DBuf<double>(ctx_, need);
     if (scratch2_.size() < need) scratch2_ = DBuf<double>(ctx_, need);
+    const bool reduce = row_sharded() && ctx_.has_comm();
+    DBuf<double> part;  // row shard: W^T x over the local rows, summed over the ranks
+    if (reduce && bot.ld != n_) part = DBuf<double>(ctx_, static_cast<size_t>(n_ * b));
     AuxScope aux(ctx_);  // W^T x on the auxiliary stream, overlapping W x
-    csr_spmm(ctx_, n_, colptr_.get(), rowidx_.get(), val_csc_.get(), m_, b, left.p, left.ld, bot.p, bot.ld,
-             scratch2_.get());
+    if (reduce && bot.ld != n_) {
+        csr_spmm(ctx_, n_, colptr_.get(), rowidx_.get(), val_csc_.get(), m_, b, left.p, left.ld, part.get(), n_,
+                 scratch2_.get());
+        ctx_.allreduce_sum(part.get(), static_cast<size_t>(n_ * b));
+        copy(ctx_, bot, View{part.get(), n_, b, n_});
+    } else {
+        csr_spmm(ctx_, n_, colptr_.get(), rowidx_.get(), val_csc_.get(), m_, b, left.p, left.ld, bot.p, bot.ld,
+                 scratch2_.get());
+        if (reduce) ctx_.allreduce_sum(bot.p, static_cast<size_t>(n_ * b));
+    }
     aux.main();
     csr_spmm(ctx_, m_, rowptr_.get(), colidx_.get(), val_csr_.get(), n_, b, right.p, right.ld, top.p, top.ld,
              scratch_.get());
@@ -374,6 +390,7 @@ void SparseOperator::pair_impl(const double* left, const double* right, double* 
                                                                 left, bot);
     ctx_.note_launch();
     ctx_.check_launch("csr_spmv");
+    if (row_sharded() && ctx_.has_comm()) ctx_.allreduce_sum(bot, static_cast<size_t>(n_));  // W^T left over the ranks
 }
 
 // ======================================================== warm start

@@ -121,9 +121,9 @@ inline unsigned gridn(long total, long cap = 4096) {
 __device__ __forceinline__ double shrink_d(double x, double eps) { return x > eps ? x - eps : (x < -eps ? x + eps : 0.0); }
 
 // W = D - E + Y / mu (solvers.hpp:112), non-finite flag
-__global__ void form_w_k(const double* D, const double* E, const double* Y, double* W, long m, long ld, double mu,
-                         int* bad) {
-    const long total = m * m;
+__global__ void form_w_k(const double* D, const double* E, const double* Y, double* W, long m, long n, long ld,
+                         double mu, int* bad) {
+    const long total = m * n;
     int b = 0;
     for (long idx = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; idx < total;
          idx += static_cast<long>(gridDim.x) * blockDim.x) {
@@ -136,8 +136,8 @@ __global__ void form_w_k(const double* D, const double* E, const double* Y, doub
 }
 
 // Y = D / s
-__global__ void scale_into_k(const double* D, double* Y, long m, long ld, double s) {
-    const long total = m * m;
+__global__ void scale_into_k(const double* D, double* Y, long m, long n, long ld, double s) {
+    const long total = m * n;
     for (long idx = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; idx < total;
          idx += static_cast<long>(gridDim.x) * blockDim.x) {
         const long o = idx % m + (idx / m) * ld;
@@ -145,8 +145,8 @@ __global__ void scale_into_k(const double* D, double* Y, long m, long ld, double
     }
 }
 
-__global__ void maxabs_partial_k(const double* x, long m, long ld, double* partial) {
-    const long total = m * m;
+__global__ void maxabs_partial_k(const double* x, long m, long n, long ld, double* partial) {
+    const long total = m * n;
     double v = 0.0;
     for (long idx = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; idx < total;
          idx += static_cast<long>(gridDim.x) * blockDim.x)
@@ -162,8 +162,8 @@ __global__ void maxabs_partial_k(const double* x, long m, long ld, double* parti
 }
 
 // e_l0 = #|E| > tol, nnz = #E != 0 (solvers.hpp:400-409)
-__global__ void e_counts_k(const double* E, long m, long ld, double tol, unsigned long long* out) {
-    const long total = m * m;
+__global__ void e_counts_k(const double* E, long m, long n, long ld, double tol, unsigned long long* out) {
+    const long total = m * n;
     unsigned long long l0 = 0, nz = 0;
     for (long idx = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; idx < total;
          idx += static_cast<long>(gridDim.x) * blockDim.x) {
@@ -185,10 +185,11 @@ __global__ void e_counts_k(const double* E, long m, long ld, double tol, unsigne
 ///   a = (U diag(s)) V^T            (DMMA mainloop, K = r)
 ///   e = shrink(D - a + Y/mu, lambda/mu); res = D - a - e; Y += mu res
 ///   W = D - e + Y/mu_next;  E = e;  partial ||res||^2, non-finite(W)
-/// One pass over D, Y (read) and Y, W, E (write): 40 B per element.
+/// One pass over D, Y (read) and Y, W, E (write): 40 B per element. m x n: the
+/// rows held here (a row shard of a square RPCA problem, or all of it).
 __global__ void __launch_bounds__(gemm_detail::THREADS) alm_fused_k(const double* __restrict__ us, long ldu,
                                                                    const double* __restrict__ v, long ldv, long m,
-                                                                   long r, const double* __restrict__ D, double* Y,
+                                                                   long n, long r, const double* __restrict__ D, double* Y,
                                                                    double* W, double* E, long ld, double mu,
                                                                    double mu_next, double lambda_mu, double* partial,
                                                                    int* bad) {
@@ -200,7 +201,7 @@ __global__ void __launch_bounds__(gemm_detail::THREADS) alm_fused_k(const double
     for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-    mainloop<false, true, 2>(acc, smem, us, ldu, v, ldv, m, m, m0, n0, 0, r);
+    mainloop<false, true, 2>(acc, smem, us, ldu, v, ldv, m, n, m0, n0, 0, r);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, t = lane & 3;
     const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
@@ -216,7 +217,7 @@ __global__ void __launch_bounds__(gemm_detail::THREADS) alm_fused_k(const double
 #pragma unroll
             for (int e2 = 0; e2 < 2; ++e2) {
                 const long col = n0 + wn + ni * 8 + 2 * t + e2;
-                if (col >= m) continue;
+                if (col >= n) continue;
                 const long o = row + col * ld;
                 const double a = acc[mi][ni][e2];
                 const double d = D[o];
@@ -371,48 +372,77 @@ double frob(Context& ctx, View x) {
 }  // namespace
 
 // ============================================================ rpca_adm
+// Row-sharded form: with `shard`, this rank holds rows [row0, row0 +
+// rows) of the m x m problem (D, Y, E, W and A row panels). The operator and the
+// SVT are sharded (U local rows, V replicated); the ALM update is row-local; the
+// scalars the loop branches on (||D||_F, max|D|, ||R||_F, the non-finite flags,
+// the final counts and norms) are allreduced, so every rank takes the same path.
 SolverStats rpca_adm(Context& ctx, Index m, const double* d_in, Index ldd, double lambda_in, SvdBackend& backend,
-                     const RpcaOptions& opts, const double* truth, double* a_out, double* e_out) {
+                     const RpcaOptions& opts, const double* truth, double* a_out, double* e_out, const RowShard* shard,
+                     Index rows_in) {
     const auto t0 = std::chrono::steady_clock::now();
     SolverStats stats;
-    const Index ld = std::max<Index>(2, round_up(m, 2));
-    DMat D(ctx, m, m, false);
-    copy(ctx, D.view(), View{const_cast<double*>(d_in), m, m, ldd});
+    const bool sharded = shard != nullptr;
+    if (sharded && (shard->m_total != m || rows_in < 1 || shard->row0 < 0 || shard->row0 + rows_in > m))
+        throw std::invalid_argument("rpca_adm: bad row shard");
+    const Index rows = sharded ? rows_in : m;
+    const bool reduce = sharded && ctx.has_comm();
+    DBuf<double> red(ctx, 2);
+    // sum over the ranks of a device scalar (read back)
+    auto total = [&](double* dev, Index count, double* host) {
+        if (reduce) ctx.allreduce_sum(dev, static_cast<size_t>(count));
+        ctx.read(dev, host, count);
+    };
+    const Index ld = std::max<Index>(2, round_up(rows, 2));
+    DMat D(ctx, rows, m, false);
+    copy(ctx, D.view(), View{const_cast<double*>(d_in), rows, m, ldd});
     {
-        DenseOperator probe(ctx, m, m, D.data(), D.ld);
-        try {
-            probe.check_finite();
-        } catch (const std::invalid_argument&) {
-            throw std::invalid_argument("rpca_adm: D has non-finite entries");
-        }
+        DBuf<int> bad0(ctx, 1);
+        nonfinite_count(ctx, D.view(), bad0.get());
+        int hb = 0;
+        BLWS_CUDA(cudaMemcpyAsync(&hb, bad0.get(), sizeof(int), cudaMemcpyDeviceToHost, ctx.stream()));
+        ctx.sync();
+        double hbad = hb ? 1.0 : 0.0;
+        ctx.write(red.get(), &hbad, 1);
+        total(red.get(), 1, &hbad);
+        if (hbad > 0.0) throw std::invalid_argument("rpca_adm: D has non-finite entries");
     }
     const double lambda = lambda_in > 0.0 ? lambda_in : 1.0 / std::sqrt(static_cast<double>(m));
-    const double norm_d_fro = frob(ctx, D.view());
+    double norm_d_fro = 0.0;
+    sumsq(ctx, D.view(), red.get());
+    total(red.get(), 1, &norm_d_fro);
+    norm_d_fro = std::sqrt(norm_d_fro);
     if (norm_d_fro == 0.0) {
-        if (a_out) fill(ctx, View{a_out, m, m, ldd}, 0.0);
-        if (e_out) fill(ctx, View{e_out, m, m, ldd}, 0.0);
+        if (a_out) fill(ctx, View{a_out, rows, m, ldd}, 0.0);
+        if (e_out) fill(ctx, View{e_out, rows, m, ldd}, 0.0);
         stats.converged = true;
         stats.e_l0 = 0;
         return stats;
     }
-    DMat Wm(ctx, m, m, false), Y(ctx, m, m, false), E(ctx, m, m, true);
+    DMat Wm(ctx, rows, m, false), Y(ctx, rows, m, false), E(ctx, rows, m, true);
     copy(ctx, Wm.view(), D.view());
-    DenseOperator op(ctx, m, m, Wm.data(), Wm.ld);
+    DenseOperator op(ctx, rows, m, Wm.data(), Wm.ld);
+    if (sharded) op.set_row_shard(m, shard->row0);
     const double norm2_d = spectral_norm(op);
     double mu = 1.25 / norm2_d;
     const double mu_max = mu * opts.mu_max_factor;
     double dmax = 0;
     {
-        const unsigned blocks = gridn(m * m, 1024);
+        const unsigned blocks = gridn(rows * m, 1024);
         DBuf<double> part(ctx, blocks);
-        maxabs_partial_k<<<blocks, kT, 0, ctx.stream()>>>(D.data(), m, ld, part.get());
+        maxabs_partial_k<<<blocks, kT, 0, ctx.stream()>>>(D.data(), rows, m, ld, part.get());
         ctx.note_launch();
         std::vector<double> h(blocks);
         ctx.read(part.get(), h.data(), blocks);
         for (double x : h) dmax = std::max(dmax, x);
+        if (reduce) {
+            ctx.write(red.get(), &dmax, 1);
+            ctx.allreduce_max(red.get(), 1);
+            ctx.read(red.get(), &dmax, 1);
+        }
     }
     const double dual_scale = std::max(norm2_d, dmax / lambda);
-    scale_into_k<<<gridn(m * m), kT, 0, ctx.stream()>>>(D.data(), Y.data(), m, ld, dual_scale);
+    scale_into_k<<<gridn(rows * m), kT, 0, ctx.stream()>>>(D.data(), Y.data(), rows, m, ld, dual_scale);
     ctx.note_launch();
 
     RankPredictor predictor;
@@ -425,10 +455,11 @@ SolverStats rpca_adm(Context& ctx, Index m, const double* d_in, Index ldd, doubl
     DBuf<int> bad(ctx, 1);
     // first W = D - E + Y/mu (later ones come out of the fused kernel)
     zero(ctx, bad.get(), sizeof(int));
-    form_w_k<<<gridn(m * m), kT, 0, ctx.stream()>>>(D.data(), E.data(), Y.data(), Wm.data(), m, ld, mu, bad.get());
+    form_w_k<<<gridn(rows * m), kT, 0, ctx.stream()>>>(D.data(), E.data(), Y.data(), Wm.data(), rows, m, ld, mu,
+                                                        bad.get());
     ctx.note_launch();
     using namespace gemm_detail;
-    const dim3 grid(static_cast<unsigned>(ceil_div(m, BM)), static_cast<unsigned>(ceil_div(m, BN)));
+    const dim3 grid(static_cast<unsigned>(ceil_div(rows, BM)), static_cast<unsigned>(ceil_div(m, BN)));
     DBuf<double> part(ctx, static_cast<size_t>(grid.x) * grid.y);
     constexpr int smem = smem_bytes<false, true>();
     BLWS_CUDA(cudaFuncSetAttribute(alm_fused_k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -437,23 +468,32 @@ SolverStats rpca_adm(Context& ctx, Index m, const double* d_in, Index ldd, doubl
         int hbad = 0;
         BLWS_CUDA(cudaMemcpyAsync(&hbad, bad.get(), sizeof(int), cudaMemcpyDeviceToHost, ctx.stream()));
         ctx.sync();
+        if (reduce) {
+            double hb = hbad ? 1.0 : 0.0;
+            ctx.write(red.get(), &hb, 1);
+            total(red.get(), 1, &hb);
+            hbad = hb > 0.0;
+        }
         if (hbad) throw std::invalid_argument("DenseOperator: non-finite entries");
         prox = svt(op, 1.0 / mu, backend, predictor);
         last_rank = prox.achieved_rank;
         const Index r = prox.achieved_rank;
-        DMat us(ctx, m, std::max<Index>(r, 1), false);
+        DMat us(ctx, rows, std::max<Index>(r, 1), false);
         if (r > 0) scale_columns(ctx, us.view().left(r), prox.trip.u(), prox.sigma_dev.get());
         const double mu_next = std::min(opts.rho * mu, mu_max);
         zero(ctx, bad.get(), sizeof(int));
-        alm_fused_k<<<grid, THREADS, smem, ctx.stream()>>>(us.data(), us.ld, prox.trip.v().p, prox.trip.uv.ld, m, r,
-                                                           D.data(), Y.data(), Wm.data(), E.data(), ld, mu, mu_next,
+        alm_fused_k<<<grid, THREADS, smem, ctx.stream()>>>(us.data(), us.ld, prox.trip.v().p, prox.trip.uv.ld, rows, m,
+                                                           r, D.data(), Y.data(), Wm.data(), E.data(), ld, mu, mu_next,
                                                            lambda / mu, part.get(), bad.get());
         ctx.note_launch();
         ctx.check_launch("alm_fused_k");
         mu = mu_next;
         stats.matvec_history.push_back(op.application_count() - mark);
         mark = op.application_count();
-        const double feas = std::sqrt(sum_partials(ctx, part.get(), static_cast<Index>(grid.x) * grid.y)) / norm_d_fro;
+        double rsq = 0.0;
+        reduce_partials(ctx, part.get(), static_cast<Index>(grid.x) * grid.y, red.get());
+        total(red.get(), 1, &rsq);
+        const double feas = std::sqrt(rsq) / norm_d_fro;
         stats.residual_history.push_back(feas);
         stats.iterations = it;
         if (feas <= opts.tol_outer) {
@@ -463,33 +503,43 @@ SolverStats rpca_adm(Context& ctx, Index m, const double* d_in, Index ldd, doubl
     }
     // A = U diag(s) V^T of the last prox; E, e_l0, rel_err
     const Index r = prox.achieved_rank;
-    DMat A(ctx, m, m, false);
+    DMat A(ctx, rows, m, false);
     if (r > 0) {
-        DMat us(ctx, m, r, false);
+        DMat us(ctx, rows, r, false);
         scale_columns(ctx, us.view(), prox.trip.u(), prox.sigma_dev.get());
-        gemm(ctx, false, true, m, m, r, 1.0, us.data(), us.ld, prox.trip.v().p, prox.trip.uv.ld, 0.0, A.data(), A.ld);
+        gemm(ctx, false, true, rows, m, r, 1.0, us.data(), us.ld, prox.trip.v().p, prox.trip.uv.ld, 0.0, A.data(),
+             A.ld);
     } else {
         fill(ctx, A.view(), 0.0);
     }
     {
         DBuf<unsigned long long> cnt(ctx, 2);
         zero(ctx, cnt.get(), 2 * sizeof(unsigned long long));
-        e_counts_k<<<gridn(m * m, 1024), kT, 0, ctx.stream()>>>(E.data(), m, ld, 1e-8 * dmax, cnt.get());
+        e_counts_k<<<gridn(rows * m, 1024), kT, 0, ctx.stream()>>>(E.data(), rows, m, ld, 1e-8 * dmax, cnt.get());
         ctx.note_launch();
         unsigned long long h[2];
         BLWS_CUDA(cudaMemcpyAsync(h, cnt.get(), sizeof(h), cudaMemcpyDeviceToHost, ctx.stream()));
         ctx.sync();
-        stats.e_l0 = static_cast<std::int64_t>(h[0]);
-        stats.e_nnz = static_cast<std::int64_t>(h[1]);
+        double hc[2] = {static_cast<double>(h[0]), static_cast<double>(h[1])};  // exact below 2^53
+        if (reduce) {
+            ctx.write(red.get(), hc, 2);
+            total(red.get(), 2, hc);
+        }
+        stats.e_l0 = static_cast<std::int64_t>(hc[0]);
+        stats.e_nnz = static_cast<std::int64_t>(hc[1]);
     }
     if (truth) {
-        DMat diff(ctx, m, m, false);
+        DMat diff(ctx, rows, m, false);
         copy(ctx, diff.view(), A.view());
-        axpy(ctx, diff.view(), View{const_cast<double*>(truth), m, m, ldd}, -1.0);
-        stats.rel_err = frob(ctx, diff.view()) / frob(ctx, View{const_cast<double*>(truth), m, m, ldd});
+        axpy(ctx, diff.view(), View{const_cast<double*>(truth), rows, m, ldd}, -1.0);
+        double nd[2];
+        sumsq(ctx, diff.view(), red.get());
+        sumsq(ctx, View{const_cast<double*>(truth), rows, m, ldd}, red.get() + 1);
+        total(red.get(), 2, nd);
+        stats.rel_err = std::sqrt(nd[0]) / std::sqrt(nd[1]);
     }
-    if (a_out) copy(ctx, View{a_out, m, m, ldd}, A.view());
-    if (e_out) copy(ctx, View{e_out, m, m, ldd}, E.view());
+    if (a_out) copy(ctx, View{a_out, rows, m, ldd}, A.view());
+    if (e_out) copy(ctx, View{e_out, rows, m, ldd}, E.view());
     ctx.sync();
     stats.rank_hat = last_rank;
     stats.matvec_count = op.application_count();
@@ -499,30 +549,57 @@ SolverStats rpca_adm(Context& ctx, Index m, const double* d_in, Index ldd, doubl
 }
 
 // ============================================================ mc_svt
+// Row-sharded form: the observed rows [row0, row0 + rows) live here as a local
+// CSC; the SpMM / SpMV Wᵀ halves are allreduced by the operator, K9 is
+// row-local, and the scalars (nnz, ||P_Ω D||_F, the residual norm, the error
+// norms) are summed over the ranks.
 McSolution mc_svt(Context& ctx, Index m, Index n, Index nnz, const std::int64_t* colptr, const std::int32_t* rowidx,
                   const double* vals, double tau_in, double delta_in, SvdBackend& backend, const McOptions& opts,
-                  const double* truth_ml, const double* truth_mr, Index r_true) {
+                  const double* truth_ml, const double* truth_mr, Index r_true, const RowShard* shard, Index rows_in) {
     const auto t0 = std::chrono::steady_clock::now();
-    if (nnz == 0) throw std::invalid_argument("mc_svt: empty observation set");
+    const bool sharded = shard != nullptr;
+    if (sharded && (shard->m_total != m || rows_in < 1 || shard->row0 < 0 || shard->row0 + rows_in > m))
+        throw std::invalid_argument("mc_svt: bad row shard");
+    const Index rows = sharded ? rows_in : m;
+    const bool reduce = sharded && ctx.has_comm();
+    DBuf<double> red(ctx, 2);
+    auto total = [&](double* host, Index count) {  // host values summed over the ranks
+        if (!reduce) return;
+        ctx.write(red.get(), host, count);
+        ctx.allreduce_sum(red.get(), static_cast<size_t>(count));
+        ctx.read(red.get(), host, count);
+    };
+    double head[2] = {static_cast<double>(nnz), 0.0};  // nnz, non-finite count (exact below 2^53)
     for (Index i = 0; i < nnz; ++i)
-        if (!std::isfinite(vals[i])) throw std::invalid_argument("mc_svt: non-finite observations");
+        if (!std::isfinite(vals[i])) head[1] += 1.0;
+    total(head, 2);
+    const double nnz_all = head[0];
+    if (nnz_all == 0.0) throw std::invalid_argument("mc_svt: empty observation set");
+    if (head[1] > 0.0) throw std::invalid_argument("mc_svt: non-finite observations");
     const double tau = tau_in > 0.0 ? tau_in : 5.0 * static_cast<double>(m);
-    const double delta = delta_in > 0.0 ? delta_in
-                                        : 1.2 * static_cast<double>(m) * static_cast<double>(n) / static_cast<double>(nnz);
-    SparseOperator op(ctx, m, n, nnz, colptr, rowidx, vals);
+    const double delta = delta_in > 0.0 ? delta_in : 1.2 * static_cast<double>(m) * static_cast<double>(n) / nnz_all;
+    SparseOperator op(ctx, rows, n, nnz, colptr, rowidx, vals);
+    if (sharded) op.set_row_shard(m, shard->row0);
     const double norm2_pd = spectral_norm(op);
     const double k0 = std::ceil(tau / (delta * norm2_pd));
-    DBuf<double> obs(ctx, static_cast<size_t>(nnz)), y(ctx, static_cast<size_t>(nnz)), resid(ctx, static_cast<size_t>(nnz));
-    BLWS_CUDA(cudaMemcpyAsync(obs.get(), op.val_csc(), sizeof(double) * nnz, cudaMemcpyDeviceToDevice, ctx.stream()));
+    const size_t nb = static_cast<size_t>(std::max<Index>(nnz, 1));
+    DBuf<double> obs(ctx, nb), y(ctx, nb), resid(ctx, nb);
+    if (nnz > 0)
+        BLWS_CUDA(cudaMemcpyAsync(obs.get(), op.val_csc(), sizeof(double) * nnz, cudaMemcpyDeviceToDevice,
+                                  ctx.stream()));
     double obs_norm = 0;
     {
-        DBuf<double> s(ctx, 1);
-        sumsq(ctx, View{obs.get(), nnz, 1, nnz}, s.get());
-        ctx.read(s.get(), &obs_norm, 1);
+        DBuf<double> s1(ctx, 1);
+        zero(ctx, s1.get(), sizeof(double));
+        if (nnz > 0) sumsq(ctx, View{obs.get(), nnz, 1, nnz}, s1.get());
+        ctx.read(s1.get(), &obs_norm, 1);
+        total(&obs_norm, 1);
         obs_norm = std::sqrt(obs_norm);
     }
-    vec_scale_k<<<gridn(nnz), kT, 0, ctx.stream()>>>(nnz, y.get(), obs.get(), k0 * delta);
-    ctx.note_launch();
+    if (nnz > 0) {
+        vec_scale_k<<<gridn(nnz), kT, 0, ctx.stream()>>>(nnz, y.get(), obs.get(), k0 * delta);
+        ctx.note_launch();
+    }
 
     RankPredictor predictor;
     predictor.r = opts.initial_rank;
@@ -532,22 +609,25 @@ McSolution mc_svt(Context& ctx, Index m, Index n, Index nnz, const std::int64_t*
     SolverStats& stats = sol.stats;
     stats.matvec_init = op.application_count();
     std::int64_t mark = stats.matvec_init;
-    const unsigned blocks = gridn(nnz, 2048);
+    const unsigned blocks = gridn(std::max<Index>(nnz, 1), 2048);
     DBuf<double> part(ctx, blocks);
     for (Index it = 1; it <= opts.max_iter; ++it) {
         op.assign_values_device(y.get());
         SvtResult prox = svt(op, tau, backend, predictor);
         stats.rank_hat = prox.achieved_rank;
         const Index r = prox.achieved_rank;
-        DBuf<double> ust(ctx, static_cast<size_t>(std::max<Index>(m * r, 1))), vt(ctx, static_cast<size_t>(std::max<Index>(n * r, 1)));
+        DBuf<double> ust(ctx, static_cast<size_t>(std::max<Index>(rows * r, 1))),
+            vt(ctx, static_cast<size_t>(std::max<Index>(n * r, 1)));
         if (r > 0) {
-            row_major_scaled_k<<<gridn(m * r), kT, 0, ctx.stream()>>>(prox.trip.u().p, prox.trip.uv.ld, m, r,
-                                                                      prox.sigma_dev.get(), ust.get());
+            row_major_scaled_k<<<gridn(rows * r), kT, 0, ctx.stream()>>>(prox.trip.u().p, prox.trip.uv.ld, rows, r,
+                                                                         prox.sigma_dev.get(), ust.get());
             row_major_scaled_k<<<gridn(n * r), kT, 0, ctx.stream()>>>(prox.trip.v().p, prox.trip.uv.ld, n, r, nullptr,
                                                                       vt.get());
             ctx.note_launch(2);
         }
-        if (r <= 32)
+        if (nnz == 0)
+            zero(ctx, part.get(), sizeof(double) * blocks);
+        else if (r <= 32)
             mc_sampled_k<1><<<blocks, kT, 0, ctx.stream()>>>(nnz, op.rowidx_csc(), op.colof_csc(), ust.get(), vt.get(),
                                                              r, obs.get(), resid.get(), part.get());
         else if (r <= 64)
@@ -564,38 +644,49 @@ McSolution mc_svt(Context& ctx, Index m, Index n, Index nnz, const std::int64_t*
         sol.uv = std::move(prox.trip);
         stats.matvec_history.push_back(op.application_count() - mark);
         mark = op.application_count();
-        const double rel = std::sqrt(sum_partials(ctx, part.get(), blocks)) / obs_norm;
+        reduce_partials(ctx, part.get(), blocks, red.get());
+        double rsq = 0.0;
+        if (reduce) ctx.allreduce_sum(red.get(), 1);
+        ctx.read(red.get(), &rsq, 1);
+        const double rel = std::sqrt(rsq) / obs_norm;
         stats.residual_history.push_back(rel);
         stats.iterations = it;
         if (rel <= opts.tol_outer) {
             stats.converged = true;
             break;
         }
-        vec_axpy_k<<<gridn(nnz), kT, 0, ctx.stream()>>>(nnz, y.get(), resid.get(), delta);
-        ctx.note_launch();
+        if (nnz > 0) {
+            vec_axpy_k<<<gridn(nnz), kT, 0, ctx.stream()>>>(nnz, y.get(), resid.get(), delta);
+            ctx.note_launch();
+        }
     }
     stats.matvec_count = op.application_count();
     stats.predicted_ranks = predictor.history;
     if (truth_ml && truth_mr && r_true > 0) {
         // ||U S V^T - ML MR^T||_F / ||ML MR^T||_F via one GEMM with K = rank + r_true
+        // (this rank's rows; the squares are summed over the ranks)
         const Index r = sol.uv.rank();
-        DMat left(ctx, m, r + r_true, false), right(ctx, n, r + r_true, false);
+        DMat left(ctx, rows, r + r_true, false), right(ctx, n, r + r_true, false);
         if (r > 0) {
             DBuf<double> sd(ctx, static_cast<size_t>(r));
             ctx.write(sd.get(), sol.uv.sigma.data(), r);
             scale_columns(ctx, left.view().left(r), sol.uv.u(), sd.get());
             copy(ctx, right.view().left(r), sol.uv.v());
         }
-        upload(ctx, left.view().cols_range(r, r_true), truth_ml, m);
+        upload(ctx, left.view().cols_range(r, r_true), truth_ml, rows);
         copy(ctx, left.view().cols_range(r, r_true), left.view().cols_range(r, r_true), -1.0);
         upload(ctx, right.view().cols_range(r, r_true), truth_mr, n);
-        DMat full(ctx, m, n, false);
-        gemm(ctx, false, true, m, n, r + r_true, 1.0, left.data(), left.ld, right.data(), right.ld, 0.0, full.data(),
+        DMat full(ctx, rows, n, false);
+        gemm(ctx, false, true, rows, n, r + r_true, 1.0, left.data(), left.ld, right.data(), right.ld, 0.0, full.data(),
              full.ld);
-        const double num = frob(ctx, full.view());
-        gemm(ctx, false, true, m, n, r_true, -1.0, left.data() + r * left.ld, left.ld, right.data() + r * right.ld,
+        double nd[2];
+        sumsq(ctx, full.view(), red.get());
+        gemm(ctx, false, true, rows, n, r_true, -1.0, left.data() + r * left.ld, left.ld, right.data() + r * right.ld,
              right.ld, 0.0, full.data(), full.ld);
-        stats.rel_err = num / frob(ctx, full.view());
+        sumsq(ctx, full.view(), red.get() + 1);
+        ctx.read(red.get(), nd, 2);
+        total(nd, 2);
+        stats.rel_err = std::sqrt(nd[0]) / std::sqrt(nd[1]);
     }
     stats.wall_time_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     return sol;

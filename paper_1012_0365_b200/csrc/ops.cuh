@@ -39,6 +39,8 @@ void copy(Context& ctx, View dst, View src, double alpha = 1.0);  // dst = alpha
 void axpy(Context& ctx, View y, View x, double alpha);            // y += alpha * x
 /// out[0] = sum of squares of x (deterministic two-pass reduction).
 void sumsq(Context& ctx, View x, double* out);
+/// *flag = 1 if x has a non-finite entry, else 0 (device; stream-ordered)
+void nonfinite_count(Context& ctx, View x, int* flag);
 /// out[0] = sum of squares of (X - I) for a square X.
 void sumsq_minus_identity(Context& ctx, View x, double* out);
 /// dst = 0.5 * (src + src^T), square.

@@ -59,3 +59,21 @@ def shard_operator(w_local, m_total: int, row0: int, ctx, device: bool = False, 
         op = api.DenseOperator(w_local, ctx=ctx)
     op.set_row_shard(m_total, row0)
     return op
+
+
+def shard_csc(colptr, rowidx, vals, row0: int, rows: int):
+    """Rows [row0, row0 + rows) of a CSC matrix as a local CSC over the same
+    columns (row indices relative to row0, positions in their original order)
+    -- the observation a rank passes to mc_svt_sharded. Also returns the
+    positions taken (indices into the global CSC arrays)."""
+    import numpy as np
+
+    colptr = np.asarray(colptr, dtype=np.int64)
+    rowidx = np.asarray(rowidx)
+    keep = (rowidx >= row0) & (rowidx < row0 + rows)
+    pos = np.nonzero(keep)[0]
+    col_of = np.repeat(np.arange(len(colptr) - 1), np.diff(colptr))
+    counts = np.bincount(col_of[pos], minlength=len(colptr) - 1)
+    local_ptr = np.zeros(len(colptr), dtype=np.int64)
+    np.cumsum(counts, out=local_ptr[1:])
+    return local_ptr, (rowidx[pos] - row0).astype(np.int32), np.asarray(vals)[pos], pos

@@ -234,3 +234,161 @@ def test_sharded_lanczos_decomposition_matches_unsharded():
     for alphas, betas in res:
         assert np.abs(alphas - ref[0]).max() <= 1e-12 * np.abs(ref[0]).max()
         assert np.abs(betas - ref[1]).max() <= 1e-12 * ref[1].max()
+
+
+# ---------------------------------------------- solver loops (row-sharded)
+def _allreduce_max(x):
+    import torch
+    import torch.distributed as dist
+
+    t = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64))
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t.numpy()
+
+
+def _gather_rows(x, m, row0):
+    # exact all-gather of row panels: zeros elsewhere, summed
+    full = np.zeros((m,) + x.shape[1:])
+    full[row0:row0 + x.shape[0]] = x
+    return _allreduce(full)
+
+
+def _shrink(x, t):
+    return np.where(x > t, x - t, np.where(x < -t, x + t, 0.0))
+
+
+def _rpca_instance():
+    from oracle import oracle as O
+    from paper_1012_0365_b200 import synth
+
+    return synth.rpca_lowrank_sparse(72, 4, 260, 2, O.Rng, O.sample_distinct)
+
+
+def _worker_rpca(rank, world):
+    # rpca_adm (solvers.hpp:72-157) as host_solvers.cu runs it row-sharded: D / Y /
+    # E / W row panels, the scalars (||D||_F, max|D|, ||R||_F) allreduced, the
+    # ALM update row-local on this rank's rows of U diag(s) V^T. The SVT itself is
+    # the oracle's on the gathered W (the sharded SVT is checked above).
+    from oracle import oracle as O
+    from paper_1012_0365_b200.dist import row_partition
+
+    d, _, _, _ = _rpca_instance()
+    m = d.shape[0]
+    row0, rows = row_partition(m, world, rank)
+    D = d[row0:row0 + rows]
+    lam = 1.0 / np.sqrt(m)
+    norm_fro = np.sqrt(_allreduce(np.array([np.sum(D * D)]))[0])
+    norm2 = O.spectral_norm(O.DenseOperator(_gather_rows(D, m, row0)))
+    mu = 1.25 / norm2
+    mu_max = mu * 1e7
+    dmax = _allreduce_max(np.array([np.abs(D).max()]))[0]
+    Y = D / max(norm2, dmax / lam)
+    E = np.zeros_like(D)
+    backend = O.SvdBackend.blws(seed=11)
+    pred = O.RankPredictor(10, 5, m)
+    it_done, A = 0, np.zeros_like(D)
+    for it in range(1, 1001):
+        W = D - E + Y / mu
+        prox = O.svt(O.DenseOperator(_gather_rows(W, m, row0)), 1.0 / mu, backend, pred)
+        A = (prox.u[row0:row0 + rows] * prox.sigma) @ prox.v.T
+        E = _shrink(D - A + Y / mu, lam / mu)
+        res = D - A - E
+        Y = Y + mu * res
+        mu = min(1.5 * mu, mu_max)
+        feas = np.sqrt(_allreduce(np.array([np.sum(res * res)]))[0]) / norm_fro
+        it_done = it
+        if feas <= 1e-7:
+            break
+    e_l0 = int(_allreduce(np.array([float(np.sum(np.abs(E) > 1e-8 * dmax))]))[0])
+    return it_done, A, list(pred.history), e_l0
+
+
+def test_sharded_rpca_loop_matches_oracle():
+    from oracle import oracle as O
+
+    res = _run(2, _worker_rpca)
+    assert not any(isinstance(r, str) for r in res), res
+    d, a0, _, _ = _rpca_instance()
+    a_ref, _, st, _ = O.rpca_adm(d, O.SvdBackend.blws(seed=11), truth=a0)
+    a = np.vstack([r[1] for r in res])
+    for it, _, hist, e_l0 in res:
+        assert it == st.iterations and hist == st.predicted_ranks and e_l0 == st.e_l0
+    assert np.linalg.norm(a - a_ref) <= 1e-9 * np.linalg.norm(a_ref)
+
+
+def _mc_instance():
+    from oracle import oracle as O
+    from paper_1012_0365_b200 import synth
+
+    return synth.mc_lowrank(120, 4, 5664, 9, O.Rng, O.sample_distinct)  # 6x oversampled (test_solvers.cpp:110)
+
+
+def _worker_mc(rank, world):
+    # mc_svt (solvers.hpp:202-270) row-sharded: this rank's observed rows as a
+    # local CSC (dist.shard_csc), nnz / ||P_Ω D|| / the residual norm summed over
+    # the ranks, the sampled evaluation on the local rows of U diag(s). The
+    # SVT is the oracle's on the gathered iterate.
+    from oracle import oracle as O
+    from paper_1012_0365_b200.dist import row_partition, shard_csc
+
+    colptr, rowidx, vals, _, _ = _mc_instance()
+    m = n = 120
+    row0, rows = row_partition(m, world, rank)
+    lp, lr, lv, pos = shard_csc(colptr, rowidx, vals, row0, rows)
+    nnz = _allreduce(np.array([float(len(lv))]))[0]
+    tau, delta = 5.0 * m, 1.2 * m * n / nnz
+    full_idx = np.zeros(len(vals))
+    full_idx[pos] = 1.0
+    assert np.array_equal(_allreduce(full_idx), np.ones(len(vals)))  # the shards cover every position once
+
+    def gathered(local_vals):
+        g = np.zeros(len(vals))
+        g[pos] = local_vals
+        return _allreduce(g)
+
+    norm2 = O.spectral_norm(O.SparseOperator(m, n, colptr, rowidx, gathered(lv)))
+    k0 = np.ceil(tau / (delta * norm2))
+    obs_norm = np.sqrt(_allreduce(np.array([np.sum(lv * lv)]))[0])
+    y = (k0 * delta) * lv
+    col_of = np.repeat(np.arange(n), np.diff(lp))
+    backend = O.SvdBackend.blws(seed=8)
+    pred = O.RankPredictor(10, 5, min(m, n))
+    it_done = 0
+    for it in range(1, 501):
+        prox = O.svt(O.SparseOperator(m, n, colptr, rowidx, gathered(y)), tau, backend, pred)
+        us = prox.u[row0:row0 + rows] * prox.sigma
+        a_vals = np.einsum("ij,ij->i", us[lr], prox.v[col_of])
+        resid = lv - a_vals
+        rel = np.sqrt(_allreduce(np.array([np.sum(resid * resid)]))[0]) / obs_norm
+        it_done = it
+        if rel <= 1e-4:
+            break
+        y = y + delta * resid
+    return it_done, list(pred.history), prox.sigma
+
+
+def test_sharded_mc_loop_matches_oracle():
+    from oracle import oracle as O
+
+    res = _run(2, _worker_mc)
+    assert not any(isinstance(r, str) for r in res), res
+    colptr, rowidx, vals, _, _ = _mc_instance()
+    _, s_ref, _, st = O.mc_svt(120, 120, colptr, rowidx, vals, O.SvdBackend.blws(seed=8))
+    for it, hist, s in res:
+        assert it == st.iterations and hist == st.predicted_ranks
+        assert np.abs(s - s_ref).max() <= 1e-8 * s_ref.max()
+
+
+def test_shard_csc_roundtrip():
+    from paper_1012_0365_b200.dist import row_partition, shard_csc
+
+    colptr, rowidx, vals, _, _ = _mc_instance()
+    seen = np.zeros(len(vals), dtype=int)
+    for r in range(3):
+        row0, rows = row_partition(120, 3, r)
+        lp, lr, lv, pos = shard_csc(colptr, rowidx, vals, row0, rows)
+        seen[pos] += 1
+        assert lp[-1] == len(lv) and np.all((lr >= 0) & (lr < rows))
+        assert np.array_equal(lv, vals[pos]) and np.array_equal(lr + row0, rowidx[pos])
+        assert np.all(np.diff(lp) >= 0)
+    assert np.all(seen == 1)

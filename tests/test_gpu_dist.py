@@ -84,3 +84,56 @@ def test_sharded_lanczos_and_svt_single_rank(G, O):
         r2 = G.svt(plain, eps, b2, p2)
         assert r1.achieved_rank == r2.achieved_rank and p1.history == p2.history
         assert np.abs(r1.sigma - r2.sigma).max() <= 1e-9 * r2.sigma.max()
+
+
+def test_sharded_rpca_single_rank(G, O):
+    # rpca_adm (solvers.hpp:72-157) row-sharded over a one-rank NCCL communicator:
+    # the allreduced scalars, the sharded operator / SVT and the row-local ALM
+    # kernel agree with the unsharded device solve and with the oracle
+    from paper_1012_0365_b200 import synth
+
+    d, a0, _, _ = synth.rpca_lowrank_sparse(160, 8, 1280, 4, O.Rng, O.sample_distinct)
+    ctx = G.Context(0)
+    ctx.init_comm(1, 0, G.api.nccl_unique_id())
+    a_s, e_s, st_s, _ = G.rpca_adm_sharded(d, 160, 0, G.SvdBackend.blws(seed=11, ctx=ctx), truth_rows=a0)
+    a_p, e_p, st_p, _ = G.rpca_adm(d, G.SvdBackend.blws(seed=11), truth=a0)
+    a_o, e_o, st_o, _ = O.rpca_adm(d, O.SvdBackend.blws(seed=11), truth=a0)
+    assert st_s.converged and st_s.iterations == st_p.iterations
+    assert abs(st_s.iterations - st_o.iterations) <= 1
+    assert st_s.rank_hat == st_p.rank_hat == 8 and st_s.predicted_ranks == st_p.predicted_ranks
+    assert st_s.e_l0 == st_p.e_l0 and st_s.matvec_count == st_p.matvec_count
+    assert np.linalg.norm(a_s - a_p) <= 1e-10 * np.linalg.norm(a_p)
+    assert np.linalg.norm(a_s - a_o) <= 1e-6 * np.linalg.norm(a_o)
+    assert abs(st_s.rel_err - st_p.rel_err) <= 1e-12 + 1e-9 * st_p.rel_err
+
+
+def test_sharded_mc_single_rank(G, O):
+    # mc_svt (solvers.hpp:202-270) row-sharded over a one-rank communicator: the
+    # sparse operator's W^T halves go through the allreduce, K9 runs on the local
+    # rows, nnz / norms are summed over the ranks
+    from paper_1012_0365_b200 import dist, synth
+
+    colptr, rowidx, vals, ml, mr = synth.mc_lowrank(200, 5, 11850, 13, O.Rng, O.sample_distinct)
+    lp, lr, lv, pos = dist.shard_csc(colptr, rowidx, vals, 0, 200)
+    assert len(pos) == len(vals)
+    ctx = G.Context(0)
+    ctx.init_comm(1, 0, G.api.nccl_unique_id())
+    us, ss, vs, st_s = G.mc_svt_sharded(200, 0, 200, 200, lp, lr, lv, G.SvdBackend.blws(seed=8, ctx=ctx),
+                                        truth_ml_rows=ml, truth_mr=mr)
+    up, sp, vp, st_p = G.mc_svt(200, 200, colptr, rowidx, vals, G.SvdBackend.blws(seed=8), truth_ml=ml, truth_mr=mr)
+    assert st_s.converged and st_s.iterations == st_p.iterations and st_s.rank_hat == st_p.rank_hat
+    assert st_s.predicted_ranks == st_p.predicted_ranks and st_s.matvec_count == st_p.matvec_count
+    a_s, a_p = (us * ss) @ vs.T, (up * sp) @ vp.T
+    assert np.linalg.norm(a_s - a_p) <= 1e-9 * np.linalg.norm(a_p)
+    assert st_s.rel_err <= 2e-4
+
+
+def test_sharded_solver_guards(G, O):
+    ctx = G.Context(0)
+    ctx.init_comm(1, 0, G.api.nccl_unique_id())
+    d = np.eye(20)
+    with pytest.raises(ValueError):
+        G.rpca_adm_sharded(d[:12], 20, 10, G.SvdBackend.blws(ctx=ctx))  # rows past m
+    with pytest.raises(ValueError):
+        G.mc_svt_sharded(20, 0, 10, 20, np.zeros(21, dtype=np.int64), np.zeros(0, dtype=np.int32), np.zeros(0),
+                         G.SvdBackend.blws(ctx=ctx))  # empty observation on every rank
