@@ -1,7 +1,9 @@
 // DMMA GEMM kernels (K1 block products W*X / W^T*X, K2 Grams, K5 Ritz lift).
 #include <algorithm>
+#include <cstdlib>
 
 #include "dgemm.cuh"
+#include "dgemm_tma.cuh"
 #include "ops.cuh"
 
 namespace blws {
@@ -151,9 +153,102 @@ int ts_occupancy(int dev) {
     return occ[dev & 7];
 }
 
+// ---- TMA variant (dgemm_tma.cuh): tensor maps encoded per call through the
+// driver entry point (no libcuda link dependency), passed as __grid_constant__.
+using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiled encode_tiled() {
+    static const EncodeTiled fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return static_cast<EncodeTiled>(nullptr);
+        return reinterpret_cast<EncodeTiled>(p);
+    }();
+    return fn;
+}
+
+// column-major `outer` x ... matrix seen as a 2D tensor {inner, outer} with row
+// stride ld; boxes of {16 (128 B, swizzled), box_outer}
+bool tensor_map(CUtensorMap* map, const double* base, long inner, long outer, long ld, int box_outer) {
+    const EncodeTiled fn = encode_tiled();
+    if (!fn || reinterpret_cast<uintptr_t>(base) % 16 != 0 || (ld * 8) % 16 != 0 || inner < 1 || outer < 1)
+        return false;
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 8};
+    const cuuint32_t box[2] = {16, static_cast<cuuint32_t>(box_outer)};
+    const cuuint32_t es[2] = {1, 1};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+constexpr int kTmaBK = 32, kTmaStages = 2, kTmaCons = 4;
+
+template <bool TA, int BN>
+bool launch_tma(Context& ctx, const double* A, long lda, const double* B, long ldb, double* C, long ldc, long M,
+                long N, long K, double alpha, double beta) {
+    static const bool enabled = [] {
+        const char* e = std::getenv("BLWS_TMA");
+        return !(e && e[0] == '0');
+    }();
+    if (!enabled || M > (1L << 31) - 64 || K > (1L << 31) - 64) return false;
+    CUtensorMap ta, tb;
+    // op(A) tile: TA -> A is K x M (k contiguous) boxes {16 k, 64 rows}; else M x K boxes {16 rows, BK k}
+    constexpr int BM = gemm_tma::Layout<kTmaBK, BN, kTmaCons>::BM, THREADS = gemm_tma::threads<kTmaCons>();
+    if (!(TA ? tensor_map(&ta, A, K, M, lda, BM) : tensor_map(&ta, A, M, K, lda, kTmaBK))) return false;
+    if (!tensor_map(&tb, B, K, N, ldb, BN)) return false;
+    constexpr int bytes = gemm_tma::smem_bytes<kTmaBK, BN, kTmaStages, kTmaCons>();
+    auto kern = gemm_tma::dgemm_tma_kernel<TA, BN, kTmaBK, kTmaStages, kTmaCons>;
+    static int occ = 0;
+    if (!occ) {
+        BLWS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+        BLWS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, THREADS, bytes));
+        occ = std::max(occ, 1);
+    }
+    const long mt = ceil_div(M, BM), nt = ceil_div(N, BN);
+    const long ktiles = ceil_div(K, kTmaBK);
+    const long slots = static_cast<long>(ctx.sm_count()) * occ;
+    long S = 1;  // split-K so the CTA count fills whole waves (as launch_ts)
+    const long tiles = mt * nt;
+    if (tiles < 2 * slots) {
+        const long smax = std::max<long>(1, std::min<long>(64, ktiles / 4));
+        double best = 1e30;
+        for (long s = 1; s <= smax; ++s) {
+            const long waves = ceil_div(tiles * s, slots);
+            const double cost = static_cast<double>(waves) / s + (s > 1 ? 0.02 : 0.0);
+            if (cost < best - 1e-12) {
+                best = cost;
+                S = s;
+            }
+        }
+    }
+    const long kchunk = ceil_div(ktiles, S) * kTmaBK;
+    S = ceil_div(K, kchunk);
+    DBuf<double> ws;
+    if (S > 1) ws = DBuf<double>(ctx, static_cast<size_t>(S * M * N));
+    dim3 grid(static_cast<unsigned>(mt), static_cast<unsigned>(nt), static_cast<unsigned>(S));
+    kern<<<grid, THREADS, bytes, ctx.stream()>>>(ta, tb, C, ldc, M, N, K, kchunk, alpha, beta,
+                                                           S > 1 ? ws.get() : nullptr);
+    ctx.note_launch();
+    ctx.check_launch("dgemm_tma_kernel");
+    if (S > 1) {
+        const long total = M * N;
+        splitk_reduce<<<static_cast<unsigned>(std::min<long>(2048, (total + 255) / 256)), 256, 0, ctx.stream()>>>(
+            ws.get(), M, N, static_cast<int>(S), alpha, beta, C, ldc);
+        ctx.note_launch();
+        ctx.check_launch("splitk_reduce");
+    }
+    return true;
+}
+
 template <bool TA, int BN>
 void launch_ts(Context& ctx, const double* A, long lda, const double* B, long ldb, double* C, long ldc, long M,
                long N, long K, double alpha, double beta) {
+    if (launch_tma<TA, BN>(ctx, A, lda, B, ldb, C, ldc, M, N, K, alpha, beta)) return;
     const int occ = ts_occupancy<TA, BN>(ctx.device());
     const long mt = ceil_div(M, gemm_ts::BM), nt = ceil_div(N, BN);
     const long ktiles = ceil_div(K, gemm_ts::BK);

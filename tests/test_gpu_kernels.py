@@ -179,3 +179,36 @@ def test_sparse_pair_block_matches_numpy(gpu, b):
     ref_top, ref_bot = dense @ right, dense.T @ left
     assert np.abs(top - ref_top).max() <= 1e-12 * np.abs(ref_top).max()
     assert np.abs(bot - ref_bot).max() <= 1e-12 * np.abs(ref_bot).max()
+
+
+@pytest.mark.parametrize("ta", [False, True])
+@pytest.mark.parametrize("m,n,k", [(1001, 37, 999), (5000, 104, 130), (300, 128, 17), (4000, 100, 4000),
+                                   (2047, 64, 61), (640, 8, 1)])
+def test_tall_skinny_gemm_edges(gpu, ta, m, n, k):
+    # the tall-skinny path (TMA-staged, dgemm_tma.cuh): ragged M / K / N and
+    # padded leading dimensions (even, as the 16-byte TMA strides require);
+    # out-of-range rows and k are zero-filled by the tensor loads
+    import torch
+
+    rs = np.random.default_rng(m + 3 * n + 7 * k + int(ta))
+    A = rs.standard_normal((k, m) if ta else (m, k))
+    B = rs.standard_normal((k, n))
+    C0 = rs.standard_normal((m, n))
+    ref = 1.25 * ((A.T if ta else A) @ B) + 0.5 * C0
+    dev = torch.device("cuda:0")
+
+    def padded(x):
+        rows, cols = x.shape
+        ld = rows + (2 if rows % 2 == 0 else 1)
+        t = torch.zeros((cols, ld), dtype=torch.float64, device=dev)  # column-major with ld
+        t[:, :rows] = torch.tensor(x.T.copy(), device=dev)
+        return t, ld
+
+    At, lda = padded(A)
+    Bt, ldb = padded(B)
+    Ct, ldc = padded(C0)
+    gpu.api.dgemm(ta, False, m, n, k, 1.25, At, lda, Bt, ldb, 0.5, Ct, ldc)
+    torch.cuda.synchronize()
+    got = Ct[:, :m].cpu().numpy().T
+    assert np.abs(got - ref).max() <= 1e-12 * max(1.0, np.abs(ref).max()) * np.sqrt(k)
+    assert torch.all(Ct[:, m:] == 0)  # the padding rows are left alone
