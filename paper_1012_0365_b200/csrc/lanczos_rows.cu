@@ -5,7 +5,9 @@
 // basis is append-only, so a step adds one column to every tile and the CGS2
 // products never re-read those columns from L2. Columns >= CS (a basis larger
 // than the GPU's aggregate shared memory) are read from global memory,
-// coalesced along the owned rows. Per step l (grid barriers marked |):
+// coalesced: each CTA keeps its rows of them in a contiguous copy (rebuilt by
+// the prologue, extended as columns are appended), so the CGS2 passes stream
+// them sequentially. Per step l (grid barriers marked |):
 //   [A] paired apply on 2D tiles of W (tr rows x tc columns): W q_bot partials
 //       per (column tile, row), W^T q_top partials per (row tile, column);
 //       q_l is r / beta of the previous step (or basis column l0)          |
@@ -31,8 +33,9 @@ namespace cg = cooperative_groups;
 namespace blws {
 namespace {
 
-constexpr int kRT = 512;  // threads per CTA (one CTA per SM)
+constexpr int kRT = 384;  // threads per CTA (one CTA per SM)
 constexpr int kRW = kRT / 32;
+constexpr int kSpillMLP = 16;  // spilled-basis loads in flight per lane in r -= Q c
 
 struct RowArgs {
     const double* w;
@@ -52,6 +55,8 @@ struct RowArgs {
     long cap, dim, l0, l1;
     long Rb, Cb, tr, tc;  // apply tiles
     long RB, CS;          // owned rows per CTA, resident basis columns
+    double* spill;        // G x (cap - CS) x RB: each CTA's rows of the spilled columns, contiguous
+    long scap;            // cap - CS (>= 1)
 #ifdef COOP_PROBE
     unsigned long long* probe;
 #endif
@@ -131,6 +136,7 @@ __global__ void __launch_bounds__(kRT, 1) lanczos_rows_k(RowArgs a) {
     double* acc2 = qp + RB;             // RB: spill sums
     double* sp = acc2 + RB;             // kRW x 32
     double* slot = sp + kRW * 32;       // 1
+    double* spb = a.spill + b * a.scap * RB;  // this CTA's spilled columns: spb[(p - CS) * RB + ii]
     // ---- prologue: owned rows of basis columns [0, l0] into the tile; q_l0, q_l0-1
     {
         const long cols = min(a.l0 + 1, CS);
@@ -138,6 +144,13 @@ __global__ void __launch_bounds__(kRT, 1) lanczos_rows_k(RowArgs a) {
             const long i = e % nown, p = e / nown;
             tile[i * CS + p] = a.q[(o0 + i) + p * a.ldq];
         }
+        // spilled columns [CS, l0] into this CTA's contiguous copy (rebuilt every
+        // launch; rows past the owned range are zero, as is rs there)
+        for (long e = threadIdx.x; CS + e / RB <= a.l0; e += kRT) {
+            const long i = e % RB, p = CS + e / RB;
+            spb[(p - CS) * RB + i] = i < nown ? a.q[(o0 + i) + p * a.ldq] : 0.0;
+        }
+        for (long i = threadIdx.x; i < RB; i += kRT) rs[i] = 0.0;
         for (long i = threadIdx.x; i < nown; i += kRT) {
             qc[i] = a.q[(o0 + i) + a.l0 * a.ldq];
             qp[i] = a.l0 > 0 ? a.q[(o0 + i) + (a.l0 - 1) * a.ldq] : 0.0;
@@ -240,19 +253,18 @@ __global__ void __launch_bounds__(kRT, 1) lanczos_rows_k(RowArgs a) {
                 if (ii < nown) s0 = fma(tile[ii * CS + p], rs[ii], s0);
                 a.pcol[p * G + b] = s0 + s1;
             }
-            for (long pc = CS + 32L * wid; pc < c; pc += 32L * kRW) {
-                double bp[32];
-#pragma unroll
-                for (int cc = 0; cc < 32; ++cc) bp[cc] = 0.0;
-                for (long i0 = 0; i0 < nown; i0 += 32) {
-                    const long ii = min(i0 + lane, nown - 1);
-                    const double ri = i0 + lane < nown ? rs[ii] : 0.0;
-                    const double* src = a.q + (o0 + ii);
-#pragma unroll
-                    for (int cc = 0; cc < 32; ++cc) bp[cc] = fma(src[min(pc + cc, c - 1) * a.ldq], ri, bp[cc]);
+            // spilled columns: a thread per column over the contiguous copy (RB even,
+            // 16-byte loads; rows past the owned range are zero in both operands)
+            for (long p = CS + threadIdx.x; p < c; p += kRT) {
+                const double2* col = reinterpret_cast<const double2*>(spb + (p - CS) * RB);
+                double s0 = 0.0, s1 = 0.0;
+#pragma unroll 7
+                for (long h = 0; h < RB / 2; ++h) {
+                    const double2 v = col[h];
+                    s0 = fma(v.x, rs[2 * h], s0);
+                    s1 = fma(v.y, rs[2 * h + 1], s1);
                 }
-                const double s = transpose_reduce(bp, lane);
-                if (pc + lane < c) a.pcol[(pc + lane) * G + b] = s;
+                a.pcol[p * G + b] = s0 + s1;
             }
         };
         // coefficient p = fixed-order sum over the CTAs of pcol[., p]; a warp per column
@@ -298,14 +310,14 @@ __global__ void __launch_bounds__(kRT, 1) lanczos_rows_k(RowArgs a) {
                     const long ii = i0 + lane;
                     double t0 = 0.0, t1 = 0.0;
                     {
-                        // columns CS + wid + kRW * k; eight loads in flight (clamped, zero weight past c)
-                        const double* src = a.q + (o0 + min(ii, nown - 1));
-                        for (long p0 = CS + wid; p0 < c; p0 += 8 * kRW) {
-                            double v[8];
+                        // columns CS + wid + kRW * k; kSpillMLP loads in flight (clamped, zero weight past c)
+                        const double* src = spb + (min(ii, nown - 1) - CS * RB);
+                        for (long p0 = CS + wid; p0 < c; p0 += kSpillMLP * kRW) {
+                            double v[kSpillMLP];
 #pragma unroll
-                            for (int u = 0; u < 8; ++u) v[u] = src[min(p0 + u * kRW, c - 1) * a.ldq];
+                            for (int u = 0; u < kSpillMLP; ++u) v[u] = src[min(p0 + u * kRW, c - 1) * RB];
 #pragma unroll
-                            for (int u = 0; u < 8; ++u) {
+                            for (int u = 0; u < kSpillMLP; ++u) {
                                 const long p = p0 + u * kRW;
                                 const double cv = p < c ? cf[p] : 0.0;
                                 if (u & 1)
@@ -372,10 +384,15 @@ __global__ void __launch_bounds__(kRT, 1) lanczos_rows_k(RowArgs a) {
         }
         if (l + 1 < a.cap) {
             const double inv = broken ? 0.0 : 1.0 / beta;
+            if (l + 1 >= CS)
+                for (long ii = nown + threadIdx.x; ii < RB; ii += kRT) spb[(l + 1 - CS) * RB + ii] = 0.0;
             for (long ii = threadIdx.x; ii < nown; ii += kRT) {
                 const double v = broken ? 0.0 : rs[ii] * inv;
                 a.q[(o0 + ii) + (l + 1) * a.ldq] = v;
-                if (l + 1 < CS) tile[ii * CS + (l + 1)] = v;
+                if (l + 1 < CS)
+                    tile[ii * CS + (l + 1)] = v;
+                else
+                    spb[(l + 1 - CS) * RB + ii] = v;
                 qp[ii] = qc[ii];
                 qc[ii] = v;
             }
@@ -405,7 +422,7 @@ bool lanczos_rows_steps(Context& ctx, const double* w, Index ldw, Index m, Index
     if (!coop || l1 <= l0) return false;
     const long G = std::min<long>(ctx.sm_count(), 512);
     const long ld = mp + n;
-    const long RB = (ld + G - 1) / G;
+    const long RB = ((ld + G - 1) / G + 1) & ~1L;  // even: 16-byte rows of the spill copy
     const long budget = static_cast<long>(smem_max) - 1024;
     const long fixed = static_cast<long>(rows_smem_fixed(RB, cap));
     if (fixed > budget) return false;
@@ -427,8 +444,10 @@ bool lanczos_rows_steps(Context& ctx, const double* w, Index ldw, Index m, Index
     const long tr = (m + Rb - 1) / Rb, tc = (n + Cb - 1) / Cb;
     DBuf<double> ptop(ctx, static_cast<size_t>(Cb * m)), pbot(ctx, static_cast<size_t>(Rb * n)),
         pcol(ctx, static_cast<size_t>(G * cap)), pscal(ctx, static_cast<size_t>(G));
+    const long scap = std::max<long>(1, cap - CS);
+    DBuf<double> spill(ctx, static_cast<size_t>(G * scap * RB));
     RowArgs args{w, ldw, m, n, mp, ld, q, ldq, r, alpha, lastbeta, coup, state, coef, ptop.get(), pbot.get(),
-                 pcol.get(), pscal.get(), cap, dim, l0, l1, Rb, Cb, tr, tc, RB, CS
+                 pcol.get(), pscal.get(), cap, dim, l0, l1, Rb, Cb, tr, tc, RB, CS, spill.get(), scap
 #ifdef COOP_PROBE
                  , g_rows_probe
 #endif

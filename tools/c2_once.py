@@ -26,7 +26,7 @@ def main(calls=2):
         ctx.synchronize()
         print(f"call {i}: {1e3 * (time.perf_counter() - t):.2f} ms, launches {ctx.launches}, "
               f"achieved {int(np.sum(res.warm.sigma() > eps))}", flush=True)
-        for reg, name in ((0, "K1 W products"), (1, "EVD"), (2, "thin_qr")):
+        for reg, name in ((0, "K1 W products"), (1, "EVD"), (2, "thin_qr"), (5, "blws_svd")):
             st = ctx.region_stats(reg)
             print(f"   {name:14s} {st['ms']:8.3f} ms over {st['count']} calls", flush=True)
 
