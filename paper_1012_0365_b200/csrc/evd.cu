@@ -11,6 +11,8 @@
 //      eigenvector, no inter-warp synchronisation.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "ops.cuh"
@@ -364,12 +366,14 @@ bool ormtr_full(Context& ctx, const double* lp, const double* tau, int n, int wa
 
 }  // namespace
 
-bool sytrd_cluster(Context& ctx, View t, double* lp, double* d, double* e, double* tau);
+bool sytrd_cluster(Context& ctx, View t, double* lp, double* d, double* e, double* tau, bool auto_pick);
 bool sytrd_fused(Context& ctx, View t, double* lp, double* d, double* e, double* tau);
 
 void sym_evd_top(Context& ctx, View t, Index want, double* values, View vectors) {
     const int n = static_cast<int>(t.rows);
     if (n <= 0 || want <= 0) return;
+    static const bool trace = std::getenv("BLWS_EVD_TRACE") != nullptr;
+    if (trace) std::fprintf(stderr, "sym_evd_top n=%d want=%lld\n", n, static_cast<long long>(want));
     if (n == 1) {
         BLWS_CUDA(cudaMemcpyAsync(values, t.p, sizeof(double), cudaMemcpyDeviceToDevice, ctx.stream()));
         fill(ctx, vectors.left(1), 1.0);
@@ -387,8 +391,9 @@ void sym_evd_top(Context& ctx, View t, Index want, double* values, View vectors)
         cfg = true;
     }
     const int smem = static_cast<int>(head + (on_chip ? np * 8 : 0));
-    if (!sytrd_cluster(ctx, t, lp.get(), d.get(), e.get(), tau.get()) &&
-        !sytrd_fused(ctx, t, lp.get(), d.get(), e.get(), tau.get())) {
+    if (!sytrd_cluster(ctx, t, lp.get(), d.get(), e.get(), tau.get(), false) &&
+        !sytrd_fused(ctx, t, lp.get(), d.get(), e.get(), tau.get()) &&
+        !sytrd_cluster(ctx, t, lp.get(), d.get(), e.get(), tau.get(), true)) {
     if (on_chip)
         sytrd_k<true><<<1, kThreads, smem, ctx.stream()>>>(t.p, t.ld, n, lp.get(), d.get(), e.get(), tau.get());
     else

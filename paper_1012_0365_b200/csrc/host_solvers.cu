@@ -189,13 +189,26 @@ __global__ void e_counts_k(const double* E, long m, long n, long ld, double tol,
 /// rows held here (a row shard of a square RPCA problem, or all of it).
 __global__ void __launch_bounds__(gemm_detail::THREADS) alm_fused_k(const double* __restrict__ us, long ldu,
                                                                    const double* __restrict__ v, long ldv, long m,
-                                                                   long n, long r, const double* __restrict__ D, double* Y,
-                                                                   double* W, double* E, long ld, double mu,
+                                                                   long n, long r, const double* __restrict__ D,
+                                                                   double* __restrict__ Y, double* __restrict__ W,
+                                                                   double* __restrict__ E, long ld, double mu,
                                                                    double mu_next, double lambda_mu, double* partial,
                                                                    int* bad) {
     using namespace gemm_detail;
     extern __shared__ __align__(16) double smem[];
     const long m0 = static_cast<long>(blockIdx.x) * BM, n0 = static_cast<long>(blockIdx.y) * BN;
+    // The streamed operands of the epilogue (this tile's columns of D and Y)
+    // are pulled into L2 by bulk prefetches issued before the DMMA mainloop, so
+    // their HBM reads overlap the reconstruction instead of following it.
+    {
+        const int c = threadIdx.x & (BN - 1);
+        const long col = n0 + c;
+        if (col < n && (ld & 1) == 0) {
+            const double* base = (threadIdx.x < BN ? D : Y) + m0 + col * ld;
+            const unsigned bytes = static_cast<unsigned>(((min(static_cast<long>(BM), m - m0) * 8) + 15) & ~15L);
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(base), "r"(bytes) : "memory");
+        }
+    }
     double acc[4][4][2];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
@@ -212,6 +225,18 @@ __global__ void __launch_bounds__(gemm_detail::THREADS) alm_fused_k(const double
     for (int mi = 0; mi < 4; ++mi) {
         const long row = m0 + wm + mi * 8 + g;
         if (row >= m) continue;
+        // a row group's 8 D and 8 Y values are loaded before any store, so the
+        // loads are in flight together (one L2 round trip per row group)
+        double dv[4][2], yv[4][2];
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+            for (int e2 = 0; e2 < 2; ++e2) {
+                const long col = n0 + wn + ni * 8 + 2 * t + e2;
+                const long o = row + col * ld;
+                dv[ni][e2] = col < n ? D[o] : 0.0;
+                yv[ni][e2] = col < n ? Y[o] : 0.0;
+            }
 #pragma unroll
         for (int ni = 0; ni < 4; ++ni)
 #pragma unroll
@@ -220,8 +245,8 @@ __global__ void __launch_bounds__(gemm_detail::THREADS) alm_fused_k(const double
                 if (col >= n) continue;
                 const long o = row + col * ld;
                 const double a = acc[mi][ni][e2];
-                const double d = D[o];
-                const double y = Y[o];
+                const double d = dv[ni][e2];
+                const double y = yv[ni][e2];
                 const double dma = d - a;
                 const double e = shrink_d(dma + y * inv_mu, lambda_mu);
                 const double res = dma - e;

@@ -88,18 +88,22 @@ __device__ __forceinline__ void form_reflector(double* a, int n, int c, double s
     *tau_out = tk;
 }
 
-template <int QN>
+// PAIR (orders 209..224, where 16 per-warp row partials do not fit next to the
+// triangle): warps w and w + 8 combine their row partials through one extra
+// barrier, so the partial buffer holds 8 rows instead of 16.
+template <int QN, bool PAIR>
 __global__ void __launch_bounds__(kFT) sytrd_fused_k(const double* __restrict__ t, long ld, int n, double* lp,
                                                      double* d, double* e, double* tau) {
     constexpr int NP = 32 * QN;  // padded vector length (<= kFT)
     constexpr int CN = 2 * QN;   // column classes per warp
+    constexpr int PWN = PAIR ? kFW / 2 : kFW;
     extern __shared__ __align__(16) double sm[];
     double* vb = sm;             // 2 x NP: v_k by parity
-    double* wb = vb + 2 * NP;    // 2 x NP: w_k by parity
-    double* pcol = wb + 2 * NP;  // NP: column-dot part of p, then p
+    double* wb = vb + 2 * NP;    // NP: w_k (w_{k-1} is dead once the sweep of step k is done)
+    double* pcol = wb + NP;      // NP: column-dot part of p, then p
     double* red = pcol + NP;     // 64
-    double* pw = red + 64;       // kFW x NP: row part of p per warp
-    double* a = pw + kFW * NP;   // packed lower triangle
+    double* pw = red + 64;       // PWN x NP: row part of p per warp (pair)
+    double* a = pw + PWN * NP;   // packed lower triangle
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int row = threadIdx.x;  // [P] phases: one row per thread
 #ifdef SYTRD_PROBE
@@ -111,7 +115,7 @@ __global__ void __launch_bounds__(kFT) sytrd_fused_k(const double* __restrict__ 
 
     for (int j = wid; j < n; j += kFW)
         for (int i = j + lane; i < n; i += 32) a[floff(j, n) + (i - j)] = 0.5 * (t[i + j * ld] + t[j + i * ld]);
-    for (int i = threadIdx.x; i < 4 * NP; i += kFT) vb[i] = 0.0;  // vb and wb
+    for (int i = threadIdx.x; i < 3 * NP; i += kFT) vb[i] = 0.0;  // vb and wb
     __syncthreads();
     // prologue: reflector of column 0
     double tk;
@@ -130,8 +134,8 @@ __global__ void __launch_bounds__(kFT) sytrd_fused_k(const double* __restrict__ 
         const int par = k & 1;
         const double* v = vb + par * NP;         // v_k
         const double* vo = vb + (1 - par) * NP;  // v_{k-1}
-        const double* wo = wb + (1 - par) * NP;  // w_{k-1}
-        double* wn = wb + par * NP;              // w_k
+        const double* wo = wb;                   // w_{k-1}
+        double* wn = wb;                         // w_k (written after the sweep barrier)
         double* vn = vb + (1 - par) * NP;        // v_{k+1} (overwrites v_{k-1} after [S])
         // ---- [S] fused sweep: pending update k-1, then p = A22 v_k
         {
@@ -199,11 +203,23 @@ __global__ void __launch_bounds__(kFT) sytrd_fused_k(const double* __restrict__ 
             const int jj = wid + 16 * cc;
             if ((lane & 1) == 0 && cc < CN && jj > k && jj < n) pcol[jj] = r[0];
 #pragma unroll
-            for (int q = 0; q < QN; ++q) pw[wid * NP + lane + 32 * q] = acc[q];
-#pragma unroll
             for (int q = 0; q < QN; ++q) qv = fma(vr[q], acc[q], qv);  // lower half incl. the diagonal
             qv = warp_sum(qv);
             if (lane == 0) red[wid] = qv;  // per-warp share: K needs no separate reduction
+            if (!PAIR) {
+#pragma unroll
+                for (int q = 0; q < QN; ++q) pw[wid * NP + lane + 32 * q] = acc[q];
+            } else {
+                if (wid >= PWN) {
+#pragma unroll
+                    for (int q = 0; q < QN; ++q) pw[(wid - PWN) * NP + lane + 32 * q] = acc[q];
+                }
+                __syncthreads();
+                if (wid < PWN) {
+#pragma unroll
+                    for (int q = 0; q < QN; ++q) pw[wid * NP + lane + 32 * q] += acc[q];
+                }
+            }
         }
 #ifdef SYTRD_PROBE
         if (threadIdx.x == 0 && k < 256) s_sweep[k] = static_cast<unsigned>(clock64() - tp_);
@@ -222,7 +238,7 @@ __global__ void __launch_bounds__(kFT) sytrd_fused_k(const double* __restrict__ 
         if (row > k && row < n) {
             double sacc = pcol[row];
 #pragma unroll
-            for (int ww = 0; ww < kFW; ++ww) sacc += pw[ww * NP + row];
+            for (int ww = 0; ww < PWN; ++ww) sacc += pw[ww * NP + row];
             p = tk * sacc;
         }
         const double vi = row < NP ? v[row] : 0.0;
@@ -231,7 +247,7 @@ __global__ void __launch_bounds__(kFT) sytrd_fused_k(const double* __restrict__ 
         const int c1 = k + 1;
         double pc = pcol[c1];
 #pragma unroll
-        for (int ww = 0; ww < kFW; ++ww) pc += pw[ww * NP + c1];
+        for (int ww = 0; ww < PWN; ++ww) pc += pw[ww * NP + c1];
         const double vc = v[c1];
         const double wc = fma(-K, vc, tk * pc);  // w_{k+1}, identical in every thread
         double xi = 0.0;
@@ -261,7 +277,7 @@ __global__ void __launch_bounds__(kFT) sytrd_fused_k(const double* __restrict__ 
         double* c1 = a + floff(n - 1, n);  // c1[0] = A(n-1, n-1)
         if (kl >= 0) {
             const double* vl = vb + (kl & 1) * NP;
-            const double* wl = wb + (kl & 1) * NP;
+            const double* wl = wb;
             c1[0] -= fma(vl[n - 1], wl[n - 1], wl[n - 1] * vl[n - 1]);
         }
         d[n - 2] = c2[0];
@@ -279,25 +295,35 @@ __global__ void __launch_bounds__(kFT) sytrd_fused_k(const double* __restrict__ 
 #endif
 }
 
-template <int QN>
+constexpr size_t kFusedSmemMax = 226 * 1024;  // the 227 KB per-block opt-in limit less 1 KB static
+
+template <int QN, bool PAIR>
 size_t fused_smem(int n) {
     constexpr int NP = 32 * QN;
-    return (5L * NP + 64 + static_cast<long>(kFW) * NP + static_cast<long>(n) * (n + 1) / 2) * 8;
+    const long pwn = PAIR ? kFW / 2 : kFW;
+    return (4L * NP + 64 + pwn * NP + static_cast<long>(n) * (n + 1) / 2) * 8;
+}
+
+template <int QN, bool PAIR>
+bool launch_fused_v(Context& ctx, View t, int n, double* lp, double* d, double* e, double* tau) {
+    const size_t bytes = fused_smem<QN, PAIR>(n);
+    if (bytes > kFusedSmemMax) return false;
+    static bool cfg = false;
+    if (!cfg) {
+        BLWS_CUDA(cudaFuncSetAttribute(sytrd_fused_k<QN, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(kFusedSmemMax)));
+        cfg = true;
+    }
+    sytrd_fused_k<QN, PAIR><<<1, kFT, bytes, ctx.stream()>>>(t.p, t.ld, n, lp, d, e, tau);
+    ctx.note_launch();
+    ctx.check_launch("sytrd_fused_k");
+    return true;
 }
 
 template <int QN>
 bool launch_fused(Context& ctx, View t, int n, double* lp, double* d, double* e, double* tau) {
-    const size_t bytes = fused_smem<QN>(n);
-    if (bytes > 220u * 1024u) return false;
-    static bool cfg = false;
-    if (!cfg) {
-        BLWS_CUDA(cudaFuncSetAttribute(sytrd_fused_k<QN>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-        cfg = true;
-    }
-    sytrd_fused_k<QN><<<1, kFT, bytes, ctx.stream()>>>(t.p, t.ld, n, lp, d, e, tau);
-    ctx.note_launch();
-    ctx.check_launch("sytrd_fused_k");
-    return true;
+    if (fused_smem<QN, false>(n) <= kFusedSmemMax) return launch_fused_v<QN, false>(ctx, t, n, lp, d, e, tau);
+    return launch_fused_v<QN, true>(ctx, t, n, lp, d, e, tau);
 }
 
 }  // namespace

@@ -96,7 +96,7 @@ def test_sym_evd_known_answers(gpu):
         gpu.sym_evd_small(np.array([[0.0, 1.0], [5.0, 0.0]]))
 
 
-@pytest.mark.parametrize("n", [12, 61, 110, 200, 222, 260, 1900])  # 1900: global-memory back-transformation
+@pytest.mark.parametrize("n", [12, 61, 110, 200, 216, 222, 224, 230, 260, 810, 1056, 1900])  # 1900: global-memory back-transformation
 def test_sym_evd_matches_oracle(gpu, O, n):
     g = O.Rng(23 + n).gaussian_matrix(n, n)
     t = 0.5 * (g + g.T)

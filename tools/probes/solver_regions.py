@@ -11,9 +11,21 @@ import paper_1012_0365_b200 as B  # noqa: E402
 from paper_1012_0365_b200 import synth  # noqa: E402
 
 
-def main(m=2000, rank=100, frac=0.10):
+def main(m=2000, rank=100, frac=0.10, mc=False):
     ctx = B.Context(0)
-    if m > 8000:  # C5-size: D formed on the device (solve_configs.rpca_device), one profiled solve
+    if mc:  # C4-style MC: m x m, frac * m^2 observed, tol 1e-6
+        colptr, rowidx, vals, ml, mr = synth.mc_lowrank(m, rank, int(round(frac * m * m)), 1, B.Rng,
+                                                       B.sample_distinct)
+
+        def solve():
+            u, s_, v, st = B.mc_svt(m, m, colptr, rowidx, vals, B.SvdBackend.blws(seed=1 ^ 0x5BDBEEF, ctx=ctx),
+                                    tol_outer=1e-6, truth_ml=ml, truth_mr=mr, cap=512)
+            return u, s_, st, v
+
+        t = time.perf_counter()
+        solve()
+        print(f"MC m={m}: profiling off: {time.perf_counter() - t:.3f} s", flush=True)
+    elif m > 8000:  # C5-size: D formed on the device (solve_configs.rpca_device), one profiled solve
         import torch
 
         dt, a0t, _, _ = synth.rpca_lowrank_sparse_device(m, rank, int(round(frac * m * m)), 1, B.Rng,
@@ -46,4 +58,6 @@ def main(m=2000, rank=100, frac=0.10):
 
 
 if __name__ == "__main__":
-    main(*(int(x) if i < 2 else float(x) for i, x in enumerate(sys.argv[1:])))
+    mc = "--mc" in sys.argv
+    args = [a for a in sys.argv[1:] if a != "--mc"]
+    main(*(int(x) if i < 2 else float(x) for i, x in enumerate(args)), mc=mc)

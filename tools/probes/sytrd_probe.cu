@@ -25,8 +25,8 @@ int main() {
     cudaMalloc(&e, sizeof(double) * n);
     cudaMalloc(&tau, sizeof(double) * n);
     cudaMemcpy(dt, t.data(), sizeof(double) * n * n, cudaMemcpyHostToDevice);
-    const size_t bytes = blws::fused_smem<7>(n);
-    cudaFuncSetAttribute(blws::sytrd_fused_k<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    const size_t bytes = blws::fused_smem<7, false>(n);
+    cudaFuncSetAttribute(blws::sytrd_fused_k<7, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     for (int rep = 0; rep < 3; ++rep) {
         unsigned long long z[8] = {};
         cudaMemcpyToSymbol(g_sytrd_phase, z, sizeof(z));
@@ -34,7 +34,7 @@ int main() {
         cudaEventCreate(&a);
         cudaEventCreate(&b);
         cudaEventRecord(a);
-        blws::sytrd_fused_k<7><<<1, blws::kFT, bytes>>>(dt, n, n, lp, d, e, tau);
+        blws::sytrd_fused_k<7, false><<<1, blws::kFT, bytes>>>(dt, n, n, lp, d, e, tau);
         cudaEventRecord(b);
         cudaEventSynchronize(b);
         float ms = 0;
