@@ -304,6 +304,11 @@ bool try_ts(Context& ctx, const double* A, long lda, const double* B, long ldb, 
 
 }  // namespace
 
+// the 2D tensor map of the TMA GEMM, for other TMA-fed kernels (K7)
+bool tma_map_2d(CUtensorMap* map, const double* base, long inner, long outer, long ld, int box_outer) {
+    return tensor_map(map, base, inner, outer, ld, box_outer);
+}
+
 void gemm(Context& ctx, bool ta, bool tb, Index M, Index N, Index K, double alpha, const double* A, Index lda,
           const double* B, Index ldb, double beta, double* C, Index ldc) {
     if (M <= 0 || N <= 0) return;

@@ -2,12 +2,19 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <sstream>
 #include <stdexcept>
+#include <string>
 
 #include "dgemm.cuh"
+#include "dgemm_tma.cuh"
 #include "host.hpp"
 #include "ops.cuh"
+
+namespace blws {
+bool tma_map_2d(CUtensorMap* map, const double* base, long inner, long outer, long ld, int box_outer);
+}  // namespace blws
 
 namespace blws {
 
@@ -267,6 +274,171 @@ __global__ void __launch_bounds__(gemm_detail::THREADS) alm_fused_k(const double
     if (threadIdx.x == 0) partial[blockIdx.x + static_cast<long>(blockIdx.y) * gridDim.x] = (sh[0] + sh[1]) + (sh[2] + sh[3]);
 }
 
+// K7 with TMA-fed operands (the default; alm_fused_k above is the fallback for
+// unaligned panels). a = us v^T has both operands with the row index
+// contiguous, so both tiles are staged as [BK k][16 rows] boxes (128-byte
+// swizzle) by one producer warp into a 2-stage mbarrier ring, the consumers
+// read DMMA fragments with the conflict-free permuted-k addressing of the
+// tall-skinny GEMM (dgemm_tma.cuh), and run the ALM epilogue on their 16 x 64
+// sub-tile. D and Y of the tile are bulk-prefetched into L2 by the producer
+// before the first operand load, so the HBM stream of the epilogue overlaps
+// the DMMA work of the CTAs sharing the SM (3 per SM).
+namespace k7 {
+constexpr int CONS = 4, BM = 16 * CONS, BN = 64, BK = 32, STAGES = 2;
+constexpr int A_BYTES = BM * BK * 8, B_BYTES = BN * BK * 8, STAGE = A_BYTES + B_BYTES;
+constexpr int SMEM = STAGES * STAGE + 1024 + 2 * STAGES * 8;
+constexpr int THREADS = 32 * (CONS + 1);
+}  // namespace k7
+
+__global__ void __launch_bounds__(k7::THREADS, 3) alm_tma_k(const __grid_constant__ CUtensorMap tmU,
+                                                          const __grid_constant__ CUtensorMap tmV, long m, long n,
+                                                          long r, const double* __restrict__ D,
+                                                          double* __restrict__ Y, double* __restrict__ W,
+                                                          double* __restrict__ E, long ld, double mu, double mu_next,
+                                                          double lambda_mu, double* partial, int* bad) {
+    using namespace k7;
+    using namespace gemm_tma;
+    extern __shared__ __align__(1024) unsigned char smraw[];
+    unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(sm + STAGES * STAGE);
+    uint64_t* empty = full + STAGES;
+    __shared__ double sh[CONS];
+    __shared__ int shbad;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long m0 = static_cast<long>(blockIdx.x) * BM, n0 = static_cast<long>(blockIdx.y) * BN;
+    const int ntiles = static_cast<int>((r + BK - 1) / BK);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, CONS);
+        }
+        shbad = 0;
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == CONS) {
+        // ---- producer: L2 prefetch of the epilogue's D / Y columns, then the operand ring
+        if ((ld & 1) == 0) {
+            const unsigned bytes = static_cast<unsigned>(((min(static_cast<long>(BM), m - m0) * 8) + 15) & ~15L);
+            for (int c = lane; c < 2 * BN; c += 32) {
+                const long col = n0 + (c & (BN - 1));
+                if (col < n) {
+                    const double* base = (c < BN ? D : Y) + m0 + col * ld;
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(base), "r"(bytes) : "memory");
+                }
+            }
+        }
+        if (lane == 0) {
+            for (int kt = 0; kt < ntiles; ++kt) {
+                const int s = kt % STAGES;
+                mbar_wait(empty + s, ((kt / STAGES) & 1) ^ 1);
+                mbar_expect_tx(full + s, STAGE);
+                unsigned char* as = sm + s * STAGE;
+                unsigned char* bs = as + A_BYTES;
+                const int k0 = kt * BK;
+#pragma unroll
+                for (int q = 0; q < BM / 16; ++q) tma_2d(as + q * (BK * 128), &tmU, full + s, static_cast<int>(m0) + 16 * q, k0);
+#pragma unroll
+                for (int q = 0; q < BN / 16; ++q) tma_2d(bs + q * (BK * 128), &tmV, full + s, static_cast<int>(n0) + 16 * q, k0);
+            }
+        }
+        return;
+    }
+    // ---- consumers: warp w owns rows [16 w, 16 w + 16) x all 64 columns
+    const int g = lane >> 2, t = lane & 3;
+    const int wm = warp * 16;
+    int off[4][2];  // [k][16 rows] box offsets of rows (8 mi + g) at k-step s
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+        const int k = kperm_tab(s, t);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int rr = h * 8 + g;
+            off[s][h] = k * 128 + ((((rr >> 1) ^ (k & 7)) & 7) << 4) + (rr & 1) * 8;
+        }
+    }
+    double acc[2][BN / 8][2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < BN / 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int kt = 0; kt < ntiles; ++kt) {
+        const int s = kt % STAGES;
+        mbar_wait(full + s, (kt / STAGES) & 1);
+        const unsigned char* as = sm + s * STAGE + warp * (BK * 128);
+        const unsigned char* bs = sm + s * STAGE + A_BYTES;
+#pragma unroll
+        for (int kb = 0; kb < BK / 16; ++kb) {
+#pragma unroll
+            for (int st = 0; st < 4; ++st) {
+                double af[2];
+#pragma unroll
+                for (int mi = 0; mi < 2; ++mi)
+                    af[mi] = *reinterpret_cast<const double*>(as + kb * (16 * 128) + off[st][mi]);
+#pragma unroll
+                for (int ni = 0; ni < BN / 8; ++ni) {
+                    const double bf = *reinterpret_cast<const double*>(bs + (ni >> 1) * (BK * 128) + kb * (16 * 128) +
+                                                                       off[st][ni & 1]);
+                    gemm_detail::dmma(acc[0][ni], af[0], bf);
+                    gemm_detail::dmma(acc[1][ni], af[1], bf);
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + s);
+    }
+    double ss = 0.0;
+    int nonfinite = 0;
+    const double inv_mu = 1.0 / mu, inv_mu_next = 1.0 / mu_next;
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi) {
+        const long row = m0 + wm + mi * 8 + g;
+        if (row >= m) continue;
+#pragma unroll
+        for (int nh = 0; nh < BN / 8; nh += 4) {  // 4 column groups' D and Y loads in flight together
+            double dv[4][2], yv[4][2];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int e2 = 0; e2 < 2; ++e2) {
+                    const long col = n0 + (nh + q) * 8 + 2 * t + e2;
+                    const long o = row + col * ld;
+                    dv[q][e2] = col < n ? D[o] : 0.0;
+                    yv[q][e2] = col < n ? Y[o] : 0.0;
+                }
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int e2 = 0; e2 < 2; ++e2) {
+                    const long col = n0 + (nh + q) * 8 + 2 * t + e2;
+                    if (col >= n) continue;
+                    const long o = row + col * ld;
+                    const double a = acc[mi][nh + q][e2];
+                    const double d = dv[q][e2];
+                    const double y = yv[q][e2];
+                    const double dma = d - a;
+                    const double e = shrink_d(dma + y * inv_mu, lambda_mu);
+                    const double res = dma - e;
+                    const double yn = y + mu * res;
+                    const double w = (d - e) + yn * inv_mu_next;
+                    Y[o] = yn;
+                    E[o] = e;
+                    W[o] = w;
+                    ss += res * res;
+                    nonfinite |= !isfinite(w);
+                }
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if (lane == 0) sh[warp] = ss;
+    if (__any_sync(0xffffffffu, nonfinite) && lane == 0) shbad = 1;
+    asm volatile("bar.sync 1, %0;" ::"n"(CONS * 32) : "memory");  // consumers only (the producer has exited)
+    if (threadIdx.x == 0) {
+        partial[blockIdx.x + static_cast<long>(blockIdx.y) * gridDim.x] = (sh[0] + sh[1]) + (sh[2] + sh[3]);
+        if (shbad) atomicOr(bad, 1);
+    }
+}
+
 // K9: a_p = sum_c us[i,c] v[j,c] over CSC positions p (solvers.hpp:181-196, :247);
 // resid_p = obs_p - a_p; per-block partial ||resid||^2. A warp takes 32
 // consecutive positions; lanes run over the rank dimension, so every U / V row
@@ -488,6 +660,12 @@ SolverStats rpca_adm(Context& ctx, Index m, const double* d_in, Index ldd, doubl
     DBuf<double> part(ctx, static_cast<size_t>(grid.x) * grid.y);
     constexpr int smem = smem_bytes<false, true>();
     BLWS_CUDA(cudaFuncSetAttribute(alm_fused_k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    BLWS_CUDA(cudaFuncSetAttribute(alm_tma_k, cudaFuncAttributeMaxDynamicSharedMemorySize, k7::SMEM));
+    static_assert(k7::BM == BM && k7::BN == BN, "K7 variants share the tile grid and the partial layout");
+    const bool use_tma = [] {
+        const char* e = std::getenv("BLWS_K7");
+        return !(e && std::string(e) == "cpasync");
+    }();
     SvtResult prox;
     for (Index it = 1; it <= opts.max_iter; ++it) {
         int hbad = 0;
@@ -507,11 +685,21 @@ SolverStats rpca_adm(Context& ctx, Index m, const double* d_in, Index ldd, doubl
         if (r > 0) scale_columns(ctx, us.view().left(r), prox.trip.u(), prox.sigma_dev.get());
         const double mu_next = std::min(opts.rho * mu, mu_max);
         zero(ctx, bad.get(), sizeof(int));
-        alm_fused_k<<<grid, THREADS, smem, ctx.stream()>>>(us.data(), us.ld, prox.trip.v().p, prox.trip.uv.ld, rows, m,
-                                                           r, D.data(), Y.data(), Wm.data(), E.data(), ld, mu, mu_next,
-                                                           lambda / mu, part.get(), bad.get());
-        ctx.note_launch();
-        ctx.check_launch("alm_fused_k");
+        CUtensorMap tmu, tmv;
+        if (use_tma && r > 0 && tma_map_2d(&tmu, us.data(), rows, r, us.ld, k7::BK) &&
+            tma_map_2d(&tmv, prox.trip.v().p, m, r, prox.trip.uv.ld, k7::BK)) {
+            alm_tma_k<<<grid, k7::THREADS, k7::SMEM, ctx.stream()>>>(tmu, tmv, rows, m, r, D.data(), Y.data(),
+                                                                     Wm.data(), E.data(), ld, mu, mu_next, lambda / mu,
+                                                                     part.get(), bad.get());
+            ctx.note_launch();
+            ctx.check_launch("alm_tma_k");
+        } else {
+            alm_fused_k<<<grid, THREADS, smem, ctx.stream()>>>(us.data(), us.ld, prox.trip.v().p, prox.trip.uv.ld, rows,
+                                                               m, r, D.data(), Y.data(), Wm.data(), E.data(), ld, mu,
+                                                               mu_next, lambda / mu, part.get(), bad.get());
+            ctx.note_launch();
+            ctx.check_launch("alm_fused_k");
+        }
         mu = mu_next;
         stats.matvec_history.push_back(op.application_count() - mark);
         mark = op.application_count();
