@@ -25,41 +25,6 @@ namespace {
 // cluster the loss of orthogonality is <= eps ||T|| / gap <= 2e-11).
 constexpr double kClusterTol = 1e-5;
 
-// Number of eigenvalues < x: sign changes of the Sturm sequence
-// p_i = det(T_i - x I) = (d_i - x) p_{i-1} - e_{i-1}^2 p_{i-2}, evaluated
-// division-free (a dependent FMA per step instead of a ~130-cycle divide) on T
-// scaled by an exact power of two s with ||sT||_1 <= 1, so |p| grows at most
-// 3x per step. Inputs (shared memory): ds = s d, e2s = (s e)^2, or -1 where
-// (s e)^2 < 2^-200, which splits T (the recurrence restarts; an eigenvalue
-// perturbation <= 2^-100 ||T||). A zero p_i becomes -2^-200 p_{i-1} (dstebz's
-// -pivmin pivot, in scaled units). Every 4 steps the pair is renormalised by an
-// exact power of two; per step max(|p_i|, |p_{i+1}|) >= (e^2 / 4) max(|p_{i-1}|,
-// |p_i|) >= 2^-202 of it, so nothing reaches the subnormal range in between.
-__device__ __forceinline__ int sturm_count(const double* ds, const double* e2s, int n, double xs) {
-    constexpr double kRepl = 0x1p-200;
-    double p0 = 1.0, p1 = ds[0] - xs;
-    p1 = p1 == 0.0 ? -kRepl : p1;
-    int cnt = p1 < 0.0;
-#pragma unroll 4
-    for (int i = 1; i < n; ++i) {
-        const double e2 = e2s[i - 1];
-        const double p1s = e2 < 0.0 ? 1.0 : p1;
-        double p2 = fma(ds[i] - xs, p1s, -fmax(e2, 0.0) * p0);
-        p2 = p2 == 0.0 ? -kRepl * p1s : p2;
-        cnt += (p2 < 0.0) != (p1s < 0.0);
-        p0 = p1s;
-        p1 = p2;
-        if ((i & 3) == 0) {
-            // renormalise (p0, p1) so the larger magnitude is in [1, 2)
-            const int ex = (__double2hiint(fmax(fabs(p0), fabs(p1))) >> 20) & 0x7ff;
-            const double sc = __hiloint2double((2046 - ex) << 20, 0);  // 2^(1023 - ex)
-            p0 *= sc;
-            p1 *= sc;
-        }
-    }
-    return cnt;
-}
-
 // Bisection interval, pivmin and ||T||_1 (dstebz's Gershgorin set-up), on the
 // device so the eigensolver needs no host round trip. params: gl, gu, pivmin,
 // onenrm (0 => T == 0), the power-of-two scale 2^-E >= 1 / ||T||_1.
@@ -110,15 +75,82 @@ __global__ void __launch_bounds__(kBoundsThreads) tridiag_bounds_k(const double*
     }
 }
 
-// one warp per wanted eigenvalue; j-th largest = ascending index n-1-j
+// Number of eigenvalues < x: sign changes of the Sturm sequence
+// p_i = det(T_i - x I) = (d_i - x) p_{i-1} - e_{i-1}^2 p_{i-2}, evaluated
+// division-free (a dependent FMA per step instead of a ~130-cycle divide) on T
+// scaled by an exact power of two s with ||sT||_1 <= 1, so |p| grows at most
+// 3x per step. Inputs (shared memory): ds = s d, e2s = (s e)^2, or -1 where
+// (s e)^2 < 2^-200, which splits T (the recurrence restarts; an eigenvalue
+// perturbation <= 2^-100 ||T||). A zero p_i becomes -2^-200 p_{i-1} (dstebz's
+// -pivmin pivot, in scaled units). Every 4 steps the pair is renormalised by an
+// exact power of two; per step max(|p_i|, |p_{i+1}|) >= (e^2 / 4) max(|p_{i-1}|,
+// |p_i|) >= 2^-202 of it, so nothing reaches the subnormal range in between.
+// Sturm counts at P shifts at once: P independent
+// chains interleaved -- one chain is latency-bound -- sharing the loads of
+// (ds, e2s).
+template <int P>
+__device__ __forceinline__ void sturm_count_multi(const double* ds, const double* e2s, int n, const double (&xs)[P],
+                                                  int (&cnt)[P]) {
+    constexpr double kRepl = 0x1p-200;
+    double p0[P], p1[P];
+    const double d0 = ds[0];
+#pragma unroll
+    for (int q = 0; q < P; ++q) {
+        p0[q] = 1.0;
+        const double t = d0 - xs[q];
+        p1[q] = t == 0.0 ? -kRepl : t;
+        cnt[q] = p1[q] < 0.0;
+    }
+#pragma unroll 4
+    for (int i = 1; i < n; ++i) {
+        const double e2 = e2s[i - 1], di = ds[i];
+        const bool split = e2 < 0.0;
+        const double me2 = -fmax(e2, 0.0);
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+            const double p1s = split ? 1.0 : p1[q];
+            double p2 = fma(di - xs[q], p1s, me2 * p0[q]);
+            p2 = p2 == 0.0 ? -kRepl * p1s : p2;
+            // sign change of two nonzero values: the sign bits differ (integer
+            // pipe; the FP64 pipe is the bottleneck of this loop)
+            cnt[q] += static_cast<unsigned>(__double2hiint(p2) ^ __double2hiint(p1s)) >> 31;
+            p0[q] = p1s;
+            p1[q] = p2;
+        }
+        if ((i & 3) == 0) {
+#pragma unroll
+            for (int q = 0; q < P; ++q) {
+                // renormalise (p0, p1) so the larger magnitude is in [1, 2): the
+                // larger exponent field of the two, by integer max
+                const int e0 = (__double2hiint(p0[q]) >> 20) & 0x7ff, e1 = (__double2hiint(p1[q]) >> 20) & 0x7ff;
+                const int ex = max(e0, e1);
+                const double sc = __hiloint2double((2046 - ex) << 20, 0);
+                p0[q] *= sc;
+                p1[q] *= sc;
+            }
+        }
+    }
+}
+
+// One block of kBisThreads per wanted eigenvalue (j-th largest = ascending
+// index n-1-j), kBisPts-way multisection per round: every thread evaluates
+// kBisP shifts, the first shift whose count exceeds the index is found by a
+// block min, and [lo, hi] shrinks by kBisPts + 1 per round (8 rounds from the
+// Gershgorin interval to the dstebz tolerance, against 11 for the former
+// 32-way one-warp search). The loop is bound by the FP64 pipe of the SMSP
+// running it, so the block's 4 warps (one per SMSP) each run one chain: 4
+// interleaved chains per thread (512-way, 6 rounds) measured slower (140 vs
+// 118 us at C2). LAPACK dstebz semantics, pivmin safeguard.
+constexpr int kBisThreads = 128, kBisP = 1, kBisPts = kBisThreads * kBisP;
 template <bool SH>
-__global__ void bisect_k(const double* __restrict__ d, const double* __restrict__ e, int n, int want,
-                         const double* __restrict__ params, double* values, double* gscratch) {
-    const int warps = (gridDim.x * blockDim.x) >> 5;
-    const int lane = threadIdx.x & 31;
+__global__ void __launch_bounds__(kBisThreads) bisect_k(const double* __restrict__ d, const double* __restrict__ e,
+                                                         int n, int want, const double* __restrict__ params,
+                                                         double* values, double* gscratch) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const double gl = params[0], gu = params[1], pivmin = params[2], scale = params[4];
     const bool zero = params[3] == 0.0;
     extern __shared__ __align__(16) double tsm[];
+    __shared__ int sfirst[2][kBisThreads / 32];
     double* ds = SH ? tsm : gscratch + 2L * n * blockIdx.x;  // n: s d
     double* e2s = ds + n;                                    // n: (s e)^2, -1 marks a split
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
@@ -130,34 +162,48 @@ __global__ void bisect_k(const double* __restrict__ d, const double* __restrict_
         }
     }
     __syncthreads();
-    for (int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < want; j += warps) {
+    for (int j = blockIdx.x; j < want; j += gridDim.x) {
         if (zero) {  // T == 0: eigenvalues exactly zero
-            if (lane == 0) values[j] = 0.0;
+            if (threadIdx.x == 0) values[j] = 0.0;
             continue;
         }
         const int k = n - 1 - j;  // want lambda_k (ascending): count(lo) <= k < count(hi)
         double lo = gl, hi = gu;
-        for (int it = 0; it < 40; ++it) {
+        for (int it = 0; it < 16; ++it) {
             const double w = hi - lo;
             const double tol = 2.0 * 2.220446049250313e-16 * fmax(fabs(lo), fabs(hi)) + 2.0 * pivmin;
-            if (w <= tol) break;
-            const double x = lo + w * static_cast<double>(lane + 1) / 33.0;
-            const int c = sturm_count(ds, e2s, n, x * scale);
-            const unsigned above = __ballot_sync(0xffffffffu, c >= k + 1);
-            if (above == 0u) {
-                lo = __shfl_sync(0xffffffffu, x, 31);
+            if (w <= tol) break;  // block-uniform
+            double xs[kBisP];
+            int c[kBisP];
+#pragma unroll
+            for (int q = 0; q < kBisP; ++q) {
+                const int idx = threadIdx.x * kBisP + q;
+                xs[q] = (lo + w * static_cast<double>(idx + 1) / static_cast<double>(kBisPts + 1)) * scale;
+            }
+            sturm_count_multi<kBisP>(ds, e2s, n, xs, c);
+            int first = kBisPts;
+#pragma unroll
+            for (int q = kBisP - 1; q >= 0; --q)
+                if (c[q] >= k + 1) first = threadIdx.x * kBisP + q;
+            first = __reduce_min_sync(0xffffffffu, first);
+            if (lane == 0) sfirst[it & 1][wid] = first;
+            __syncthreads();  // the other parity slot is free: one barrier per round
+#pragma unroll
+            for (int ww = 0; ww < kBisThreads / 32; ++ww) first = min(first, sfirst[it & 1][ww]);
+            auto xat = [&](int idx) { return lo + w * static_cast<double>(idx + 1) / static_cast<double>(kBisPts + 1); };
+            if (first == kBisPts) {
+                lo = xat(kBisPts - 1);
             } else {
-                const int l = __ffs(above) - 1;
-                const double xh = __shfl_sync(0xffffffffu, x, l);
-                const double xl = __shfl_sync(0xffffffffu, x, l > 0 ? l - 1 : 0);
-                if (l > 0) lo = xl;
+                const double xh = xat(first);
+                if (first > 0) lo = xat(first - 1);
                 hi = xh;
             }
         }
-        if (lane == 0) {
+        if (threadIdx.x == 0) {
             const double lam = 0.5 * (lo + hi);
             values[j] = fabs(lam) <= 4.0 * pivmin ? 0.0 : lam;
         }
+        __syncthreads();
     }
 }
 
@@ -349,10 +395,10 @@ void tridiag_eig_top(Context& ctx, Index n_, const double* d, const double* e, I
     DBuf<double> gscratch;
     if (!small) gscratch = DBuf<double>(ctx, static_cast<size_t>(want) * 9 * n);
     if (small)
-        bisect_k<true><<<static_cast<unsigned>(want), 32, 2 * n * sizeof(double), ctx.stream()>>>(
+        bisect_k<true><<<static_cast<unsigned>(want), kBisThreads, 2 * n * sizeof(double), ctx.stream()>>>(
             d, e, n, want, params.get(), values, nullptr);
     else
-        bisect_k<false><<<static_cast<unsigned>(want), 32, 0, ctx.stream()>>>(d, e, n, want, params.get(), values,
+        bisect_k<false><<<static_cast<unsigned>(want), kBisThreads, 0, ctx.stream()>>>(d, e, n, want, params.get(), values,
                                                                              gscratch.get());
     ctx.note_launch();
     ctx.check_launch("bisect_k");
