@@ -127,6 +127,17 @@ def lib():
     if _lib is None:
         if not os.path.exists(LIB_PATH):
             raise ImportError(f"{LIB_PATH} missing: run paper_1012_0365_b200/build.py (no CPU fallback exists)")
+        if "BLWS_NCCL_LIB" not in os.environ:
+            # the NCCL torch bundles (nvidia-nccl wheel), found without importing
+            # torch: comm.cu dlopens it in preference to the system libnccl
+            import importlib.util
+
+            spec = importlib.util.find_spec("nvidia")
+            for root in list(spec.submodule_search_locations or []) if spec else []:
+                cand = os.path.join(root, "nccl", "lib", "libnccl.so.2")
+                if os.path.exists(cand):
+                    os.environ["BLWS_NCCL_LIB"] = cand
+                    break
         L = C.CDLL(LIB_PATH)
         for name, (res, args) in SIGNATURES.items():
             f = getattr(L, name)

@@ -3,6 +3,8 @@
 // process per GPU; torch's bundled libnccl.so.2 is picked up when torch is
 // already loaded, else the system one).
 #include <dlfcn.h>
+
+#include <cstdlib>
 #include <nccl.h>
 
 #include <cstring>
@@ -28,7 +30,13 @@ const NcclApi& nccl() {
     static std::once_flag once;
     static std::string err;
     std::call_once(once, [] {
-        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        // BLWS_NCCL_LIB (set by the Python package to the NCCL that torch
+        // bundles): loading the system libnccl first would shadow it, and a
+        // later `import torch` in the same process then fails on symbols only
+        // the bundled version has
+        void* h = nullptr;
+        if (const char* lib = std::getenv("BLWS_NCCL_LIB")) h = dlopen(lib, RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
         if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
         if (!h) {
             err = std::string("NCCL not found: ") + dlerror();

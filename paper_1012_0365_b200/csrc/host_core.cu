@@ -76,16 +76,47 @@ __global__ void nonfinite_count_k(const double* x, long rows, long cols, long ld
     if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
 }
 
-// warp per row SpMV: y[i] = sum_p val[p] x[col[p]]
-__global__ void csr_spmv_k(long rows, const std::int64_t* __restrict__ ptr, const std::int32_t* __restrict__ idx,
-                           const double* __restrict__ val, const double* __restrict__ x, double* y) {
+// Paired SpMV of the sparse Lanczos apply (one launch for W x over the CSR
+// rows and W^T y over the CSC columns; warps [0, rows_a) take the first,
+// the rest the second): warp per row, y[i] = sum_p val[p] x[col[p]]. Each
+// lane keeps 4 nonzeros in flight (index loads, then the gathers, then the
+// FMAs) so a row's ~1000 nonzeros are not one dependent load chain.
+__device__ __forceinline__ double spmv_row(long b, long e, const std::int32_t* __restrict__ idx,
+                                           const double* __restrict__ val, const double* __restrict__ x, int lane) {
+    double s0 = 0.0, s1 = 0.0;
+    long p = b + lane;
+    for (; p + 96 < e; p += 128) {
+        const int c0 = idx[p], c1 = idx[p + 32], c2 = idx[p + 64], c3 = idx[p + 96];
+        const double v0 = val[p], v1 = val[p + 32], v2 = val[p + 64], v3 = val[p + 96];
+        const double x0 = x[c0], x1 = x[c1], x2 = x[c2], x3 = x[c3];
+        s0 = fma(v0, x0, s0);
+        s1 = fma(v1, x1, s1);
+        s0 = fma(v2, x2, s0);
+        s1 = fma(v3, x3, s1);
+    }
+    for (; p < e; p += 32) s0 = fma(val[p], x[idx[p]], s0);
+    double s = s0 + s1;
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    return s;
+}
+
+__global__ void csr_spmv_pair_k(long rows_a, const std::int64_t* __restrict__ ptr_a,
+                                const std::int32_t* __restrict__ idx_a, const double* __restrict__ val_a,
+                                const double* __restrict__ x_a, double* y_a, long rows_b,
+                                const std::int64_t* __restrict__ ptr_b, const std::int32_t* __restrict__ idx_b,
+                                const double* __restrict__ val_b, const double* __restrict__ x_b, double* y_b) {
     const long warps = (static_cast<long>(gridDim.x) * blockDim.x) >> 5;
     const int lane = threadIdx.x & 31;
-    for (long i = (blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x) >> 5; i < rows; i += warps) {
-        double s = 0.0;
-        for (long p = ptr[i] + lane; p < ptr[i + 1]; p += 32) s += val[p] * x[idx[p]];
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (lane == 0) y[i] = s;
+    for (long w = (blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x) >> 5; w < rows_a + rows_b;
+         w += warps) {
+        if (w < rows_a) {
+            const double s = spmv_row(ptr_a[w], ptr_a[w + 1], idx_a, val_a, x_a, lane);
+            if (lane == 0) y_a[w] = s;
+        } else {
+            const long i = w - rows_a;
+            const double s = spmv_row(ptr_b[i], ptr_b[i + 1], idx_b, val_b, x_b, lane);
+            if (lane == 0) y_b[i] = s;
+        }
     }
 }
 
@@ -383,13 +414,11 @@ void SparseOperator::pair_block_impl(View left, View right, View top, View bot) 
 }
 
 void SparseOperator::pair_impl(const double* left, const double* right, double* top, double* bot) {
-    csr_spmv_k<<<gridn(m_ * 32, 8192), kT, 0, ctx_.stream()>>>(m_, rowptr_.get(), colidx_.get(), val_csr_.get(),
-                                                                right, top);
+    csr_spmv_pair_k<<<gridn((m_ + n_) * 32, 8192), kT, 0, ctx_.stream()>>>(
+        m_, rowptr_.get(), colidx_.get(), val_csr_.get(), right, top, n_, colptr_.get(), rowidx_.get(),
+        val_csc_.get(), left, bot);
     ctx_.note_launch();
-    csr_spmv_k<<<gridn(n_ * 32, 8192), kT, 0, ctx_.stream()>>>(n_, colptr_.get(), rowidx_.get(), val_csc_.get(),
-                                                                left, bot);
-    ctx_.note_launch();
-    ctx_.check_launch("csr_spmv");
+    ctx_.check_launch("csr_spmv_pair");
     if (row_sharded() && ctx_.has_comm()) ctx_.allreduce_sum(bot, static_cast<size_t>(n_));  // W^T left over the ranks
 }
 
