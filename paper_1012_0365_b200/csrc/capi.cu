@@ -139,7 +139,7 @@ int blws_context_set_profiling(blws_context* ctx, int on) {
 int blws_context_region_stats(blws_context* ctx, int region, double* total_ms, int64_t* count, double* flops,
                               double* bytes) {
     return guard([&] {
-        need(region >= 0 && region < 8, "region out of range");
+        need(region >= 0 && region < Context::kRegions, "region out of range");
         ctx->ctx->region_stats(region, total_ms, count, flops, bytes);
     });
 }

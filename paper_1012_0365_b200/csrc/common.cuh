@@ -47,6 +47,9 @@ inline Index ceil_div(Index x, Index a) { return (x + a - 1) / a; }
 /// and a counter of kernel launches issued through it.
 class Context {
 public:
+    // region timers: 0 K1, 1 EVD of T, 2 thin_qr, 3 Lanczos reseed, 4 Ritz checkpoints,
+    // 5 blws_svd, 6 svt, 7 MC loop outside svt, 8 solver set-up, 9 solver epilogue
+    static constexpr int kRegions = 10;
     explicit Context(int device);
     ~Context();
     Context(const Context&) = delete;
@@ -124,11 +127,11 @@ private:
         double flops = 0, bytes = 0, ms = 0;
         std::int64_t count = 0;
     };
-    Region regions_[8];
+    Region regions_[kRegions];
     bool capturing_ = false;
     std::uint64_t* stamps_ = nullptr;
     int nstamps_ = 0, stamp_cap_ = 0;
-    int open_[8] = {};
+    int open_[kRegions] = {};
     std::vector<CapturedRegion> captured_;
     void stamp(int idx);
     void ensure_pinned(size_t bytes);

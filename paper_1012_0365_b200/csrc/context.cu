@@ -34,6 +34,7 @@ void Context::stamp(int idx) {
 }
 
 void Context::region_begin(int id) {
+    if (id < 0 || id >= kRegions) throw std::logic_error("region id out of range");
     if (capturing_) {
         if (!profiling_) return;
         open_[id] = nstamps_++;
@@ -48,6 +49,7 @@ void Context::region_begin(int id) {
 }
 
 void Context::region_end(int id, double flops, double bytes) {
+    if (id < 0 || id >= kRegions) throw std::logic_error("region id out of range");
     if (capturing_) {
         if (!profiling_) return;
         const int e = nstamps_++;

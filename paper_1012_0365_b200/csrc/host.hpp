@@ -341,4 +341,17 @@ McSolution mc_svt(Context& ctx, Index m, Index n, Index nnz, const std::int64_t*
                   const double* truth_ml, const double* truth_mr, Index r_true, const RowShard* shard = nullptr,
                   Index rows = 0);
 
+// region timer scope (Context::region_begin / region_end; a no-op unless profiling)
+struct RegionGuard {
+    Context& ctx;
+    int id;
+    RegionGuard(Context& c, int i) : ctx(c), id(i) { ctx.region_begin(id); }
+    ~RegionGuard() {
+        try {
+            ctx.region_end(id, 0.0, 0.0);
+        } catch (...) {
+        }
+    }
+};
+
 }  // namespace blws

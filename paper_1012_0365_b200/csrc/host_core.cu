@@ -222,17 +222,7 @@ void share_flag(Context& ctx, const int* flag, double* dst) {
 
 // region timing for whole calls (regions 3: Lanczos reseed, 4: Ritz checkpoint,
 // 5: blws_svd) -- host-side event records, also around graph launches
-struct RegionGuard {
-    Context& ctx;
-    int id;
-    RegionGuard(Context& c, int i) : ctx(c), id(i) { ctx.region_begin(id); }
-    ~RegionGuard() {
-        try {
-            ctx.region_end(id, 0.0, 0.0);
-        } catch (...) {
-        }
-    }
-};
+
 
 // ======================================================== row sharding
 void LinearOperator::set_row_shard(Index m_total, Index row0) {
@@ -341,39 +331,33 @@ void DenseOperator::pair_impl(const double* left, const double* right, double* t
 SparseOperator::SparseOperator(Context& ctx, Index m, Index n, Index nnz, const std::int64_t* colptr,
                                const std::int32_t* rowidx, const double* values)
     : LinearOperator(ctx), m_(m), n_(n), nnz_(nnz) {
-    for (Index i = 0; i < nnz; ++i)
-        if (!std::isfinite(values[i])) throw std::invalid_argument("SparseOperator: non-finite entries");
-    // CSC -> CSR with the position permutation
-    std::vector<std::int64_t> rowptr(static_cast<size_t>(m + 1), 0), perm(static_cast<size_t>(nnz));
-    std::vector<std::int32_t> colidx(static_cast<size_t>(nnz)), colof(static_cast<size_t>(nnz));
-    for (Index p = 0; p < nnz; ++p) ++rowptr[static_cast<size_t>(rowidx[p]) + 1];
-    for (Index i = 0; i < m; ++i) rowptr[i + 1] += rowptr[i];
-    std::vector<std::int64_t> next(rowptr.begin(), rowptr.end() - 1);
-    for (Index j = 0; j < n; ++j)
-        for (std::int64_t p = colptr[j]; p < colptr[j + 1]; ++p) {
-            const std::int64_t q = next[static_cast<size_t>(rowidx[p])]++;
-            colidx[static_cast<size_t>(q)] = static_cast<std::int32_t>(j);
-            perm[static_cast<size_t>(q)] = p;
-            colof[static_cast<size_t>(p)] = static_cast<std::int32_t>(j);
-        }
-    auto up64 = [&](DBuf<std::int64_t>& d, const std::int64_t* h, size_t c) {
-        d = DBuf<std::int64_t>(ctx, std::max<size_t>(c, 1));
-        BLWS_CUDA(cudaMemcpyAsync(d.get(), h, sizeof(std::int64_t) * c, cudaMemcpyHostToDevice, ctx.stream()));
-    };
-    auto up32 = [&](DBuf<std::int32_t>& d, const std::int32_t* h, size_t c) {
-        d = DBuf<std::int32_t>(ctx, std::max<size_t>(c, 1));
-        BLWS_CUDA(cudaMemcpyAsync(d.get(), h, sizeof(std::int32_t) * c, cudaMemcpyHostToDevice, ctx.stream()));
-    };
-    up64(rowptr_, rowptr.data(), rowptr.size());
-    up64(colptr_, colptr, static_cast<size_t>(n + 1));
-    up64(perm_, perm.data(), perm.size());
-    up32(colidx_, colidx.data(), colidx.size());
-    up32(rowidx_, rowidx, static_cast<size_t>(nnz));
-    up32(colof_, colof.data(), colof.size());
-    val_csr_ = DBuf<double>(ctx, std::max<size_t>(nnz, 1));
-    val_csc_ = DBuf<double>(ctx, std::max<size_t>(nnz, 1));
+    // The CSC arrays are uploaded as given; the CSR view and the CSC -> CSR
+    // position permutation are built on the device: a stable radix sort of the
+    // positions by row (equal rows keep CSC = column order, the order of the
+    // reference-order host transpose), a row histogram and its exclusive scan.
+    // (Host-side, the random-scatter transpose of 10^7 entries took ~0.2 s of
+    // the C4 solve.)
+    const size_t nz = static_cast<size_t>(std::max<Index>(nnz, 1));
+    colptr_ = DBuf<std::int64_t>(ctx, static_cast<size_t>(n + 1));
+    rowidx_ = DBuf<std::int32_t>(ctx, nz);
+    val_csc_ = DBuf<double>(ctx, nz);
+    val_csr_ = DBuf<double>(ctx, nz);
+    rowptr_ = DBuf<std::int64_t>(ctx, static_cast<size_t>(m + 1));
+    perm_ = DBuf<std::int64_t>(ctx, nz);
+    colidx_ = DBuf<std::int32_t>(ctx, nz);
+    colof_ = DBuf<std::int32_t>(ctx, nz);
+    BLWS_CUDA(cudaMemcpyAsync(colptr_.get(), colptr, sizeof(std::int64_t) * (n + 1), cudaMemcpyHostToDevice,
+                              ctx.stream()));
+    if (nnz > 0) {
+        BLWS_CUDA(cudaMemcpyAsync(rowidx_.get(), rowidx, sizeof(std::int32_t) * nnz, cudaMemcpyHostToDevice,
+                                  ctx.stream()));
+        BLWS_CUDA(cudaMemcpyAsync(val_csc_.get(), values, sizeof(double) * nnz, cudaMemcpyHostToDevice,
+                                  ctx.stream()));
+    }
+    build_csr_device(ctx, m, n, nnz, colptr_.get(), rowidx_.get(), val_csc_.get(), rowptr_.get(), colidx_.get(),
+                     perm_.get(), colof_.get());
+    gather_values(ctx, nnz_, val_csr_.get(), val_csc_.get(), perm_.get());
     ctx.sync();
-    assign_values_host(values);
 }
 
 void SparseOperator::assign_values_host(const double* vals) {

@@ -3,6 +3,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
+#include <optional>
 #include <sstream>
 #include <stdexcept>
 #include <string>
@@ -82,6 +83,7 @@ SvdBackend::Triplets SvdBackend::compute(LinearOperator& w, Index r) {
 SvtResult svt(LinearOperator& w, double eps, SvdBackend& backend, RankPredictor& predictor) {
     if (eps < 0.0) throw std::invalid_argument("svt: negative threshold");
     Context& ctx = w.ctx();
+    RegionGuard region(ctx, 6);
     const Index p = std::min(global_rows(w), w.cols());
     Index r = std::clamp<Index>(predictor.r, 1, p);
     SvdBackend::Triplets t;
@@ -578,6 +580,7 @@ SolverStats rpca_adm(Context& ctx, Index m, const double* d_in, Index ldd, doubl
                      const RpcaOptions& opts, const double* truth, double* a_out, double* e_out, const RowShard* shard,
                      Index rows_in) {
     const auto t0 = std::chrono::steady_clock::now();
+    std::optional<RegionGuard> phase(std::in_place, ctx, 8);  // set-up, then (9) the epilogue
     SolverStats stats;
     const bool sharded = shard != nullptr;
     if (sharded && (shard->m_total != m || rows_in < 1 || shard->row0 < 0 || shard->row0 + rows_in > m))
@@ -667,6 +670,7 @@ SolverStats rpca_adm(Context& ctx, Index m, const double* d_in, Index ldd, doubl
         return !(e && std::string(e) == "cpasync");
     }();
     SvtResult prox;
+    phase.reset();
     for (Index it = 1; it <= opts.max_iter; ++it) {
         int hbad = 0;
         BLWS_CUDA(cudaMemcpyAsync(&hbad, bad.get(), sizeof(int), cudaMemcpyDeviceToHost, ctx.stream()));
@@ -714,6 +718,7 @@ SolverStats rpca_adm(Context& ctx, Index m, const double* d_in, Index ldd, doubl
             break;
         }
     }
+    phase.emplace(ctx, 9);
     // A = U diag(s) V^T of the last prox; E, e_l0, rel_err
     const Index r = prox.achieved_rank;
     DMat A(ctx, rows, m, false);
@@ -770,6 +775,7 @@ McSolution mc_svt(Context& ctx, Index m, Index n, Index nnz, const std::int64_t*
                   const double* vals, double tau_in, double delta_in, SvdBackend& backend, const McOptions& opts,
                   const double* truth_ml, const double* truth_mr, Index r_true, const RowShard* shard, Index rows_in) {
     const auto t0 = std::chrono::steady_clock::now();
+    std::optional<RegionGuard> phase(std::in_place, ctx, 8);  // set-up, then (9) the epilogue
     const bool sharded = shard != nullptr;
     if (sharded && (shard->m_total != m || rows_in < 1 || shard->row0 < 0 || shard->row0 + rows_in > m))
         throw std::invalid_argument("mc_svt: bad row shard");
@@ -824,9 +830,13 @@ McSolution mc_svt(Context& ctx, Index m, Index n, Index nnz, const std::int64_t*
     std::int64_t mark = stats.matvec_init;
     const unsigned blocks = gridn(std::max<Index>(nnz, 1), 2048);
     DBuf<double> part(ctx, blocks);
+    phase.reset();
     for (Index it = 1; it <= opts.max_iter; ++it) {
+        ctx.region_begin(7);
         op.assign_values_device(y.get());
+        ctx.region_end(7, 0.0, 0.0);
         SvtResult prox = svt(op, tau, backend, predictor);
+        ctx.region_begin(7);
         stats.rank_hat = prox.achieved_rank;
         const Index r = prox.achieved_rank;
         DBuf<double> ust(ctx, static_cast<size_t>(std::max<Index>(rows * r, 1))),
@@ -865,6 +875,7 @@ McSolution mc_svt(Context& ctx, Index m, Index n, Index nnz, const std::int64_t*
         stats.residual_history.push_back(rel);
         stats.iterations = it;
         if (rel <= opts.tol_outer) {
+            ctx.region_end(7, 0.0, 0.0);
             stats.converged = true;
             break;
         }
@@ -872,7 +883,9 @@ McSolution mc_svt(Context& ctx, Index m, Index n, Index nnz, const std::int64_t*
             vec_axpy_k<<<gridn(nnz), kT, 0, ctx.stream()>>>(nnz, y.get(), resid.get(), delta);
             ctx.note_launch();
         }
+        ctx.region_end(7, 0.0, 0.0);
     }
+    phase.emplace(ctx, 9);
     stats.matvec_count = op.application_count();
     stats.predicted_ranks = predictor.history;
     if (truth_ml && truth_mr && r_true > 0) {

@@ -97,6 +97,12 @@ void dot(Context& ctx, Index n, const double* x, const double* y, double* out);
 void csr_spmm(Context& ctx, Index rows, const std::int64_t* rowptr, const std::int32_t* colidx,
               const double* val, Index ncols, Index b, const double* X, Index ldx, double* Y, Index ldy,
               double* xt);
+/// CSR view of a CSC pattern on the device (csr_build.cu): rowptr (m + 1),
+/// colidx and perm (CSR slot -> CSC position) in column order within a row,
+/// colof (column of each CSC position); throws on bad row indices / non-finite values
+void build_csr_device(Context& ctx, Index m, Index n, Index nnz, const std::int64_t* colptr,
+                      const std::int32_t* rowidx, const double* val, std::int64_t* rowptr, std::int32_t* colidx,
+                      std::int64_t* perm, std::int32_t* colof);
 void gather_values(Context& ctx, Index nnz, double* dst, const double* src, const std::int64_t* perm);
 
 // ------------------------------------------------------------------ misc

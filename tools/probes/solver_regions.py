@@ -51,7 +51,8 @@ def main(m=2000, rank=100, frac=0.10, mc=False):
     tot = time.perf_counter() - t
     print(f"m={m}: {tot:.3f} s, {st.iterations} iterations, {st.matvec_count} matvecs", flush=True)
     names = {0: "K1 paired products", 1: "EVD of T", 2: "thin_qr", 3: "Lanczos reseed (whole)", 4: "Ritz checkpoints",
-             5: "blws_svd (whole)"}
+             5: "blws_svd (whole)", 6: "svt (whole)", 7: "MC loop outside svt",
+             8: "solver set-up", 9: "solver epilogue"}
     for i, nm in names.items():
         r = ctx.region_stats(i)
         print(f"  {nm:26s} {r['ms']:9.1f} ms over {r['count']:5d}", flush=True)
