@@ -181,6 +181,28 @@ def test_sparse_pair_block_matches_numpy(gpu, b):
     assert np.abs(bot - ref_bot).max() <= 1e-12 * np.abs(ref_bot).max()
 
 
+@pytest.mark.parametrize("b", [9, 55, 100])
+def test_sparse_spmm_large_ragged(gpu, b):
+    # K8 at a larger size: 21000 x 1500 at 1% density, odd b, a dense row and
+    # an empty column (more rows than the grid has warps: grid-stride rows)
+    import scipy.sparse as sp
+
+    rs = np.random.default_rng(100 + b)
+    m, n = 21000, 1500
+    a = sp.random(m, n, density=0.01, format="csc", random_state=rs, data_rvs=rs.standard_normal)
+    a = a.tolil()
+    a[5, :] = rs.standard_normal(n)
+    a[:, 7] = 0.0
+    a = a.tocsc()
+    a.sort_indices()
+    op = gpu.api.SparseOperator(m, n, a.indptr.astype(np.int64), a.indices.astype(np.int32), a.data.copy())
+    left, right = rs.standard_normal((m, b)), rs.standard_normal((n, b))
+    top, bot = op.apply_pair_block(left, right)
+    ref_top, ref_bot = a @ right, a.T @ left
+    assert np.abs(top - ref_top).max() <= 1e-12 * np.abs(ref_top).max()
+    assert np.abs(bot - ref_bot).max() <= 1e-12 * np.abs(ref_bot).max()
+
+
 @pytest.mark.parametrize("ta", [False, True])
 @pytest.mark.parametrize("m,n,k", [(1001, 37, 999), (5000, 104, 130), (300, 128, 17), (4000, 100, 4000),
                                    (2047, 64, 61), (640, 8, 1)])
