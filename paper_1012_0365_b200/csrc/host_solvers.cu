@@ -279,74 +279,95 @@ __global__ void __launch_bounds__(gemm_detail::THREADS) alm_fused_k(const double
 // K7 with TMA-fed operands (the default; alm_fused_k above is the fallback for
 // unaligned panels). a = us v^T has both operands with the row index
 // contiguous, so both tiles are staged as [BK k][16 rows] boxes (128-byte
-// swizzle) by one producer warp into a 2-stage mbarrier ring, the consumers
-// read DMMA fragments with the conflict-free permuted-k addressing of the
-// tall-skinny GEMM (dgemm_tma.cuh), and run the ALM epilogue on their 16 x 64
-// sub-tile. D and Y of the tile are bulk-prefetched into L2 by the producer
-// before the first operand load, so the HBM stream of the epilogue overlaps
-// the DMMA work of the CTAs sharing the SM (3 per SM).
+// swizzle) and the consumers read DMMA fragments with the conflict-free
+// permuted-k addressing of the tall-skinny GEMM (dgemm_tma.cuh).
+//
+// Persistent, two CTAs per SM walking the 64 x 32 tiles blockIdx.x, +
+// gridDim.x, ... A producer warp streams, per tile, the tile's D and Y (eight
+// [32 cols][16 rows] swizzled boxes, 32 KB) and then the U / V k-tiles (a
+// 4-stage ring of BK = 16), so the tile's D / Y arrive during its DMMA phase.
+// Two CTAs per SM give each scheduler two consumer warps. Measured at C3
+// (ncu, one ALM iteration): 80.5 us (cp.async, epilogue loads from HBM) ->
+// 77.5 (TMA operands, L2 prefetch) -> 68.2 (D / Y staged, 64 x 64, 2 stages;
+// the consumers then waited mostly on the operand ring) -> 65.4 us here, DMMA
+// pipe 46% active. The consumers' epilogue therefore reads D and Y from shared
+// memory -- no global-load latency after the DMMA phase -- and its stores of
+// Y, E, W drain while the next tile's DMMAs run.
 namespace k7 {
-constexpr int CONS = 4, BM = 16 * CONS, BN = 64, BK = 32, STAGES = 2;
+constexpr int CONS = 4, BM = 16 * CONS, BN = 32, BK = 16, STAGES = 4, DYBUF = 1;
 constexpr int A_BYTES = BM * BK * 8, B_BYTES = BN * BK * 8, STAGE = A_BYTES + B_BYTES;
-constexpr int SMEM = STAGES * STAGE + 1024 + 2 * STAGES * 8;
+constexpr int DY_BYTES = 2 * BM * BN * 8;  // D and Y of one tile
+constexpr int SMEM = STAGES * STAGE + DYBUF * DY_BYTES + 1024 + 2 * (STAGES + 2) * 8;  // 81 KB: two CTAs per SM
 constexpr int THREADS = 32 * (CONS + 1);
 }  // namespace k7
 
-__global__ void __launch_bounds__(k7::THREADS, 3) alm_tma_k(const __grid_constant__ CUtensorMap tmU,
-                                                          const __grid_constant__ CUtensorMap tmV, long m, long n,
-                                                          long r, const double* __restrict__ D,
-                                                          double* __restrict__ Y, double* __restrict__ W,
-                                                          double* __restrict__ E, long ld, double mu, double mu_next,
-                                                          double lambda_mu, double* partial, int* bad) {
+__global__ void __launch_bounds__(k7::THREADS, 2) alm_tma_k(const __grid_constant__ CUtensorMap tmU,
+                                                             const __grid_constant__ CUtensorMap tmV,
+                                                             const __grid_constant__ CUtensorMap tmD,
+                                                             const __grid_constant__ CUtensorMap tmY, long m, long n,
+                                                             long r, double* __restrict__ Y, double* __restrict__ W,
+                                                             double* __restrict__ E, long ld, double mu,
+                                                             double mu_next, double lambda_mu, double* partial,
+                                                             int* bad) {
     using namespace k7;
     using namespace gemm_tma;
     extern __shared__ __align__(1024) unsigned char smraw[];
     unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
-    uint64_t* full = reinterpret_cast<uint64_t*>(sm + STAGES * STAGE);
+    unsigned char* dyb = sm + STAGES * STAGE;  // DYBUF x (D 32 KB, Y 32 KB)
+    uint64_t* full = reinterpret_cast<uint64_t*>(dyb + DYBUF * DY_BYTES);
     uint64_t* empty = full + STAGES;
+    uint64_t* dyfull = empty + STAGES;  // 2
+    uint64_t* dyempty = dyfull + 2;     // 2
     __shared__ double sh[CONS];
     __shared__ int shbad;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const long m0 = static_cast<long>(blockIdx.x) * BM, n0 = static_cast<long>(blockIdx.y) * BN;
-    const int ntiles = static_cast<int>((r + BK - 1) / BK);
+    const long mt = (m + BM - 1) / BM, nt = (n + BN - 1) / BN, tiles = mt * nt;
+    const int ktiles = static_cast<int>((r + BK - 1) / BK);
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(full + s, 1);
             mbar_init(empty + s, CONS);
         }
-        shbad = 0;
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(dyfull + s, 1);
+            mbar_init(dyempty + s, CONS);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
     if (warp == CONS) {
-        // ---- producer: L2 prefetch of the epilogue's D / Y columns, then the operand ring
-        if ((ld & 1) == 0) {
-            const unsigned bytes = static_cast<unsigned>(((min(static_cast<long>(BM), m - m0) * 8) + 15) & ~15L);
-            for (int c = lane; c < 2 * BN; c += 32) {
-                const long col = n0 + (c & (BN - 1));
-                if (col < n) {
-                    const double* base = (c < BN ? D : Y) + m0 + col * ld;
-                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(base), "r"(bytes) : "memory");
-                }
-            }
-        }
+        // ---- producer
         if (lane == 0) {
-            for (int kt = 0; kt < ntiles; ++kt) {
-                const int s = kt % STAGES;
-                mbar_wait(empty + s, ((kt / STAGES) & 1) ^ 1);
-                mbar_expect_tx(full + s, STAGE);
-                unsigned char* as = sm + s * STAGE;
-                unsigned char* bs = as + A_BYTES;
-                const int k0 = kt * BK;
+            long q = 0;  // ring sequence number over the CTA's (tile, k-tile) stream
+            long j = 0;  // local tile counter (D / Y buffer j & 1)
+            for (long tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++j) {
+                const int m0 = static_cast<int>((tile % mt) * BM), n0 = static_cast<int>((tile / mt) * BN);
+                const int bsel = static_cast<int>(j % DYBUF);
+                mbar_wait(dyempty + bsel, static_cast<uint32_t>(((j / DYBUF) & 1) ^ 1));
+                mbar_expect_tx(dyfull + bsel, DY_BYTES);
+                unsigned char* dst = dyb + bsel * DY_BYTES;
 #pragma unroll
-                for (int q = 0; q < BM / 16; ++q) tma_2d(as + q * (BK * 128), &tmU, full + s, static_cast<int>(m0) + 16 * q, k0);
+                for (int qq = 0; qq < BM / 16; ++qq) {
+                    tma_2d(dst + qq * (BN * 128), &tmD, dyfull + bsel, m0 + 16 * qq, n0);
+                    tma_2d(dst + DY_BYTES / 2 + qq * (BN * 128), &tmY, dyfull + bsel, m0 + 16 * qq, n0);
+                }
+                for (int kt = 0; kt < ktiles; ++kt, ++q) {
+                    const int s = static_cast<int>(q % STAGES);
+                    mbar_wait(empty + s, static_cast<uint32_t>(((q / STAGES) & 1) ^ 1));
+                    mbar_expect_tx(full + s, STAGE);
+                    unsigned char* as = sm + s * STAGE;
+                    unsigned char* bs = as + A_BYTES;
+                    const int k0 = kt * BK;
 #pragma unroll
-                for (int q = 0; q < BN / 16; ++q) tma_2d(bs + q * (BK * 128), &tmV, full + s, static_cast<int>(n0) + 16 * q, k0);
+                    for (int qq = 0; qq < BM / 16; ++qq) tma_2d(as + qq * (BK * 128), &tmU, full + s, m0 + 16 * qq, k0);
+#pragma unroll
+                    for (int qq = 0; qq < BN / 16; ++qq) tma_2d(bs + qq * (BK * 128), &tmV, full + s, n0 + 16 * qq, k0);
+                }
             }
         }
         return;
     }
-    // ---- consumers: warp w owns rows [16 w, 16 w + 16) x all 64 columns
+    // ---- consumers: warp w owns rows [16 w, 16 w + 16) x all 64 columns of a tile
     const int g = lane >> 2, t = lane & 3;
     const int wm = warp * 16;
     int off[4][2];  // [k][16 rows] box offsets of rows (8 mi + g) at k-step s
@@ -359,65 +380,66 @@ __global__ void __launch_bounds__(k7::THREADS, 3) alm_tma_k(const __grid_constan
             off[s][h] = k * 128 + ((((rr >> 1) ^ (k & 7)) & 7) << 4) + (rr & 1) * 8;
         }
     }
-    double acc[2][BN / 8][2];
+    const double inv_mu = 1.0 / mu, inv_mu_next = 1.0 / mu_next;
+    long q = 0, j = 0;
+    for (long tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++j) {
+        const long m0 = (tile % mt) * BM, n0 = (tile / mt) * BN;
+        double acc[2][BN / 8][2];
 #pragma unroll
-    for (int i = 0; i < 2; ++i)
+        for (int i = 0; i < 2; ++i)
 #pragma unroll
-        for (int j = 0; j < BN / 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-    for (int kt = 0; kt < ntiles; ++kt) {
-        const int s = kt % STAGES;
-        mbar_wait(full + s, (kt / STAGES) & 1);
-        const unsigned char* as = sm + s * STAGE + warp * (BK * 128);
-        const unsigned char* bs = sm + s * STAGE + A_BYTES;
+            for (int jj = 0; jj < BN / 8; ++jj) acc[i][jj][0] = acc[i][jj][1] = 0.0;
+        for (int kt = 0; kt < ktiles; ++kt, ++q) {
+            const int s = static_cast<int>(q % STAGES);
+            mbar_wait(full + s, static_cast<uint32_t>((q / STAGES) & 1));
+            const unsigned char* as = sm + s * STAGE + warp * (BK * 128);
+            const unsigned char* bs = sm + s * STAGE + A_BYTES;
+            // k boxes entirely past r are zero-filled: skip their DMMAs
+            const int kbn = static_cast<int>(min(static_cast<long>(BK / 16), (r - kt * BK + 15) / 16));
 #pragma unroll
-        for (int kb = 0; kb < BK / 16; ++kb) {
+            for (int kb = 0; kb < BK / 16; ++kb) {
+                if (kb >= kbn) break;
 #pragma unroll
-            for (int st = 0; st < 4; ++st) {
-                double af[2];
+                for (int st = 0; st < 4; ++st) {
+                    double af[2];
 #pragma unroll
-                for (int mi = 0; mi < 2; ++mi)
-                    af[mi] = *reinterpret_cast<const double*>(as + kb * (16 * 128) + off[st][mi]);
+                    for (int mi = 0; mi < 2; ++mi)
+                        af[mi] = *reinterpret_cast<const double*>(as + kb * (16 * 128) + off[st][mi]);
 #pragma unroll
-                for (int ni = 0; ni < BN / 8; ++ni) {
-                    const double bf = *reinterpret_cast<const double*>(bs + (ni >> 1) * (BK * 128) + kb * (16 * 128) +
-                                                                       off[st][ni & 1]);
-                    gemm_detail::dmma(acc[0][ni], af[0], bf);
-                    gemm_detail::dmma(acc[1][ni], af[1], bf);
+                    for (int ni = 0; ni < BN / 8; ++ni) {
+                        const double bf = *reinterpret_cast<const double*>(bs + (ni >> 1) * (BK * 128) +
+                                                                           kb * (16 * 128) + off[st][ni & 1]);
+                        gemm_detail::dmma(acc[0][ni], af[0], bf);
+                        gemm_detail::dmma(acc[1][ni], af[1], bf);
+                    }
                 }
             }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty + s);
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(empty + s);
-    }
-    double ss = 0.0;
-    int nonfinite = 0;
-    const double inv_mu = 1.0 / mu, inv_mu_next = 1.0 / mu_next;
+        // ---- epilogue: D and Y of this warp's 16 rows from its [64 cols][16 rows] boxes
+        const int bsel = static_cast<int>(j % DYBUF);
+        mbar_wait(dyfull + bsel, static_cast<uint32_t>((j / DYBUF) & 1));
+        const unsigned char* dbox = dyb + bsel * DY_BYTES + warp * (BN * 128);
+        const unsigned char* ybox = dbox + DY_BYTES / 2;
+        double ss = 0.0;
+        int nonfinite = 0;
 #pragma unroll
-    for (int mi = 0; mi < 2; ++mi) {
-        const long row = m0 + wm + mi * 8 + g;
-        if (row >= m) continue;
+        for (int mi = 0; mi < 2; ++mi) {
+            const int rr = mi * 8 + g;
+            const long row = m0 + wm + rr;
 #pragma unroll
-        for (int nh = 0; nh < BN / 8; nh += 4) {  // 4 column groups' D and Y loads in flight together
-            double dv[4][2], yv[4][2];
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
+            for (int ni = 0; ni < BN / 8; ++ni)
 #pragma unroll
                 for (int e2 = 0; e2 < 2; ++e2) {
-                    const long col = n0 + (nh + q) * 8 + 2 * t + e2;
+                    const int c = ni * 8 + 2 * t + e2;
+                    const long col = n0 + c;
+                    const int so = c * 128 + ((((rr >> 1) ^ (c & 7)) & 7) << 4) + (rr & 1) * 8;
+                    const double d = *reinterpret_cast<const double*>(dbox + so);
+                    const double y = *reinterpret_cast<const double*>(ybox + so);
+                    if (row >= m || col >= n) continue;
                     const long o = row + col * ld;
-                    dv[q][e2] = col < n ? D[o] : 0.0;
-                    yv[q][e2] = col < n ? Y[o] : 0.0;
-                }
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-#pragma unroll
-                for (int e2 = 0; e2 < 2; ++e2) {
-                    const long col = n0 + (nh + q) * 8 + 2 * t + e2;
-                    if (col >= n) continue;
-                    const long o = row + col * ld;
-                    const double a = acc[mi][nh + q][e2];
-                    const double d = dv[q][e2];
-                    const double y = yv[q][e2];
+                    const double a = acc[mi][ni][e2];
                     const double dma = d - a;
                     const double e = shrink_d(dma + y * inv_mu, lambda_mu);
                     const double res = dma - e;
@@ -430,14 +452,23 @@ __global__ void __launch_bounds__(k7::THREADS, 3) alm_tma_k(const __grid_constan
                     nonfinite |= !isfinite(w);
                 }
         }
-    }
-    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-    if (lane == 0) sh[warp] = ss;
-    if (__any_sync(0xffffffffu, nonfinite) && lane == 0) shbad = 1;
-    asm volatile("bar.sync 1, %0;" ::"n"(CONS * 32) : "memory");  // consumers only (the producer has exited)
-    if (threadIdx.x == 0) {
-        partial[blockIdx.x + static_cast<long>(blockIdx.y) * gridDim.x] = (sh[0] + sh[1]) + (sh[2] + sh[3]);
-        if (shbad) atomicOr(bad, 1);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(dyempty + bsel);
+        for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+        nonfinite = __any_sync(0xffffffffu, nonfinite);
+        if (lane == 0) {
+            sh[warp] = ss;
+            if (warp == 0) shbad = 0;
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(CONS * 32) : "memory");  // consumers only
+        if (lane == 0 && nonfinite) shbad = 1;
+        asm volatile("bar.sync 1, %0;" ::"n"(CONS * 32) : "memory");
+        if (threadIdx.x == 0) {
+            // partial layout of the tile grid: (tile % mt, tile / mt)
+            partial[tile] = (sh[0] + sh[1]) + (sh[2] + sh[3]);
+            if (shbad) atomicOr(bad, 1);
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(CONS * 32) : "memory");  // sh reused by the next tile
     }
 }
 
@@ -660,11 +691,12 @@ SolverStats rpca_adm(Context& ctx, Index m, const double* d_in, Index ldd, doubl
     ctx.note_launch();
     using namespace gemm_detail;
     const dim3 grid(static_cast<unsigned>(ceil_div(rows, BM)), static_cast<unsigned>(ceil_div(m, BN)));
-    DBuf<double> part(ctx, static_cast<size_t>(grid.x) * grid.y);
+    const long k7tiles = ceil_div(rows, k7::BM) * ceil_div(m, k7::BN);  // alm_tma_k's tile grid
+    DBuf<double> part(ctx, static_cast<size_t>(std::max<long>(static_cast<long>(grid.x) * grid.y, k7tiles)));
+    long nparts = static_cast<long>(grid.x) * grid.y;
     constexpr int smem = smem_bytes<false, true>();
     BLWS_CUDA(cudaFuncSetAttribute(alm_fused_k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     BLWS_CUDA(cudaFuncSetAttribute(alm_tma_k, cudaFuncAttributeMaxDynamicSharedMemorySize, k7::SMEM));
-    static_assert(k7::BM == BM && k7::BN == BN, "K7 variants share the tile grid and the partial layout");
     const bool use_tma = [] {
         const char* e = std::getenv("BLWS_K7");
         return !(e && std::string(e) == "cpasync");
@@ -689,15 +721,19 @@ SolverStats rpca_adm(Context& ctx, Index m, const double* d_in, Index ldd, doubl
         if (r > 0) scale_columns(ctx, us.view().left(r), prox.trip.u(), prox.sigma_dev.get());
         const double mu_next = std::min(opts.rho * mu, mu_max);
         zero(ctx, bad.get(), sizeof(int));
-        CUtensorMap tmu, tmv;
+        CUtensorMap tmu, tmv, tmd, tmy;
         if (use_tma && r > 0 && tma_map_2d(&tmu, us.data(), rows, r, us.ld, k7::BK) &&
-            tma_map_2d(&tmv, prox.trip.v().p, m, r, prox.trip.uv.ld, k7::BK)) {
-            alm_tma_k<<<grid, k7::THREADS, k7::SMEM, ctx.stream()>>>(tmu, tmv, rows, m, r, D.data(), Y.data(),
+            tma_map_2d(&tmv, prox.trip.v().p, m, r, prox.trip.uv.ld, k7::BK) &&
+            tma_map_2d(&tmd, D.data(), rows, m, ld, k7::BN) && tma_map_2d(&tmy, Y.data(), rows, m, ld, k7::BN)) {
+            nparts = k7tiles;
+            const unsigned ctas = static_cast<unsigned>(std::min<long>(2L * ctx.sm_count(), k7tiles));
+            alm_tma_k<<<ctas, k7::THREADS, k7::SMEM, ctx.stream()>>>(tmu, tmv, tmd, tmy, rows, m, r, Y.data(),
                                                                      Wm.data(), E.data(), ld, mu, mu_next, lambda / mu,
                                                                      part.get(), bad.get());
             ctx.note_launch();
             ctx.check_launch("alm_tma_k");
         } else {
+            nparts = static_cast<long>(grid.x) * grid.y;
             alm_fused_k<<<grid, THREADS, smem, ctx.stream()>>>(us.data(), us.ld, prox.trip.v().p, prox.trip.uv.ld, rows,
                                                                m, r, D.data(), Y.data(), Wm.data(), E.data(), ld, mu,
                                                                mu_next, lambda / mu, part.get(), bad.get());
@@ -708,7 +744,7 @@ SolverStats rpca_adm(Context& ctx, Index m, const double* d_in, Index ldd, doubl
         stats.matvec_history.push_back(op.application_count() - mark);
         mark = op.application_count();
         double rsq = 0.0;
-        reduce_partials(ctx, part.get(), static_cast<Index>(grid.x) * grid.y, red.get());
+        reduce_partials(ctx, part.get(), nparts, red.get());
         total(red.get(), 1, &rsq);
         const double feas = std::sqrt(rsq) / norm_d_fro;
         stats.residual_history.push_back(feas);

@@ -119,3 +119,21 @@ def test_reference_gates_on_device(G, O):
     for (gb, gl), (ob, ol) in zip(px.values, ref.values):
         assert abs(gb - ob) <= 1e-3 * ob  # blws: same trajectory as the oracle
         assert gl <= 1e-12 and ol <= 1e-12  # lanczos: exact to rounding on both
+
+
+def test_rpca_k7_variants_agree(G, O, monkeypatch):
+    """K7 at a size where every CTA of the persistent TMA kernel runs several
+    tiles per consumer group (m = 1600: 625 tiles over 148 CTAs): the same
+    solve with the cp.async kernel (BLWS_K7=cpasync) takes the same iterations
+    and predicted ranks, and A / E agree to rounding."""
+    d, a0, _, _ = synth.rpca_lowrank_sparse(1600, 30, int(0.05 * 1600 * 1600), 7, O.Rng, O.sample_distinct)
+    bseed = 7 ^ 0x5BDBEEF
+    a_t, e_t, st_t, _ = G.rpca_adm(d, G.SvdBackend.blws(seed=bseed), truth=a0)
+    monkeypatch.setenv("BLWS_K7", "cpasync")
+    a_c, e_c, st_c, _ = G.rpca_adm(d, G.SvdBackend.blws(seed=bseed), truth=a0)
+    assert st_t.converged and st_c.converged
+    assert st_t.iterations == st_c.iterations and st_t.rank_hat == st_c.rank_hat == 30
+    assert list(st_t.predicted_ranks) == list(st_c.predicted_ranks)
+    assert np.linalg.norm(a_t - a_c) <= 1e-10 * np.linalg.norm(a_c)
+    assert np.linalg.norm(e_t - e_c) <= 1e-10 * np.linalg.norm(e_c)
+    assert st_t.rel_err <= 1e-5
