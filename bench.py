@@ -371,7 +371,7 @@ def run_gpu(args):
                          "frac": achieved_tf / peak if peak else None, "traffic": traffic,
                          "traffic_unit": "bytes per K1 launch group (ncu, profiles/r01_k1_traffic.json)",
                          "algorithmic_bytes_per_launch": 16.0 * M * N,
-                         "kernel": "K1 paired W products (dgemm_kernel NN + TN, split-K reduce)",
+                         "kernel": "K1 paired W products (dgemm_tma_kernel NN + TN, split-K reduce)",
                          "flops_per_launch": k1_flops, "avg_launch_ms": k1_avg_ms,
                          "peak_source": "measured in this run: DMMA microbenchmark %.2f, DFMA %.2f TFLOP/s; "
                                         "cuBLAS DGEMM 8192^3 %.2f TFLOP/s" % (peak_dmma, peak_dfma, cublas_tf),
@@ -388,10 +388,44 @@ def run_gpu(args):
                                     "single_thread": {"value": len(t1) / sum(t1), "unit": "calls/s", "cores": 1,
                                                       "sample": f"{len(t1)} calls, 1 thread"},
                                     "host": {"nproc": os.cpu_count(), "cpu": cpu_model()}}
+        if not args.no_solves and world == 1:
+            line["solves"] = solver_configs()
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
     return 0
+
+
+def solver_configs():
+    """BASELINE's other headline metric, RPCA / MC solve time, on configs[0],
+    [2], [3] (C1, C3, C4; seeded synthetic instances, reference RNG recipe):
+    wall clock around each solve call only (solvers.hpp:75,154), one solve
+    each after a small warm-up solve. The oracle's times for the same
+    instances are in profiles/r01e_solve_configs.jsonl (C3's takes ~4 min)."""
+    import paper_1012_0365_b200 as B
+    from paper_1012_0365_b200 import synth
+
+    ctx = B.Context(0)
+    out = {}
+    bseed = 1 ^ 0x5BDBEEF
+    for name, m, rank, frac in (("C1", 500, 25, 0.05), ("C3", 2000, 100, 0.10)):
+        d, a0, _, _ = synth.rpca_lowrank_sparse(m, rank, int(round(frac * m * m)), 1, B.Rng, B.sample_distinct)
+        B.rpca_adm(d[:64, :64].copy(order="F"), B.SvdBackend.blws(seed=bseed, ctx=ctx))
+        t = time.perf_counter()
+        _, _, st, _ = B.rpca_adm(d, B.SvdBackend.blws(seed=bseed, ctx=ctx), truth=a0, want_outputs=False)
+        out[name] = {"workload": f"RPCA {m}^2 rank {rank}, {int(frac * 100)}% corrupted", "solve_s":
+                     time.perf_counter() - t, "iterations": st.iterations, "rank_hat": st.rank_hat,
+                     "rel_err": st.rel_err, "converged": st.converged}
+    colptr, rowidx, vals, ml, mr = synth.mc_lowrank(10000, 50, 10_000_000, 1, B.Rng, B.sample_distinct)
+    t = time.perf_counter()
+    _, _, _, st = B.mc_svt(10000, 10000, colptr, rowidx, vals, B.SvdBackend.blws(seed=bseed, ctx=ctx), tol_outer=1e-6,
+                           truth_ml=ml, truth_mr=mr, cap=512)
+    out["C4"] = {"workload": "MC 10000^2 rank 50, 10^7 observed", "solve_s": time.perf_counter() - t,
+                 "iterations": st.iterations, "rank_hat": st.rank_hat, "rel_err": st.rel_err,
+                 "converged": st.converged}
+    out["unit"] = "s"
+    out["higher_is_better"] = False
+    return out
 
 
 def main():
@@ -401,6 +435,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-solves", action="store_true", help="skip the C1 / C3 / C4 solve-time leg")
     ap.add_argument("--mode", default="replicas", choices=["replicas", "sharded"],
                     help="replicas: N independent C2 calls per step (weak scaling, default); sharded: one C2 "
                          "call with W row-sharded over the N GPUs (strong scaling)")
