@@ -28,6 +28,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+
 import subprocess
 import sys
 import threading
@@ -37,6 +38,23 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# The bench contract is one JSON line on stdout. Libraries write banners to
+# fd 1 (NCCL prints its version there under the image's NCCL_DEBUG=VERSION),
+# so fd 1 is pointed at stderr for the run and the line goes to a saved copy.
+_JSON_OUT = None
+
+
+def emit(line):
+    global _JSON_OUT
+    out = _JSON_OUT if _JSON_OUT is not None else sys.stdout
+    print(json.dumps(line), file=out, flush=True)
+
+
+def _stdout_to_stderr():
+    global _JSON_OUT
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
 
 M = N = 4000
 K_SIGNAL = 200
@@ -187,7 +205,7 @@ def run_reference(args):
                              "host": {"nproc": os.cpu_count(), "cpu": cpu_model()},
                              "sample": f"{args.steps} oracle blws_svd calls on the C2 W (OpenBLAS, {cores} threads)"},
             "e2e": {"value": value, "unit": "calls/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
@@ -390,7 +408,7 @@ def run_gpu(args):
                                     "host": {"nproc": os.cpu_count(), "cpu": cpu_model()}}
         if not args.no_solves and world == 1:
             line["solves"] = solver_configs()
-        print(json.dumps(line), flush=True)
+        emit(line)
     if world > 1:
         torch.distributed.destroy_process_group()
     return 0
@@ -440,6 +458,7 @@ def main():
                     help="replicas: N independent C2 calls per step (weak scaling, default); sharded: one C2 "
                          "call with W row-sharded over the N GPUs (strong scaling)")
     args = ap.parse_args()
+    _stdout_to_stderr()
     if args.impl == "reference":
         return run_reference(args)
     return run_gpu(args)
