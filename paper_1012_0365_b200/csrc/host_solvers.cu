@@ -489,18 +489,43 @@ __global__ void mc_sampled_k(long nnz, const std::int32_t* __restrict__ rowidx, 
         const long p = p0 + lane;
         const long myi = p < nnz ? rowidx[p] : 0, myj = p < nnz ? colof[p] : 0;
         double pd[32];
-#pragma unroll
-        for (int t = 0; t < 32; ++t) {
-            const long i = __shfl_sync(0xffffffffu, myi, t), j = __shfl_sync(0xffffffffu, myj, t);
-            const double* a = ust + i * r;
-            const double* bb = vt + j * r;
-            double d = 0.0;
+        // CSC order: the 32 positions usually share one column (~1000 observed
+        // entries per column at C4); then V's row is loaded once into registers
+        // and only the U rows are gathered (same products, same order)
+        const long j0 = __shfl_sync(0xffffffffu, myj, 0);
+        if (__all_sync(0xffffffffu, p >= nnz || myj == j0)) {
+            double vv[SLOTS];
 #pragma unroll
             for (int q = 0; q < SLOTS; ++q) {
                 const long c = lane + 32 * q;
-                if (c < r) d = fma(a[c], bb[c], d);
+                vv[q] = c < r ? vt[j0 * r + c] : 0.0;
             }
-            pd[t] = d;
+#pragma unroll
+            for (int t = 0; t < 32; ++t) {
+                const long i = __shfl_sync(0xffffffffu, myi, t);
+                const double* a = ust + i * r;
+                double d = 0.0;
+#pragma unroll
+                for (int q = 0; q < SLOTS; ++q) {
+                    const long c = lane + 32 * q;
+                    if (c < r) d = fma(a[c], vv[q], d);
+                }
+                pd[t] = d;
+            }
+        } else {
+#pragma unroll
+            for (int t = 0; t < 32; ++t) {
+                const long i = __shfl_sync(0xffffffffu, myi, t), j = __shfl_sync(0xffffffffu, myj, t);
+                const double* a = ust + i * r;
+                const double* bb = vt + j * r;
+                double d = 0.0;
+#pragma unroll
+                for (int q = 0; q < SLOTS; ++q) {
+                    const long c = lane + 32 * q;
+                    if (c < r) d = fma(a[c], bb[c], d);
+                }
+                pd[t] = d;
+            }
         }
 #pragma unroll
         for (int stage = 0; stage < 5; ++stage) {
