@@ -191,9 +191,6 @@ int blws_dgemm(blws_context* ctx, int ta, int tb, int64_t m, int64_t n, int64_t 
 /* development: average device microseconds of one hot-path piece on a seeded
  * input (0 chol_inv n, 1 sym_evd_top n, 2 thin_qr n x b, 3 gemm NN, 4 gemm TN) */
 int blws_microbench(blws_context* ctx, int which, int64_t n, int64_t b, int reps, double* us);
-/* development: out[0] SM MHz under a spin, out[1] cycles per __syncthreads (1024
- * threads), out[2] microseconds per empty kernel launch */
-int blws_probe(blws_context* ctx, double* out);
 
 /* ------------------------------------------------------------ backend/svt */
 #define BLWS_BACKEND_LANCZOS 1

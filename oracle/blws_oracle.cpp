@@ -810,14 +810,17 @@ static Vec project_low_rank(const Csc& pattern, const Mat& u, const Vec& s, cons
     Mat us = u;
     for (Index j = 0; j < us.c; ++j)
         for (Index i = 0; i < us.r; ++i) us(i, j) *= s[j];
-    Index idx = 0;
-    for (Index k = 0; k < pattern.cols; ++k)
-        for (auto p = pattern.colptr[k]; p < pattern.colptr[k + 1]; ++p) {
-            const Index row = pattern.rowidx[p];
-            double acc = 0;
-            for (Index c = 0; c < us.c; ++c) acc += us(row, c) * v(k, c);
-            out[idx++] = acc;
-        }
+    const Index chunks = 4 * loop_threads();
+    const Index cs = (pattern.cols + chunks - 1) / chunks;
+    parallel_tasks(chunks, [&](Index t) {
+        for (Index k = t * cs; k < std::min(pattern.cols, (t + 1) * cs); ++k)
+            for (auto p = pattern.colptr[k]; p < pattern.colptr[k + 1]; ++p) {
+                const Index row = pattern.rowidx[p];
+                double acc = 0;
+                for (Index c = 0; c < us.c; ++c) acc += us(row, c) * v(k, c);
+                out[static_cast<size_t>(p)] = acc;
+            }
+    });
     return out;
 }
 

@@ -241,23 +241,40 @@ protected:
         Mat X = apply_adjoint_block_impl(Y);
         return Vec(X.col(0), X.col(0) + X.r);
     }
+    // Threaded over (column of x, row slab): each y(i, c) is accumulated by one
+    // thread over j ascending, the serial order, so the result is bitwise the
+    // same for any thread count.
     Mat apply_block_impl(const Mat& x) const override {
         Mat y(mat_.rows, x.c);
-        for (Index c = 0; c < x.c; ++c)
+        const Index slabs = std::max<Index>(1, (4 * loop_threads() + x.c - 1) / std::max<Index>(x.c, 1));
+        const Index rs = (mat_.rows + slabs - 1) / slabs;
+        parallel_tasks(x.c * slabs, [&](Index t) {
+            const Index c = t / slabs, r0 = (t % slabs) * rs, r1 = std::min(mat_.rows, r0 + rs);
+            if (r0 >= r1) return;
+            double* yc = y.col(c);
             for (Index j = 0; j < mat_.cols; ++j) {
                 const double xj = x(j, c);
-                for (auto p = mat_.colptr[j]; p < mat_.colptr[j + 1]; ++p) y(mat_.rowidx[p], c) += mat_.val[p] * xj;
+                const std::int32_t* b = mat_.rowidx.data() + mat_.colptr[j];
+                const std::int32_t* e = mat_.rowidx.data() + mat_.colptr[j + 1];
+                const std::int32_t* p0 = slabs == 1 ? b : std::lower_bound(b, e, static_cast<std::int32_t>(r0));
+                for (const std::int32_t* p = p0; p < e && *p < r1; ++p)
+                    yc[*p] += mat_.val[static_cast<size_t>(p - mat_.rowidx.data())] * xj;
             }
+        });
         return y;
     }
     Mat apply_adjoint_block_impl(const Mat& y) const override {
         Mat x(mat_.cols, y.c);
-        for (Index c = 0; c < y.c; ++c)
-            for (Index j = 0; j < mat_.cols; ++j) {
+        const Index chunks = 4 * loop_threads();
+        const Index cs = (mat_.cols + chunks - 1) / chunks;
+        parallel_tasks(y.c * chunks, [&](Index t) {
+            const Index c = t / chunks, j0 = (t % chunks) * cs, j1 = std::min(mat_.cols, j0 + cs);
+            for (Index j = j0; j < j1; ++j) {
                 double s = 0;
                 for (auto p = mat_.colptr[j]; p < mat_.colptr[j + 1]; ++p) s += mat_.val[p] * y(mat_.rowidx[p], c);
                 x(j, c) = s;
             }
+        });
         return x;
     }
 

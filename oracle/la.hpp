@@ -13,6 +13,7 @@
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 namespace orc {
@@ -126,6 +127,34 @@ inline Mat mul(const Mat& A, const Mat& B, char ta = 'N', char tb = 'N') {
     return C;
 }
 
-inline void set_threads(int n) { scipy_openblas_set_num_threads64_(n); }
+/// Host threads for the oracle's own loops (sparse products, sampled
+/// evaluation); set together with OpenBLAS's count. Each output element is
+/// still accumulated by one thread in the serial order, so results are
+/// bitwise independent of the thread count.
+inline int& loop_threads() {
+    static int n = std::max(1u, std::thread::hardware_concurrency());
+    return n;
+}
+
+inline void set_threads(int n) {
+    scipy_openblas_set_num_threads64_(n);
+    loop_threads() = std::max(1, n);
+}
+
+/// Runs f(t, T) for t in [0, T) on T = min(loop_threads(), tasks) threads.
+template <typename F>
+inline void parallel_tasks(Index tasks, F&& f) {
+    const Index T = std::max<Index>(1, std::min<Index>(loop_threads(), tasks));
+    if (T == 1) {
+        for (Index t = 0; t < tasks; ++t) f(t);
+        return;
+    }
+    std::vector<std::thread> pool;
+    for (Index w = 0; w < T; ++w)
+        pool.emplace_back([&, w] {
+            for (Index t = w; t < tasks; t += T) f(t);
+        });
+    for (auto& th : pool) th.join();
+}
 
 }  // namespace orc

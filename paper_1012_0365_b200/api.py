@@ -56,7 +56,6 @@ SIGNATURES = {
     "blws_context_region_reset": (ci, [vp]),
     "blws_fp64_peak": (ci, [vp, ci, P(dbl)]),
     "blws_microbench": (ci, [vp, ci, i64, i64, ci, vp]),
-    "blws_probe": (ci, [vp, vp]),
     "blws_rng_create": (ci, [u64, P(vp)]),
     "blws_rng_destroy": (ci, [vp]),
     "blws_rng_split": (ci, [vp, u64, P(vp)]),
@@ -229,12 +228,6 @@ class Context:
         out = np.zeros(8)
         _check(lib().blws_microbench(self._h, which, n, b, reps, _ptr(out)))
         return out if detail else float(out[0])
-
-    def probe(self):
-        out = np.zeros(8)
-        _check(lib().blws_probe(self._h, _ptr(out)))
-        return dict(sm_mhz=out[0], sync_cycles=out[1], launch_us=out[2], dfma_cyc=out[3], ddiv_cyc=out[4],
-                    dsqrt_cyc=out[5], drsqrt_cyc=out[6])
 
     def fp64_peak(self, mode: int = 0) -> float:
         out = dbl(0)

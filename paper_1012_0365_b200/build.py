@@ -53,7 +53,10 @@ def build(verbose: bool = False, jobs: int = 8) -> str:
     hdr_t = _headers_mtime()
     with cf.ThreadPoolExecutor(max_workers=jobs) as ex:
         objs = list(ex.map(lambda s: _compile(s, hdr_t, verbose), srcs))
-    if os.path.exists(LIB) and os.path.getmtime(LIB) >= max(os.path.getmtime(o) for o in objs):
+    stamp = LIB + ".objs"  # relink when the object set changes (a source removed)
+    listing = "\n".join(objs)
+    same_set = os.path.exists(stamp) and open(stamp).read() == listing
+    if same_set and os.path.exists(LIB) and os.path.getmtime(LIB) >= max(os.path.getmtime(o) for o in objs):
         return LIB
     cmd = [NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", *objs, "-o", LIB + ".tmp", "-lcudart_static", "-lrt",
            "-ldl", "-lpthread"]
@@ -61,6 +64,8 @@ def build(verbose: bool = False, jobs: int = 8) -> str:
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")
     os.replace(LIB + ".tmp", LIB)
+    with open(stamp, "w") as f:
+        f.write(listing)
     return LIB
 
 

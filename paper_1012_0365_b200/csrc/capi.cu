@@ -778,83 +778,6 @@ extern "C" int blws_microbench(blws_context* ctx, int which, int64_t n, int64_t 
     });
 }
 
-namespace {
-__global__ void probe_clock_k(long long spin_ns, double* out) {
-    unsigned long long t0, t1;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-    const long long c0 = clock64();
-    do {
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-    } while (static_cast<long long>(t1 - t0) < spin_ns);
-    const long long c1 = clock64();
-    if (threadIdx.x == 0) out[0] = static_cast<double>(c1 - c0) / static_cast<double>(t1 - t0) * 1e3;  // MHz
-}
-__global__ void probe_sync_k(int iters, double* out) {
-    __shared__ double s[1024];
-    double v = threadIdx.x;
-    const long long c0 = clock64();
-    for (int i = 0; i < iters; ++i) {
-        s[threadIdx.x] = v;
-        __syncthreads();
-        v += s[(threadIdx.x + 1) & 1023];
-        __syncthreads();
-    }
-    const long long c1 = clock64();
-    if (threadIdx.x == 0) out[0] = static_cast<double>(c1 - c0) / (2.0 * iters);  // cycles per barrier
-    if (v == 12345.0) out[1] = v;
-}
-__global__ void probe_empty_k() {}
-__global__ void probe_ops_k(double x0, double* out) {
-    // cycles per dependent op: 0 DFMA, 1 div, 2 sqrt, 3 rsqrt, 4 rcp(approx)+2 Newton
-    double x = x0;
-    long long c0 = clock64();
-    for (int i = 0; i < 256; ++i) x = fma(x, 1.0000001, 1e-9);
-    long long c1 = clock64();
-    out[0] = (c1 - c0) / 256.0;
-    c0 = clock64();
-    for (int i = 0; i < 256; ++i) x = 1.0 / x + 0.5;
-    c1 = clock64();
-    out[1] = (c1 - c0) / 256.0;
-    c0 = clock64();
-    for (int i = 0; i < 256; ++i) x = sqrt(x) + 0.5;
-    c1 = clock64();
-    out[2] = (c1 - c0) / 256.0;
-    c0 = clock64();
-    for (int i = 0; i < 256; ++i) x = rsqrt(x) + 0.5;
-    c1 = clock64();
-    out[3] = (c1 - c0) / 256.0;
-    out[4] = x;
-}
-}  // namespace
-
-// probe: out[0] SM MHz during a 200 us spin, out[1] cycles per __syncthreads
-// (1024 threads), out[2] us per empty launch (event-timed, 100 launches)
-extern "C" int blws_probe(blws_context* ctx, double* out) {
-    return guard([&] {
-        Context& c = *ctx->ctx;
-        DBuf<double> d(c, 4);
-        probe_clock_k<<<1, 32, 0, c.stream()>>>(200000, d.get());
-        c.read(d.get(), out, 1);
-        probe_sync_k<<<1, 1024, 0, c.stream()>>>(1000, d.get());
-        c.read(d.get(), out + 1, 1);
-        DBuf<double> ops(c, 8);
-        probe_ops_k<<<1, 1, 0, c.stream()>>>(1.5, ops.get());
-        c.read(ops.get(), out + 3, 4);
-        cudaEvent_t e0, e1;
-        BLWS_CUDA(cudaEventCreate(&e0));
-        BLWS_CUDA(cudaEventCreate(&e1));
-        BLWS_CUDA(cudaEventRecord(e0, c.stream()));
-        for (int i = 0; i < 100; ++i) probe_empty_k<<<1, 32, 0, c.stream()>>>();
-        BLWS_CUDA(cudaEventRecord(e1, c.stream()));
-        BLWS_CUDA(cudaEventSynchronize(e1));
-        float ms = 0;
-        BLWS_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-        out[2] = ms * 10.0;
-        cudaEventDestroy(e0);
-        cudaEventDestroy(e1);
-    });
-}
-
 int blws_mm_write_dense(const char* path, int64_t rows, int64_t cols, const double* a, int64_t lda) {
     return guard([&] {
         need(path && a && rows > 0 && cols > 0 && lda >= rows, "mm_write_dense: bad argument");

@@ -5,6 +5,7 @@
 // constants, same RNG draw order. All matrices live on the device; the host
 // reads back only the scalars and small vectors the control flow branches on.
 #pragma once
+#include <atomic>
 #include <cstdint>
 #include <memory>
 #include <optional>
@@ -82,6 +83,9 @@ public:
     /// its verdict (nonzero = non-finite entries) written to the device int
     /// `*flag`, instead of the synchronous check at the next use.
     virtual void defer_pending_check(int* flag) { (void)flag; }
+    /// A deferred check found non-finite data: every later use throws until
+    /// the operator is reassigned (the reference rejects it at assign time).
+    virtual void mark_poisoned() {}
     /// Identity of the data the kernels read (graph cache key).
     virtual const void* data_key() const { return this; }
     void add_applications(std::int64_t n) { count_ += n; }
@@ -132,6 +136,7 @@ public:
     /// overlap) until that use.
     void assign_host_async(const double* w, Index ldw);
     void defer_pending_check(int* flag) override;
+    void mark_poisoned() override { poisoned_ = true; }
     const void* data_key() const override { return p_; }
     /// Device copy with the non-finite check.
     void assign_device(const double* w, Index ldw);
@@ -148,6 +153,7 @@ private:
     DBuf<double> own_;
     double* p_ = nullptr;
     mutable bool pending_ = false;
+    mutable bool poisoned_ = false;
     cudaEvent_t consumed_ = nullptr, ready_ = nullptr;
 };
 
@@ -176,7 +182,6 @@ private:
     DBuf<std::int64_t> rowptr_, colptr_, perm_;  // perm: csr position -> csc position
     DBuf<std::int32_t> colidx_, rowidx_, colof_;
     DBuf<double> val_csr_, val_csc_;
-    DBuf<double> scratch_, scratch2_;
 };
 
 // ------------------------------------------------------------ warm start
@@ -216,8 +221,8 @@ DWarm adapt_subspace(Context& ctx, const DWarm* warm, Index r_new, Index m, Inde
                      const RowShard* shard = nullptr);
 /// blws_svd (block_lanczos.hpp:204-261).
 BlwsResult blws_svd(LinearOperator& w, const DWarm& warm, Index k, Index r, Rng& rng);
-extern std::int64_t g_blws_deferred_fallbacks;
-extern std::int64_t g_blws_graph_launches;
+extern std::atomic<std::int64_t> g_blws_deferred_fallbacks;
+extern std::atomic<std::int64_t> g_blws_graph_launches;
 
 /// Factorisation for tests: block_lanczos_procedure on the augmented view.
 struct BlockLanczos {

@@ -254,21 +254,30 @@ DenseOperator::~DenseOperator() {
     if (ready_) cudaEventDestroy(ready_);
 }
 
-void DenseOperator::check_finite() { check_finite_view(ctx_, w(), "DenseOperator: non-finite entries"); }
-
-void DenseOperator::ensure_ready() const {
-    if (!pending_) return;
-    pending_ = false;
-    BLWS_CUDA(cudaStreamWaitEvent(ctx_.stream(), ready_, 0));
+void DenseOperator::check_finite() {
     check_finite_view(ctx_, View{p_, m_, n_, ld_}, "DenseOperator: non-finite entries");
 }
 
+void DenseOperator::ensure_ready() const {
+    if (poisoned_) throw std::invalid_argument("DenseOperator: non-finite entries");
+    if (!pending_) return;
+    pending_ = false;
+    BLWS_CUDA(cudaStreamWaitEvent(ctx_.stream(), ready_, 0));
+    poisoned_ = true;  // until the check passes
+    check_finite_view(ctx_, View{p_, m_, n_, ld_}, "DenseOperator: non-finite entries");
+    poisoned_ = false;
+}
+
 void DenseOperator::assign_host(const double* w_host, Index ldw) {
+    poisoned_ = false;
     upload(ctx_, w(), w_host, ldw);
+    poisoned_ = true;  // until the check passes
     check_finite();
+    poisoned_ = false;
 }
 
 void DenseOperator::defer_pending_check(int* flag) {
+    if (poisoned_) throw std::invalid_argument("DenseOperator: non-finite entries");
     if (!pending_) return;
     pending_ = false;
     BLWS_CUDA(cudaStreamWaitEvent(ctx_.stream(), ready_, 0));
@@ -277,7 +286,9 @@ void DenseOperator::defer_pending_check(int* flag) {
 
 void DenseOperator::assign_host_async(const double* w_host, Index ldw) {
     if (ldw < m_) throw std::invalid_argument("assign: ldw < rows");
-    ensure_ready();  // a previous pending upload is checked and ordered first
+    if (!poisoned_) ensure_ready();  // a previous pending upload is checked and ordered first
+    else if (pending_) BLWS_CUDA(cudaStreamWaitEvent(ctx_.stream(), ready_, 0));
+    poisoned_ = false;
     if (!consumed_) {
         BLWS_CUDA(cudaEventCreateWithFlags(&consumed_, cudaEventDisableTiming));
         BLWS_CUDA(cudaEventCreateWithFlags(&ready_, cudaEventDisableTiming));
@@ -293,8 +304,11 @@ void DenseOperator::assign_host_async(const double* w_host, Index ldw) {
 }
 
 void DenseOperator::assign_device(const double* w_dev, Index ldw) {
+    poisoned_ = false;
     if (w_dev != p_) copy(ctx_, w(), View{const_cast<double*>(w_dev), m_, n_, ldw});
+    poisoned_ = true;  // until the check passes
     check_finite();
+    poisoned_ = false;
 }
 
 void DenseOperator::pair_block_impl(View left, View right, View top, View bot) {
@@ -375,26 +389,30 @@ void SparseOperator::assign_values_device(const double* vals) {
 
 void SparseOperator::pair_block_impl(View left, View right, View top, View bot) {
     const Index b = right.cols;
+    // Row-major staging of X for the two SpMMs, allocated per call from the
+    // stream-ordered pool: under CUDA-graph capture they become the graph's own
+    // memory nodes, so a replayed graph never writes into a buffer a later call
+    // (with another block width) reallocated. Declared before the AuxScope so
+    // they are freed on the main stream after the join.
     const size_t need = static_cast<size_t>(std::max(m_, n_) * b);
-    if (scratch_.size() < need) scratch_ = DBuf<double>(ctx_, need);
-    if (scratch2_.size() < need) scratch2_ = DBuf<double>(ctx_, need);
+    DBuf<double> scratch(ctx_, need), scratch2(ctx_, need);
     const bool reduce = row_sharded() && ctx_.has_comm();
     DBuf<double> part;  // row shard: W^T x over the local rows, summed over the ranks
     if (reduce && bot.ld != n_) part = DBuf<double>(ctx_, static_cast<size_t>(n_ * b));
     AuxScope aux(ctx_);  // W^T x on the auxiliary stream, overlapping W x
     if (reduce && bot.ld != n_) {
         csr_spmm(ctx_, n_, colptr_.get(), rowidx_.get(), val_csc_.get(), m_, b, left.p, left.ld, part.get(), n_,
-                 scratch2_.get());
+                 scratch2.get());
         ctx_.allreduce_sum(part.get(), static_cast<size_t>(n_ * b));
         copy(ctx_, bot, View{part.get(), n_, b, n_});
     } else {
         csr_spmm(ctx_, n_, colptr_.get(), rowidx_.get(), val_csc_.get(), m_, b, left.p, left.ld, bot.p, bot.ld,
-                 scratch2_.get());
+                 scratch2.get());
         if (reduce) ctx_.allreduce_sum(bot.p, static_cast<size_t>(n_ * b));
     }
     aux.main();
     csr_spmm(ctx_, m_, rowptr_.get(), colidx_.get(), val_csr_.get(), n_, b, right.p, right.ld, top.p, top.ld,
-             scratch_.get());
+             scratch.get());
 }
 
 void SparseOperator::pair_impl(const double* left, const double* right, double* top, double* bot) {
@@ -1100,10 +1118,12 @@ struct SvdGraph {
     }
 };
 
-std::int64_t g_blws_deferred_fallbacks = 0;  // diagnostics (tests)
+// diagnostics (tests) and the graph-cache LRU clock; atomic because
+// independent solves may run on several threads (one context each)
+std::atomic<std::int64_t> g_blws_deferred_fallbacks{0};
 constexpr size_t kMaxSvdGraphs = 4;
-static std::uint64_t g_svd_graph_clock = 0;
-std::int64_t g_blws_graph_launches = 0;
+static std::atomic<std::uint64_t> g_svd_graph_clock{0};
+std::atomic<std::int64_t> g_blws_graph_launches{0};
 
 BlwsResult blws_svd(LinearOperator& w, const DWarm& warm, Index k, Index r, Rng& rng) {
     Context& ctx = w.ctx();
@@ -1226,8 +1246,10 @@ BlwsResult blws_svd(LinearOperator& w, const DWarm& warm, Index k, Index r, Rng&
     }
     sl->fetch(ctx);  // the one host round trip
     if (graphed) ctx.add_replayed_regions(plan->regions, plan->stamps.get());
-    if (ctx.has_comm() ? sl->val(finite_slot + 1) != 0.0 : sl->as_int(finite_slot) != 0)
+    if (ctx.has_comm() ? sl->val(finite_slot + 1) != 0.0 : sl->as_int(finite_slot) != 0) {
+        w.mark_poisoned();
         throw std::invalid_argument("DenseOperator: non-finite entries");
+    }
     if (!finish_deferred(rec, *sl, sh)) {
         ++g_blws_deferred_fallbacks;
         return blws_svd_exact(w, warm, k, r, rng);

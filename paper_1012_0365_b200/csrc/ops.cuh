@@ -72,9 +72,6 @@ void add_diagonal(Context& ctx, View g, const double* s_dev);
 /// count of diag(R) > tau (tau = scale * sqrt(sumsq[0])) -> out[0]
 void count_diag_above(Context& ctx, View r, const double* sumsq_dev, double scale, std::int64_t* out);
 
-/// Symmetric EVD (Jacobi). values descending, vectors columns (n x n).
-/// Returns sweeps used (host value, requires a sync).
-int sym_evd_jacobi(Context& ctx, View t, double* values, View vectors);
 /// Top `want` eigenpairs (descending) of a dense symmetric n x n T:
 /// Householder tridiagonalisation + bisection / inverse iteration + back-transform.
 void sym_evd_top(Context& ctx, View t, Index want, double* values, View vectors);

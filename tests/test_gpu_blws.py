@@ -225,6 +225,32 @@ def test_assign_async_matches_sync(G, O):
     op.assign_async(h3.data_ptr(), m)
     with pytest.raises(ValueError):
         op.apply_pair_block(x, y)
+    # the verdict sticks until the operator is reassigned
+    with pytest.raises(ValueError):
+        op.apply_pair_block(x, y)
+    op.assign_async(h.data_ptr(), m)
+    top, bot = op.apply_pair_block(x, y)
+    assert np.abs(top - w2 @ y).max() <= 1e-12
+
+
+def test_blws_svd_non_finite_async_w_stays_rejected(G, O):
+    # blws_svd's deferred check (one slot read) rejects an async-assigned NaN W;
+    # later calls on the same operator keep rejecting it until reassigned
+    m, n, r = 200, 150, 6
+    w = O.Rng(8).gaussian_matrix(m, n)
+    u, v, s = exact_warm(O, w, r)
+    op = G.DenseOperator(w)
+    bad = w.copy()
+    bad[3, 4] = np.inf
+    hb, hg = _pinned_colmajor(bad), _pinned_colmajor(w)
+    op.assign_async(hb.data_ptr(), m)
+    for _ in range(2):
+        with pytest.raises(ValueError):
+            G.blws_svd(op, G.WarmStart(u, v, s), 2, r, G.Rng(3))
+    op.assign_async(hg.data_ptr(), m)
+    got = G.blws_svd(op, G.WarmStart(u, v, s), 2, r, G.Rng(3))
+    ref = O.blws_svd(O.DenseOperator(w), O.WarmStart(u, v, s), 2, r, O.Rng(3))
+    assert np.abs(got.warm.sigma - ref.warm.sigma).max() <= 1e-10 * ref.warm.sigma.max()
 
 
 def test_assign_async_double_buffered_solves(G, O):
@@ -343,3 +369,38 @@ def test_graph_cache_is_bounded_and_exact(G, O, monkeypatch):
         ref = G.blws_svd(plain, warm, 2, r, G.Rng(1))
         for o in res:
             assert np.array_equal(o.warm.sigma, ref.warm.sigma) and np.array_equal(o.warm.u, ref.warm.u)
+
+
+def test_sparse_graph_replay_across_widths(G, O, monkeypatch):
+    # a sparse operator's SpMM staging must not outlive a
+    # captured graph. Widths 8 -> 16 -> 8 -> 16 with each key captured and
+    # replayed (third call onwards); every replay must equal the graph-free path.
+    m, n, nnz = 600, 500, 60000
+    rng = O.Rng(77)
+    pos = O.sample_distinct(m * n, nnz, rng.split(1))
+    rows, cols = (pos % m).astype(np.int32), (pos // m).astype(np.int64)
+    vals = rng.split(2).gaussian_matrix(nnz, 1)[:, 0]
+    colptr = np.zeros(n + 1, dtype=np.int64)
+    np.add.at(colptr, cols + 1, 1)
+    colptr = np.cumsum(colptr)
+    dense = np.zeros((m, n))
+    dense[rows, cols] = vals
+    monkeypatch.delenv("BLWS_EXACT", raising=False)
+    monkeypatch.delenv("BLWS_GRAPHS", raising=False)
+    op = G.SparseOperator(m, n, colptr, rows, vals)
+    g0 = G.graph_launches()
+    warms = {}
+    outs = []
+    for r in (8, 16, 8, 16, 8):
+        if r not in warms:
+            u, v, s = exact_warm(O, dense + 1e-2 * rng.gaussian_matrix(m, n), r)
+            warms[r] = G.DeviceWarmStart.from_host(u, v, s, op.ctx)
+        outs.append((r, [G.blws_svd(op, warms[r], 2, r, G.Rng(1)) for _ in range(4)]))
+    assert G.graph_launches() > g0
+    monkeypatch.setenv("BLWS_GRAPHS", "0")
+    plain = G.SparseOperator(m, n, colptr, rows, vals)
+    for r, res in outs:
+        ref = G.blws_svd(plain, warms[r], 2, r, G.Rng(1))
+        for o in res:
+            assert np.array_equal(o.warm.sigma, ref.warm.sigma)
+            assert np.array_equal(o.warm.u, ref.warm.u) and np.array_equal(o.warm.v, ref.warm.v)

@@ -6,9 +6,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1012_0365_b200 as B  # noqa: E402
 
 ctx = B.Context(0)
-print("probe", ctx.probe(), flush=True)
 ctx.fp64_peak(0)
-print("probe after load", ctx.probe(), flush=True)
 for n in (32, 64, 100, 111, 200):
     d = ctx.microbench(0, n, 0, 20, detail=True)
     print(f"chol_inv n={n}: {d[0]:8.1f} us   diag {d[1]:.0f} chol {d[2]:.0f} inv {d[3]:.0f} "
