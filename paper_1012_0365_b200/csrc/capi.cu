@@ -708,7 +708,56 @@ extern "C" int blws_microbench(blws_context* ctx, int which, int64_t n, int64_t 
         BLWS_CUDA(cudaEventCreate(&e0));
         BLWS_CUDA(cudaEventCreate(&e1));
         float total = 0;
-        if (which == 0 || which == 1) {
+        if (which >= 5 && which <= 7) {
+            // cholqr_factor on G = A^T A + n I (5), I + 1e-12 E (6), 4 I (7)
+            fill_host(n * n);
+            DMat a(c, n, n), g0(c, n, n), work(c, n, n), rinv(c, n, n);
+            upload(c, a.view(), h.data(), n);
+            if (which == 5) {
+                gemm(c, true, false, n, n, n, 1.0, a.data(), a.ld, a.data(), a.ld, 0.0, g0.data(), g0.ld);
+            } else {
+                symmetrize(c, g0.view(), a.view());
+                DMat id(c, n, n);
+                std::vector<double> eye(static_cast<size_t>(n * n), 0.0);
+                for (Index i = 0; i < n; ++i) eye[static_cast<size_t>(i + i * n)] = which == 6 ? 1.0 : 4.0;
+                upload(c, id.view(), eye.data(), n);
+                copy(c, g0.view(), g0.view(), which == 6 ? 1e-12 : 0.0);
+                axpy(c, g0.view(), id.view(), 1.0);
+            }
+            DBuf<int> st(c, 1);
+            DBuf<double> dg(c, 8);
+            for (int r = -1; r < reps; ++r) {
+                copy(c, work.view(), g0.view());
+                BLWS_CUDA(cudaEventRecord(e0, c.stream()));
+                cholqr_factor(c, work.view(), rinv.view(), nullptr, 0, nullptr, st.get(), dg.get(), dg.get() + 2,
+                              nullptr, nullptr);
+                BLWS_CUDA(cudaEventRecord(e1, c.stream()));
+                BLWS_CUDA(cudaEventSynchronize(e1));
+                float ms = 0;
+                BLWS_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+                if (r >= 0) total += ms;
+            }
+            int hst = 0;
+            BLWS_CUDA(cudaMemcpy(&hst, st.get(), sizeof(int), cudaMemcpyDeviceToHost));
+            us[1] = hst;  // factor status (0 ok)
+        } else if (which == 8 || which == 9) {
+            // 8: Gram X^T X of an n x b panel; 9: X * R (n x b times b x b)
+            fill_host(n * b);
+            DMat x(c, n, b), y(c, n, b), gg(c, b, b);
+            upload(c, x.view(), h.data(), n);
+            for (int r = -1; r < reps; ++r) {
+                BLWS_CUDA(cudaEventRecord(e0, c.stream()));
+                if (which == 8)
+                    gemm(c, true, false, b, b, n, 1.0, x.data(), x.ld, x.data(), x.ld, 0.0, gg.data(), gg.ld);
+                else
+                    gemm(c, false, false, n, b, b, 1.0, x.data(), x.ld, gg.data(), gg.ld, 0.0, y.data(), y.ld);
+                BLWS_CUDA(cudaEventRecord(e1, c.stream()));
+                BLWS_CUDA(cudaEventSynchronize(e1));
+                float ms = 0;
+                BLWS_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+                if (r >= 0) total += ms;
+            }
+        } else if (which == 0 || which == 1) {
             fill_host(n * n);
             DMat a(c, n, n), s(c, n, n), g0(c, n, n), work(c, n, n), rinv(c, n, n), vec(c, n, std::max<int64_t>(1, n / 2));
             upload(c, a.view(), h.data(), n);

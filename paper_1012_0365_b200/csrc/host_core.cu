@@ -455,6 +455,31 @@ constexpr double kSkipRel = 1e-14;  // CholQR pass skip: ||G - cI||_F <= 1e-14 c
 // R = chol(G) in place (or sqrt(c) I for a scaled-identity Gram), Rinv = R^{-1};
 // reads back status, diag range and tr(G) (one sync). `trace_dev`, if set,
 // receives tr(G) on the device too (the rank threshold reads it there).
+// the same through cholqr_factor (b <= 112): with r_prev, also R_total =
+// R * R_prev into *r_total and its rank into *rank_dev (the deferred path's
+// second pass, so both paths stay bitwise identical)
+CholStep chol_step_q(Context& ctx, DMat g, double* trace_dev, double* trace_host, const DMat* r_prev = nullptr,
+                     View* r_total = nullptr, const double* trace_ref = nullptr, std::int64_t* rank_dev = nullptr) {
+    CholStep s;
+    const Index b = g.rows;
+    s.r = std::move(g);
+    s.rinv = DMat(ctx, b, b, false);
+    DBuf<int> status(ctx, 1);
+    DBuf<double> diag(ctx, 3);
+    cholqr_factor(ctx, s.r.view(), s.rinv.view(), r_prev ? r_prev->data() : nullptr, r_prev ? r_prev->ld : 0,
+                  r_total, status.get(), diag.get(), diag.get() + 2, trace_ref, rank_dev);
+    if (trace_dev) copy(ctx, View{trace_dev, 1, 1, 2}, View{diag.get() + 2, 1, 1, 2});
+    int st = 0;
+    double dd[3] = {0, 0, 0};
+    BLWS_CUDA(cudaMemcpyAsync(&st, status.get(), sizeof(int), cudaMemcpyDeviceToHost, ctx.stream()));
+    ctx.read(diag.get(), dd, 3);
+    s.ok = st == 0;
+    s.dmin = dd[0];
+    s.dmax = dd[1];
+    if (trace_host) *trace_host = dd[2];
+    return s;
+}
+
 CholStep chol_step(Context& ctx, DMat g, double* trace_dev = nullptr, double* trace_host = nullptr) {
     CholStep s;
     const Index b = g.rows;
@@ -566,10 +591,26 @@ Index thin_qr_impl(Context& ctx, View x, View* r_out, RowSplit split) {
     DBuf<double> ss(ctx, 2);  // ss[0] = ||X||_F^2 = tr(X^T X)
     std::vector<CholStep> steps;
     double hss = 0;
-    CholStep s1 = chol_step(ctx, gram(ctx, x, split), ss.get(), &hss);
+    const bool q = cholqr_factor_fits(b);
+    CholStep s1 = q ? chol_step_q(ctx, gram(ctx, x, split), ss.get(), &hss)
+                    : chol_step(ctx, gram(ctx, x, split), ss.get(), &hss);
     if (!std::isfinite(hss)) throw std::invalid_argument("thin_qr: non-finite entries");
     const bool ill = !s1.ok || !(s1.dmin > 0) || s1.dmax / s1.dmin > 1e6;
     DMat y(ctx, rows, b, false);
+    if (!ill && q) {
+        gemm(ctx, false, false, rows, b, b, 1.0, x.p, x.ld, s1.rinv.data(), s1.rinv.ld, 0.0, y.data(), y.ld);
+        DMat rt(ctx, b, b, false);
+        View rtv = rt.view();
+        DBuf<std::int64_t> rank(ctx, 1);
+        CholStep s2 = chol_step_q(ctx, gram(ctx, y.view(), split), nullptr, nullptr, &s1.r, &rtv, ss.get(),
+                                  rank.get());
+        if (!s2.ok) throw NumericalError("thin_qr: CholQR2 second pass failed");
+        gemm(ctx, false, false, rows, b, b, 1.0, y.data(), y.ld, s2.rinv.data(), s2.rinv.ld, 0.0, x.p, x.ld);
+        std::int64_t hr = 0;
+        ctx.read_i64(rank.get(), &hr, 1);
+        if (r_out) copy(ctx, *r_out, rtv);
+        return hr;
+    }
     if (!ill) {
         gemm(ctx, false, false, rows, b, b, 1.0, x.p, x.ld, s1.rinv.data(), s1.rinv.ld, 0.0, y.data(), y.ld);
         steps.push_back(std::move(s1));
@@ -885,9 +926,23 @@ QrRec thin_qr_deferred(Context& ctx, View x, View* r_out, Slots& sl, RowSplit sp
     ctx.region_begin(2);
     DMat r1 = gram(ctx, x, split);
     DMat ri1(ctx, b, b, false);
+    DMat y(ctx, rows, b, false);
+    if (cholqr_factor_fits(b)) {
+        // one launch per pass (cholqr.cu): factor + inverse, and in the second
+        // pass R = R2 R1 and the rank count as well
+        cholqr_factor(ctx, r1.view(), ri1.view(), nullptr, 0, nullptr, reinterpret_cast<int*>(sl.at(q.st1)),
+                      sl.at(q.dg1), sl.at(q.hss), nullptr, nullptr);
+        gemm(ctx, false, false, rows, b, b, 1.0, x.p, x.ld, ri1.data(), ri1.ld, 0.0, y.data(), y.ld);
+        DMat r2 = gram(ctx, y.view(), split);
+        DMat ri2(ctx, b, b, false);
+        cholqr_factor(ctx, r2.view(), ri2.view(), r1.data(), r1.ld, r_out, reinterpret_cast<int*>(sl.at(q.st2)),
+                      sl.at(q.dg2), sl.at(q.dg2 + 2), sl.at(q.hss), reinterpret_cast<std::int64_t*>(sl.at(q.rank)));
+        gemm(ctx, false, false, rows, b, b, 1.0, y.data(), y.ld, ri2.data(), ri2.ld, 0.0, x.p, x.ld);
+        ctx.region_end(2, 0.0, 0.0);
+        return q;
+    }
     chol_inv_upper(ctx, r1.view(), ri1.view(), reinterpret_cast<int*>(sl.at(q.st1)), sl.at(q.dg1), kSkipRel,
                    sl.at(q.hss));
-    DMat y(ctx, rows, b, false);
     gemm(ctx, false, false, rows, b, b, 1.0, x.p, x.ld, ri1.data(), ri1.ld, 0.0, y.data(), y.ld);
     DMat r2 = gram(ctx, y.view(), split);
     DMat ri2(ctx, b, b, false);

@@ -63,6 +63,14 @@ void potrf_upper(Context& ctx, View g, int* status, double* diag);
 /// factorising (device-predicated CholQR pass skip); tr(G) -> *trace_out if set.
 void chol_inv_upper(Context& ctx, View g, View rinv, int* status, double* diag, double skip_rel = 0.0,
                     double* trace_out = nullptr);
+/// One CholQR pass factor for n <= 112 (cholqr.cu): G <- R (upper), rinv <-
+/// R^{-1}; with r_prev, r_out <- R * r_prev (upper) when r_out is set and
+/// rank_out <- #diag(R * r_prev) > 1e-12 sqrt(trace_ref[0]) (trace_ref = null:
+/// this G's trace). The factorisation (scaled identity / near identity / blocked
+/// Cholesky) is picked on the device; status, diag, trace_out as chol_inv_upper.
+bool cholqr_factor_fits(Index n);
+void cholqr_factor(Context& ctx, View g, View rinv, const double* r_prev, Index ldp, View* r_out, int* status,
+                   double* diag, double* trace_out, const double* trace_ref, std::int64_t* rank_out);
 /// R^{-1} of an upper-triangular n x n R (out may not alias r).
 void trtri_upper(Context& ctx, View out, View r);
 /// C = A * B for upper-triangular n x n A, B (C upper triangular).

@@ -234,3 +234,28 @@ def test_tall_skinny_gemm_edges(gpu, ta, m, n, k):
     got = Ct[:, :m].cpu().numpy().T
     assert np.abs(got - ref).max() <= 1e-12 * max(1.0, np.abs(ref).max()) * np.sqrt(k)
     assert torch.all(Ct[:, m:] == 0)  # the padding rows are left alone
+
+
+@pytest.mark.parametrize("m,b", [(600, 16), (3000, 100), (2000, 111), (900, 37), (400, 112), (300, 113)])
+@pytest.mark.parametrize("kind", ["orthonormal", "near", "general", "graded"])
+def test_thin_qr_factor_modes(gpu, O, m, b, kind):
+    # cholqr.cu picks the factorisation on the device: a scaled-identity Gram
+    # (skip), a near-identity Gram (closed form I + F, ||E|| <= 1e-9), or the
+    # blocked Cholesky; b = 113 takes the chol_inv_upper path. Every mode must
+    # reproduce the oracle's Householder Q / R.
+    rng = O.Rng(1000 + m + b)
+    a = rng.gaussian_matrix(m, b)
+    if kind in ("orthonormal", "near"):
+        a = O.thin_qr(a).q * 3.0
+        if kind == "near":
+            a = a + 1e-12 * rng.gaussian_matrix(m, b)
+    elif kind == "graded":
+        a = a * np.logspace(0, -4, b)
+    q, r, rank = gpu.thin_qr(a)
+    ref = O.thin_qr(a)
+    assert rank == ref.rank == b
+    assert np.linalg.norm(q.T @ q - np.eye(b)) <= 1e-13
+    assert np.linalg.norm(a - q @ r) <= 1e-13 * np.linalg.norm(a)
+    assert np.allclose(np.tril(r, -1), 0.0) and np.all(np.diag(r) > 0)
+    assert np.abs(q - ref.q).max() <= 1e-9
+    assert np.abs(r - ref.r).max() <= 1e-12 * np.abs(ref.r).max()
