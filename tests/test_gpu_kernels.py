@@ -259,3 +259,32 @@ def test_thin_qr_factor_modes(gpu, O, m, b, kind):
     assert np.allclose(np.tril(r, -1), 0.0) and np.all(np.diag(r) > 0)
     assert np.abs(q - ref.q).max() <= 1e-9
     assert np.abs(r - ref.r).max() <= 1e-12 * np.abs(ref.r).max()
+
+
+@pytest.mark.parametrize("m,n,k,sym", [(100, 100, 8000, True), (100, 100, 8000, False), (7, 13, 300, False),
+                                       (128, 128, 5000, True), (111, 111, 2001, True), (64, 32, 777, False)])
+def test_dgemm_tn_small_output(gpu, m, n, k, sym):
+    # the K2 Grams / projections: A^T B with M, N <= 128 over many rows (split-K
+    # with a deterministic reduction); beta != 0, ragged K, a Gram (A == B), and
+    # the result bitwise reproducible run to run (fixed reduction order)
+    import torch
+
+    rs = np.random.default_rng(m + 5 * n + k)
+    A = rs.standard_normal((k, m))
+    B = A if sym else rs.standard_normal((k, n))
+    C0 = rs.standard_normal((m, n))
+    ref = 0.75 * (A.T @ B) + 0.25 * C0
+    dev = torch.device("cuda:0")
+    At = torch.tensor(A.T.copy(), device=dev)
+    Bt = At if sym else torch.tensor(B.T.copy(), device=dev)
+    outs = []
+    for _ in range(2):
+        Ct = torch.tensor(C0.T.copy(), device=dev)
+        gpu.api.dgemm(True, False, m, n, k, 0.75, At, k, Bt, k, 0.25, Ct, m)
+        torch.cuda.synchronize()
+        outs.append(Ct.cpu().numpy().T)
+    assert np.abs(outs[0] - ref).max() <= 1e-12 * max(1.0, np.abs(ref).max()) * np.sqrt(k)
+    assert np.array_equal(outs[0], outs[1])
+    if sym:
+        assert np.array_equal(outs[0] - 0.25 * C0, (outs[0] - 0.25 * C0).T) or np.abs(
+            (outs[0] - 0.25 * C0) - (outs[0] - 0.25 * C0).T).max() <= 1e-12 * np.abs(ref).max()
