@@ -47,6 +47,24 @@ constexpr int kFW = kFT / 32;
 
 __device__ __forceinline__ int floff(int j, int n) { return j * n - ((j * (j - 1)) >> 1); }
 
+// 1/sqrt(x), 1/x for positive / nonzero normal x: MUFU approximation + Newton
+// (within an ulp; every BLWS path uses the same kernel)
+__device__ __forceinline__ double rsqrt_nr(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    const double hx = 0.5 * x;
+    y = y * fma(-hx * y, y, 1.5);
+    y = y * fma(-hx * y, y, 1.5);
+    return y;
+}
+__device__ __forceinline__ double rcp_nr(double x) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    y = y * fma(-x, y, 2.0);
+    y = y * fma(-x, y, 2.0);
+    return fma(y, fma(-x, y, 1.0), y);
+}
+
 __device__ __forceinline__ double warp_sum(double x) {
     for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
     return x;
@@ -59,21 +77,17 @@ __device__ __forceinline__ void form_reflector(double* a, int n, int c, double s
                                                double* e, double* tau, double* tau_out) {
     const int i = threadIdx.x;
     double* colc = a + floff(c, n);  // colc[r - c] = A(r, c)
-    // the scalar chain (sqrt, two divides) once per warp, then broadcast: 512
-    // redundant copies would queue on the slow double-precision units
-    double tk = 0.0, beta = 0.0, scl = 0.0;
-    if ((threadIdx.x & 31) == 0) {
-        const double alpha = colc[1];
-        beta = alpha;
-        if (s2 > 0.0) {
-            beta = -copysign(sqrt(fma(alpha, alpha, s2)), alpha);
-            tk = (beta - alpha) / beta;
-            scl = 1.0 / (alpha - beta);
-        }
-    }
-    tk = __shfl_sync(0xffffffffu, tk, 0);
-    beta = __shfl_sync(0xffffffffu, beta, 0);
-    scl = __shfl_sync(0xffffffffu, scl, 0);
+    // the scalar chain on every thread, branch-free: MUFU rsqrt / rcp refined by
+    // Newton steps (no IEEE div / sqrt slow-path calls, no lane-0 divergence
+    // and shuffle broadcast; measured 1361 -> see DESIGN cycles per step)
+    const double alpha = colc[1];
+    const double nrm2 = fma(alpha, alpha, s2);
+    const bool refl = s2 > 0.0;
+    const double rn = rsqrt_nr(refl ? nrm2 : 1.0);         // 1 / ||x||
+    const double sg = alpha >= 0.0 ? 1.0 : -1.0;           // copysign(1, alpha) for finite alpha
+    const double beta = refl ? -sg * nrm2 * rn : alpha;    // -sign(alpha) ||x||
+    const double tk = refl ? fma(alpha, sg * rn, 1.0) : 0.0;  // (beta - alpha) / beta = 1 + alpha sign / ||x||
+    const double scl = refl ? rcp_nr(alpha - beta) : 0.0;
     if (i < n) {
         double vi = 0.0;
         if (i > c) vi = tk == 0.0 ? 0.0 : (i == c + 1 ? 1.0 : xi * scl);
