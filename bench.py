@@ -210,10 +210,49 @@ def parity_vs_oracle(gpu_out, gpu_flags, ref, eps):
             "achieved_rank": list(ach)}
 
 
+def run_reference_c5(args):
+    """--impl reference for --mode sharded: the oracle's blws_svd on the same
+    C5-scale W (generated with the same seeded device generators when a GPU is
+    present, downloaded to the host), all host threads, a bounded sample of one
+    call per step."""
+    import torch
+
+    from oracle import oracle as O
+
+    m, r = args.m, args.r
+    dev = torch.device("cuda:0") if torch.cuda.is_available() else torch.device("cpu")
+    Wt, Uw, Vw, sigma, _, _ = c5_inputs(m, r, 0, m, dev)
+    W = Wt.cpu().numpy().T  # column-major view of the row-major (n, m) tensor
+    U, V, s = np.asfortranarray(Uw.cpu().numpy()), np.asfortranarray(Vw.cpu().numpy()), sigma[:r].cpu().numpy()
+    del Wt
+    cores = os.cpu_count() or 1
+    O.set_threads(cores)
+    op = O.DenseOperator(W)
+    warm = O.WarmStart(U, V, s)
+    steps = max(1, min(args.steps, 2))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        O.blws_svd(op, warm, 2, r, O.Rng(SEED ^ 0x5BDBEEF))
+    dt = time.perf_counter() - t0
+    value = steps / dt
+    emit({"metric": METRIC.replace("C2: 4000x4000", f"row-sharded {m}x{m}").replace("r=100", f"r={r}"),
+          "value": value, "unit": "calls/s", "n_gpus": args.gpus, "steps": steps, "warmup": 0,
+          "ms_per_step": 1e3 * dt / steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+          "dtype": "f64", "data": "synthetic (seeded torch Philox, same instance as the GPU arm)",
+          "config": {"workload": "C5-scale standalone BLWS partial SVT", "m": m, "n": m, "r": r, "k": 2},
+          "impl": "reference",
+          "cpu_baseline": {"value": value, "unit": "calls/s", "cores": cores, "kind": "port",
+                           "sample": f"{steps} oracle blws_svd call(s) on the {m}x{m} W (OpenBLAS, {cores} threads)"},
+          "e2e": {"value": value, "unit": "calls/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
+    return 0
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
+    if args.mode == "sharded":
+        return run_reference_c5(args)
     from oracle import oracle as O
 
     W, U, V, s, _ = make_instance(O.Rng)
@@ -258,7 +297,7 @@ def run_gpu(args):
     dev = torch.device(f"cuda:{local}")
     ctx = B.Context(local)
     stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
-    sharded = args.mode == "sharded"
+    sharded = args.mode == "sharded-c2"
 
     W, U, V, s, _ = make_instance(B.Rng)
     row0, rows = 0, M
@@ -488,6 +527,169 @@ def solver_configs():
     return out
 
 
+def _chunked_noise(rows0, rows, n, seed, dev, chunk=512):
+    """1e-3-scaled N(0,1) rows [rows0, rows0 + rows) of an m x n noise matrix,
+    generated in fixed 512-row chunks (torch Philox, one seed per chunk), so a
+    row shard equals the same rows of the whole matrix on any rank count."""
+    import torch
+
+    out = torch.empty((rows, n), dtype=torch.float64, device=dev)
+    c0, c1 = rows0 // chunk, (rows0 + rows - 1) // chunk
+    for c in range(c0, c1 + 1):
+        g = torch.Generator(device=dev).manual_seed(seed * 1_000_003 + c)
+        blk = torch.randn((chunk, n), dtype=torch.float64, device=dev, generator=g)
+        a, b = max(rows0, c * chunk), min(rows0 + rows, (c + 1) * chunk)
+        out[a - rows0:b - rows0] = blk[a - c * chunk:b - c * chunk]
+    return out.mul_(1e-3)
+
+
+def _haar(m, k, seed, dev):
+    import torch
+
+    g = torch.Generator(device=dev).manual_seed(seed)
+    q, r = torch.linalg.qr(torch.randn((m, k), dtype=torch.float64, device=dev, generator=g))
+    return q * torch.where(torch.diagonal(r) < 0, -1.0, 1.0)
+
+
+def c5_inputs(m, r, row0, rows, dev):
+    """The --mode sharded instance (see run_sharded_c5) on device `dev`: this
+    rank's column-major W panel as a row-major (n, rows) tensor, the warm start
+    (Uw, Vw full), sigma, and the Haar factors."""
+    import torch
+
+    n, ks = m, 2 * r
+    # C2's spectrum shape stretched to rank r: sigma_i = 100 * 0.97^(100 i / r)
+    sigma = 100.0 * 0.97 ** (torch.arange(ks, dtype=torch.float64, device=dev) * (100.0 / r))
+    U0 = _haar(m, ks, SEED, dev)
+    V0 = _haar(n, ks, SEED + 1, dev)
+    Wt = (V0 * sigma) @ U0[row0:row0 + rows].T
+    Wt += _chunked_noise(row0, rows, n, SEED + 2, dev).T
+    # the warm-start perturbation keeps C2's per-column size (1e-2 sqrt(4000) ~ 0.63)
+    eps = 1e-2 * (4000.0 / m) ** 0.5
+    gw = torch.Generator(device=dev).manual_seed(SEED + 3)
+    Uw = torch.linalg.qr(U0[:, :r] + eps * torch.randn((m, r), dtype=torch.float64, device=dev, generator=gw))[0]
+    Vw = torch.linalg.qr(V0[:, :r] + eps * torch.randn((n, r), dtype=torch.float64, device=dev, generator=gw))[0]
+    return Wt.contiguous(), Uw, Vw, sigma, U0, V0
+
+
+def run_sharded_c5(args):
+    """Row-sharded strong scaling on a C5-scale standalone BLWS call:
+    W (m x m, default 40000^2 as BASELINE configs[4]) = U0 diag(sigma) V0^T +
+    1e-3 N(0,1), U0 / V0 Haar m x 2r, sigma_i = 100 * 0.97^(100 i / r), r = 400 (C5's
+    rank), warm start QR(U0[:, :r] + eps N) / likewise V with eps = 1e-2
+    sqrt(4000 / m) (C2's per-column perturbation). Rank p holds rows
+    [row0, row0 + rows) of W and U (V replicated); blws_svd allreduces the
+    W^T U partials and every panel reduction over NCCL. Inputs are generated
+    on the devices with seeded torch generators (chunked, so every rank count
+    sees the same W). After the timed calls rank 0 runs the same call on the
+    whole (unsharded) W and reports the singular-value agreement with N = 1."""
+    import torch
+
+    import paper_1012_0365_b200 as B
+    from paper_1012_0365_b200 import dist as D
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    if world > 1:
+        import torch.distributed as tdist
+
+        tdist.init_process_group("nccl", device_id=dev)
+    m = n = args.m
+    r = args.r
+    ks = 2 * r
+    ctx = B.Context(local)
+    if world > 1:
+        D.init_comm(ctx)
+    else:
+        ctx.init_comm(1, 0, B.api.nccl_unique_id())
+    row0, rows = D.row_partition(m, world, rank)
+    Wt, Uw, Vw, sigma, U0, V0 = c5_inputs(m, r, row0, rows, dev)
+    u_loc = np.asfortranarray(Uw[row0:row0 + rows].cpu().numpy())
+    v_all = np.asfortranarray(Vw.cpu().numpy())
+    s_warm = sigma[:r].cpu().numpy()
+    op = B.DenseOperator(Wt, ctx=ctx, device=True, shape=(rows, n), ld=rows)
+    op.set_row_shard(m, row0)
+    warm0 = B.DeviceWarmStart.from_host(u_loc, v_all, s_warm, ctx)
+    for _ in range(max(1, args.warmup)):
+        res = B.blws_svd(op, warm0, 2, r, B.Rng(SEED ^ 0x5BDBEEF), keep_device=True)
+    ctx.synchronize()
+    launches0 = ctx.launches
+    stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        with torch.cuda.stream(stream):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+        for _ in range(args.steps):
+            res = B.blws_svd(op, warm0, 2, r, B.Rng(SEED ^ 0x5BDBEEF), keep_device=True)
+        with torch.cuda.stream(stream):
+            e1.record(stream)
+        ctx.synchronize()
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    launches = ctx.launches - launches0
+    sig_sharded = res.warm.sigma()
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    ms = float(t[0])
+    parity = None
+    if rank == 0:
+        # N = 1 reference: the whole W on this GPU, unsharded operator, same call
+        del Wt
+        torch.cuda.empty_cache()
+        Wf = c5_inputs(m, r, 0, m, dev)[0]
+        ctx1 = B.Context(local)
+        op1 = B.DenseOperator(Wf.contiguous(), ctx=ctx1, device=True, shape=(m, n), ld=m)
+        w1 = B.DeviceWarmStart.from_host(np.asfortranarray(Uw.cpu().numpy()), v_all, s_warm, ctx1)
+        s1 = B.blws_svd(op1, w1, 2, r, B.Rng(SEED ^ 0x5BDBEEF), keep_device=True).warm.sigma()
+        same = s1.size == sig_sharded.size and s1.size > 0
+        big = np.abs(s1) >= 1e-8 * np.abs(s1).max() if same else None
+        rel = float(np.max(np.abs(sig_sharded - s1)[big] / np.abs(s1[big]))) if same else float("inf")
+        rel1 = float(np.max(np.abs(sig_sharded - s1)) / np.abs(s1).max()) if same else float("inf")
+        parity = {"status": "green" if rel <= 1e-10 and rel1 <= 1e-12 else "red",
+                  "against": "the same call on the whole W, 1 GPU", "sigma_max_rel_err": rel,
+                  "sigma_tol": 1e-10, "sigma_max_err_rel_sigma1": rel1, "keep": [int(sig_sharded.size), int(s1.size)]}
+        line = {"metric": METRIC.replace("C2: 4000x4000", f"row-sharded {m}x{n}").replace("r=100", f"r={r}"),
+                "value": args.steps / (ms / 1e3), "unit": "calls/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded torch Philox on device, chunked by 512 rows)",
+                "config": {"workload": f"C5-scale standalone BLWS partial SVT, W row-sharded x{world}",
+                           "m": m, "n": n, "r": r, "k": 2, "signal_rank": ks,
+                           "parallelism": f"rowshard x{world} (NCCL allreduce of W^T U and panel reductions)",
+                           "l2": f"W {m * n * 8 / 1e9:.1f} GB >> L2"},
+                "gpu_launches": launches, "parity_vs_n1": parity, "clocks": clocks.summary(),
+                "nccl": {"ranks": world, "backend": "NCCL (dlopen, torch-bundled)"}}
+        emit(line)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def self_launch(args):
+    """`bench.py --gpus N` without a torchrun environment: launch N ranks here
+    (127.0.0.1 rendezvous) and pass rank 0's JSON line through."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # the driver can see N ranks and the transport in stderr
+    proc = subprocess.run(cmd, env=env, stdout=subprocess.PIPE, text=True)
+    for line in proc.stdout.splitlines():
+        if line.startswith("{"):
+            print(line, file=_JSON_OUT or sys.stdout, flush=True)
+    return proc.returncode
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -496,13 +698,22 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-solves", action="store_true", help="skip the C1 / C3 / C4 solve-time leg")
-    ap.add_argument("--mode", default="replicas", choices=["replicas", "sharded"],
-                    help="replicas: N independent C2 calls per step (weak scaling, default); sharded: one C2 "
-                         "call with W row-sharded over the N GPUs (strong scaling)")
+    ap.add_argument("--mode", default=None, choices=["replicas", "sharded", "sharded-c2"],
+                    help="replicas: N independent C2 calls per step (weak scaling; default at N = 1); sharded: "
+                         "one C5-scale call with W row-sharded over the N GPUs (strong scaling; default at N > 1); "
+                         "sharded-c2: the C2 call row-sharded")
+    ap.add_argument("--m", type=int, default=40000, help="order of W in --mode sharded (BASELINE configs[4]: 40000)")
+    ap.add_argument("--r", type=int, default=400, help="rank r of the --mode sharded call (C5: 400)")
     args = ap.parse_args()
+    if args.mode is None:
+        args.mode = "replicas" if args.gpus == 1 else "sharded"
     _stdout_to_stderr()
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args)
+    if args.mode == "sharded":
+        return run_sharded_c5(args)
     return run_gpu(args)
 
 

@@ -392,3 +392,18 @@ def test_shard_csc_roundtrip():
         assert np.array_equal(lv, vals[pos]) and np.array_equal(lr + row0, rowidx[pos])
         assert np.all(np.diff(lp) >= 0)
     assert np.all(seen == 1)
+
+
+def test_bench_sharded_inputs_are_rank_count_independent():
+    # bench.py --mode sharded generates W per rank in 512-row chunks: the
+    # shards of any rank count concatenate to the whole matrix
+    import torch
+
+    import bench
+    from paper_1012_0365_b200 import dist as D
+
+    m, n = 1300, 40
+    full = bench._chunked_noise(0, m, n, 7, torch.device("cpu"))
+    for world in (1, 2, 3, 8):
+        parts = [bench._chunked_noise(*D.row_partition(m, world, r), n, 7, torch.device("cpu")) for r in range(world)]
+        assert torch.equal(torch.cat(parts), full)
