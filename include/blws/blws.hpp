@@ -18,6 +18,7 @@
 #ifndef BLWS_BLWS_HPP
 #define BLWS_BLWS_HPP
 
+#include <cmath>
 #include <cstdint>
 #include <memory>
 #include <optional>
@@ -49,6 +50,17 @@ struct Matrix {
     double operator()(Index i, Index j) const { return data[static_cast<size_t>(i + j * rows)]; }
 };
 
+/// Compressed sparse column matrix (the reference's SparseMatrix<double>,
+/// Eigen's default column-major storage): colptr (cols + 1), row indices
+/// sorted within a column, values in the same order.
+struct SparseMatrix {
+    Index rows = 0, cols = 0;
+    std::vector<std::int64_t> colptr;
+    std::vector<std::int32_t> rowidx;
+    std::vector<double> values;
+    Index nonZeros() const { return static_cast<Index>(values.size()); }
+};
+
 /// One device context per solve.
 class Context {
 public:
@@ -66,6 +78,14 @@ private:
     };
     std::unique_ptr<blws_context, Del> h_;
 };
+
+/// The process-wide context on device 0 that the reference-shaped overloads
+/// (no Context argument) use; created on first use and never destroyed (its
+/// teardown would race the CUDA runtime's own at process exit).
+inline Context& default_context() {
+    static Context* ctx = new Context(0);
+    return *ctx;
+}
 
 class Rng {
 public:
@@ -117,6 +137,8 @@ protected:
 
 class DenseOperator : public LinearOperator {
 public:
+    /// DenseOperator(W) (linear_operator.hpp:109) on the default context
+    explicit DenseOperator(const Matrix& w) : DenseOperator(default_context(), w) {}
     DenseOperator(Context& ctx, const Matrix& w) : LinearOperator(ctx) {
         blws_operator* o = nullptr;
         check(blws_dense_operator_create(ctx.get(), w.rows, w.cols, w.data.data(), w.rows, BLWS_HOST, 0, &o));
@@ -133,6 +155,10 @@ public:
 
 class SparseOperator : public LinearOperator {
 public:
+    /// SparseOperator(S) (linear_operator.hpp:141) on the default context
+    explicit SparseOperator(const SparseMatrix& s) : SparseOperator(default_context(), s) {}
+    SparseOperator(Context& ctx, const SparseMatrix& s)
+        : SparseOperator(ctx, s.rows, s.cols, s.colptr, s.rowidx, s.values) {}
     SparseOperator(Context& ctx, Index m, Index n, const std::vector<std::int64_t>& colptr,
                    const std::vector<std::int32_t>& rowidx, const std::vector<double>& values)
         : LinearOperator(ctx), nnz_(static_cast<Index>(values.size())) {
@@ -224,7 +250,7 @@ struct RankPredictor {
 
 class SvdBackend {
 public:
-    enum class Kind { Lanczos = BLWS_BACKEND_LANCZOS, Blws = BLWS_BACKEND_BLWS };
+    enum class Kind { ExactFull = BLWS_BACKEND_EXACT_FULL, Lanczos = BLWS_BACKEND_LANCZOS, Blws = BLWS_BACKEND_BLWS };
     struct Options {
         Index block_steps = 2;
         double ritz_tol = 1e-8;
@@ -232,6 +258,14 @@ public:
         Index seed_margin = 5;
         std::uint64_t seed = 0xb10c;
     };
+    // svt.hpp:96-98: the reference's factories, on the default context
+    static SvdBackend exact_full() { return SvdBackend(default_context(), Kind::ExactFull, Options()); }
+    static SvdBackend lanczos(Options o) { return SvdBackend(default_context(), Kind::Lanczos, o); }
+    static SvdBackend lanczos() { return SvdBackend(default_context(), Kind::Lanczos, Options()); }
+    static SvdBackend blws(Options o) { return SvdBackend(default_context(), Kind::Blws, o); }
+    static SvdBackend blws() { return SvdBackend(default_context(), Kind::Blws, Options()); }
+    // the same on an explicit context (one context per solve)
+    static SvdBackend exact_full(Context& ctx) { return SvdBackend(ctx, Kind::ExactFull, Options()); }
     static SvdBackend blws(Context& ctx, Options o) { return SvdBackend(ctx, Kind::Blws, o); }
     static SvdBackend blws(Context& ctx) { return SvdBackend(ctx, Kind::Blws, Options()); }
     static SvdBackend lanczos(Context& ctx, Options o) { return SvdBackend(ctx, Kind::Lanczos, o); }
@@ -302,8 +336,18 @@ struct RpcaOptions {
     const Matrix* truth = nullptr;
 };
 
+/// RpcaProblem (solvers.hpp:17-26)
+struct RpcaProblem {
+    Matrix d;           ///< square observation, low rank + sparse
+    double lambda = 0;  ///< sparsity weight; <= 0 selects 1/sqrt(m)
+    double effective_lambda() const { return lambda > 0 ? lambda : 1.0 / std::sqrt(static_cast<double>(d.rows)); }
+};
+
+/// RpcaSolution (solvers.hpp:49-54): A dense, E sparse (the nonzeros of the
+/// final shrink, column-major order, as solvers.hpp:133-146)
 struct RpcaSolution {
-    Matrix a, e;  // e dense (the reference returns the same values as a sparse matrix)
+    Matrix a;
+    SparseMatrix e;
     SolverStats stats;
 };
 
@@ -324,25 +368,52 @@ inline SolverStats stats(const blws_solver_stats& s, const std::vector<std::int6
     o.residual_history.assign(rh.begin(), rh.begin() + s.iterations);
     return o;
 }
+
+/// the nonzeros of a dense column-major m x n matrix as CSC (solvers.hpp:133-146)
+inline SparseMatrix sparse_from_dense(const std::vector<double>& e, Index m, Index n) {
+    SparseMatrix s;
+    s.rows = m;
+    s.cols = n;
+    s.colptr.assign(static_cast<size_t>(n + 1), 0);
+    for (Index j = 0; j < n; ++j) {
+        for (Index i = 0; i < m; ++i) {
+            const double v = e[static_cast<size_t>(i + j * m)];
+            if (v != 0.0) {
+                s.rowidx.push_back(static_cast<std::int32_t>(i));
+                s.values.push_back(v);
+            }
+        }
+        s.colptr[static_cast<size_t>(j + 1)] = static_cast<std::int64_t>(s.values.size());
+    }
+    return s;
+}
 }  // namespace detail
 
-/// rpca_adm (solvers.hpp:72-157); lambda <= 0 selects 1/sqrt(m)
-inline RpcaSolution rpca_adm(const Matrix& d, double lambda, SvdBackend& backend, const RpcaOptions& opts = {}) {
+/// rpca_adm (solvers.hpp:72-157) as the reference declares it; the solve runs
+/// on the backend's context
+inline RpcaSolution rpca_adm(const RpcaProblem& problem, SvdBackend& backend, const RpcaOptions& opts = {}) {
+    const Matrix& d = problem.d;
     const Index m = d.rows;
     if (d.rows != d.cols) throw std::invalid_argument("rpca_adm: D must be square");
     blws_rpca_options o{opts.tol_outer, opts.max_iter, opts.rho, opts.mu_max_factor, opts.initial_rank,
                         opts.rank_increment};
     RpcaSolution sol;
     sol.a = Matrix(m, m);
-    sol.e = Matrix(m, m);
+    std::vector<double> e(static_cast<size_t>(m * m));
     blws_solver_stats st{};
     std::vector<std::int64_t> pr(static_cast<size_t>(opts.max_iter + 1)), mh(pr.size());
     std::vector<double> rh(pr.size());
-    check(blws_rpca_adm(backend.context().get(), m, d.data.data(), m, BLWS_HOST, lambda, backend.get(), &o,
-                        opts.truth ? opts.truth->data.data() : nullptr, sol.a.data.data(), sol.e.data.data(), &st,
-                        pr.data(), mh.data(), rh.data(), static_cast<std::int64_t>(pr.size())));
+    check(blws_rpca_adm(backend.context().get(), m, d.data.data(), m, BLWS_HOST, problem.lambda, backend.get(), &o,
+                        opts.truth ? opts.truth->data.data() : nullptr, sol.a.data.data(), e.data(), &st, pr.data(),
+                        mh.data(), rh.data(), static_cast<std::int64_t>(pr.size())));
+    sol.e = detail::sparse_from_dense(e, m, m);
     sol.stats = detail::stats(st, pr, mh, rh);
     return sol;
+}
+
+/// the same with D and lambda given directly
+inline RpcaSolution rpca_adm(const Matrix& d, double lambda, SvdBackend& backend, const RpcaOptions& opts = {}) {
+    return rpca_adm(RpcaProblem{d, lambda}, backend, opts);
 }
 
 struct McOptions {
@@ -357,6 +428,13 @@ struct McSolution {
     Matrix u, v;
     std::vector<double> sigma;
     SolverStats stats;
+};
+
+/// McProblem (solvers.hpp:28-33)
+struct McProblem {
+    SparseMatrix observed;  ///< observed entries of A on the support
+    double tau = 0;         ///< threshold; <= 0 selects 5 m
+    double delta = 0;       ///< step size; <= 0 selects 1.2 m^2 / s
 };
 
 /// mc_svt (solvers.hpp:202-270); observation as CSC; tau/delta <= 0 select the defaults
@@ -386,6 +464,13 @@ inline McSolution mc_svt(Context& ctx, Index m, Index n, const std::vector<std::
     sol.sigma.resize(static_cast<size_t>(rank));
     sol.stats = detail::stats(st, pr, mh, rh);
     return sol;
+}
+
+/// mc_svt (solvers.hpp:202-270) as the reference declares it
+inline McSolution mc_svt(const McProblem& problem, SvdBackend& backend, const McOptions& opts = {}) {
+    const SparseMatrix& s = problem.observed;
+    return mc_svt(backend.context(), s.rows, s.cols, s.colptr, s.rowidx, s.values, problem.tau, problem.delta,
+                  backend, opts);
 }
 
 }  // namespace blws

@@ -193,6 +193,7 @@ int blws_dgemm(blws_context* ctx, int ta, int tb, int64_t m, int64_t n, int64_t 
 int blws_microbench(blws_context* ctx, int which, int64_t n, int64_t b, int reps, double* us);
 
 /* ------------------------------------------------------------ backend/svt */
+#define BLWS_BACKEND_EXACT_FULL 0 /* svt.hpp:108-116: dense full SVD (m + n <= 4096) */
 #define BLWS_BACKEND_LANCZOS 1
 #define BLWS_BACKEND_BLWS 2
 /* SvdBackend<double>::lanczos / ::blws (svt.hpp:84-98) with Options (:88-94). */

@@ -623,9 +623,9 @@ def dgemm(ta, tb, m, n, k, alpha, a, lda, b, ldb, beta, c, ldc, ctx: Context | N
 
 # ------------------------------------------------------------ backend / svt
 class SvdBackend:
-    """SvdBackend<double> (svt.hpp:84-196); kinds LANCZOS=1, BLWS=2."""
+    """SvdBackend<double> (svt.hpp:84-196); kinds EXACT_FULL=0, LANCZOS=1, BLWS=2."""
 
-    LANCZOS, BLWS = 1, 2
+    EXACT_FULL, LANCZOS, BLWS = 0, 1, 2
 
     def __init__(self, kind=2, block_steps=2, ritz_tol=1e-8, max_k=0, seed_margin=5, seed=0xB10C,
                  ctx: Context | None = None):
@@ -635,6 +635,11 @@ class SvdBackend:
                                              int(seed) & (2**64 - 1), C.byref(h)))
         self._h = h
         self.kind = kind
+
+    @classmethod
+    def exact_full(cls, **kw):
+        """svt.hpp:108-116: full SVD of the dense W on the device (m + n <= 4096)."""
+        return cls(kind=0, **kw)
 
     @classmethod
     def lanczos(cls, **kw):

@@ -524,8 +524,8 @@ int blws_dgemm(blws_context* ctx, int ta, int tb, int64_t m, int64_t n, int64_t 
 int blws_svd_backend_create(blws_context* ctx, int kind, int64_t block_steps, double ritz_tol, int64_t max_k,
                             int64_t seed_margin, uint64_t seed, blws_svd_backend** out) {
     return guard([&] {
-        need(kind == BLWS_BACKEND_LANCZOS || kind == BLWS_BACKEND_BLWS,
-             "SvdBackend: kind must be lanczos (1) or blws (2); exact-full is the CPU test oracle");
+        need(kind == BLWS_BACKEND_EXACT_FULL || kind == BLWS_BACKEND_LANCZOS || kind == BLWS_BACKEND_BLWS,
+             "SvdBackend: kind must be exact-full (0), lanczos (1) or blws (2)");
         SvdBackend::Options o;
         o.block_steps = block_steps;
         o.ritz_tol = ritz_tol;

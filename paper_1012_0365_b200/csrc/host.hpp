@@ -170,6 +170,7 @@ public:
     void assign_values_device(const double* vals_csc);
     void assign_values_host(const double* vals_csc);
     const double* val_csc() const { return val_csc_.get(); }
+    const std::int64_t* colptr_csc() const { return colptr_.get(); }
     const std::int32_t* rowidx_csc() const { return rowidx_.get(); }
     const std::int32_t* colof_csc() const { return colof_.get(); }
 
@@ -277,7 +278,8 @@ public:
         bool hit_cap = false;
         const DWarm& get() const { return held ? *held : own; }
     };
-    /// SvdBackend::compute (svt.hpp:104-186); ExactFull is not provided on the device.
+    /// SvdBackend::compute (svt.hpp:104-186). ExactFull runs the device
+    /// full_svd_small (small_dense.hpp:72-87, m + n <= 4096) on a dense copy.
     Triplets compute(LinearOperator& w, Index r);
     Kind kind() const { return kind_; }
     const std::optional<DWarm>& warm_state() const { return warm_; }

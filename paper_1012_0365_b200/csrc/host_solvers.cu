@@ -27,16 +27,50 @@ RankPredictor predict_rank(RankPredictor p, Index achieved, bool all_above) {
     return p;
 }
 
-SvdBackend::SvdBackend(Context& ctx, Kind k, Options o) : ctx_(ctx), kind_(k), opt_(o), rng_(o.seed) {
-    if (k == Kind::ExactFull)
-        throw std::invalid_argument("SvdBackend: ExactFull is the dense test oracle and has no device path");
+SvdBackend::SvdBackend(Context& ctx, Kind k, Options o) : ctx_(ctx), kind_(k), opt_(o), rng_(o.seed) {}
+
+namespace {
+// dense m x n copy of a CSC operator (ExactFull on a sparse W)
+__global__ void csc_to_dense_k(long n, const std::int64_t* colptr, const std::int32_t* rowidx, const double* val,
+                               double* out, long ld) {
+    for (long j = blockIdx.x; j < n; j += gridDim.x)
+        for (long q = colptr[j] + threadIdx.x; q < colptr[j + 1]; q += blockDim.x) out[rowidx[q] + j * ld] = val[q];
 }
+}  // namespace
 
 // svt.hpp:104-186
 SvdBackend::Triplets SvdBackend::compute(LinearOperator& w, Index r) {
     const Index p = std::min(global_rows(w), w.cols());
     if (r < 1 || r > p) throw std::invalid_argument("SvdBackend: bad r");
     Triplets t;
+    if (kind_ == Kind::ExactFull) {
+        // svt.hpp:108-116: full SVD of the dense W, top r triplets
+        if (w.row_sharded()) throw std::invalid_argument("SvdBackend: ExactFull on a row-sharded operator");
+        const Index m = w.rows(), n = w.cols();
+        DMat wd;
+        View wv;
+        if (auto* dop = dynamic_cast<DenseOperator*>(&w)) {
+            wv = dop->w();
+        } else if (auto* sop = dynamic_cast<SparseOperator*>(&w)) {
+            wd = DMat(ctx_, m, n, true);
+            csc_to_dense_k<<<static_cast<unsigned>(std::min<Index>(n, 4096)), 128, 0, ctx_.stream()>>>(
+                n, sop->colptr_csc(), sop->rowidx_csc(), sop->val_csc(), wd.data(), wd.ld);
+            ctx_.note_launch();
+            ctx_.check_launch("csc_to_dense");
+            wv = wd.view();
+        } else {
+            throw std::invalid_argument("SvdBackend: ExactFull needs a dense or sparse operator");
+        }
+        DWarm all = make_warm(ctx_, m, n, p);
+        DBuf<double> sig(ctx_, static_cast<size_t>(p));
+        full_svd_small(ctx_, wv, sig.get(), all.u(), all.v());
+        std::vector<double> hs(static_cast<size_t>(p));
+        ctx_.read(sig.get(), hs.data(), static_cast<size_t>(p));
+        t.own = copy_warm(ctx_, all, r);
+        t.own.sigma.assign(hs.begin(), hs.begin() + r);
+        t.converged = r;
+        return t;
+    }
     if (kind_ == Kind::Lanczos) {
         LanczosOptions lo;
         lo.tol = opt_.ritz_tol;

@@ -28,3 +28,9 @@ def test_shim_example_runs(G):
     r = subprocess.run([EXE], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "rpca_adm: converged 1" in r.stdout
+    assert "rpca_adm exact_full: converged 1" in r.stdout and "mc_svt: converged 1" in r.stdout
+    # E comes back sparse (the reference's SparseMatrix): its nonzeros are the final shrink's support
+    line = next(x for x in r.stdout.splitlines() if x.startswith("rpca_adm: converged"))
+    nnz = int(line.split("E nonzeros ")[1].split()[0])
+    planted = int(line.split("(planted ")[1].split(")")[0])
+    assert 0 < nnz < 200 * 200 and nnz >= planted

@@ -137,3 +137,32 @@ def test_rpca_k7_variants_agree(G, O, monkeypatch):
     assert np.linalg.norm(a_t - a_c) <= 1e-10 * np.linalg.norm(a_c)
     assert np.linalg.norm(e_t - e_c) <= 1e-10 * np.linalg.norm(e_c)
     assert st_t.rel_err <= 1e-5
+
+
+def test_exact_full_backend_rank_one_and_growth(G, O):
+    # test_solvers.cpp:12-22: the ExactFull backend recovers a clean rank-1 matrix
+    rng = O.Rng(3)
+    a, b = rng.gaussian_vector(40), rng.gaussian_vector(40)
+    d = np.outer(a, b)
+    a_g, e_g, st, _ = G.rpca_adm(d, G.SvdBackend.exact_full())
+    a_o, e_o, sto, _ = O.rpca_adm(d, O.SvdBackend.exact_full())
+    assert st.converged and st.rank_hat == 1 and st.e_l0 == 0
+    assert st.iterations == sto.iterations
+    assert np.linalg.norm(a_g - d) <= 1e-6 * np.linalg.norm(d)
+    # the RPCA 80^2 instance of test_solvers.cpp:25-67 through the device ExactFull:
+    # the same trace as the oracle's ExactFull (rank 9, e_l0 728)
+    from tests_support import gen_rpca_reference
+
+    d, a0 = gen_rpca_reference(O, 80, 0.1, 0.1, 21)
+    a_g, e_g, st, _ = G.rpca_adm(d, G.SvdBackend.exact_full(), truth=a0)
+    a_o, e_o, sto, _ = O.rpca_adm(d, O.SvdBackend.exact_full(), truth=a0)
+    assert (st.iterations, st.rank_hat, st.e_l0) == (sto.iterations, sto.rank_hat, sto.e_l0) == (32, 9, 728)
+    assert np.linalg.norm(a_g - a_o) <= 1e-8 * np.linalg.norm(a_o)
+
+
+def test_exact_full_backend_sparse_operator(G, O):
+    colptr, rowidx, vals, ml, mr = synth.mc_lowrank(120, 4, 4000, 5, O.Rng, O.sample_distinct)
+    ug, sg, vg, stg = G.mc_svt(120, 120, colptr, rowidx, vals, G.SvdBackend.exact_full(), truth_ml=ml, truth_mr=mr)
+    uo, so, vo, sto = O.mc_svt(120, 120, colptr, rowidx, vals, O.SvdBackend.exact_full(), truth_ml=ml, truth_mr=mr)
+    assert abs(stg.iterations - sto.iterations) <= 1 and stg.rank_hat == sto.rank_hat
+    assert np.linalg.norm((ug * sg) @ vg.T - (uo * so) @ vo.T) <= 1e-6 * np.linalg.norm((uo * so) @ vo.T)
