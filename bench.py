@@ -443,7 +443,7 @@ def run_gpu(args):
     achieved_tf = k1_flops / (k1_avg_ms * 1e-3) / 1e12 if k1_avg_ms > 0 else 0.0
     peak = max(peak_dmma, peak_dfma)
     traffic = None
-    tp = os.path.join(ROOT, "profiles", "r01_k1_traffic.json")
+    tp = os.path.join(ROOT, "profiles", "r02_k1_traffic.json")
     if os.path.exists(tp):  # one ncu --set full capture of the same K1 launch group
         traffic = json.load(open(tp))["dram_bytes_per_launch"]
 
@@ -466,7 +466,7 @@ def run_gpu(args):
                         "max": float(np.max(step_ms))},
             "roofline": {"bound": "tensor", "achieved": achieved_tf, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved_tf / peak if peak else None, "traffic": traffic,
-                         "traffic_unit": "bytes per K1 launch group (ncu, profiles/r01_k1_traffic.json)",
+                         "traffic_unit": "bytes per K1 launch group (ncu, profiles/r02_k1_traffic.json: dgemm_tma_kernel NN + TN + split-K reduces)",
                          "algorithmic_bytes_per_launch": 16.0 * M * N,
                          "kernel": "K1 paired W products (dgemm_tma_kernel NN + TN, split-K reduce)",
                          "flops_per_launch": k1_flops, "avg_launch_ms": k1_avg_ms,
