@@ -498,28 +498,39 @@ def run_gpu(args):
 def solver_configs():
     """BASELINE's other headline metric, RPCA / MC solve time, on configs[0],
     [2], [3] (C1, C3, C4; seeded synthetic instances, reference RNG recipe):
-    wall clock around each solve call only (solvers.hpp:75,154), one solve
-    each after a small warm-up solve. The oracle's times for the same
-    instances are in profiles/r01e_solve_configs.jsonl (C3's takes ~4 min)."""
+    wall clock around each solve call only (solvers.hpp:75,154). Each config is
+    solved twice in this process: `first_solve_s` pays the one-time costs (lazy
+    CUDA module loading of kernels first used at this size, CUDA-graph capture
+    of each new blws_svd shape, memory-pool growth: C3 1.39 vs 1.21 s,
+    tools/c3_variance.py), `solve_s` is the second (warm) solve. The oracle's
+    times for the same instances are in profiles/r01e_solve_configs.jsonl and
+    the committed traces of tests/golden/ (C3 157 s, C4 124 s on 8 host threads)."""
     import paper_1012_0365_b200 as B
     from paper_1012_0365_b200 import synth
 
     ctx = B.Context(0)
     out = {}
     bseed = 1 ^ 0x5BDBEEF
+
+    def twice(fn):
+        ts = []
+        for _ in range(2):
+            t = time.perf_counter()
+            st = fn()
+            ts.append(time.perf_counter() - t)
+        return ts, st
+
     for name, m, rank, frac in (("C1", 500, 25, 0.05), ("C3", 2000, 100, 0.10)):
         d, a0, _, _ = synth.rpca_lowrank_sparse(m, rank, int(round(frac * m * m)), 1, B.Rng, B.sample_distinct)
-        B.rpca_adm(d[:64, :64].copy(order="F"), B.SvdBackend.blws(seed=bseed, ctx=ctx))
-        t = time.perf_counter()
-        _, _, st, _ = B.rpca_adm(d, B.SvdBackend.blws(seed=bseed, ctx=ctx), truth=a0, want_outputs=False)
-        out[name] = {"workload": f"RPCA {m}^2 rank {rank}, {int(frac * 100)}% corrupted", "solve_s":
-                     time.perf_counter() - t, "iterations": st.iterations, "rank_hat": st.rank_hat,
+        ts, st = twice(lambda: B.rpca_adm(d, B.SvdBackend.blws(seed=bseed, ctx=ctx), truth=a0,
+                                          want_outputs=False)[2])
+        out[name] = {"workload": f"RPCA {m}^2 rank {rank}, {int(frac * 100)}% corrupted", "solve_s": ts[1],
+                     "first_solve_s": ts[0], "iterations": st.iterations, "rank_hat": st.rank_hat,
                      "rel_err": st.rel_err, "converged": st.converged}
     colptr, rowidx, vals, ml, mr = synth.mc_lowrank(10000, 50, 10_000_000, 1, B.Rng, B.sample_distinct)
-    t = time.perf_counter()
-    _, _, _, st = B.mc_svt(10000, 10000, colptr, rowidx, vals, B.SvdBackend.blws(seed=bseed, ctx=ctx), tol_outer=1e-6,
-                           truth_ml=ml, truth_mr=mr, cap=512)
-    out["C4"] = {"workload": "MC 10000^2 rank 50, 10^7 observed", "solve_s": time.perf_counter() - t,
+    ts, st = twice(lambda: B.mc_svt(10000, 10000, colptr, rowidx, vals, B.SvdBackend.blws(seed=bseed, ctx=ctx),
+                                    tol_outer=1e-6, truth_ml=ml, truth_mr=mr, cap=512)[3])
+    out["C4"] = {"workload": "MC 10000^2 rank 50, 10^7 observed", "solve_s": ts[1], "first_solve_s": ts[0],
                  "iterations": st.iterations, "rank_hat": st.rank_hat, "rel_err": st.rel_err,
                  "converged": st.converged}
     out["unit"] = "s"
