@@ -292,8 +292,12 @@ void launch_ts(Context& ctx, const double* A, long lda, const double* B, long ld
 template <bool TA>
 bool try_ts(Context& ctx, const double* A, long lda, const double* B, long ldb, double* C, long ldc, long M, long N,
             long K, double alpha, double beta) {
-    // column tile: smallest of {32, 64, 104, 128} covering ceil(N / ntiles)
-    const long ntiles = ceil_div(N, 128);
+    // column tile: smallest of {32, 64, 104, 128} covering ceil(N / ntiles);
+    // 64-wide column tiles when the row tiles alone leave SMs idle and K is too
+    // short for split-K to fill them (the CholQR applies X R^{-1}: 4000 x 100
+    // 18.0 -> 14.7 us)
+    long ntiles = ceil_div(N, 128);
+    if (N > 64 && K < 1024 && ceil_div(M, 64L) * ntiles < 2L * ctx.sm_count()) ntiles = ceil_div(N, 64);
     const long per = ceil_div(N, ntiles);
     if (per <= 32) launch_ts<TA, 32>(ctx, A, lda, B, ldb, C, ldc, M, N, K, alpha, beta);
     else if (per <= 64) launch_ts<TA, 64>(ctx, A, lda, B, ldb, C, ldc, M, N, K, alpha, beta);
