@@ -1,4 +1,5 @@
 // TEST INFRASTRUCTURE ONLY — CPU oracle implementation (see blws_oracle.hpp).
+#include <cstdlib>
 #include "blws_oracle.hpp"
 
 #include <chrono>
@@ -60,10 +61,27 @@ ThinQr thin_qr(const Mat& m_in) {
 }
 
 // ---------------------------------------------------------- small_dense.hpp
+// kSmallDenseLimit (small_dense.hpp:13) is the reference's guard; with
+// ORC_LIFT_SMALL_DENSE_LIMIT=1 the oracle runs past it (the device path has no
+// such limit: DESIGN.md §3) and records the largest order it met.
+static Index g_small_dense_max = 0;
+static bool small_dense_limit_lifted() {
+    static const bool lifted = [] {
+        const char* e = std::getenv("ORC_LIFT_SMALL_DENSE_LIMIT");
+        return e && e[0] == '1';
+    }();
+    return lifted;
+}
+static void small_dense_guard(Index n, const char* what) {
+    g_small_dense_max = std::max(g_small_dense_max, n);
+    if (n > kSmallDenseLimit && !small_dense_limit_lifted()) throw std::invalid_argument(what);
+}
+Index small_dense_max_order() { return g_small_dense_max; }
+
 // small_dense.hpp:24-43: checks, symmetrise, EVD, descending order.
 SymEvd sym_evd_small(const Mat& t_in) {
     if (t_in.r != t_in.c) throw std::invalid_argument("sym_evd_small: not square");
-    if (t_in.r > kSmallDenseLimit) throw std::invalid_argument("sym_evd_small: too large");
+    small_dense_guard(t_in.r, "sym_evd_small: too large");
     if (!all_finite(t_in)) throw std::invalid_argument("sym_evd_small: non-finite entries");
     const Index n = t_in.r;
     const double nrm = fro(t_in);
@@ -105,7 +123,7 @@ SymEvd sym_evd_tridiagonal(const Vec& diag, const Vec& subdiag) {
     if (diag.empty()) throw std::invalid_argument("sym_evd_tridiagonal: empty");
     if (subdiag.size() + 1 != diag.size()) throw std::invalid_argument("sym_evd_tridiagonal: size mismatch");
     const Index n = static_cast<Index>(diag.size());
-    if (n > kSmallDenseLimit) throw std::invalid_argument("sym_evd_tridiagonal: too large");
+    small_dense_guard(n, "sym_evd_tridiagonal: too large");
     Vec d = diag, e = subdiag;
     e.push_back(0.0);
     Mat z(n, n);

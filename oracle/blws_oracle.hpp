@@ -337,6 +337,8 @@ ThinQr thin_qr(const Mat& m);  // core/qr.hpp:24-47
 
 // ---------------------------------------------------------- small_dense.hpp
 constexpr Index kSmallDenseLimit = 4096;  // small_dense.hpp:13
+/// largest symmetric / tridiagonal EVD order met so far (see blws_oracle.cpp)
+Index small_dense_max_order();
 struct SymEvd {
     Mat vectors;
     Vec values;  // descending

@@ -42,6 +42,7 @@ def lib():
         sig = {
             "orc_last_error": (C.c_char_p, []),
             "orc_set_threads": (None, [C.c_int]),
+            "orc_small_dense_max_order": (i64, []),
             "orc_rng_new": (vp, [u64]),
             "orc_rng_free": (None, [vp]),
             "orc_rng_split": (vp, [vp, u64]),
@@ -109,6 +110,11 @@ def _check(rc):
 
 def F(a, dtype=np.float64):
     return np.asfortranarray(a, dtype=dtype)
+
+
+def small_dense_max_order() -> int:
+    """Largest EVD order met so far (the reference guards it at 4096, small_dense.hpp:13)."""
+    return int(lib().orc_small_dense_max_order())
 
 
 def set_threads(n: int) -> None:

@@ -51,6 +51,7 @@ extern "C" {
 
 const char* orc_last_error() { return g_err.c_str(); }
 void orc_set_threads(int n) { set_threads(n); }
+int64_t orc_small_dense_max_order() { return small_dense_max_order(); }
 
 // ---------------------------------------------------------------- rng
 void* orc_rng_new(std::uint64_t seed) { return new Rng(seed); }

@@ -12,6 +12,18 @@
 
 namespace blws {
 
+// kSmallDenseLimit (small_dense.hpp:13): the reference throws
+// std::invalid_argument for a symmetric / tridiagonal EVD above order 4096. The
+// device path has no such limit (the C5 reseeds exceed it); BLWS_STRICT_SMALL_DENSE=1
+// restores the reference's error.
+static void small_dense_guard(Index n, const char* what) {
+    static const bool strict = [] {
+        const char* e = std::getenv("BLWS_STRICT_SMALL_DENSE");
+        return e && e[0] == '1';
+    }();
+    if (strict && n > 4096) throw std::invalid_argument(what);
+}
+
 // =================================================================== Rng
 std::uint64_t Rng::uniform_index(std::uint64_t n) {
     const std::uint64_t limit = UINT64_MAX - UINT64_MAX % n;
@@ -836,6 +848,7 @@ static BlwsResult blws_svd_exact(LinearOperator& w, const DWarm& warm, Index k, 
     DBuf<double> vals(ctx, static_cast<size_t>(want));
     DMat vecs(ctx, d, want, false);
     ctx.region_begin(1);
+    small_dense_guard(t.rows, "sym_evd_small: too large");
     sym_evd_top(ctx, t.view(), want, vals.get(), vecs.view());
     ctx.region_end(1, 0.0, 0.0);
     std::vector<double> hv(static_cast<size_t>(want));
@@ -1087,6 +1100,7 @@ DeferredRecs enqueue_deferred(LinearOperator& w, View src, const DeferredShape& 
     rec.vslot = sl.take(static_cast<int>(want));
     DMat vecs(ctx, d, want, false);
     ctx.region_begin(1);
+    small_dense_guard(t.rows, "sym_evd_small: too large");
     sym_evd_top(ctx, t.view(), want, sl.at(rec.vslot), vecs.view());
     ctx.region_end(1, 0.0, 0.0);
     // keep = want is assumed (verified by finish_deferred); lift + sqrt(2) unpack
@@ -1506,6 +1520,7 @@ Checkpoint ritz_checkpoint(Context& ctx, DeviceLanczos& run, Index r, double tol
     const Index want = std::min(r, k);
     DBuf<double> vals(ctx, static_cast<size_t>(want));
     cp.vecs = DMat(ctx, k, want, false);
+    small_dense_guard(k, "sym_evd_tridiagonal: too large");
     tridiag_eig_top(ctx, k, run.alpha_dev(), run.coup_dev() + 1, want, vals.get(), cp.vecs.view());
     cp.values.resize(static_cast<size_t>(want));
     ctx.read(vals.get(), cp.values.data(), want);

@@ -111,3 +111,35 @@ def test_c4_recipe_3000_matches_oracle(G, O):
     g = _sketch(O, m)
     a_g, a_o = (ug * sg) @ (vg.T @ g), (uo * so) @ (vo.T @ g)
     assert np.linalg.norm(a_g - a_o) <= 1e-6 * np.linalg.norm(a_o)
+
+
+def test_c5_recipe_4000_matches_oracle_trace(G, O):
+    # BASELINE configs[4]'s recipe (rank m / 100, 5 % corrupted) at a tenth of
+    # the order, against the oracle's committed trace
+    ref = _trace("c5s")
+    m = 4000
+    d, a0, _, _ = synth.rpca_lowrank_sparse(m, 40, 800000, 1, G.Rng, G.sample_distinct)
+    a, e, st, _ = G.rpca_adm(d, G.SvdBackend.blws(seed=BSEED), truth=a0)
+    _check_history(st, ref)
+    assert abs(st.e_l0 - int(ref["e_l0"])) <= max(2, 1e-3 * int(ref["e_l0"]))
+    g = _sketch(O, m)
+    assert np.linalg.norm(a @ g - ref["a_sketch"]) <= 1e-6 * np.linalg.norm(ref["a_sketch"])
+    assert np.linalg.norm(e @ g - ref["e_sketch"]) <= 1e-6 * np.linalg.norm(ref["e_sketch"])
+
+
+def test_c5_full_size_properties(G):
+    # BASELINE configs[4] itself (40000^2, rank 400, 5 % corrupted, D formed on
+    # the device: 12.8 GB per matrix). No oracle fits, so the check
+    # is size-independent: convergence to tol 1e-7, the planted rank recovered,
+    # A0 recovered, and the planted support size (8e7 entries) found by E.
+    import torch
+
+    m = 40000
+    dev = torch.device("cuda:0")
+    dt, a0t, _, _ = synth.rpca_lowrank_sparse_device(m, 400, 80_000_000, 1, G.Rng, G.sample_distinct, dev)
+    _, _, st, _ = G.rpca_adm(dt, G.SvdBackend.blws(seed=BSEED), truth=a0t, device=True, m=m, ld=m)
+    assert st.converged and st.residual_history[-1] <= 1e-7
+    assert st.rank_hat == 400
+    assert st.rel_err <= 1e-6
+    assert abs(st.e_l0 - 80_000_000) <= 1e-3 * 80_000_000
+    assert st.matvec_init + sum(st.matvec_history) == st.matvec_count

@@ -61,3 +61,35 @@ def test_switch_variant_matches_oracle(env):
     r = subprocess.run([sys.executable, "-c", CASE % {"root": ROOT}], env=e, capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0 and "variant ok" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
+
+
+STRICT_CASE = r"""
+import sys, numpy as np
+sys.path.insert(0, %(root)r)
+import paper_1012_0365_b200 as B
+from oracle import oracle as O
+w = O.Rng(5).gaussian_matrix(2600, 2600)
+try:
+    u, s, v, st = B.lanczos_partial_svd(B.DenseOperator(w), 410, tol=1e-30, seed=3)  # never converges: k -> 4120
+    print("completed", len(s))
+except ValueError as e:
+    print("raised", e)
+"""
+
+
+@pytest.mark.parametrize("strict", [False, True])
+def test_small_dense_limit(strict):
+    # the reference's kSmallDenseLimit (small_dense.hpp:13): a Ritz checkpoint of
+    # order 4120 > 4096 throws std::invalid_argument there. The device path runs
+    # past it by default; BLWS_STRICT_SMALL_DENSE=1 restores the reference's error.
+    e = dict(os.environ)
+    e.pop("BLWS_STRICT_SMALL_DENSE", None)
+    if strict:
+        e["BLWS_STRICT_SMALL_DENSE"] = "1"
+    r = subprocess.run([sys.executable, "-c", STRICT_CASE % {"root": ROOT}], env=e, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    if strict:
+        assert "raised sym_evd_tridiagonal: too large" in r.stdout, r.stdout
+    else:
+        assert "completed 410" in r.stdout, r.stdout

@@ -215,3 +215,12 @@ def test_sparse_operator(O):
         op.assign_values(np.zeros(len(vals) - 1))
     with pytest.raises(ValueError):
         O.DenseOperator(np.array([[0.0, np.nan]]))
+
+
+def test_small_dense_limit_matches_reference(O):
+    # kSmallDenseLimit = 4096 (small_dense.hpp:13): the reference throws
+    # std::invalid_argument above it, and so does the oracle by default
+    with pytest.raises(ValueError, match="too large"):
+        O.sym_evd_tridiagonal(np.ones(4097), np.ones(4096))
+    vals, vecs = O.sym_evd_tridiagonal(np.arange(5.0), np.ones(4))
+    assert vals[0] > vals[-1]
