@@ -997,10 +997,14 @@ BlockLanczos block_lanczos_deferred(LinearOperator& w, View x1, Index k, Slots& 
     const Index bs = x1.cols, ld = geo.ld();
     const RowSplit split = w.panel_split();
     BlockLanczos out;
-    out.q = DMat(ctx, ld, k * bs, true);
+    // no zero fills unless a padding row exists: every block of Q is written
+    // over all ld rows (copies of full panels), and Z's rows are all written by
+    // the paired apply when m and n are even
+    const bool pad = (geo.m % 2) != 0 || (geo.n % 2) != 0;
+    out.q = DMat(ctx, ld, k * bs, false);
     View Q = out.q.view();
     copy(ctx, Q.cols_range(0, bs), x1);
-    DMat z(ctx, ld, bs, true);
+    DMat z(ctx, ld, bs, pad);
     DMat mtmp(ctx, bs, bs, false);
     auto block = [&](Index l) { return View{Q.p + l * bs * Q.ld, ld, bs, Q.ld}; };
     aug_apply(w, geo, block(0), z.view());
@@ -1023,7 +1027,7 @@ BlockLanczos block_lanczos_deferred(LinearOperator& w, View x1, Index k, Slots& 
         panel_sumsq(ctx, z.view(), split, sl.at(rec.rn.back()));
         View xn = block(l);
         copy(ctx, xn, z.view());
-        DMat rb(ctx, bs, bs, true);
+        DMat rb(ctx, bs, bs, false);  // thin_qr writes all of R (zeros below the diagonal)
         View rv = rb.view();
         rec.qr.push_back(thin_qr_deferred(ctx, xn, &rv, sl, split));
         out.b.push_back(std::move(rb));
@@ -1089,7 +1093,7 @@ DeferredRecs enqueue_deferred(LinearOperator& w, View src, const DeferredShape& 
     }
     BlockLanczos fac = block_lanczos_deferred(w, x1.view(), sh.k_eff, sl, rec.lrec);
     const Index bs = sh.bs, d = sh.d, want = sh.want;
-    DMat t(ctx, d, d, true);
+    DMat t(ctx, d, d, fac.built > 2);  // built <= 2 blocks cover all of T
     for (Index l = 0; l < fac.built; ++l) {
         place_block(ctx, t.view().sub(l * bs, l * bs, bs, bs), fac.m[l].view(), false);
         if (l + 1 < fac.built) {
