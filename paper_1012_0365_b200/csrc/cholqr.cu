@@ -117,7 +117,9 @@ __global__ void __launch_bounds__(kQT) cholqr_factor_k(double* g, long ldg, doub
     // ---- load (padding: identity), trace, distance to a scaled identity
     // column j per warp, rows lane + 32 r per lane; each batch issues its 16
     // loads (clamped, always in bounds) before any store, so they overlap
-    // instead of paying one global latency each
+    // instead of paying one global latency each. The off-diagonal part of
+    // ||G - cI||_F^2 is summed from the registers on the way.
+    double offd = 0.0;
     for (int j0 = wid; j0 < np; j0 += 4 * kQW) {
         double v[4][4];
 #pragma unroll
@@ -133,6 +135,7 @@ __global__ void __launch_bounds__(kQT) cholqr_factor_k(double* g, long ldg, doub
             for (int r = 0; r < 4; ++r) {
                 const int i = lane + 32 * r;
                 if (i < np && j < np) A[i + j * ld] = (i < n && j < n) ? v[c][r] : (i == j ? 1.0 : 0.0);
+                if (i < n && j < n && i != j) offd = fma(v[c][r], v[c][r], offd);
             }
         }
     }
@@ -142,13 +145,11 @@ __global__ void __launch_bounds__(kQT) cholqr_factor_k(double* g, long ldg, doub
     tr = qr_block_sum(tr, red);
     if (trace_out && threadIdx.x == 0) *trace_out = tr;
     const double c = tr / n;
-    double off = 0.0;
-    for (int j = wid; j < n; j += kQW)
-        for (int i = lane; i < n; i += 32) {
-            const double v = A[i + j * ld] - (i == j ? c : 0.0);
-            off = fma(v, v, off);
-        }
-    off = qr_block_sum(off, red);
+    for (int i = threadIdx.x; i < n; i += kQT) {
+        const double v = A[i + i * ld] - c;
+        offd = fma(v, v, offd);
+    }
+    const double off = qr_block_sum(offd, red);
     const bool finite = isfinite(tr) && isfinite(off) && tr > 0.0;
     CQ_MARK(1);
     const int mode = !finite ? 3 : off <= 1e-28 * c * c ? 0 : off <= 1e-18 * c * c ? 1 : 2;
@@ -160,8 +161,70 @@ __global__ void __launch_bounds__(kQT) cholqr_factor_k(double* g, long ldg, doub
         }
         return;
     }
+    if (mode <= 1 && !(r_prev && r_out)) {
+        // R = sqrt(c) (I + F), Rinv = (I - F) / sqrt(c); F = 0 for the skip.
+        // Elementwise in G, so every output goes straight from the staged G to
+        // global memory (the same arithmetic as the on-chip branch below, so
+        // both give identical bits); only R_total = R R_prev needs the tile.
+        const double rc = sqrt(c), ric = 1.0 / rc, ic = 1.0 / c;
+        const double tau = rank_out ? 1e-12 * sqrt(trace_ref ? trace_ref[0] : tr) : 0.0;
+        double mn = INFINITY, mx = 0.0, cnt = 0.0;
+        for (int j = wid; j < n; j += kQW) {
+            double rv[4], xv[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const int i = lane + 32 * r;
+                double f = 0.0;
+                if (mode == 1 && i <= j) f = i == j ? 0.5 * fma(A[i + j * ld], ic, -1.0) : A[i + j * ld] * ic;
+                rv[r] = i == j ? rc * (1.0 + f) : (i < j ? rc * f : 0.0);
+                xv[r] = i == j ? ric * (1.0 - f) : (i < j ? -ric * f : 0.0);
+            }
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const int i = lane + 32 * r;
+                if (i < n) {
+                    if (rinv) rinv[i + j * ldri] = xv[r];
+                    g[i + j * ldg] = rv[r];
+                }
+                if (i == j) {
+                    mn = fmin(mn, rv[r]);
+                    mx = fmax(mx, rv[r]);
+                    if (rank_out) {
+                        double d = rv[r];
+                        if (r_prev) d *= r_prev[j + static_cast<long>(j) * ldp];
+                        cnt += d > tau ? 1.0 : 0.0;
+                    }
+                }
+            }
+        }
+        if (rank_out) {
+            cnt = qr_block_sum(cnt, red);
+            if (threadIdx.x == 0) rank_out[0] = static_cast<std::int64_t>(cnt + 0.5);
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+            mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        }
+        __syncthreads();  // red[] is free again
+        if (lane == 0) {
+            red[wid] = mn;
+            red[kQW + wid] = mx;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int w2 = 1; w2 < kQW; ++w2) {
+                mn = fmin(mn, red[w2]);
+                mx = fmax(mx, red[kQW + w2]);
+            }
+            status[0] = 0;
+            diag[0] = mn;
+            diag[1] = mx;
+        }
+        CQ_MARK(19);
+        return;
+    }
     if (mode <= 1) {
-        // R = sqrt(c) (I + F), Rinv = (I - F) / sqrt(c); F = 0 for the skip
+        // the same R and Rinv on chip, for the R_total product below
         const double rc = sqrt(c), ric = 1.0 / rc, ic = 1.0 / c;
         __syncthreads();
         for (int j = wid; j < np; j += kQW)

@@ -136,7 +136,10 @@ __global__ void __launch_bounds__(kFT) sytrd_fused_k(const double* __restrict__ 
     {
         const double xi = row < n ? a[row] : 0.0;  // column 0 packed at offset 0
         double s2 = warp_sum(row >= 2 && row < n ? xi * xi : 0.0);
-        if (lane == 0) red[wid] = s2;
+        if (lane == 0) {
+            red[wid] = s2;
+            red[32 + wid] = 0.0;  // the [P] s2 share of warps without live rows stays 0
+        }
         __syncthreads();
         s2 = warp_sum(lane < kFW ? red[lane] : 0.0);
         form_reflector(a, n, 0, s2, xi, vb, d, e, tau, &tk);
@@ -184,7 +187,7 @@ __global__ void __launch_bounds__(kFT) sytrd_fused_k(const double* __restrict__ 
                 for (int q = c / 2; q < QN; ++q) {
                     const int i = lane + 32 * q;
                     const bool ok = (q != c / 2 || i >= j) && (q != QN - 1 || i < n);
-                    const double x = ok ? xs[q] - fma(vor[q], woj, wor[q] * voj) : 0.0;
+                    const double x = ok ? fma(-vor[q], woj, fma(-wor[q], voj, xs[q])) : 0.0;
                     xs[q] = x;
                     acc[q] = fma(x, vj, acc[q]);
                     if (i > j) dp[c] = fma(x, vr[q], dp[c]);
@@ -244,6 +247,12 @@ __global__ void __launch_bounds__(kFT) sytrd_fused_k(const double* __restrict__ 
         // ---- [P] K = tau/2 p^T v = tau^2/2 v^T A v (per-warp shares); p_i, w_i;
         //      look-ahead update of column k+1 (w_{k+1} formed by every thread
         //      from broadcast reads) and its squared norm below the subdiagonal
+        // warps whose rows are all >= n have no [P] / [P3] work (their s2 share
+        // in red[32 + wid] was zeroed in the prologue)
+        const bool rows_live = 32 * wid < n;
+        const int c1 = k + 1;
+        double xi = 0.0;
+        if (rows_live) {
         double vav = 0.0;
 #pragma unroll
         for (int ww = 0; ww < kFW; ++ww) vav += red[ww];
@@ -258,25 +267,24 @@ __global__ void __launch_bounds__(kFT) sytrd_fused_k(const double* __restrict__ 
         const double vi = row < NP ? v[row] : 0.0;
         const double wi = fma(-K, vi, p);
         if (row < NP) wn[row] = wi;
-        const int c1 = k + 1;
         double pc = pcol[c1];
 #pragma unroll
         for (int ww = 0; ww < PWN; ++ww) pc += pw[ww * NP + c1];
         const double vc = v[c1];
         const double wc = fma(-K, vc, tk * pc);  // w_{k+1}, identical in every thread
-        double xi = 0.0;
         if (row >= c1 && row < n) {
             double* col1 = a + floff(c1, n) - c1;
-            xi = col1[row] - fma(vi, wc, wi * vc);
+            xi = fma(-vi, wc, fma(-wi, vc, col1[row]));
             col1[row] = xi;
         }
-        double s2 = warp_sum(row >= c1 + 2 && row < n ? xi * xi : 0.0);
+        const double s2 = warp_sum(row >= c1 + 2 && row < n ? xi * xi : 0.0);
         if (lane == 0) red[32 + wid] = s2;  // second half: red[0..] holds the v^T A v shares
+        }
         PHASE_MARK(5);
         __syncthreads();
         // ---- [P3] reflector of column k+1 (if any)
-        if (k + 1 < n - 2) {
-            s2 = warp_sum(lane < kFW ? red[32 + lane] : 0.0);
+        if (k + 1 < n - 2 && rows_live) {
+            const double s2 = warp_sum(lane < kFW ? red[32 + lane] : 0.0);
             form_reflector(a, n, c1, s2, xi, vn, d, e, tau, &tk);
         }
         PHASE_MARK(6);
