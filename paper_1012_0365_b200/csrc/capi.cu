@@ -757,6 +757,31 @@ extern "C" int blws_microbench(blws_context* ctx, int which, int64_t n, int64_t 
                 BLWS_CUDA(cudaEventElapsedTime(&ms, e0, e1));
                 if (r >= 0) total += ms;
             }
+        } else if (which == 10) {
+            // 10: gram16 (cluster Gram) of an n x b panel; us[1] = max |G16 - G_gemm| / max |G_gemm|
+            fill_host(n * b);
+            DMat x(c, n, b), g1(c, b, b), g2(c, b, b);
+            upload(c, x.view(), h.data(), n);
+            for (int r = -1; r < reps; ++r) {
+                BLWS_CUDA(cudaEventRecord(e0, c.stream()));
+                gram16(c, x.view(), g1.data(), g1.ld);
+                BLWS_CUDA(cudaEventRecord(e1, c.stream()));
+                BLWS_CUDA(cudaEventSynchronize(e1));
+                float ms = 0;
+                BLWS_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+                if (r >= 0) total += ms;
+            }
+            gemm(c, true, false, b, b, n, 1.0, x.data(), x.ld, x.data(), x.ld, 0.0, g2.data(), g2.ld);
+            std::vector<double> h1(static_cast<size_t>(g1.ld * b)), h2(static_cast<size_t>(g2.ld * b));
+            BLWS_CUDA(cudaMemcpy(h1.data(), g1.data(), h1.size() * 8, cudaMemcpyDeviceToHost));
+            BLWS_CUDA(cudaMemcpy(h2.data(), g2.data(), h2.size() * 8, cudaMemcpyDeviceToHost));
+            double md = 0, mx = 0;
+            for (int64_t j = 0; j < b; ++j)
+                for (int64_t i = 0; i < b; ++i) {
+                    md = std::max(md, std::abs(h1[i + j * g1.ld] - h2[i + j * g2.ld]));
+                    mx = std::max(mx, std::abs(h2[i + j * g2.ld]));
+                }
+            us[1] = mx > 0 ? md / mx : md;
         } else if (which == 0 || which == 1) {
             fill_host(n * n);
             DMat a(c, n, n), s(c, n, n), g0(c, n, n), work(c, n, n), rinv(c, n, n), vec(c, n, std::max<int64_t>(1, n / 2));

@@ -576,6 +576,14 @@ namespace {
 
 DMat gram(Context& ctx, View x, RowSplit split = {}) {
     DMat g(ctx, x.cols, x.cols, false);
+    static const bool g16 = [] {
+        const char* e = std::getenv("BLWS_GRAM16");
+        return !(e && e[0] == '0');
+    }();
+    if (g16 && (split.sharded == 0 || !ctx.has_comm()) && gram16_fits(x.rows, x.cols)) {
+        gram16(ctx, x, g.data(), g.ld);
+        return g;
+    }
     panel_tn(ctx, x, x, split, g.data(), g.ld);
     return g;
 }

@@ -68,6 +68,10 @@ void chol_inv_upper(Context& ctx, View g, View rinv, int* status, double* diag, 
 /// rank_out <- #diag(R * r_prev) > 1e-12 sqrt(trace_ref[0]) (trace_ref = null:
 /// this G's trace). The factorisation (scaled identity / near identity / blocked
 /// Cholesky) is picked on the device; status, diag, trace_out as chol_inv_upper.
+/// G = X^T X (full, exactly symmetric) for b = x.cols <= 112 (gram16.cu): one
+/// cluster launch, no split-K workspace, fixed summation order.
+bool gram16_fits(Index rows, Index b);
+void gram16(Context& ctx, View x, double* g, Index ldg);
 bool cholqr_factor_fits(Index n);
 void cholqr_factor(Context& ctx, View g, View rinv, const double* r_prev, Index ldp, View* r_out, int* status,
                    double* diag, double* trace_out, const double* trace_ref, std::int64_t* rank_out);

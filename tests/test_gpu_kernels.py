@@ -288,3 +288,16 @@ def test_dgemm_tn_small_output(gpu, m, n, k, sym):
     if sym:
         assert np.array_equal(outs[0] - 0.25 * C0, (outs[0] - 0.25 * C0).T) or np.abs(
             (outs[0] - 0.25 * C0) - (outs[0] - 0.25 * C0).T).max() <= 1e-12 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("rows,b", [(4000, 100), (4003, 97), (37, 7), (5, 112), (20001, 64), (1, 1), (9000, 16)])
+def test_gram16_matches_split_k(gpu, rows, b):
+    # gram16.cu (the CholQR Grams, b <= 112): one cluster launch per Gram, every
+    # 16 x 16 tile of the upper triangle reduced over an 8-CTA cluster through
+    # DSMEM and mirrored. Compared with the split-K GEMM on the same panel
+    # (microbench mode 10 returns max |G16 - G| / max |G|), ragged rows / widths
+    # included, and run repeatedly (the DSMEM hand-off must not race).
+    ctx = gpu.Context(0)
+    for _ in range(3):
+        d = ctx.microbench(10, rows, b, 2, detail=True)
+        assert d[1] <= 1e-14 * max(1.0, np.sqrt(rows)), (rows, b, d[1])
