@@ -757,6 +757,10 @@ extern "C" int blws_microbench(blws_context* ctx, int which, int64_t n, int64_t 
                 BLWS_CUDA(cudaEventElapsedTime(&ms, e0, e1));
                 if (r >= 0) total += ms;
             }
+        } else if (which == 11 || which == 12) {
+            // 11: K7 (fused ALM update) on an n x n problem of rank b; 12: its E-only pass.
+            // us[1] = checksum (sum of the residual partials / ||E||_F)
+            total = static_cast<float>(alm_microbench(c, n, b, reps, which == 12, &us[1]) * reps / 1e3);
         } else if (which == 10) {
             // 10: gram16 (cluster Gram) of an n x b panel; us[1] = max |G16 - G_gemm| / max |G_gemm|
             fill_host(n * b);

@@ -105,7 +105,10 @@ __global__ void __launch_bounds__(threads<CONS>(), CONS <= 4 ? 2 : 1)
     using L = Layout<BK, BN, CONS>;
     constexpr int BM = L::BM;
     extern __shared__ __align__(1024) unsigned char smraw[];
-    unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+    // 1024-byte aligned base by an offset on the shared array itself (a round trip
+    // through uintptr_t loses the address space: every fragment load became a
+    // generic LD with 64-bit address arithmetic instead of an LDS)
+    unsigned char* sm = smraw + ((1024u - (static_cast<uint32_t>(__cvta_generic_to_shared(smraw)) & 1023u)) & 1023u);
     uint64_t* full = reinterpret_cast<uint64_t*>(sm + STAGES * L::STAGE);
     uint64_t* empty = full + STAGES;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;

@@ -323,6 +323,10 @@ struct RpcaOptions {
     double mu_max_factor = 1e7;
     Index initial_rank = 10, rank_increment = 5;
 };
+/// K7 microbenchmark (development): average device us of one fused ALM launch
+/// on a seeded m x m problem of rank r (eonly: the end-of-solve E pass).
+double alm_microbench(Context& ctx, Index m, Index r, int reps, bool eonly, double* checksum);
+
 /// rpca_adm (solvers.hpp:72-157). d / truth / a_out / e_out are device
 /// pointers with leading dimension ldd (truth, a_out, e_out may be null).
 /// With `shard` (m_total = m), they hold this rank's `rows` rows starting at

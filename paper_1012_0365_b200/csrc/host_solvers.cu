@@ -226,14 +226,20 @@ __global__ void e_counts_k(const double* E, long m, long n, long ld, double tol,
 
 /// K7: fused rank-r reconstruction + ALM update (solvers.hpp:114-124):
 ///   a = (U diag(s)) V^T            (DMMA mainloop, K = r)
-///   e = shrink(D - a + Y/mu, lambda/mu); res = D - a - e; Y += mu res
-///   W = D - e + Y/mu_next;  E = e;  partial ||res||^2, non-finite(W)
-/// One pass over D, Y (read) and Y, W, E (write): 40 B per element. m x n: the
-/// rows held here (a row shard of a square RPCA problem, or all of it).
+///   e = shrink(D - a + Y/mu, lambda/mu); res = D - a - e; Y' = Y + mu res
+///   W = D - e + Y'/mu_next;  partial ||res||^2, non-finite(W)
+/// One pass over D, Y (read) and Y', W (write): 32 B per element. Y and Y' are
+/// different buffers (ping-pong), so E is never stored during the iterations:
+/// after the last one the EONLY instance recomputes the same tile from the
+/// same inputs (U, V, D, Y, mu of that iteration -- bitwise the same a and e)
+/// and stores E alone (solvers.hpp:133-146 needs E only at the end).
+/// m x n: the rows held here (a row shard of a square RPCA problem, or all of it).
+template <bool EONLY>
 __global__ void __launch_bounds__(gemm_detail::THREADS) alm_fused_k(const double* __restrict__ us, long ldu,
                                                                    const double* __restrict__ v, long ldv, long m,
                                                                    long n, long r, const double* __restrict__ D,
-                                                                   double* __restrict__ Y, double* __restrict__ W,
+                                                                   const double* __restrict__ Y,
+                                                                   double* __restrict__ Yout, double* __restrict__ W,
                                                                    double* __restrict__ E, long ld, double mu,
                                                                    double mu_next, double lambda_mu, double* partial,
                                                                    int* bad) {
@@ -292,22 +298,28 @@ __global__ void __launch_bounds__(gemm_detail::THREADS) alm_fused_k(const double
                 const double y = yv[ni][e2];
                 const double dma = d - a;
                 const double e = shrink_d(dma + y * inv_mu, lambda_mu);
+                if (EONLY) {
+                    E[o] = e;
+                    continue;
+                }
                 const double res = dma - e;
                 const double yn = y + mu * res;
                 const double w = (d - e) + yn * inv_mu_next;
-                Y[o] = yn;
-                E[o] = e;
+                Yout[o] = yn;
                 W[o] = w;
                 ss += res * res;
                 nonfinite |= !isfinite(w);
             }
     }
-    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-    __shared__ double sh[4];
-    __syncthreads();
-    if (lane == 0) sh[warp] = ss;
-    if (__syncthreads_or(nonfinite) && threadIdx.x == 0) atomicOr(bad, 1);
-    if (threadIdx.x == 0) partial[blockIdx.x + static_cast<long>(blockIdx.y) * gridDim.x] = (sh[0] + sh[1]) + (sh[2] + sh[3]);
+    if constexpr (!EONLY) {
+        for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+        __shared__ double sh[4];
+        __syncthreads();
+        if (lane == 0) sh[warp] = ss;
+        if (__syncthreads_or(nonfinite) && threadIdx.x == 0) atomicOr(bad, 1);
+        if (threadIdx.x == 0)
+            partial[blockIdx.x + static_cast<long>(blockIdx.y) * gridDim.x] = (sh[0] + sh[1]) + (sh[2] + sh[3]);
+    }
 }
 
 // K7 with TMA-fed operands (the default; alm_fused_k above is the fallback for
@@ -327,33 +339,47 @@ __global__ void __launch_bounds__(gemm_detail::THREADS) alm_fused_k(const double
 // pipe 46% active. The consumers' epilogue therefore reads D and Y from shared
 // memory -- no global-load latency after the DMMA phase -- and its stores of
 // Y, E, W drain while the next tile's DMMAs run.
+#ifndef K7_DYBUF
+#define K7_DYBUF 1
+#endif
+#ifndef K7_STAGES
+#define K7_STAGES 4
+#endif
+#ifndef K7_BN
+#define K7_BN 32
+#endif
+#ifndef K7_KFIRST
+#define K7_KFIRST 1
+#endif
 namespace k7 {
-constexpr int CONS = 4, BM = 16 * CONS, BN = 32, BK = 16, STAGES = 4, DYBUF = 1;
+constexpr int CONS = 4, BM = 16 * CONS, BN = K7_BN, BK = 16, STAGES = K7_STAGES, DYBUF = K7_DYBUF;
 constexpr int A_BYTES = BM * BK * 8, B_BYTES = BN * BK * 8, STAGE = A_BYTES + B_BYTES;
 constexpr int DY_BYTES = 2 * BM * BN * 8;  // D and Y of one tile
 constexpr int SMEM = STAGES * STAGE + DYBUF * DY_BYTES + 1024 + 2 * (STAGES + 2) * 8;  // 81 KB: two CTAs per SM
 constexpr int THREADS = 32 * (CONS + 1);
 }  // namespace k7
 
+template <bool EONLY>
 __global__ void __launch_bounds__(k7::THREADS, 2) alm_tma_k(const __grid_constant__ CUtensorMap tmU,
                                                              const __grid_constant__ CUtensorMap tmV,
                                                              const __grid_constant__ CUtensorMap tmD,
                                                              const __grid_constant__ CUtensorMap tmY, long m, long n,
-                                                             long r, double* __restrict__ Y, double* __restrict__ W,
+                                                             long r, double* __restrict__ Yout, double* __restrict__ W,
                                                              double* __restrict__ E, long ld, double mu,
                                                              double mu_next, double lambda_mu, double* partial,
                                                              int* bad) {
     using namespace k7;
     using namespace gemm_tma;
     extern __shared__ __align__(1024) unsigned char smraw[];
-    unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+    // 1024-byte aligned base by an offset on the shared array itself (a round trip
+    // through uintptr_t loses the address space: every fragment load became a
+    // generic LD with 64-bit address arithmetic instead of an LDS)
+    unsigned char* sm = smraw + ((1024u - (static_cast<uint32_t>(__cvta_generic_to_shared(smraw)) & 1023u)) & 1023u);
     unsigned char* dyb = sm + STAGES * STAGE;  // DYBUF x (D 32 KB, Y 32 KB)
     uint64_t* full = reinterpret_cast<uint64_t*>(dyb + DYBUF * DY_BYTES);
     uint64_t* empty = full + STAGES;
     uint64_t* dyfull = empty + STAGES;  // 2
     uint64_t* dyempty = dyfull + 2;     // 2
-    __shared__ double sh[CONS];
-    __shared__ int shbad;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long mt = (m + BM - 1) / BM, nt = (n + BN - 1) / BN, tiles = mt * nt;
     const int ktiles = static_cast<int>((r + BK - 1) / BK);
@@ -377,14 +403,17 @@ __global__ void __launch_bounds__(k7::THREADS, 2) alm_tma_k(const __grid_constan
             for (long tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++j) {
                 const int m0 = static_cast<int>((tile % mt) * BM), n0 = static_cast<int>((tile / mt) * BN);
                 const int bsel = static_cast<int>(j % DYBUF);
-                mbar_wait(dyempty + bsel, static_cast<uint32_t>(((j / DYBUF) & 1) ^ 1));
-                mbar_expect_tx(dyfull + bsel, DY_BYTES);
-                unsigned char* dst = dyb + bsel * DY_BYTES;
+                auto issue_dy = [&] {
+                    mbar_wait(dyempty + bsel, static_cast<uint32_t>(((j / DYBUF) & 1) ^ 1));
+                    mbar_expect_tx(dyfull + bsel, DY_BYTES);
+                    unsigned char* dst = dyb + bsel * DY_BYTES;
 #pragma unroll
-                for (int qq = 0; qq < BM / 16; ++qq) {
-                    tma_2d(dst + qq * (BN * 128), &tmD, dyfull + bsel, m0 + 16 * qq, n0);
-                    tma_2d(dst + DY_BYTES / 2 + qq * (BN * 128), &tmY, dyfull + bsel, m0 + 16 * qq, n0);
-                }
+                    for (int qq = 0; qq < BM / 16; ++qq) {
+                        tma_2d(dst + qq * (BN * 128), &tmD, dyfull + bsel, m0 + 16 * qq, n0);
+                        tma_2d(dst + DY_BYTES / 2 + qq * (BN * 128), &tmY, dyfull + bsel, m0 + 16 * qq, n0);
+                    }
+                };
+                if (!K7_KFIRST) issue_dy();
                 for (int kt = 0; kt < ktiles; ++kt, ++q) {
                     const int s = static_cast<int>(q % STAGES);
                     mbar_wait(empty + s, static_cast<uint32_t>(((q / STAGES) & 1) ^ 1));
@@ -397,6 +426,7 @@ __global__ void __launch_bounds__(k7::THREADS, 2) alm_tma_k(const __grid_constan
 #pragma unroll
                     for (int qq = 0; qq < BN / 16; ++qq) tma_2d(bs + qq * (BK * 128), &tmV, full + s, n0 + 16 * qq, k0);
                 }
+                if (K7_KFIRST) issue_dy();
             }
         }
         return;
@@ -476,11 +506,14 @@ __global__ void __launch_bounds__(k7::THREADS, 2) alm_tma_k(const __grid_constan
                     const double a = acc[mi][ni][e2];
                     const double dma = d - a;
                     const double e = shrink_d(dma + y * inv_mu, lambda_mu);
+                    if (EONLY) {
+                        E[o] = e;
+                        continue;
+                    }
                     const double res = dma - e;
                     const double yn = y + mu * res;
                     const double w = (d - e) + yn * inv_mu_next;
-                    Y[o] = yn;
-                    E[o] = e;
+                    Yout[o] = yn;
                     W[o] = w;
                     ss += res * res;
                     nonfinite |= !isfinite(w);
@@ -488,21 +521,15 @@ __global__ void __launch_bounds__(k7::THREADS, 2) alm_tma_k(const __grid_constan
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(dyempty + bsel);
-        for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-        nonfinite = __any_sync(0xffffffffu, nonfinite);
-        if (lane == 0) {
-            sh[warp] = ss;
-            if (warp == 0) shbad = 0;
+        if constexpr (!EONLY) {
+            // one partial per (tile, warp): no consumer barrier in the epilogue
+            for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+            nonfinite = __any_sync(0xffffffffu, nonfinite);
+            if (lane == 0) {
+                partial[tile * CONS + warp] = ss;
+                if (nonfinite) atomicOr(bad, 1);
+            }
         }
-        asm volatile("bar.sync 1, %0;" ::"n"(CONS * 32) : "memory");  // consumers only
-        if (lane == 0 && nonfinite) shbad = 1;
-        asm volatile("bar.sync 1, %0;" ::"n"(CONS * 32) : "memory");
-        if (threadIdx.x == 0) {
-            // partial layout of the tile grid: (tile % mt, tile / mt)
-            partial[tile] = (sh[0] + sh[1]) + (sh[2] + sh[3]);
-            if (shbad) atomicOr(bad, 1);
-        }
-        asm volatile("bar.sync 1, %0;" ::"n"(CONS * 32) : "memory");  // sh reused by the next tile
     }
 }
 
@@ -650,6 +677,60 @@ double sum_partials(Context& ctx, const double* part, Index count) {
     return h;
 }
 
+// One K7 launch (alm_tma_k, or alm_fused_k when a panel cannot be TMA-mapped or
+// BLWS_K7=cpasync). eonly: store E = shrink(D - a + Y/mu, lambda/mu) alone (Yout,
+// W, partial, bad untouched). Returns the number of partials written.
+long alm_launch(Context& ctx, bool eonly, Index rows, Index m, Index r, const DMat& us, View v, const double* D,
+                const double* Y, double* Yout, double* W, double* E, Index ld, double mu, double mu_next,
+                double lambda_mu, double* part, int* bad) {
+    using namespace gemm_detail;
+    static const bool use_tma = [] {
+        const char* e = std::getenv("BLWS_K7");
+        return !(e && std::string(e) == "cpasync");
+    }();
+    static bool cfg = false;
+    constexpr int smem = smem_bytes<false, true>();
+    if (!cfg) {
+        BLWS_CUDA(cudaFuncSetAttribute(alm_fused_k<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        BLWS_CUDA(cudaFuncSetAttribute(alm_fused_k<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        BLWS_CUDA(cudaFuncSetAttribute(alm_tma_k<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, k7::SMEM));
+        BLWS_CUDA(cudaFuncSetAttribute(alm_tma_k<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, k7::SMEM));
+        cfg = true;
+    }
+    CUtensorMap tmu, tmv, tmd, tmy;
+    if (use_tma && r > 0 && tma_map_2d(&tmu, us.data(), rows, r, us.ld, k7::BK) &&
+        tma_map_2d(&tmv, v.p, m, r, v.ld, k7::BK) && tma_map_2d(&tmd, D, rows, m, ld, k7::BN) &&
+        tma_map_2d(&tmy, Y, rows, m, ld, k7::BN)) {
+        const long tiles = ceil_div(rows, k7::BM) * ceil_div(m, k7::BN);
+        const unsigned ctas = static_cast<unsigned>(std::min<long>(2L * ctx.sm_count(), tiles));
+        const long nparts = tiles * k7::CONS;
+        if (eonly)
+            alm_tma_k<true><<<ctas, k7::THREADS, k7::SMEM, ctx.stream()>>>(tmu, tmv, tmd, tmy, rows, m, r, Yout, W, E,
+                                                                           ld, mu, mu_next, lambda_mu, part, bad);
+        else
+            alm_tma_k<false><<<ctas, k7::THREADS, k7::SMEM, ctx.stream()>>>(tmu, tmv, tmd, tmy, rows, m, r, Yout, W, E,
+                                                                            ld, mu, mu_next, lambda_mu, part, bad);
+        ctx.note_launch();
+        ctx.check_launch("alm_tma_k");
+        return nparts;
+    }
+    const dim3 grid(static_cast<unsigned>(ceil_div(rows, BM)), static_cast<unsigned>(ceil_div(m, BN)));
+    if (eonly)
+        alm_fused_k<true><<<grid, THREADS, smem, ctx.stream()>>>(us.data(), us.ld, v.p, v.ld, rows, m, r, D, Y, Yout, W,
+                                                                 E, ld, mu, mu_next, lambda_mu, part, bad);
+    else
+        alm_fused_k<false><<<grid, THREADS, smem, ctx.stream()>>>(us.data(), us.ld, v.p, v.ld, rows, m, r, D, Y, Yout,
+                                                                  W, E, ld, mu, mu_next, lambda_mu, part, bad);
+    ctx.note_launch();
+    ctx.check_launch("alm_fused_k");
+    return static_cast<long>(grid.x) * grid.y;
+}
+
+long alm_partials_max(Index rows, Index m) {
+    using namespace gemm_detail;
+    return std::max<long>(ceil_div(rows, BM) * ceil_div(m, BN), ceil_div(rows, k7::BM) * ceil_div(m, k7::BN) * k7::CONS);
+}
+
 double frob(Context& ctx, View x) {
     DBuf<double> s(ctx, 1);
     sumsq(ctx, x, s.get());
@@ -659,6 +740,57 @@ double frob(Context& ctx, View x) {
 }
 
 }  // namespace
+
+// ============================================================ K7 microbenchmark
+namespace {
+__global__ void hash_fill_k(double* x, long rows, long cols, long ld, unsigned long long seed, double scale) {
+    const long total = rows * cols;
+    for (long idx = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<long>(gridDim.x) * blockDim.x) {
+        unsigned long long z = seed + 0x9e3779b97f4a7c15ull * static_cast<unsigned long long>(idx + 1);
+        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+        z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+        z ^= z >> 31;
+        x[idx % rows + (idx / rows) * ld] = scale * (static_cast<double>(z >> 11) * 0x1.0p-53 * 2.0 - 1.0);
+    }
+}
+}  // namespace
+
+// Average device microseconds of one K7 launch (one ALM iteration's fused
+// reconstruction + update) on an m x m problem with rank r, seeded inputs;
+// eonly: the end-of-solve E pass. out[1] = the partials' sum (a checksum).
+double alm_microbench(Context& ctx, Index m, Index r, int reps, bool eonly, double* checksum) {
+    const Index ld = std::max<Index>(2, round_up(m, 2));
+    DMat D(ctx, m, m, false), Y0(ctx, m, m, false), Y1(ctx, m, m, false), W(ctx, m, m, false);
+    DMat us(ctx, m, r, false), v(ctx, m, r, false);
+    const unsigned g = gridn(m * m, 8192);
+    hash_fill_k<<<g, kT, 0, ctx.stream()>>>(D.data(), m, m, ld, 1, 1.0);
+    hash_fill_k<<<g, kT, 0, ctx.stream()>>>(Y0.data(), m, m, ld, 2, 0.01);
+    hash_fill_k<<<gridn(m * r), kT, 0, ctx.stream()>>>(us.data(), m, r, us.ld, 3, 1.0 / std::sqrt(double(r)));
+    hash_fill_k<<<gridn(m * r), kT, 0, ctx.stream()>>>(v.data(), m, r, v.ld, 4, 1.0);
+    ctx.note_launch(4);
+    DBuf<double> part(ctx, static_cast<size_t>(alm_partials_max(m, m)));
+    DBuf<int> bad(ctx, 1);
+    cudaEvent_t e0, e1;
+    BLWS_CUDA(cudaEventCreate(&e0));
+    BLWS_CUDA(cudaEventCreate(&e1));
+    float total = 0;
+    long nparts = 0;
+    for (int it = -1; it < reps; ++it) {
+        BLWS_CUDA(cudaEventRecord(e0, ctx.stream()));
+        nparts = alm_launch(ctx, eonly, m, m, r, us, v.view(), D.data(), Y0.data(), Y1.data(), W.data(), Y1.data(), ld,
+                            0.5, 0.6, 0.3, part.get(), bad.get());
+        BLWS_CUDA(cudaEventRecord(e1, ctx.stream()));
+        BLWS_CUDA(cudaEventSynchronize(e1));
+        float ms = 0;
+        BLWS_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        if (it >= 0) total += ms;
+    }
+    BLWS_CUDA(cudaEventDestroy(e0));
+    BLWS_CUDA(cudaEventDestroy(e1));
+    if (checksum) *checksum = eonly ? frob(ctx, Y1.view()) : sum_partials(ctx, part.get(), nparts);
+    return 1e3 * total / std::max(reps, 1);
+}
 
 // ============================================================ rpca_adm
 // Row-sharded form: with `shard`, this rank holds rows [row0, row0 +
@@ -709,7 +841,10 @@ SolverStats rpca_adm(Context& ctx, Index m, const double* d_in, Index ldd, doubl
         stats.e_l0 = 0;
         return stats;
     }
-    DMat Wm(ctx, rows, m, false), Y(ctx, rows, m, false), E(ctx, rows, m, true);
+    // Y ping-pong (K7 reads one, writes the other); E exists only as the zero
+    // initial iterate until the end, where it is recomputed into the free Y buffer
+    DMat Wm(ctx, rows, m, false), Ybuf[2] = {DMat(ctx, rows, m, false), DMat(ctx, rows, m, true)};
+    int ycur = 0;
     copy(ctx, Wm.view(), D.view());
     DenseOperator op(ctx, rows, m, Wm.data(), Wm.ld);
     if (sharded) op.set_row_shard(m, shard->row0);
@@ -732,7 +867,7 @@ SolverStats rpca_adm(Context& ctx, Index m, const double* d_in, Index ldd, doubl
         }
     }
     const double dual_scale = std::max(norm2_d, dmax / lambda);
-    scale_into_k<<<gridn(rows * m), kT, 0, ctx.stream()>>>(D.data(), Y.data(), rows, m, ld, dual_scale);
+    scale_into_k<<<gridn(rows * m), kT, 0, ctx.stream()>>>(D.data(), Ybuf[0].data(), rows, m, ld, dual_scale);
     ctx.note_launch();
 
     RankPredictor predictor;
@@ -745,21 +880,13 @@ SolverStats rpca_adm(Context& ctx, Index m, const double* d_in, Index ldd, doubl
     DBuf<int> bad(ctx, 1);
     // first W = D - E + Y/mu (later ones come out of the fused kernel)
     zero(ctx, bad.get(), sizeof(int));
-    form_w_k<<<gridn(rows * m), kT, 0, ctx.stream()>>>(D.data(), E.data(), Y.data(), Wm.data(), rows, m, ld, mu,
-                                                        bad.get());
+    form_w_k<<<gridn(rows * m), kT, 0, ctx.stream()>>>(D.data(), Ybuf[1].data() /* E0 = 0 */, Ybuf[0].data(),
+                                                        Wm.data(), rows, m, ld, mu, bad.get());
     ctx.note_launch();
-    using namespace gemm_detail;
-    const dim3 grid(static_cast<unsigned>(ceil_div(rows, BM)), static_cast<unsigned>(ceil_div(m, BN)));
-    const long k7tiles = ceil_div(rows, k7::BM) * ceil_div(m, k7::BN);  // alm_tma_k's tile grid
-    DBuf<double> part(ctx, static_cast<size_t>(std::max<long>(static_cast<long>(grid.x) * grid.y, k7tiles)));
-    long nparts = static_cast<long>(grid.x) * grid.y;
-    constexpr int smem = smem_bytes<false, true>();
-    BLWS_CUDA(cudaFuncSetAttribute(alm_fused_k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    BLWS_CUDA(cudaFuncSetAttribute(alm_tma_k, cudaFuncAttributeMaxDynamicSharedMemorySize, k7::SMEM));
-    const bool use_tma = [] {
-        const char* e = std::getenv("BLWS_K7");
-        return !(e && std::string(e) == "cpasync");
-    }();
+    DBuf<double> part(ctx, static_cast<size_t>(alm_partials_max(rows, m)));
+    long nparts = 0;
+    DMat us;                         // U diag(s) of the last prox (kept for the E pass)
+    double mu_last = mu;             // mu of the last K7 launch
     SvtResult prox;
     phase.reset();
     for (Index it = 1; it <= opts.max_iter; ++it) {
@@ -776,29 +903,15 @@ SolverStats rpca_adm(Context& ctx, Index m, const double* d_in, Index ldd, doubl
         prox = svt(op, 1.0 / mu, backend, predictor);
         last_rank = prox.achieved_rank;
         const Index r = prox.achieved_rank;
-        DMat us(ctx, rows, std::max<Index>(r, 1), false);
+        us = DMat(ctx, rows, std::max<Index>(r, 1), false);
         if (r > 0) scale_columns(ctx, us.view().left(r), prox.trip.u(), prox.sigma_dev.get());
         const double mu_next = std::min(opts.rho * mu, mu_max);
         zero(ctx, bad.get(), sizeof(int));
-        CUtensorMap tmu, tmv, tmd, tmy;
-        if (use_tma && r > 0 && tma_map_2d(&tmu, us.data(), rows, r, us.ld, k7::BK) &&
-            tma_map_2d(&tmv, prox.trip.v().p, m, r, prox.trip.uv.ld, k7::BK) &&
-            tma_map_2d(&tmd, D.data(), rows, m, ld, k7::BN) && tma_map_2d(&tmy, Y.data(), rows, m, ld, k7::BN)) {
-            nparts = k7tiles;
-            const unsigned ctas = static_cast<unsigned>(std::min<long>(2L * ctx.sm_count(), k7tiles));
-            alm_tma_k<<<ctas, k7::THREADS, k7::SMEM, ctx.stream()>>>(tmu, tmv, tmd, tmy, rows, m, r, Y.data(),
-                                                                     Wm.data(), E.data(), ld, mu, mu_next, lambda / mu,
-                                                                     part.get(), bad.get());
-            ctx.note_launch();
-            ctx.check_launch("alm_tma_k");
-        } else {
-            nparts = static_cast<long>(grid.x) * grid.y;
-            alm_fused_k<<<grid, THREADS, smem, ctx.stream()>>>(us.data(), us.ld, prox.trip.v().p, prox.trip.uv.ld, rows,
-                                                               m, r, D.data(), Y.data(), Wm.data(), E.data(), ld, mu,
-                                                               mu_next, lambda / mu, part.get(), bad.get());
-            ctx.note_launch();
-            ctx.check_launch("alm_fused_k");
-        }
+        nparts = alm_launch(ctx, false, rows, m, r, us, prox.trip.v(), D.data(), Ybuf[ycur].data(),
+                            Ybuf[1 - ycur].data(), Wm.data(), nullptr, ld, mu, mu_next, lambda / mu, part.get(),
+                            bad.get());
+        ycur = 1 - ycur;
+        mu_last = mu;
         mu = mu_next;
         stats.matvec_history.push_back(op.application_count() - mark);
         mark = op.application_count();
@@ -816,6 +929,15 @@ SolverStats rpca_adm(Context& ctx, Index m, const double* d_in, Index ldd, doubl
     phase.emplace(ctx, 9);
     // A = U diag(s) V^T of the last prox; E, e_l0, rel_err
     const Index r = prox.achieved_rank;
+    // E of the last iteration: the K7 tile recomputed from that iteration's
+    // inputs (U diag(s), V, D, the Y it read, its mu), bitwise the values the
+    // iteration formed, stored into the Y buffer it wrote (not needed any more)
+    DMat& E = Ybuf[ycur];
+    if (stats.iterations > 0)
+        alm_launch(ctx, true, rows, m, r, us, prox.trip.v(), D.data(), Ybuf[1 - ycur].data(), nullptr, nullptr,
+                   E.data(), ld, mu_last, mu, lambda / mu_last, nullptr, nullptr);
+    else
+        fill(ctx, E.view(), 0.0);
     DMat A(ctx, rows, m, false);
     if (r > 0) {
         DMat us(ctx, rows, r, false);
