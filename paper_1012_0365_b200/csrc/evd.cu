@@ -15,6 +15,9 @@
 #include <cstdlib>
 #include <vector>
 
+#include <string>
+
+#include "bulk.cuh"
 #include "ops.cuh"
 
 namespace blws {
@@ -335,6 +338,147 @@ __global__ void __launch_bounds__(kOrmFullWarps * 32) ormtr_full_k(const double*
     }
 }
 
+// The same product with the reflectors taken G at a time in compact WY form
+// (LAPACK dlarft, forward / columnwise): H_lo H_lo+1 ... H_lo+G-1 = I - V T V^T,
+// so each eigenvector needs ceil((n-2) / G) sequential steps, each with G
+// independent dot products reduced together, instead of n - 2 steps with one
+// warp reduction each (the reduction latency was the whole cost). The T factors
+// (G x G upper triangular per group, from the pairwise v_i^T v_j and tau) are
+// formed once per block in shared memory. Group g = 0 holds the highest
+// reflector indices (applied first).
+template <int QN, int G>
+__global__ void __launch_bounds__(kOrmFullWarps * 32) ormtr_wy_k(const double* __restrict__ lp,
+                                                                  const double* __restrict__ tau, int n, int want,
+                                                                  double* z, long ldz) {
+    extern __shared__ __align__(16) double sm[];
+    __shared__ __align__(8) uint64_t bar;
+    const long np = static_cast<long>(n) * (n + 1) / 2;
+    double* a = sm;                 // packed lower triangle with the reflectors
+    double* ts = sm + (np + 1) / 2 * 2;  // n (16-byte aligned)
+    double* tf = ts + n;            // groups x G x G
+    const int nref = n - 2;   // reflectors 0 .. n-3
+    const int groups = (nref + G - 1) / G;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) ts[i] = tau[i];
+    block_load_bulk(a, lp, np, &bar);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // ---- T factors, one group per warp at a time
+    for (int g = warp; g < groups; g += kOrmFullWarps) {
+        const int hi = nref - g * G, lo = max(0, hi - G), cnt = hi - lo;
+        double d[G][G];  // d[l][j] = v_l^T v_j (l < j), rows > lo + j
+#pragma unroll
+        for (int l = 0; l < G; ++l)
+#pragma unroll
+            for (int j = 0; j < G; ++j) d[l][j] = 0.0;
+#pragma unroll
+        for (int q = 0; q < QN; ++q) {
+            const int i = lane + 32 * q;
+            double vr[G];
+#pragma unroll
+            for (int l = 0; l < G; ++l) {
+                const int k = lo + l;
+                vr[l] = (l < cnt && i > k && i < n) ? a[lidx(k, k, n) - k + i] : 0.0;
+            }
+#pragma unroll
+            for (int j = 1; j < G; ++j)
+#pragma unroll
+                for (int l = 0; l < j; ++l) d[l][j] = fma(vr[l], vr[j], d[l][j]);
+        }
+#pragma unroll
+        for (int j = 1; j < G; ++j)
+#pragma unroll
+            for (int l = 0; l < j; ++l)
+                for (int o = 16; o > 0; o >>= 1) d[l][j] += __shfl_xor_sync(0xffffffffu, d[l][j], o);
+        if (lane == 0) {
+            double* T = tf + static_cast<long>(g) * G * G;  // T[i + j G]
+#pragma unroll
+            for (int j = 0; j < G; ++j) {
+                const double tj = j < cnt ? ts[lo + j] : 0.0;
+#pragma unroll
+                for (int i = 0; i < G; ++i) {
+                    double w = 0.0;
+                    if (i < j) {
+#pragma unroll
+                        for (int l = 0; l < G; ++l)
+                            if (l >= i && l < j) w = fma(T[i + l * G], d[l][j], w);
+                    }
+                    T[i + j * G] = i < j ? -tj * w : (i == j ? tj : 0.0);
+                }
+            }
+        }
+    }
+    __syncthreads();
+    const long jv = static_cast<long>(blockIdx.x) * kOrmFullWarps + warp;
+    if (jv >= want) return;
+    double zr[QN];
+#pragma unroll
+    for (int q = 0; q < QN; ++q) {
+        const int i = lane + 32 * q;
+        zr[q] = i < n ? z[i + jv * ldz] : 0.0;
+    }
+    for (int g = 0; g < groups; ++g) {
+        const int hi = nref - g * G, lo = max(0, hi - G), cnt = hi - lo;
+        double sv[G], vq[QN][G];
+#pragma unroll
+        for (int l = 0; l < G; ++l) sv[l] = 0.0;
+#pragma unroll
+        for (int q = 0; q < QN; ++q) {
+            const int i = lane + 32 * q;
+#pragma unroll
+            for (int l = 0; l < G; ++l) {
+                const int k = lo + l;
+                // slots whose rows are all <= lo hold no reflector entries (warp-uniform)
+                vq[q][l] = (32 * q + 31 > lo && l < cnt && i > k && i < n) ? a[lidx(k, k, n) - k + i] : 0.0;
+                sv[l] = fma(vq[q][l], zr[q], sv[l]);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+            for (int l = 0; l < G; ++l) sv[l] += __shfl_xor_sync(0xffffffffu, sv[l], o);
+        const double* T = tf + static_cast<long>(g) * G * G;
+        double u[G];  // u = T s (upper triangular)
+#pragma unroll
+        for (int i = 0; i < G; ++i) {
+            double acc = 0.0;
+#pragma unroll
+            for (int j = i; j < G; ++j) acc = fma(T[i + j * G], sv[j], acc);
+            u[i] = acc;
+        }
+#pragma unroll
+        for (int q = 0; q < QN; ++q)
+#pragma unroll
+            for (int l = 0; l < G; ++l) zr[q] = fma(-u[l], vq[q][l], zr[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < QN; ++q) {
+        const int i = lane + 32 * q;
+        if (i < n) z[i + jv * ldz] = zr[q];
+    }
+}
+
+#ifndef BLWS_ORM_G
+#define BLWS_ORM_G 4
+#endif
+template <int QN>
+bool launch_ormtr_wy(Context& ctx, const double* lp, const double* tau, int n, int want, View z) {
+    constexpr int G = BLWS_ORM_G;
+    const int groups = (n - 2 + G - 1) / G;
+    const size_t bytes =
+        (static_cast<size_t>(n) + 1 + static_cast<size_t>(n) * (n + 1) / 2 + static_cast<size_t>(groups) * G * G) *
+        sizeof(double);
+    if (bytes > 220u * 1024u) return false;
+    static bool cfg = false;
+    if (!cfg) {
+        BLWS_CUDA(cudaFuncSetAttribute(ormtr_wy_k<QN, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+        cfg = true;
+    }
+    ormtr_wy_k<QN, G><<<static_cast<unsigned>((want + kOrmFullWarps - 1) / kOrmFullWarps), kOrmFullWarps * 32, bytes,
+                        ctx.stream()>>>(lp, tau, n, want, z.p, z.ld);
+    ctx.note_launch();
+    ctx.check_launch("ormtr_wy_k");
+    return true;
+}
+
 template <int QN>
 bool launch_ormtr_full(Context& ctx, const double* lp, const double* tau, int n, int want, View z) {
     const size_t bytes = (static_cast<size_t>(n) + static_cast<size_t>(n) * (n + 1) / 2) * sizeof(double);
@@ -352,6 +496,22 @@ bool launch_ormtr_full(Context& ctx, const double* lp, const double* tau, int n,
 }
 
 bool ormtr_full(Context& ctx, const double* lp, const double* tau, int n, int want, View z) {
+    static const bool wy = [] {
+        const char* e = std::getenv("BLWS_ORMTR");
+        return !(e && std::string(e) == "single");
+    }();
+    if (wy && n >= 3) {
+        switch ((n + 31) / 32) {
+            case 1: if (launch_ormtr_wy<1>(ctx, lp, tau, n, want, z)) return true; break;
+            case 2: if (launch_ormtr_wy<2>(ctx, lp, tau, n, want, z)) return true; break;
+            case 3: if (launch_ormtr_wy<3>(ctx, lp, tau, n, want, z)) return true; break;
+            case 4: if (launch_ormtr_wy<4>(ctx, lp, tau, n, want, z)) return true; break;
+            case 5: if (launch_ormtr_wy<5>(ctx, lp, tau, n, want, z)) return true; break;
+            case 6: if (launch_ormtr_wy<6>(ctx, lp, tau, n, want, z)) return true; break;
+            case 7: if (launch_ormtr_wy<7>(ctx, lp, tau, n, want, z)) return true; break;
+            default: break;
+        }
+    }
     switch ((n + 31) / 32) {
         case 1: return launch_ormtr_full<1>(ctx, lp, tau, n, want, z);
         case 2: return launch_ormtr_full<2>(ctx, lp, tau, n, want, z);

@@ -8,6 +8,7 @@ oracle on the same seeded inputs.
   BLWS_COOP=cols    the column-owned cooperative Lanczos kernel (lanczos_coop.cu)
   BLWS_NO_COOP=1    the per-kernel Lanczos steps
   BLWS_SYTRD=cluster the cluster tridiagonalisation below order 224
+  BLWS_ORMTR=single one reflector at a time in the back-transformation (ormtr_full_k)
   BLWS_EXACT=1, BLWS_GRAPHS=0  the host-branching blws_svd path, no CUDA graphs
 """
 import os
@@ -53,7 +54,7 @@ print("variant ok")
 
 
 @pytest.mark.parametrize("env", [{"BLWS_TMA": "0"}, {"BLWS_K7": "cpasync"}, {"BLWS_COOP": "cols"},
-                                 {"BLWS_NO_COOP": "1"}, {"BLWS_SYTRD": "cluster"},
+                                 {"BLWS_NO_COOP": "1"}, {"BLWS_SYTRD": "cluster"}, {"BLWS_ORMTR": "single"},
                                  {"BLWS_EXACT": "1", "BLWS_GRAPHS": "0"}])
 def test_switch_variant_matches_oracle(env):
     e = dict(os.environ)
