@@ -23,6 +23,7 @@
 #ifndef BLWS_CUDA_H
 #define BLWS_CUDA_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -97,6 +98,13 @@ int blws_dense_operator_create(blws_context* ctx, int64_t m, int64_t n, const do
 int blws_nccl_unique_id(uint8_t* out128);
 /* Collective over all ranks: attach an NCCL communicator to the context. */
 int blws_context_init_comm(blws_context* ctx, int nranks, int rank, const uint8_t* id128);
+/* Host-staged collectives instead of NCCL (several ranks sharing one GPU in
+ * tests): every reduction synchronises the context's stream and calls
+ * fn(buf, count, op, user) on a host copy (op 0 sum, 1 max); fn returns 0 after
+ * leaving the reduced values in buf on every rank. No CUDA-graph capture while
+ * set. Not a product path: NCCL (blws_context_init_comm) is. */
+typedef int (*blws_host_allreduce_fn)(double* buf, size_t count, int op, void* user);
+int blws_context_init_host_comm(blws_context* ctx, int nranks, int rank, blws_host_allreduce_fn fn, void* user);
 int blws_context_comm_info(const blws_context* ctx, int* nranks, int* rank);
 /* Mark a dense operator holding m_local = rows() rows as rows [row0, row0 +
    m_local) of an m_total x n matrix distributed over the context's ranks. */

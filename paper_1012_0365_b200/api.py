@@ -71,6 +71,7 @@ SIGNATURES = {
     "blws_dense_operator_assign_async": (ci, [vp, vp, i64]),
     "blws_nccl_unique_id": (ci, [vp]),
     "blws_context_init_comm": (ci, [vp, ci, ci, vp]),
+    "blws_context_init_host_comm": (ci, [vp, ci, ci, vp, vp]),
     "blws_context_comm_info": (ci, [vp, P(ci), P(ci)]),
     "blws_dense_operator_set_row_shard": (ci, [vp, i64, i64]),
     "blws_sparse_operator_create": (ci, [vp, i64, i64, i64, vp, vp, vp, P(vp)]),
@@ -207,6 +208,26 @@ class Context:
         """Attach an NCCL communicator (collective over all ranks; see dist.init_comm)."""
         buf = (C.c_uint8 * 128).from_buffer_copy(bytes(unique_id))
         _check(lib().blws_context_init_comm(self._h, int(nranks), int(rank), C.cast(buf, vp)))
+
+    # int (*)(double* buf, size_t count, int op, void* user)
+    HOST_ALLREDUCE = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_double), C.c_size_t, C.c_int, C.c_void_p)
+
+    def init_host_comm(self, nranks: int, rank: int, allreduce):
+        """Host-staged collectives (tests: several ranks on one GPU). `allreduce(arr, op)`
+        reduces the float64 numpy array in place over the ranks (op 0 sum, 1 max)."""
+        import numpy as _np
+
+        def _cb(buf, count, op, user):
+            try:
+                allreduce(_np.ctypeslib.as_array(buf, shape=(int(count),)), int(op))
+                return 0
+            except Exception:  # noqa: BLE001 -- reported to the library as a failed collective
+                import traceback
+                traceback.print_exc()
+                return 1
+
+        self._host_cb = self.HOST_ALLREDUCE(_cb)  # kept alive with the context
+        _check(lib().blws_context_init_host_comm(self._h, int(nranks), int(rank), C.cast(self._host_cb, vp), None))
 
     def comm_info(self):
         nr, rk = ci(0), ci(0)

@@ -242,6 +242,13 @@ int blws_nccl_unique_id(uint8_t* out128) {
         comm_unique_id(out128);
     });
 }
+int blws_context_init_host_comm(blws_context* ctx, int nranks, int rank, blws_host_allreduce_fn fn, void* user) {
+    return guard([&] {
+        need(ctx && fn, "init_host_comm: null argument");
+        ctx->ctx->init_host_comm(nranks, rank, fn, user);
+    });
+}
+
 int blws_context_init_comm(blws_context* ctx, int nranks, int rank, const uint8_t* id128) {
     return guard([&] {
         need(ctx && id128, "init_comm: null argument");

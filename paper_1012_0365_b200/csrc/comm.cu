@@ -10,6 +10,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "common.cuh"
 
@@ -83,14 +84,38 @@ void Context::init_comm(int nranks, int rank, const void* id128) {
     rank_ = rank;
 }
 
+void Context::init_host_comm(int nranks, int rank, HostAllreduceFn fn, void* user) {
+    if (nranks < 1 || rank < 0 || rank >= nranks || !fn) throw std::invalid_argument("init_host_comm: bad arguments");
+    if (comm_ || host_fn_) throw std::invalid_argument("init_host_comm: communicator already set");
+    host_fn_ = fn;
+    host_user_ = user;
+    nranks_ = nranks;
+    rank_ = rank;
+}
+
+void Context::host_allreduce(double* p, size_t count, int op) {
+    // stream-ordered copies (a pageable cudaMemcpy to the device may return
+    // before the DMA lands, and the context's streams do not sync with it)
+    std::vector<double> h(count);
+    BLWS_CUDA(cudaMemcpyAsync(h.data(), p, sizeof(double) * count, cudaMemcpyDeviceToHost, stream()));
+    BLWS_CUDA(cudaStreamSynchronize(stream()));
+    if (host_fn_(h.data(), count, op, host_user_) != 0) throw CommError("host allreduce callback failed");
+    BLWS_CUDA(cudaMemcpyAsync(p, h.data(), sizeof(double) * count, cudaMemcpyHostToDevice, stream()));
+    BLWS_CUDA(cudaStreamSynchronize(stream()));  // h is freed on return
+}
+
 void Context::allreduce_sum(double* p, size_t count) {
-    if (!comm_ || count == 0) return;
+    if (count == 0) return;
+    if (host_fn_) return host_allreduce(p, count, 0);
+    if (!comm_) return;
     check(nccl().all_reduce(p, p, count, ncclDouble, ncclSum, static_cast<ncclComm_t>(comm_), stream()),
           "ncclAllReduce");
 }
 
 void Context::allreduce_max(double* p, size_t count) {
-    if (!comm_ || count == 0) return;
+    if (count == 0) return;
+    if (host_fn_) return host_allreduce(p, count, 1);
+    if (!comm_) return;
     check(nccl().all_reduce(p, p, count, ncclDouble, ncclMax, static_cast<ncclComm_t>(comm_), stream()),
           "ncclAllReduce");
 }

@@ -61,12 +61,20 @@ public:
     /// Row-sharded path: an NCCL communicator over `nranks`
     /// processes (one GPU each); allreduce_sum is a no-op without one.
     void init_comm(int nranks, int rank, const void* id128);
+    /// Host-staged collectives (testing the sharded path with several ranks on
+    /// one GPU): each collective synchronises the stream, copies the buffer to
+    /// the host and calls `fn(buf, count, op, user)` (op 0 sum, 1 max), which
+    /// must leave the reduced values in buf on every rank (e.g. a gloo
+    /// allreduce). CUDA graphs are not captured while it is set.
+    using HostAllreduceFn = int (*)(double* buf, size_t count, int op, void* user);
+    void init_host_comm(int nranks, int rank, HostAllreduceFn fn, void* user);
     void allreduce_sum(double* p, size_t count);
     void allreduce_max(double* p, size_t count);
     int nranks() const { return nranks_; }
     int rank() const { return rank_; }
-    bool distributed() const { return comm_ != nullptr && nranks_ > 1; }
-    bool has_comm() const { return comm_ != nullptr; }
+    bool distributed() const { return has_comm() && nranks_ > 1; }
+    bool has_comm() const { return comm_ != nullptr || host_fn_ != nullptr; }
+    bool host_comm() const { return host_fn_ != nullptr; }
     /// Fork/join onto a second compute stream (see AuxScope).
     void fork_aux();
     void join_aux();
@@ -115,7 +123,10 @@ private:
     cudaStream_t aux_ = nullptr, cur_ = nullptr;
     bool aux_open_ = false;  // forked, not yet joined
     void* comm_ = nullptr;
+    HostAllreduceFn host_fn_ = nullptr;
+    void* host_user_ = nullptr;
     int nranks_ = 1, rank_ = 0;
+    void host_allreduce(double* p, size_t count, int op);
     void destroy_comm() noexcept;
     cudaEvent_t fork_ev_ = nullptr, join_ev_ = nullptr;
     void* pinned_ = nullptr;

@@ -1229,7 +1229,7 @@ BlwsResult blws_svd(LinearOperator& w, const DWarm& warm, Index k, Index r, Rng&
 
     // ---- graph plan for this (operator data, shape); eager on first sight
     SvdGraph* plan = nullptr;
-    if (graphs_enabled()) {
+    if (graphs_enabled() && !ctx.host_comm()) {  // host-staged collectives cannot be captured
         for (auto& g : w.svd_graphs())
             if (g->key_data == w.data_key() && g->bs == bs && g->k == k && g->r == r && g->comm == ctx.has_comm())
                 plan = g.get();

@@ -47,6 +47,23 @@ def init_comm(ctx, group=None) -> None:
     ctx.init_comm(dist.get_world_size(group), dist.get_rank(group), uid)
 
 
+def init_host_comm(ctx, group=None) -> None:
+    """Attach host-staged collectives over a gloo process group to `ctx`: the
+    device buffer of every reduction is copied to the host and all-reduced with
+    torch.distributed (so several ranks can share one GPU in tests; NCCL through
+    init_comm is the product path)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    def allreduce(arr, op):
+        t = torch.from_numpy(arr)  # shares memory with the library's host copy
+        dist.all_reduce(t, op=dist.ReduceOp.SUM if op == 0 else dist.ReduceOp.MAX, group=group)
+        np.copyto(arr, t.numpy())
+
+    ctx.init_host_comm(dist.get_world_size(group), dist.get_rank(group), allreduce)
+
+
 def shard_operator(w_local, m_total: int, row0: int, ctx, device: bool = False, ld=None):
     """DenseOperator over this rank's row panel (host array or device tensor),
     marked as rows [row0, row0 + rows) of m_total."""
