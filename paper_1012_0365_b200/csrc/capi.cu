@@ -393,6 +393,7 @@ int blws_block_lanczos_procedure(blws_operator* w, int64_t b, const double* x1, 
                                  int64_t* built, int* terminated_early) {
     return guard([&] {
         Context& c = w->op->ctx();
+        need(!w->op->col_sharded(), "block_lanczos_procedure: a column-sharded operator's panels are split");
         const Stack geo{w->op->rows(), w->op->cols()};
         const Index dim = geo.m + geo.n;
         DMat x(c, geo.ld(), b, true);

@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "ops.cuh"
 
 namespace blws {
 namespace {
@@ -22,6 +23,9 @@ struct NcclApi {
     ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
     ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                                cudaStream_t) = nullptr;
+    ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*reduce_scatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                                   cudaStream_t) = nullptr;
     ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
     const char* (*error_string)(ncclResult_t) = nullptr;
 };
@@ -46,9 +50,12 @@ const NcclApi& nccl() {
         api.get_unique_id = reinterpret_cast<decltype(api.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
         api.comm_init_rank = reinterpret_cast<decltype(api.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
         api.all_reduce = reinterpret_cast<decltype(api.all_reduce)>(dlsym(h, "ncclAllReduce"));
+        api.all_gather = reinterpret_cast<decltype(api.all_gather)>(dlsym(h, "ncclAllGather"));
+        api.reduce_scatter = reinterpret_cast<decltype(api.reduce_scatter)>(dlsym(h, "ncclReduceScatter"));
         api.comm_destroy = reinterpret_cast<decltype(api.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
         api.error_string = reinterpret_cast<decltype(api.error_string)>(dlsym(h, "ncclGetErrorString"));
-        if (!api.get_unique_id || !api.comm_init_rank || !api.all_reduce || !api.comm_destroy)
+        if (!api.get_unique_id || !api.comm_init_rank || !api.all_reduce || !api.comm_destroy || !api.all_gather ||
+            !api.reduce_scatter)
             err = "NCCL: missing symbols";
     });
     if (!err.empty()) throw CommError(err);
@@ -118,6 +125,42 @@ void Context::allreduce_max(double* p, size_t count) {
     if (!comm_) return;
     check(nccl().all_reduce(p, p, count, ncclDouble, ncclMax, static_cast<ncclComm_t>(comm_), stream()),
           "ncclAllReduce");
+}
+
+// recv[r count, (r+1) count) = send of rank r (recv holds nranks x count)
+void Context::allgather(const double* send, double* recv, size_t count) {
+    if (count == 0) return;
+    if (host_fn_) {
+        // through the host allreduce: every rank contributes its block into a
+        // zeroed buffer (x + 0 is exact)
+        zero(*this, recv, sizeof(double) * count * static_cast<size_t>(nranks_));
+        BLWS_CUDA(cudaMemcpyAsync(recv + count * static_cast<size_t>(rank_), send, sizeof(double) * count,
+                                  cudaMemcpyDeviceToDevice, stream()));
+        return host_allreduce(recv, count * static_cast<size_t>(nranks_), 0);
+    }
+    if (!comm_) {
+        BLWS_CUDA(cudaMemcpyAsync(recv, send, sizeof(double) * count, cudaMemcpyDeviceToDevice, stream()));
+        return;
+    }
+    check(nccl().all_gather(send, recv, count, ncclDouble, static_cast<ncclComm_t>(comm_), stream()),
+          "ncclAllGather");
+}
+
+// recv (count) = sum over the ranks of send[rank count, (rank+1) count)
+void Context::reduce_scatter_sum(double* send, double* recv, size_t count) {
+    if (count == 0) return;
+    if (host_fn_) {
+        host_allreduce(send, count * static_cast<size_t>(nranks_), 0);  // send is scratch
+        BLWS_CUDA(cudaMemcpyAsync(recv, send + count * static_cast<size_t>(rank_), sizeof(double) * count,
+                                  cudaMemcpyDeviceToDevice, stream()));
+        return;
+    }
+    if (!comm_) {
+        BLWS_CUDA(cudaMemcpyAsync(recv, send, sizeof(double) * count, cudaMemcpyDeviceToDevice, stream()));
+        return;
+    }
+    check(nccl().reduce_scatter(send, recv, count, ncclDouble, ncclSum, static_cast<ncclComm_t>(comm_), stream()),
+          "ncclReduceScatter");
 }
 
 void Context::destroy_comm() noexcept {

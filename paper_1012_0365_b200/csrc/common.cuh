@@ -70,6 +70,11 @@ public:
     void init_host_comm(int nranks, int rank, HostAllreduceFn fn, void* user);
     void allreduce_sum(double* p, size_t count);
     void allreduce_max(double* p, size_t count);
+    /// recv (nranks x count) = every rank's `send` block in rank order.
+    void allgather(const double* send, double* recv, size_t count);
+    /// recv (count) = sum over the ranks of their send block `rank()`
+    /// (send: nranks x count, used as scratch by the host-staged form).
+    void reduce_scatter_sum(double* send, double* recv, size_t count);
     int nranks() const { return nranks_; }
     int rank() const { return rank_; }
     bool distributed() const { return has_comm() && nranks_ > 1; }

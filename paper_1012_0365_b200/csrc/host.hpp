@@ -93,8 +93,21 @@ public:
     void set_row_shard(Index m_total, Index row0);
     bool row_sharded() const { return shard_.m_total > 0; }
     const RowShard& shard() const { return shard_; }
-    /// The split of a stacked panel of this operator (top rows sharded).
+    /// The split of a stacked panel of this operator: the top rows, and with
+    /// column sharding the bottom rows too, are summed over the ranks.
     RowSplit panel_split() const;
+    /// Column (n-side) sharding of the stacked panels: a row-sharded
+    /// operator with a communicator keeps only the bottom rows [col0, col0 +
+    /// chunk) of every panel (chunk = ceil(n / nranks); rows past n are zero
+    /// padding), so V, the bottom halves of the Lanczos bases and every
+    /// n-length vector are split across the ranks instead of replicated. The
+    /// paired apply all-gathers X_bot before W X_bot and reduce-scatters W^T
+    /// X_top. BLWS_NSHARD=0 keeps the bottom rows replicated.
+    bool col_sharded() const;
+    Index col_chunk() const;
+    Index col0() const { return col_sharded() ? col_chunk() * ctx_.rank() : 0; }
+    /// bottom rows of this operator's stacked panels (chunk, or n unsharded)
+    Index panel_n() const { return col_sharded() ? col_chunk() : cols(); }
     std::vector<std::shared_ptr<SvdGraph>>& svd_graphs() { return svd_graphs_; }
 
 protected:
@@ -218,8 +231,10 @@ struct BlwsResult {
 /// adapt_subspace (block_lanczos.hpp:157-187).
 /// With `shard`, m is the local row count and the Gaussian padding of U is
 /// drawn for all m_total rows (the reference's draw order) and sliced.
+/// With chunk >= 0, V holds only rows [col0, col0 + chunk) of the n drawn
+/// (a column-sharded panel; rows past n zero).
 DWarm adapt_subspace(Context& ctx, const DWarm* warm, Index r_new, Index m, Index n, Rng& rng,
-                     const RowShard* shard = nullptr);
+                     const RowShard* shard = nullptr, Index col0 = 0, Index chunk = -1);
 /// blws_svd (block_lanczos.hpp:204-261).
 BlwsResult blws_svd(LinearOperator& w, const DWarm& warm, Index k, Index r, Rng& rng);
 extern std::atomic<std::int64_t> g_blws_deferred_fallbacks;

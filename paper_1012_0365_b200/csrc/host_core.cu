@@ -244,8 +244,43 @@ void LinearOperator::set_row_shard(Index m_total, Index row0) {
 }
 
 RowSplit LinearOperator::panel_split() const {
-    // the top of a stacked panel (rows [0, mp), padding row included: it is zero)
+    // the top of a stacked panel (rows [0, mp), padding row included: it is zero);
+    // with column sharding the whole panel
+    if (col_sharded()) return RowSplit{Stack{rows(), panel_n()}.ld()};
     return RowSplit{row_sharded() && ctx_.has_comm() ? round_up(rows(), 2) : 0};
+}
+
+bool LinearOperator::col_sharded() const {
+    static const bool off = [] {
+        const char* e = std::getenv("BLWS_NSHARD");
+        return e && std::string(e) == "0";
+    }();
+    return !off && row_sharded() && ctx_.has_comm();
+}
+
+Index LinearOperator::col_chunk() const { return ceil_div(cols(), std::max(1, ctx_.nranks())); }
+
+// ---- column-sharded panels: gather / scatter of the bottom rows
+// dst (npad x b, col-major, ld npad) = the bottom rows of every rank, in rank
+// order (chunk x b each, `src` with its own ld)
+void gather_cols(LinearOperator& w, View src, double* dst) {
+    Context& ctx = w.ctx();
+    const Index chunk = w.col_chunk(), b = src.cols, N = ctx.nranks();
+    DBuf<double> send(ctx, static_cast<size_t>(chunk * b)), recv(ctx, static_cast<size_t>(chunk * b * N));
+    pack_rows(ctx, src, send.get());  // row-major chunk x b: one contiguous block per rank
+    ctx.allgather(send.get(), recv.get(), static_cast<size_t>(chunk * b));
+    unpack_rows(ctx, recv.get(), View{dst, chunk * N, b, chunk * N});
+}
+
+// dst (chunk x b, this rank's bottom rows) = sum over the ranks of the rows
+// [col0, col0 + chunk) of `part` (npad x b, col-major, ld npad; rows past n zero)
+void scatter_cols(LinearOperator& w, View part, View dst) {
+    Context& ctx = w.ctx();
+    const Index chunk = w.col_chunk(), b = part.cols, N = ctx.nranks();
+    DBuf<double> send(ctx, static_cast<size_t>(chunk * b * N)), recv(ctx, static_cast<size_t>(chunk * b));
+    pack_rows(ctx, part, send.get());
+    ctx.reduce_scatter_sum(send.get(), recv.get(), static_cast<size_t>(chunk * b));
+    unpack_rows(ctx, recv.get(), dst);
 }
 
 // ======================================================== DenseOperator
@@ -328,7 +363,22 @@ void DenseOperator::pair_block_impl(View left, View right, View top, View bot) {
     const Index b = right.cols;
     // K1: region 0 times the paired product (both GEMMs incl. split-K reduce)
     ctx_.region_begin(0);
-    if (row_sharded() && ctx_.has_comm()) {
+    if (col_sharded()) {
+        // X_bot is split over the ranks: all-gather it for W X_bot; W^T X_top
+        // over the local rows is reduce-scattered into this rank's bottom rows
+        const Index npad = col_chunk() * ctx_.nranks();
+        DBuf<double> xfull(ctx_, static_cast<size_t>(npad * b)), part(ctx_, static_cast<size_t>(npad * b));
+        if (npad > n_) zero(ctx_, part.get(), sizeof(double) * static_cast<size_t>(npad * b));  // padding rows
+        {
+            // the collectives stay on the main stream, in the same order on every rank
+            AuxScope aux(ctx_);
+            gemm(ctx_, true, false, n_, b, m_, 1.0, p_, ld_, left.p, left.ld, 0.0, part.get(), npad);
+            aux.main();
+            gather_cols(*this, right, xfull.get());
+            gemm(ctx_, false, false, m_, b, n_, 1.0, p_, ld_, xfull.get(), npad, 0.0, top.p, top.ld);
+        }
+        scatter_cols(*this, View{part.get(), npad, b, npad}, bot);
+    } else if (row_sharded() && ctx_.has_comm()) {
         // W^T U over the local rows, summed over the ranks (contiguous n x b
         // buffer for the allreduce), while W V runs on the local rows only
         DBuf<double> part(ctx_, static_cast<size_t>(n_ * b));
@@ -349,6 +399,16 @@ void DenseOperator::pair_block_impl(View left, View right, View top, View bot) {
 
 void DenseOperator::pair_impl(const double* left, const double* right, double* top, double* bot) {
     ensure_ready();
+    if (col_sharded()) {
+        // right / bot are this rank's chunk of the n-length halves
+        const Index chunk = col_chunk(), npad = chunk * ctx_.nranks();
+        DBuf<double> xfull(ctx_, static_cast<size_t>(npad)), part(ctx_, static_cast<size_t>(npad));
+        if (npad > n_) zero(ctx_, part.get() + n_, sizeof(double) * static_cast<size_t>(npad - n_));
+        ctx_.allgather(right, xfull.get(), static_cast<size_t>(chunk));
+        pair_gemv(ctx_, m_, n_, p_, ld_, xfull.get(), left, top, part.get());  // one read of W for both products
+        ctx_.reduce_scatter_sum(part.get(), bot, static_cast<size_t>(chunk));
+        return;
+    }
     pair_gemv(ctx_, m_, n_, p_, ld_, right, left, top, bot);  // one read of W for both products
     if (row_sharded() && ctx_.has_comm()) ctx_.allreduce_sum(bot, static_cast<size_t>(n_));  // W^T left over the ranks
 }
@@ -408,6 +468,23 @@ void SparseOperator::pair_block_impl(View left, View right, View top, View bot) 
     // they are freed on the main stream after the join.
     const size_t need = static_cast<size_t>(std::max(m_, n_) * b);
     DBuf<double> scratch(ctx_, need), scratch2(ctx_, need);
+    if (col_sharded()) {
+        // as DenseOperator: all-gather X_bot, reduce-scatter the W^T X_top partial
+        const Index npad = col_chunk() * ctx_.nranks();
+        DBuf<double> xfull(ctx_, static_cast<size_t>(npad * b)), part(ctx_, static_cast<size_t>(npad * b));
+        if (npad > n_) zero(ctx_, part.get(), sizeof(double) * static_cast<size_t>(npad * b));
+        {
+            AuxScope aux(ctx_);
+            csr_spmm(ctx_, n_, colptr_.get(), rowidx_.get(), val_csc_.get(), m_, b, left.p, left.ld, part.get(), npad,
+                     scratch2.get());
+            aux.main();
+            gather_cols(*this, right, xfull.get());
+            csr_spmm(ctx_, m_, rowptr_.get(), colidx_.get(), val_csr_.get(), n_, b, xfull.get(), npad, top.p, top.ld,
+                     scratch.get());
+        }
+        scatter_cols(*this, View{part.get(), npad, b, npad}, bot);
+        return;
+    }
     const bool reduce = row_sharded() && ctx_.has_comm();
     DBuf<double> part;  // row shard: W^T x over the local rows, summed over the ranks
     if (reduce && bot.ld != n_) part = DBuf<double>(ctx_, static_cast<size_t>(n_ * b));
@@ -428,6 +505,19 @@ void SparseOperator::pair_block_impl(View left, View right, View top, View bot) 
 }
 
 void SparseOperator::pair_impl(const double* left, const double* right, double* top, double* bot) {
+    if (col_sharded()) {
+        const Index chunk = col_chunk(), npad = chunk * ctx_.nranks();
+        DBuf<double> xfull(ctx_, static_cast<size_t>(npad)), part(ctx_, static_cast<size_t>(npad));
+        if (npad > n_) zero(ctx_, part.get() + n_, sizeof(double) * static_cast<size_t>(npad - n_));
+        ctx_.allgather(right, xfull.get(), static_cast<size_t>(chunk));
+        csr_spmv_pair_k<<<gridn((m_ + n_) * 32, 8192), kT, 0, ctx_.stream()>>>(
+            m_, rowptr_.get(), colidx_.get(), val_csr_.get(), xfull.get(), top, n_, colptr_.get(), rowidx_.get(),
+            val_csc_.get(), left, part.get());
+        ctx_.note_launch();
+        ctx_.check_launch("csr_spmv_pair");
+        ctx_.reduce_scatter_sum(part.get(), bot, static_cast<size_t>(chunk));
+        return;
+    }
     csr_spmv_pair_k<<<gridn((m_ + n_) * 32, 8192), kT, 0, ctx_.stream()>>>(
         m_, rowptr_.get(), colidx_.get(), val_csr_.get(), right, top, n_, colptr_.get(), rowidx_.get(),
         val_csc_.get(), left, bot);
@@ -683,39 +773,48 @@ Index thin_qr_impl(Context& ctx, View x, View* r_out, RowSplit split) {
 
 // ======================================================== adapt_subspace
 DWarm adapt_subspace(Context& ctx, const DWarm* warm, Index r_new, Index m, Index n, Rng& rng,
-                     const RowShard* shard) {
+                     const RowShard* shard, Index col0, Index chunk) {
     // with a row shard, U's Gaussian columns are drawn for all m_total rows in the
-    // reference's (column-major) order and this rank keeps rows [row0, row0 + m)
+    // reference's (column-major) order and this rank keeps rows [row0, row0 + m);
+    // with a column slice (chunk >= 0) V's are drawn for all n rows and this rank
+    // keeps rows [col0, col0 + chunk) (rows past n stay zero padding)
     const bool sh = shard && shard->m_total > 0;
-    const Index mt = sh ? shard->m_total : m, r0 = sh ? shard->row0 : 0;
+    const bool cs = chunk >= 0;
+    const Index mt = sh ? shard->m_total : m, r0 = sh ? shard->row0 : 0, pn = cs ? chunk : n;
     const RowSplit usplit{sh && ctx.has_comm() ? m : 0};
+    const RowSplit vsplit{cs && ctx.has_comm() ? pn : 0};
     if (r_new < 1 || r_new > std::min(mt, n)) throw std::invalid_argument("adapt_subspace: r_new out of range");
+    auto put_v = [&](View dst, const double* h) {  // the drawn n x cols block, this rank's rows
+        if (!cs) return upload(ctx, dst, h, n);
+        const Index take = std::max<Index>(0, std::min(n, col0 + chunk) - col0);
+        if (take > 0) upload(ctx, View{dst.p, take, dst.cols, dst.ld}, h + col0, n);
+    };
     if (!warm || warm->rank() == 0) {
-        DWarm out = make_warm(ctx, m, n, r_new);
+        DWarm out = make_warm(ctx, m, pn, r_new);
         std::vector<double> h(static_cast<size_t>(std::max(mt, n) * r_new));
         rng.gaussian_matrix(mt, r_new, h.data(), mt);
         upload(ctx, out.u(), h.data() + r0, mt);
         rng.gaussian_matrix(n, r_new, h.data(), n);
-        upload(ctx, out.v(), h.data(), n);
+        put_v(out.v(), h.data());
         View u = out.u(), v = out.v();
         thin_qr(ctx, u, nullptr, usplit);
-        thin_qr(ctx, v, nullptr);
+        thin_qr(ctx, v, nullptr, vsplit);
         return out;
     }
     const Index r_old = warm->rank();
     if (r_new == r_old) return copy_warm(ctx, *warm, r_old);
     if (r_new < r_old) return copy_warm(ctx, *warm, r_new);
     const Index add = r_new - r_old;
-    DWarm out = make_warm(ctx, m, n, r_new);
+    DWarm out = make_warm(ctx, m, pn, r_new);
     copy(ctx, out.panel().left(r_old), warm->panel().left(r_old));
     std::vector<double> h(static_cast<size_t>(std::max(mt, n) * add));
     rng.gaussian_matrix(mt, add, h.data(), mt);
     upload(ctx, out.u().cols_range(r_old, add), h.data() + r0, mt);
     rng.gaussian_matrix(n, add, h.data(), n);
-    upload(ctx, out.v().cols_range(r_old, add), h.data(), n);
+    put_v(out.v().cols_range(r_old, add), h.data());
     View u = out.u(), v = out.v();
     thin_qr(ctx, u, nullptr, usplit);
-    thin_qr(ctx, v, nullptr);
+    thin_qr(ctx, v, nullptr, vsplit);
     std::copy(warm->sigma.begin(), warm->sigma.end(), out.sigma.begin());
     return out;
 }
@@ -741,8 +840,8 @@ double read_scalar(Context& ctx, const double* d) {
 // block_lanczos.hpp:70-126 on the augmented view; x1 is a stacked panel.
 BlockLanczos block_lanczos_procedure(LinearOperator& w, View x1, Index k) {
     Context& ctx = w.ctx();
-    const Stack geo{w.rows(), w.cols()};
-    const Index dim = (w.row_sharded() ? w.shard().m_total : geo.m) + geo.n, bs = x1.cols, ld = geo.ld();
+    const Stack geo{w.rows(), w.panel_n()};  // bottom rows: this rank's columns when column-sharded
+    const Index dim = global_rows(w) + w.cols(), bs = x1.cols, ld = geo.ld();
     if (k < 1) throw std::invalid_argument("block_lanczos_procedure: k must be >= 1");
     if (bs < 1 || x1.rows != ld) throw std::invalid_argument("block_lanczos_procedure: bad initial block");
     if (k * bs > dim) throw std::invalid_argument("block_lanczos_procedure: k*b exceeds dimension");
@@ -812,12 +911,12 @@ BlockLanczos block_lanczos_procedure(LinearOperator& w, View x1, Index k) {
 // exact path; blws_svd() below tries the deferred path first).
 static BlwsResult blws_svd_exact(LinearOperator& w, const DWarm& warm, Index k, Index r, Rng& rng) {
     Context& ctx = w.ctx();
-    const Index m = w.rows(), n = w.cols();
+    const Index m = w.rows(), n = w.cols(), pn = w.panel_n();  // pn: the panels' bottom rows
     const Index bs = warm.rank();
     if (bs < 1) throw std::invalid_argument("blws_svd: empty warm start (seed via adapt_subspace)");
     const Index m_all = w.row_sharded() ? w.shard().m_total : m;
     if (r < 1 || r > std::min(m_all, n)) throw std::invalid_argument("blws_svd: bad r");
-    if (warm.geo.m != m || warm.geo.n != n) throw std::invalid_argument("blws_svd: warm start does not match operator");
+    if (warm.geo.m != m || warm.geo.n != pn) throw std::invalid_argument("blws_svd: warm start does not match operator");
     BlwsResult out;
     Index k_eff = k;
     if (r > k_eff * bs) {
@@ -826,7 +925,7 @@ static BlwsResult blws_svd_exact(LinearOperator& w, const DWarm& warm, Index k, 
     }
     k_eff = std::min(k_eff, (m_all + n) / bs);
     k_eff = std::max<Index>(k_eff, 1);
-    const Stack geo{m, n};
+    const Stack geo{m, pn};
 
     // X1 = qr([U; V] / sqrt(2)).q -- Q is invariant under the positive scale,
     // so the 1/sqrt(2) is folded away.
@@ -834,6 +933,7 @@ static BlwsResult blws_svd_exact(LinearOperator& w, const DWarm& warm, Index k, 
     copy(ctx, x1.view(), warm.panel());
     const RowSplit split = w.panel_split();
     const RowSplit usplit{split.sharded ? m : 0};
+    const RowSplit vsplit{w.col_sharded() ? pn : 0};
     {
         View xv = x1.view();
         thin_qr(ctx, xv, nullptr, split);
@@ -870,7 +970,7 @@ static BlwsResult blws_svd_exact(LinearOperator& w, const DWarm& warm, Index k, 
     Index keep = 0;
     while (keep < avail && keep < r && hv[static_cast<size_t>(keep)] > floor) ++keep;
 
-    DWarm next = make_warm(ctx, m, n, keep);
+    DWarm next = make_warm(ctx, m, pn, keep);
     if (keep > 0) {
         // Ritz lift of the kept columns only, sqrt(2) unpack fused (:240-248)
         gemm(ctx, false, false, geo.ld(), keep, d, std::sqrt(2.0), fac.q.data(), fac.q.ld, vecs.data(), vecs.ld, 0.0,
@@ -878,11 +978,11 @@ static BlwsResult blws_svd_exact(LinearOperator& w, const DWarm& warm, Index k, 
         std::copy(hv.begin(), hv.begin() + keep, next.sigma.begin());
         View u = next.u(), v = next.v();
         thin_qr(ctx, u, nullptr, usplit);
-        thin_qr(ctx, v, nullptr);
+        thin_qr(ctx, v, nullptr, vsplit);
     }
     if (keep < r) {
-        next = adapt_subspace(ctx, keep > 0 ? &next : nullptr, r, m, n, rng,
-                              w.row_sharded() ? &w.shard() : nullptr);
+        next = adapt_subspace(ctx, keep > 0 ? &next : nullptr, r, m, n, rng, w.row_sharded() ? &w.shard() : nullptr,
+                              w.col0(), w.col_sharded() ? pn : -1);
         out.padded = true;
     }
     out.warm = std::move(next);
@@ -1001,7 +1101,7 @@ struct LanczosRec {
 // so the caller-input orthonormality check of the exact path is not repeated.
 BlockLanczos block_lanczos_deferred(LinearOperator& w, View x1, Index k, Slots& sl, LanczosRec& rec) {
     Context& ctx = w.ctx();
-    const Stack geo{w.rows(), w.cols()};
+    const Stack geo{w.rows(), w.panel_n()};
     const Index bs = x1.cols, ld = geo.ld();
     const RowSplit split = w.panel_split();
     BlockLanczos out;
@@ -1121,7 +1221,7 @@ DeferredRecs enqueue_deferred(LinearOperator& w, View src, const DeferredShape& 
     View u{next_uv.p, sh.m, want, next_uv.ld}, v{next_uv.p + geo.mp(), sh.n, want, next_uv.ld};
     {
         AuxScope aux(ctx);  // the two QRs are independent
-        rec.qv = thin_qr_deferred(ctx, v, nullptr, sl, RowSplit{});
+        rec.qv = thin_qr_deferred(ctx, v, nullptr, sl, RowSplit{w.col_sharded() ? sh.n : 0});
         aux.main();
         rec.qu = thin_qr_deferred(ctx, u, nullptr, sl, usplit);
     }
@@ -1206,15 +1306,17 @@ constexpr size_t kMaxSvdGraphs = 4;
 static std::atomic<std::uint64_t> g_svd_graph_clock{0};
 std::atomic<std::int64_t> g_blws_graph_launches{0};
 
-BlwsResult blws_svd(LinearOperator& w, const DWarm& warm, Index k, Index r, Rng& rng) {
+// blws_svd on warm starts in the operator's panel layout (V = this rank's
+// columns when column-sharded); blws_svd() converts at the boundary.
+static BlwsResult blws_svd_panel(LinearOperator& w, const DWarm& warm, Index k, Index r, Rng& rng) {
     Context& ctx = w.ctx();
     RegionGuard region(ctx, 5);
-    const Index m = w.rows(), n = w.cols();
+    const Index m = w.rows(), n = w.cols(), pn = w.panel_n();
     const Index bs = warm.rank();
     const Index m_all = w.row_sharded() ? w.shard().m_total : m;  // global rows of a row shard
-    if (bs < 1 || r < 1 || r > std::min(m_all, n) || warm.geo.m != m || warm.geo.n != n)
+    if (bs < 1 || r < 1 || r > std::min(m_all, n) || warm.geo.m != m || warm.geo.n != pn)
         return blws_svd_exact(w, warm, k, r, rng);  // throws the reference's errors
-    DeferredShape sh{m, n, bs, k, r, k, 0, 0, false};
+    DeferredShape sh{m, pn, bs, k, r, k, 0, 0, false};
     if (r > sh.k_eff * bs) {
         sh.k_eff = (r + bs - 1) / bs;
         sh.k_raised = true;
@@ -1224,7 +1326,7 @@ BlwsResult blws_svd(LinearOperator& w, const DWarm& warm, Index k, Index r, Rng&
     sh.want = std::min(r, sh.d);
     // keep < r needs the Rng padding: the exact path owns that case
     if (force_exact() || sh.want < r || k < 1 || k * bs > m_all + n) return blws_svd_exact(w, warm, k, r, rng);
-    const Stack geo{m, n};
+    const Stack geo{m, pn};
     const int cap = 16 * static_cast<int>(sh.k_eff + 3) + static_cast<int>(sh.want) + 9;
 
     // ---- graph plan for this (operator data, shape); eager on first sight
@@ -1322,7 +1424,7 @@ BlwsResult blws_svd(LinearOperator& w, const DWarm& warm, Index k, Index r, Rng&
         finite_slot = sl->take(2);
         w.defer_pending_check(reinterpret_cast<int*>(sl->at(finite_slot)));  // async-assigned W
         share_flag(ctx, reinterpret_cast<int*>(sl->at(finite_slot)), sl->at(finite_slot + 1));
-        next = make_warm(ctx, m, n, sh.want);
+        next = make_warm(ctx, m, pn, sh.want);
         rec = enqueue_deferred(w, warm.panel(), sh, *sl, next.panel());
     }
     sl->fetch(ctx);  // the one host round trip
@@ -1336,7 +1438,7 @@ BlwsResult blws_svd(LinearOperator& w, const DWarm& warm, Index k, Index r, Rng&
         return blws_svd_exact(w, warm, k, r, rng);
     }
     if (graphed) {
-        next = make_warm(ctx, m, n, sh.want);
+        next = make_warm(ctx, m, pn, sh.want);
         copy(ctx, next.panel(), plan->next.view().left(sh.want));
     }
     BlwsResult out;
@@ -1345,6 +1447,44 @@ BlwsResult blws_svd(LinearOperator& w, const DWarm& warm, Index k, Index r, Rng&
     next.sigma.assign(hv, hv + sh.want);
     out.warm = std::move(next);
     return out;
+}
+
+// ---- column-sharded warm starts: the public form holds V whole (n rows), the
+// panel form this rank's rows [col0, col0 + chunk) (zero past n)
+DWarm to_panel_warm(LinearOperator& w, const DWarm& a) {
+    Context& ctx = w.ctx();
+    const Index n = w.cols(), chunk = w.col_chunk(), c0 = w.col0();
+    DWarm p = make_warm(ctx, a.geo.m, chunk, a.rank());
+    if (a.rank() > 0) {
+        copy(ctx, p.u(), a.u());
+        const Index take = std::max<Index>(0, std::min(n, c0 + chunk) - c0);
+        if (take > 0) copy(ctx, View{p.v().p, take, a.rank(), p.uv.ld}, View{a.v().p + c0, take, a.rank(), a.uv.ld});
+    }
+    p.sigma = a.sigma;
+    return p;
+}
+
+DWarm to_api_warm(LinearOperator& w, const DWarm& p) {
+    Context& ctx = w.ctx();
+    const Index n = w.cols(), npad = w.col_chunk() * ctx.nranks();
+    DWarm a = make_warm(ctx, p.geo.m, n, p.rank());
+    if (p.rank() > 0) {
+        copy(ctx, a.u(), p.u());
+        DBuf<double> full(ctx, static_cast<size_t>(npad * p.rank()));
+        gather_cols(w, p.v(), full.get());
+        copy(ctx, a.v(), View{full.get(), n, p.rank(), npad});
+    }
+    a.sigma = p.sigma;
+    return a;
+}
+
+BlwsResult blws_svd(LinearOperator& w, const DWarm& warm, Index k, Index r, Rng& rng) {
+    if (!w.col_sharded()) return blws_svd_panel(w, warm, k, r, rng);
+    if (warm.geo.m != w.rows() || warm.geo.n != w.cols())
+        throw std::invalid_argument("blws_svd: warm start does not match operator");
+    BlwsResult res = blws_svd_panel(w, to_panel_warm(w, warm), k, r, rng);
+    res.warm = to_api_warm(w, res.warm);
+    return res;
 }
 
 // ======================================================== Lanczos (reseed)
@@ -1356,9 +1496,10 @@ namespace {
 class DeviceLanczos {
 public:
     DeviceLanczos(LinearOperator& w, const std::vector<double>& q1_logical, Index cap)
-        : w_(w), ctx_(w.ctx()), geo_{w.rows(), w.cols()},
+        : w_(w), ctx_(w.ctx()), geo_{w.rows(), w.panel_n()},
           m_all_(w.row_sharded() ? w.shard().m_total : geo_.m), row0_(w.row_sharded() ? w.shard().row0 : 0),
-          dim_(m_all_ + geo_.n), ld_(geo_.ld()), cap_(cap), split_(w.panel_split()) {
+          n_all_(w.cols()), col0_(w.col0()), dim_(m_all_ + n_all_), ld_(geo_.ld()), cap_(cap),
+          split_(w.panel_split()) {
         q_ = DMat(ctx_, ld_, cap_, true);
         next_ = DMat(ctx_, ld_, 1, true);
         r_ = DMat(ctx_, ld_, 1, true);
@@ -1431,11 +1572,13 @@ public:
     const double* coup_dev() const { return coup_.get(); }
 
 private:
-    // a logical (m_all + n) vector into this rank's panel layout (its top rows, all bottom rows)
+    // a logical (m_all + n) vector into this rank's panel layout (its top rows,
+    // its bottom rows: all of them, or [col0, col0 + chunk) when column-sharded)
     void set_logical(double* dst, const std::vector<double>& v) {
         std::vector<double> h(static_cast<size_t>(ld_), 0.0);
         std::copy(v.begin() + row0_, v.begin() + row0_ + geo_.m, h.begin());
-        std::copy(v.begin() + m_all_, v.end(), h.begin() + geo_.mp());
+        const Index b0 = std::min(n_all_, col0_), b1 = std::min(n_all_, col0_ + geo_.n);
+        std::copy(v.begin() + m_all_ + b0, v.begin() + m_all_ + b1, h.begin() + geo_.mp());
         BLWS_CUDA(cudaMemcpyAsync(dst, h.data(), sizeof(double) * ld_, cudaMemcpyHostToDevice, ctx_.stream()));
         ctx_.sync();
     }
@@ -1509,7 +1652,7 @@ private:
     LinearOperator& w_;
     Context& ctx_;
     Stack geo_;
-    Index m_all_, row0_, dim_, ld_, cap_;
+    Index m_all_, row0_, n_all_, col0_, dim_, ld_, cap_;
     RowSplit split_;
     DMat q_, next_, r_;
     DBuf<double> alpha_, lastbeta_, coup_, state_, coef_, ss_;
@@ -1595,13 +1738,14 @@ PartialSvd lanczos_partial_svd(LinearOperator& w, Index r, const LanczosOptions&
             Index keep = 0;
             while (keep < avail && cp.values[static_cast<size_t>(keep)] > 0.0) ++keep;
             PartialSvd out;
-            out.uv = make_warm(ctx, m, n, keep);
+            out.uv = make_warm(ctx, m, w.panel_n(), keep);
             if (keep > 0) {
                 View B = run.basis();
                 gemm(ctx, false, false, B.rows, keep, B.cols, std::sqrt(2.0), B.p, B.ld, cp.vecs.data(), cp.vecs.ld,
                      0.0, out.uv.uv.data(), out.uv.uv.ld);
                 std::copy(cp.values.begin(), cp.values.begin() + keep, out.uv.sigma.begin());
             }
+            if (w.col_sharded()) out.uv = to_api_warm(w, out.uv);  // V whole for the caller
             stats.steps = run.cols();
             stats.converged = std::min(cp.converged, avail);
             stats.all_converged = avail == r && cp.converged >= r;

@@ -401,6 +401,24 @@ __global__ void csr_spmm_wide_k(long rows, const std::int64_t* __restrict__ rowp
     }
 }
 
+__global__ void pack_rows_k(const double* __restrict__ x, long ld, long rows, long cols, double* __restrict__ out) {
+    const long total = rows * cols;
+    for (long idx = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<long>(gridDim.x) * blockDim.x) {
+        const long i = idx / cols, c = idx % cols;
+        out[idx] = x[i + c * ld];
+    }
+}
+
+__global__ void unpack_rows_k(const double* __restrict__ in, long rows, long cols, double* __restrict__ x, long ld) {
+    const long total = rows * cols;
+    for (long idx = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<long>(gridDim.x) * blockDim.x) {
+        const long i = idx / cols, c = idx % cols;
+        x[i + c * ld] = in[idx];
+    }
+}
+
 __global__ void gather_vals_k(long nnz, double* dst, const double* src, const std::int64_t* perm) {
     for (long p = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; p < nnz;
          p += static_cast<long>(gridDim.x) * blockDim.x)
@@ -591,6 +609,18 @@ void csr_spmm(Context& ctx, Index rows, const std::int64_t* rowptr, const std::i
     else
         csr_spmm_wide_k<<<blocks, kThreads, 0, ctx.stream()>>>(rows, rowptr, colidx, val, b, xt, Y, ldy);
     LAUNCH(ctx, "csr_spmm");
+}
+
+void pack_rows(Context& ctx, View x, double* dst) {
+    if (x.rows <= 0 || x.cols <= 0) return;
+    pack_rows_k<<<grid_for(x.rows * x.cols), kThreads, 0, ctx.stream()>>>(x.p, x.ld, x.rows, x.cols, dst);
+    LAUNCH(ctx, "pack_rows");
+}
+
+void unpack_rows(Context& ctx, const double* src, View dst) {
+    if (dst.rows <= 0 || dst.cols <= 0) return;
+    unpack_rows_k<<<grid_for(dst.rows * dst.cols), kThreads, 0, ctx.stream()>>>(src, dst.rows, dst.cols, dst.p, dst.ld);
+    LAUNCH(ctx, "unpack_rows");
 }
 
 void gather_values(Context& ctx, Index nnz, double* dst, const double* src, const std::int64_t* perm) {

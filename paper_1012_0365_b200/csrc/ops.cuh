@@ -35,6 +35,9 @@ void pair_gemv(Context& ctx, Index m, Index n, const double* w, Index ld, const 
 /// Zeroes `bytes` (multiple of 4) with a kernel: a cudaMemsetAsync may be
 /// queued on a copy engine behind a pending host upload.
 void zero(Context& ctx, void* p, size_t bytes);
+/// dst (x.rows x x.cols, row-major) = x; and back (column-major view dst).
+void pack_rows(Context& ctx, View x, double* dst);
+void unpack_rows(Context& ctx, const double* src, View dst);
 void copy(Context& ctx, View dst, View src, double alpha = 1.0);  // dst = alpha * src
 void axpy(Context& ctx, View y, View x, double alpha);            // y += alpha * x
 /// out[0] = sum of squares of x (deterministic two-pass reduction).

@@ -124,7 +124,7 @@ def sharded_blws(w_loc, u_loc, v, k, r):
     return _cholqr2_rows(u_new, True), _cholqr2_rows(v_new, False), vals
 
 
-def _case(seed=7, m=120, n=90, r=6):
+def _case(seed=7, m=120, n=90, r=6):  # noqa: E302
     sys.path.insert(0, ROOT)
     from oracle import oracle as O
 
@@ -185,6 +185,103 @@ def test_sharded_blws_decomposition_matches_oracle():
     assert np.allclose(np.abs(u_all), np.abs(ref.warm.u), atol=1e-8)
     # both ranks computed identical replicated parts
     assert np.array_equal(res[0][3], res[1][3]) and np.array_equal(res[0][4], res[1][4])
+
+
+# ---- column (n-side) sharding: the bottom rows of every panel split too
+def _allgather_rows(x_loc):
+    """rows of every rank's block in rank order (NCCL all-gather of the chunks)."""
+    import torch
+    import torch.distributed as dist
+
+    t = torch.from_numpy(np.ascontiguousarray(x_loc, dtype=np.float64))
+    parts = [torch.empty_like(t) for _ in range(dist.get_world_size())]
+    dist.all_gather(parts, t)
+    return np.concatenate([q.numpy() for q in parts], axis=0)
+
+
+def _reduce_scatter_rows(x_full, rank, chunk):
+    """this rank's rows of the sum over the ranks (NCCL reduce-scatter)."""
+    return _allreduce(x_full)[rank * chunk:(rank + 1) * chunk]
+
+
+def sharded2_blws(w_loc, u_loc, v_loc, rank, chunk, n, k, r):
+    """blws_svd with W and U row-sharded AND V / the panel bottoms split into
+    chunks (csrc/host_core.cu col_sharded: gather_cols before W X_bot,
+    scatter_cols after W^T X_top); every Gram / norm allreduced over all rows."""
+    b = u_loc.shape[1]
+    npad = chunk * 2
+
+    def apply(xt, xb):
+        xfull = _allgather_rows(xb)[:n]
+        part = np.zeros((npad, xt.shape[1]))
+        part[:n] = w_loc.T @ xt
+        return w_loc @ xfull, _reduce_scatter_rows(part, rank, chunk)
+
+    def gram(top, bot):
+        return _allreduce(top.T @ top + bot.T @ bot)
+
+    def cholqr2(top, bot):
+        rs = []
+        for _ in range(2):
+            rr = np.linalg.cholesky(gram(top, bot)).T
+            ri = np.linalg.inv(rr)
+            top, bot = top @ ri, bot @ ri
+            rs.append(rr)
+        return top, bot, rs[1] @ rs[0]
+
+    xt, xb, _ = cholqr2(u_loc.copy(), v_loc.copy())
+    qs, ms, bs_ = [(xt, xb)], [], []
+    zt, zb = apply(xt, xb)
+    ms.append(_allreduce(xt.T @ zt + xb.T @ zb))
+    for _ in range(1, k):
+        m1 = 0.5 * (ms[-1] + ms[-1].T)
+        rt, rb = zt - qs[-1][0] @ m1, zb - qs[-1][1] @ m1
+        nt, nb, rr = cholqr2(rt, rb)
+        bs_.append(rr)
+        qs.append((nt, nb))
+        zt, zb = apply(nt, nb)
+        ms.append(_allreduce(nt.T @ zt + nb.T @ zb))
+    d = k * b
+    t = np.zeros((d, d))
+    for l in range(k):
+        t[l * b:(l + 1) * b, l * b:(l + 1) * b] = 0.5 * (ms[l] + ms[l].T)
+        if l + 1 < k:
+            t[(l + 1) * b:(l + 2) * b, l * b:(l + 1) * b] = bs_[l]
+            t[l * b:(l + 1) * b, (l + 1) * b:(l + 2) * b] = bs_[l].T
+    vals, vecs = np.linalg.eigh(t)
+    vals, vecs = vals[::-1][:r], vecs[:, ::-1][:, :r]
+    u_new = np.sqrt(2.0) * np.hstack([q[0] for q in qs]) @ vecs
+    v_new = np.sqrt(2.0) * np.hstack([q[1] for q in qs]) @ vecs
+    return _cholqr2_rows(u_new, True), _cholqr2_rows(v_new, True), vals
+
+
+def _worker_blws_cols(rank, world):
+    from paper_1012_0365_b200.dist import row_partition
+
+    O, w, uw, vw, s = _case(n=91)  # odd n: rank 1 carries a zero padding row
+    m, n = w.shape
+    row0, rows = row_partition(m, world, rank)
+    chunk = -(-n // world)
+    v_loc = np.zeros((chunk, vw.shape[1]))
+    take = max(0, min(n, (rank + 1) * chunk) - rank * chunk)
+    v_loc[:take] = vw[rank * chunk:rank * chunk + take]
+    un, vn, vals = sharded2_blws(w[row0:row0 + rows], uw[row0:row0 + rows], v_loc, rank, chunk, n, 2, uw.shape[1])
+    return row0, rows, un, vn, vals, take
+
+
+def test_col_sharded_blws_decomposition_matches_oracle():
+    res = _run(2, _worker_blws_cols)
+    assert not any(isinstance(r, str) for r in res), res
+    O, w, uw, vw, s = _case(n=91)
+    ref = O.blws_svd(O.DenseOperator(w), O.WarmStart(uw, vw, s), 2, uw.shape[1], O.Rng(3))
+    for row0, rows, un, vn, vals, take in res:
+        assert np.abs(vals - ref.warm.sigma).max() <= 1e-10 * ref.warm.sigma.max()
+        assert np.abs(vn[take:]).max(initial=0.0) == 0.0  # padding rows stay exactly zero
+    u_all = np.vstack([r[2] for r in res])
+    v_all = np.vstack([r[3][:r[5]] for r in res])
+    assert np.allclose(np.abs(u_all), np.abs(ref.warm.u), atol=1e-8)
+    assert np.allclose(np.abs(v_all), np.abs(ref.warm.v), atol=1e-8)
+    assert np.array_equal(res[0][4], res[1][4])  # the same T and Ritz values on both ranks
 
 
 def _lanczos(apply, dot, reorth_coef, q1t, q1b, steps):

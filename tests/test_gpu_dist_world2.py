@@ -37,7 +37,7 @@ def _instance(O, m=700, n=500, r=24, seed=123):
     return w, su[:, :r].copy(order="F"), sv[:, :r].copy(order="F"), ss[:r].copy()
 
 
-def _worker(rank, port, outdir, case):
+def _worker(rank, port, outdir, case, shape=(700, 500, 24)):
     import torch.distributed as dist
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -53,7 +53,7 @@ def _worker(rank, port, outdir, case):
         gd.init_host_comm(ctx)
         out = {}
         if case == "blws":
-            w, u, v, s = _instance(O)
+            w, u, v, s = _instance(O, *shape)
             m, r = w.shape[0], u.shape[1]
             row0, rows = gd.row_partition(m, WORLD, rank)
             op = G.DenseOperator(np.asfortranarray(w[row0:row0 + rows]), ctx=ctx)
@@ -102,10 +102,10 @@ def _worker(rank, port, outdir, case):
         dist.destroy_process_group()
 
 
-def _run(case, tmp_path):
+def _run(case, tmp_path, *extra):
     import torch.multiprocessing as mp
 
-    mp.spawn(_worker, args=(_free_port(), str(tmp_path), case), nprocs=WORLD, join=True)
+    mp.spawn(_worker, args=(_free_port(), str(tmp_path), case, *extra), nprocs=WORLD, join=True)
     return [dict(np.load(tmp_path / f"r{r}.npz")) for r in range(WORLD)]
 
 
@@ -113,9 +113,13 @@ def _stack_rows(parts, key):
     return np.concatenate([p[key] for p in sorted(parts, key=lambda p: int(p["row0"]))], axis=0)
 
 
-def test_world2_blws_svd_matches_oracle(G, O, tmp_path):
-    parts = _run("blws", tmp_path)
-    w, u, v, s = _instance(O)
+@pytest.mark.parametrize("nshard,shape", [("1", (700, 500, 24)), ("1", (300, 251, 20)), ("0", (700, 500, 24))])
+def test_world2_blws_svd_matches_oracle(G, O, tmp_path, monkeypatch, nshard, shape):
+    # nshard 1: V and the bottom rows of every panel split over the ranks (the
+    # default; n = 251 leaves a zero padding row on rank 1); 0: replicated
+    monkeypatch.setenv("BLWS_NSHARD", nshard)
+    parts = _run("blws", tmp_path, shape)
+    w, u, v, s = _instance(O, *shape)
     r = u.shape[1]
     ref = O.blws_svd(O.DenseOperator(w), O.WarmStart(u, v, s), 2, r, O.Rng(1))
     plain = G.blws_svd(G.DenseOperator(w), G.WarmStart(u, v, s), 2, r, G.Rng(1))
