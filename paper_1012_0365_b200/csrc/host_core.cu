@@ -251,11 +251,16 @@ RowSplit LinearOperator::panel_split() const {
 }
 
 bool LinearOperator::col_sharded() const {
-    static const bool off = [] {
+    // BLWS_NSHARD=0: bottom rows replicated; =force: split even on a one-rank
+    // communicator (tests of the NCCL all-gather / reduce-scatter, graph capture)
+    static const int mode = [] {
         const char* e = std::getenv("BLWS_NSHARD");
-        return e && std::string(e) == "0";
+        if (!e) return 1;
+        const std::string v(e);
+        return v == "0" ? 0 : (v == "force" ? 2 : 1);
     }();
-    return !off && row_sharded() && ctx_.has_comm();
+    if (mode == 0 || !row_sharded() || !ctx_.has_comm()) return false;
+    return ctx_.nranks() > 1 || mode == 2;
 }
 
 Index LinearOperator::col_chunk() const { return ceil_div(cols(), std::max(1, ctx_.nranks())); }
@@ -369,12 +374,15 @@ void DenseOperator::pair_block_impl(View left, View right, View top, View bot) {
         const Index npad = col_chunk() * ctx_.nranks();
         DBuf<double> xfull(ctx_, static_cast<size_t>(npad * b)), part(ctx_, static_cast<size_t>(npad * b));
         if (npad > n_) zero(ctx_, part.get(), sizeof(double) * static_cast<size_t>(npad * b));  // padding rows
+        // collectives on the main stream only, outside the fork (same order on
+        // every rank; a gather issued while the W^T X_top GEMM ran on the
+        // auxiliary stream raced at large panels): gather, then the two GEMMs
+        // side by side, then the scatter after the join
+        gather_cols(*this, right, xfull.get());
         {
-            // the collectives stay on the main stream, in the same order on every rank
             AuxScope aux(ctx_);
             gemm(ctx_, true, false, n_, b, m_, 1.0, p_, ld_, left.p, left.ld, 0.0, part.get(), npad);
             aux.main();
-            gather_cols(*this, right, xfull.get());
             gemm(ctx_, false, false, m_, b, n_, 1.0, p_, ld_, xfull.get(), npad, 0.0, top.p, top.ld);
         }
         scatter_cols(*this, View{part.get(), npad, b, npad}, bot);
@@ -473,12 +481,12 @@ void SparseOperator::pair_block_impl(View left, View right, View top, View bot) 
         const Index npad = col_chunk() * ctx_.nranks();
         DBuf<double> xfull(ctx_, static_cast<size_t>(npad * b)), part(ctx_, static_cast<size_t>(npad * b));
         if (npad > n_) zero(ctx_, part.get(), sizeof(double) * static_cast<size_t>(npad * b));
+        gather_cols(*this, right, xfull.get());  // collectives outside the fork (see DenseOperator)
         {
             AuxScope aux(ctx_);
             csr_spmm(ctx_, n_, colptr_.get(), rowidx_.get(), val_csc_.get(), m_, b, left.p, left.ld, part.get(), npad,
                      scratch2.get());
             aux.main();
-            gather_cols(*this, right, xfull.get());
             csr_spmm(ctx_, m_, rowptr_.get(), colidx_.get(), val_csr_.get(), n_, b, xfull.get(), npad, top.p, top.ld,
                      scratch.get());
         }

@@ -6,6 +6,8 @@ with the oracle and with the unsharded device path. Multi-rank runs need one
 GPU per rank; the decomposition itself is checked with gloo in
 test_dist_cpu.py.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -28,6 +30,26 @@ def test_sharded_single_rank_matches_oracle_and_unsharded(G, O, exact, monkeypat
         monkeypatch.setenv("BLWS_EXACT", "1")
     else:
         monkeypatch.delenv("BLWS_EXACT", raising=False)
+    _sharded_single_rank(G, O, exact)
+
+
+def test_col_sharded_single_rank_nccl(G, O):
+    # the column-sharded panels on a one-rank NCCL communicator (BLWS_NSHARD=force,
+    # set in a subprocess: the switch is read once per process): NCCL all-gather /
+    # reduce-scatter, eager and captured in the blws_svd graph
+    import subprocess
+    import sys
+
+    code = ("import sys; sys.path.insert(0, 'tests'); import conftest, test_gpu_dist as t; "
+            "import paper_1012_0365_b200 as G; from oracle import oracle as O; t._sharded_single_rank(G, O, False); "
+            "t.test_sharded_lanczos_and_svt_single_rank(G, O)")
+    env = dict(os.environ, BLWS_NSHARD="force")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0, r.stderr[-3000:]
+
+
+def _sharded_single_rank(G, O, exact):
     w, u, v, s = _instance(O)
     m, n = w.shape
     r = u.shape[1]
