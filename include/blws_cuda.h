@@ -65,6 +65,10 @@ int blws_context_region_stats(blws_context* ctx, int region, double* total_ms, i
 int blws_context_region_reset(blws_context* ctx);
 /* FP64 peak microbenchmark on this GPU, TFLOP/s (mode 0 DMMA, 1 DFMA). */
 int blws_fp64_peak(blws_context* ctx, int mode, double* tflops);
+/* L2 throughput probe, GB/s of requested bytes (roofline of the gather-form
+ * sparse kernels): mode 0 streams an L2-resident buffer; mode 1 gathers random
+ * rows of `row` doubles from a 4 MB matrix (K8 / K9's access pattern). */
+int blws_l2_probe(blws_context* ctx, int mode, int row, double* gbps);
 
 /* -------------------------------------------------------------------- rng
  * blws::Rng (core/rng.hpp:17-90), bit-exact: std::mt19937_64 + 53-bit

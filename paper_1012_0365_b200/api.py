@@ -72,6 +72,7 @@ SIGNATURES = {
     "blws_nccl_unique_id": (ci, [vp]),
     "blws_context_init_comm": (ci, [vp, ci, ci, vp]),
     "blws_context_init_host_comm": (ci, [vp, ci, ci, vp, vp]),
+    "blws_l2_probe": (ci, [vp, ci, ci, vp]),
     "blws_context_comm_info": (ci, [vp, P(ci), P(ci)]),
     "blws_dense_operator_set_row_shard": (ci, [vp, i64, i64]),
     "blws_sparse_operator_create": (ci, [vp, i64, i64, i64, vp, vp, vp, P(vp)]),
@@ -249,6 +250,12 @@ class Context:
         out = np.zeros(8)
         _check(lib().blws_microbench(self._h, which, n, b, reps, _ptr(out)))
         return out if detail else float(out[0])
+
+    def l2_probe(self, mode: int = 0, row: int = 50) -> float:
+        """L2 throughput in GB/s: mode 0 streaming, mode 1 random `row`-double row gathers."""
+        out = dbl(0)
+        _check(lib().blws_l2_probe(self._h, int(mode), int(row), C.byref(out)))
+        return out.value
 
     def fp64_peak(self, mode: int = 0) -> float:
         out = dbl(0)

@@ -150,6 +150,13 @@ int blws_fp64_peak(blws_context* ctx, int mode, double* tflops) {
     return guard([&] { *tflops = fp64_peak_tflops(*ctx->ctx, mode); });
 }
 
+int blws_l2_probe(blws_context* ctx, int mode, int row, double* gbps) {
+    return guard([&] {
+        need(mode == 0 || (mode == 1 && row >= 1 && row <= 128), "l2_probe: bad mode / row");
+        *gbps = l2_probe_gbps(*ctx->ctx, mode, row);
+    });
+}
+
 // -------------------------------------------------------------------- rng
 int blws_rng_create(uint64_t seed, blws_rng** out) {
     return guard([&] { *out = new blws_rng{Rng(seed)}; });

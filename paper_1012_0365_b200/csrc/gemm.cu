@@ -413,6 +413,74 @@ __global__ void __launch_bounds__(256) fp64_dfma_peak_k(double* sink, int iters)
 
 }  // namespace
 
+// L2 throughput probes (the bound of the gather-form sparse kernels K8 / K9):
+// mode 0 streams a 16 MB L2-resident buffer in 512-byte warp segments; mode 1
+// gathers random rows of `row` doubles (lanes over the row, as K8 / K9 read X /
+// U rows) from a rows x row matrix of 4 MB. Bytes counted = bytes requested.
+__global__ void l2_probe_k(const double* __restrict__ buf, long n, int row, int mode, int iters, double* sink) {
+    const int lane = threadIdx.x & 31;
+    const long gw = (blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x) >> 5;
+    const long nw = (static_cast<long>(gridDim.x) * blockDim.x) >> 5;
+    double acc = 0.0;
+    if (mode == 0) {
+        const long segs = n / 64;  // 64 doubles per warp segment (2 per lane, 16 B loads)
+        for (int it = 0; it < iters; ++it)
+            for (long sgm = (gw + it * 7919) % segs, c = 0; c < 4; ++c, sgm = (sgm + nw) % segs) {
+                const double2 v = reinterpret_cast<const double2*>(buf + sgm * 64)[lane];
+                acc += v.x + v.y;
+            }
+    } else {
+        // 8 independent rows in flight per warp (as K9's unrolled 32-position batch)
+        const long rows = n / row;
+        unsigned long long z = 0x9e3779b97f4a7c15ull * static_cast<unsigned long long>(gw + 1);
+        for (int it = 0; it < iters / 2; ++it) {
+            double part[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                z = z * 6364136223846793005ull + 1442695040888963407ull;
+                const long i = static_cast<long>((z >> 33) % static_cast<unsigned long long>(rows));
+                const double* a = buf + i * row;
+                double t = 0.0;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int c = lane + 32 * q;
+                    if (c < row) t += a[c];
+                }
+                part[u] = t;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc += part[u];
+        }
+    }
+    if (acc == 12345.678) sink[0] = acc;  // keeps the loads
+}
+
+double l2_probe_gbps(Context& ctx, int mode, int row) {
+    const long n = mode == 0 ? (16L << 20) / 8 : (4L << 20) / 8;
+    DBuf<double> buf(ctx, static_cast<size_t>(n)), sink(ctx, 1);
+    zero(ctx, buf.get(), sizeof(double) * n);
+    const int blocks = ctx.sm_count() * 8, threads = 256, iters = 400;
+    cudaEvent_t e0, e1;
+    BLWS_CUDA(cudaEventCreate(&e0));
+    BLWS_CUDA(cudaEventCreate(&e1));
+    double best = 0;
+    for (int rep = 0; rep < 4; ++rep) {
+        BLWS_CUDA(cudaEventRecord(e0, ctx.stream()));
+        l2_probe_k<<<blocks, threads, 0, ctx.stream()>>>(buf.get(), n, row, mode, iters, sink.get());
+        BLWS_CUDA(cudaEventRecord(e1, ctx.stream()));
+        BLWS_CUDA(cudaEventSynchronize(e1));
+        ctx.note_launch();
+        float ms = 0;
+        BLWS_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        const double warps = static_cast<double>(blocks) * threads / 32.0;
+        const double bytes = mode == 0 ? warps * iters * 4 * 512.0 : warps * (iters / 2) * 8 * 8.0 * row;
+        if (rep > 0) best = std::max(best, bytes / (ms * 1e-3) / 1e9);
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return best;
+}
+
 double fp64_peak_tflops(Context& ctx, int mode) {
     DBuf<double> sink(ctx, 1);
     const int blocks = ctx.sm_count() * 4, threads = 256, iters = 20000;

@@ -120,6 +120,8 @@ void gather_values(Context& ctx, Index nnz, double* dst, const double* src, cons
 // ------------------------------------------------------------------ misc
 /// FP64 peak microbenchmark in TFLOP/s (mode 0 DMMA tensor pipe, 1 DFMA).
 double fp64_peak_tflops(Context& ctx, int mode);
+/// L2 throughput probe (GB/s): mode 0 stream, mode 1 random row gathers of `row` doubles.
+double l2_probe_gbps(Context& ctx, int mode, int row);
 void reduce_partials(Context& ctx, const double* partials, Index count, double* out);
 
 }  // namespace blws
