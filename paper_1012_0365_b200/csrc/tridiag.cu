@@ -132,6 +132,51 @@ __device__ __forceinline__ void sturm_count_multi(const double* ds, const double
     }
 }
 
+// The same counts with the zero-pivot replacement taken off the dependent
+// chain: the chain per step is the split select and one FMA. A step that hits
+// an exact zero sets `zero` and the caller redoes the round with
+// sturm_count_multi (dstebz's -pivmin rule), so the counts always equal it.
+template <int P>
+__device__ __forceinline__ void sturm_count_fast(const double* ds, const double* e2s, int n, const double (&xs)[P],
+                                                 int (&cnt)[P], bool& zero) {
+    double p0[P], p1[P];
+    const double d0 = ds[0];
+    bool z = false;
+#pragma unroll
+    for (int q = 0; q < P; ++q) {
+        p0[q] = 1.0;
+        p1[q] = d0 - xs[q];
+        z |= p1[q] == 0.0;
+        cnt[q] = p1[q] < 0.0;
+    }
+#pragma unroll 4
+    for (int i = 1; i < n; ++i) {
+        const double e2 = e2s[i - 1], di = ds[i];
+        const bool split = e2 < 0.0;
+        const double me2 = -fmax(e2, 0.0);
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+            const double p1s = split ? 1.0 : p1[q];
+            const double p2 = fma(di - xs[q], p1s, me2 * p0[q]);
+            z |= p2 == 0.0;
+            cnt[q] += static_cast<unsigned>(__double2hiint(p2) ^ __double2hiint(p1s)) >> 31;
+            p0[q] = p1s;
+            p1[q] = p2;
+        }
+        if ((i & 3) == 0) {
+#pragma unroll
+            for (int q = 0; q < P; ++q) {
+                const int e0 = (__double2hiint(p0[q]) >> 20) & 0x7ff, e1 = (__double2hiint(p1[q]) >> 20) & 0x7ff;
+                const int ex = max(e0, e1);
+                const double sc = __hiloint2double((2046 - ex) << 20, 0);
+                p0[q] *= sc;
+                p1[q] *= sc;
+            }
+        }
+    }
+    zero = z;
+}
+
 // One block of kBisThreads per wanted eigenvalue (j-th largest = ascending
 // index n-1-j), kBisPts-way multisection per round: every thread evaluates
 // kBisP shifts, the first shift whose count exceeds the index is found by a
@@ -141,6 +186,7 @@ __device__ __forceinline__ void sturm_count_multi(const double* ds, const double
 // running it, so the block's 4 warps (one per SMSP) each run one chain: 4
 // interleaved chains per thread (512-way, 6 rounds) measured slower (140 vs
 // 118 us at C2). LAPACK dstebz semantics, pivmin safeguard.
+// (256 / 512 threads, 256- / 512-way: 69 / 94 vs 60 us at order 200, r02f)
 constexpr int kBisThreads = 128, kBisP = 1, kBisPts = kBisThreads * kBisP;
 template <bool SH>
 __global__ void __launch_bounds__(kBisThreads) bisect_k(const double* __restrict__ d, const double* __restrict__ e,
@@ -180,7 +226,9 @@ __global__ void __launch_bounds__(kBisThreads) bisect_k(const double* __restrict
                 const int idx = threadIdx.x * kBisP + q;
                 xs[q] = (lo + w * static_cast<double>(idx + 1) / static_cast<double>(kBisPts + 1)) * scale;
             }
-            sturm_count_multi<kBisP>(ds, e2s, n, xs, c);
+            bool hit = false;
+            sturm_count_fast<kBisP>(ds, e2s, n, xs, c, hit);
+            if (__syncthreads_or(hit)) sturm_count_multi<kBisP>(ds, e2s, n, xs, c);  // an exact zero pivot
             int first = kBisPts;
 #pragma unroll
             for (int q = kBisP - 1; q >= 0; --q)
@@ -222,6 +270,19 @@ __device__ __forceinline__ double hash_uniform(unsigned long long seed, long i) 
 // and (d, e) live in shared memory (9 n doubles); the serial recurrences carry
 // their state in registers (lane 0), loads are independent of the chain.
 constexpr int kInvitMaxN = 2048;  // shared-memory path; larger orders use global scratch
+constexpr int kCh = 8;            // recurrence steps per load / store chunk
+
+// 1 / x for the LU pivots: MUFU rcp + Newton (within an ulp) in the normal
+// range, IEEE division outside it (the rcp approximation flushes subnormals)
+__device__ __forceinline__ double rcp_pivot(double x) {
+    const double ax = fabs(x);
+    if (!(ax >= 1e-290 && ax <= 1e290)) return x != 0.0 ? 1.0 / x : 0.0;
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    y = y * fma(-x, y, 2.0);
+    y = y * fma(-x, y, 2.0);
+    return fma(y, fma(-x, y, 1.0), y);
+}
 template <bool SH>
 __global__ void __launch_bounds__(32) inverse_iteration_k(const double* __restrict__ d_g,
                                                            const double* __restrict__ e_g, int n,
@@ -273,17 +334,18 @@ __global__ void __launch_bounds__(32) inverse_iteration_k(const double* __restri
             double* xg = vecs + static_cast<long>(j) * ldv;
             for (int i = lane; i < n; i += 32) x[i] = hash_uniform(0x5eedull + static_cast<unsigned long long>(j), i);
             if (lane == 0) {
-                // LU of T - xj I with partial pivoting (dstein's dlagtf), reciprocal pivots
+                // LU of T - xj I with partial pivoting (dstein's dlagtf), reciprocal pivots.
+                // Chunks of kCh steps: the chunk's loads are issued ahead of its
+                // dependent chain and its stores after it; the pivot reciprocal is
+                // one MUFU rcp + Newton (no IEEE division on the chain).
                 double a = d[0] - xj, b = e[0];
-                for (int k = 0; k < n - 1; ++k) {
-                    const double ck = e[k];
-                    const double an = d[k + 1] - xj;
-                    const double bn = e[k + 1];
+                auto lu_step = [&](int k, double ck, double dk1, double bn) {
+                    const double an = dk1 - xj;
                     const bool sw = !(fabs(a) >= fabs(ck));
-                    const double num = sw ? a : ck, den = sw ? ck : a;
-                    const double l = den != 0.0 ? num / den : 0.0;
-                    const double pv = sw ? ck : a;
-                    u0[k] = fabs(pv) < eps3 ? (pv >= 0.0 ? 1.0 / eps3 : -1.0 / eps3) : 1.0 / pv;
+                    const double num = sw ? a : ck, den = sw ? ck : a;  // den is the pivot
+                    const double rden = rcp_pivot(den);
+                    const double l = den != 0.0 ? num * rden : 0.0;
+                    u0[k] = fabs(den) < eps3 ? (den >= 0.0 ? 1.0 / eps3 : -1.0 / eps3) : rden;
                     u1[k] = sw ? an : b;
                     u2[k] = sw ? bn : 0.0;
                     lm[k] = l;
@@ -291,7 +353,20 @@ __global__ void __launch_bounds__(32) inverse_iteration_k(const double* __restri
                     const double na = sw ? fma(-l, an, b) : fma(-l, b, an);
                     b = sw ? -l * bn : bn;
                     a = na;
+                };
+                int k0 = 0;
+                for (; k0 + kCh <= n - 1; k0 += kCh) {  // full chunks: loads first, straight-line chain
+                    double ek[kCh], dn[kCh], en[kCh];
+#pragma unroll
+                    for (int u = 0; u < kCh; ++u) {
+                        ek[u] = e[k0 + u];
+                        dn[u] = d[k0 + u + 1];
+                        en[u] = e[k0 + u + 1];
+                    }
+#pragma unroll
+                    for (int u = 0; u < kCh; ++u) lu_step(k0 + u, ek[u], dn[u], en[u]);
                 }
+                for (; k0 < n - 1; ++k0) lu_step(k0, e[k0], d[k0 + 1], e[k0 + 1]);
                 u0[n - 1] = fabs(a) < eps3 ? (a >= 0.0 ? 1.0 / eps3 : -1.0 / eps3) : 1.0 / a;
                 u1[n - 1] = 0.0;  // read (times zero) by the back substitution
                 u2[n - 1] = 0.0;
@@ -309,24 +384,58 @@ __global__ void __launch_bounds__(32) inverse_iteration_k(const double* __restri
                 for (int i = lane; i < n; i += 32) y[i] = x[i] * scl;
                 __syncwarp();
                 if (lane == 0) {
-                    // forward: L^{-1} P y, state in registers
+                    // forward: L^{-1} P y, state in registers; chunked like the LU
+                    // (y[k+1..] are not written before they are read)
                     double cur = y[0];
-                    for (int k = 0; k < n - 1; ++k) {
-                        double nxt = y[k + 1];
-                        const bool sw = piv[k] != 0.0;
+                    auto fwd = [&](int k, double nxt, double lv, double pv) {
+                        const bool sw = pv != 0.0;
                         const double lo = sw ? nxt : cur, hi = sw ? cur : nxt;
-                        y[k] = lo;
-                        cur = fma(-lm[k], lo, hi);
+                        cur = fma(-lv, lo, hi);
+                        return lo;
+                    };
+                    int k0 = 0;
+                    for (; k0 + kCh <= n - 1; k0 += kCh) {
+                        double yn[kCh], lv[kCh], pv[kCh], out[kCh];
+#pragma unroll
+                        for (int u = 0; u < kCh; ++u) {
+                            yn[u] = y[k0 + u + 1];
+                            lv[u] = lm[k0 + u];
+                            pv[u] = piv[k0 + u];
+                        }
+#pragma unroll
+                        for (int u = 0; u < kCh; ++u) out[u] = fwd(k0 + u, yn[u], lv[u], pv[u]);
+#pragma unroll
+                        for (int u = 0; u < kCh; ++u) y[k0 + u] = out[u];
+                    }
+                    for (; k0 < n - 1; ++k0) {
+                        const double lo = fwd(k0, y[k0 + 1], lm[k0], piv[k0]);
+                        y[k0] = lo;
                     }
                     y[n - 1] = cur;
                     // backward: U^{-1}
                     double x1 = 0.0, x2 = 0.0;  // x[k+1], x[k+2]
-                    for (int k = n - 1; k >= 0; --k) {
-                        const double v = fma(-u2[k], x2, fma(-u1[k], x1, y[k])) * u0[k];
-                        x[k] = v;
+                    auto bwd = [&](double a0, double a1, double a2, double yv) {
+                        const double v = fma(-a2, x2, fma(-a1, x1, yv)) * a0;
                         x2 = x1;
                         x1 = v;
+                        return v;
+                    };
+                    int k1 = n - 1;
+                    for (; k1 - kCh + 1 >= 0; k1 -= kCh) {
+                        double a0[kCh], a1[kCh], a2[kCh], yv[kCh], out[kCh];
+#pragma unroll
+                        for (int u = 0; u < kCh; ++u) {
+                            a0[u] = u0[k1 - u];
+                            a1[u] = u1[k1 - u];
+                            a2[u] = u2[k1 - u];
+                            yv[u] = y[k1 - u];
+                        }
+#pragma unroll
+                        for (int u = 0; u < kCh; ++u) out[u] = bwd(a0[u], a1[u], a2[u], yv[u]);
+#pragma unroll
+                        for (int u = 0; u < kCh; ++u) x[k1 - u] = out[u];
                     }
+                    for (; k1 >= 0; --k1) x[k1] = bwd(u0[k1], u1[k1], u2[k1], y[k1]);
                 }
                 __syncwarp();
                 // MGS against earlier members of the cluster that are within ortol
