@@ -49,6 +49,13 @@ ag, eg, stg, _ = B.rpca_adm(d, B.SvdBackend.blws(seed=4), truth=a0)
 ao, eo, sto, _ = O.rpca_adm(d, O.SvdBackend.blws(seed=4), truth=a0)
 assert abs(stg.iterations - sto.iterations) <= 1 and stg.rank_hat == sto.rank_hat
 assert np.linalg.norm(ag - ao) <= 1e-6 * np.linalg.norm(ao)
+# an MC solve (sparse operator: K8 / K9, the sparse Lanczos reseeds)
+colptr, rowidx, vals, ml, mr = synth.mc_lowrank(300, 6, 27000, 13, O.Rng, O.sample_distinct)
+ug, sg, vg, stg = B.mc_svt(300, 300, colptr, rowidx, vals, B.SvdBackend.blws(seed=8), truth_ml=ml, truth_mr=mr)
+uo, so, vo, sto = O.mc_svt(300, 300, colptr, rowidx, vals, O.SvdBackend.blws(seed=8), truth_ml=ml, truth_mr=mr)
+assert abs(stg.iterations - sto.iterations) <= 1 and stg.rank_hat == sto.rank_hat
+ag, ao = (ug * sg) @ vg.T, (uo * so) @ vo.T
+assert np.linalg.norm(ag - ao) <= 1e-6 * np.linalg.norm(ao)
 print("variant ok")
 """
 
