@@ -589,8 +589,9 @@ def run_sharded_c5(args):
     1e-3 N(0,1), U0 / V0 Haar m x 2r, sigma_i = 100 * 0.97^(100 i / r), r = 400 (C5's
     rank), warm start QR(U0[:, :r] + eps N) / likewise V with eps = 1e-2
     sqrt(4000 / m) (C2's per-column perturbation). Rank p holds rows
-    [row0, row0 + rows) of W and U (V replicated); blws_svd allreduces the
-    W^T U partials and every panel reduction over NCCL. Inputs are generated
+    [row0, row0 + rows) of W and U; with N > 1, V and the bottom half of every
+    working panel are column-sharded (all-gather before W X_bot, reduce-scatter
+    after W^T X_top) and every panel reduction is allreduced over NCCL. Inputs are generated
     on the devices with seeded torch generators (chunked, so every rank count
     sees the same W). After the timed calls rank 0 runs the same call on the
     whole (unsharded) W and reports the singular-value agreement with N = 1."""
@@ -672,7 +673,9 @@ def run_sharded_c5(args):
                 "data": "synthetic (seeded torch Philox on device, chunked by 512 rows)",
                 "config": {"workload": f"C5-scale standalone BLWS partial SVT, W row-sharded x{world}",
                            "m": m, "n": n, "r": r, "k": 2, "signal_rank": ks,
-                           "parallelism": f"rowshard x{world} (NCCL allreduce of W^T U and panel reductions)",
+                           "parallelism": (f"rowshard x{world}: W / U rows, V / panel bottoms column-sharded "
+                                           "(NCCL all-gather, reduce-scatter, allreduce)" if world > 1 else
+                                           "rowshard x1 (one-rank NCCL communicator)"),
                            "l2": f"W {m * n * 8 / 1e9:.1f} GB >> L2"},
                 "gpu_launches": launches, "parity_vs_n1": parity, "clocks": clocks.summary(),
                 "nccl": {"ranks": world, "backend": "NCCL (dlopen, torch-bundled)"}}

@@ -1177,6 +1177,16 @@ bool force_exact() {
     return e && *e && std::string(e) != "0";
 }
 
+// BLWS_EXACT_PAD=1: a deferred call that needs padding is redone on the exact
+// path (the r01 behaviour) instead of padding its own kept columns
+bool force_exact_pad() {
+    static const bool on = [] {
+        const char* e = std::getenv("BLWS_EXACT_PAD");
+        return e && *e && std::string(e) != "0";
+    }();
+    return on;
+}
+
 }  // namespace
 
 namespace {
@@ -1237,8 +1247,11 @@ DeferredRecs enqueue_deferred(LinearOperator& w, View src, const DeferredShape& 
 }
 
 // the exact path's host tests on the fetched slots (BLWS_DEBUG=1: the failing one on stderr)
-bool finish_deferred(const DeferredRecs& rec, const Slots& sl, const DeferredShape& sh) {
+// *kept_short: set to the kept count when keep < want is the ONLY failed test
+// (the call then needs just the exact path's Rng padding), else -1.
+bool finish_deferred(const DeferredRecs& rec, const Slots& sl, const DeferredShape& sh, Index* kept_short) {
     const bool dbg = std::getenv("BLWS_DEBUG") != nullptr;
+    *kept_short = -1;
     auto fail = [&](const char* why) {
         if (dbg) std::fprintf(stderr, "blws_svd deferred -> exact: %s\n", why);
         return false;
@@ -1272,7 +1285,10 @@ bool finish_deferred(const DeferredRecs& rec, const Slots& sl, const DeferredSha
     const double floor = 1e-12 * std::fabs(hv[0]);
     Index kept = 0;
     while (kept < sh.want && hv[kept] > floor) ++kept;
-    if (kept != sh.want) return fail("keep < min(r, d)");
+    if (kept != sh.want) {
+        *kept_short = kept;
+        return fail("keep < min(r, d)");
+    }
     return true;
 }
 
@@ -1441,9 +1457,27 @@ static BlwsResult blws_svd_panel(LinearOperator& w, const DWarm& warm, Index k, 
         w.mark_poisoned();
         throw std::invalid_argument("DenseOperator: non-finite entries");
     }
-    if (!finish_deferred(rec, *sl, sh)) {
+    Index kept_short = -1;
+    if (!finish_deferred(rec, *sl, sh, &kept_short)) {
         ++g_blws_deferred_fallbacks;
-        return blws_svd_exact(w, warm, k, r, rng);
+        if (kept_short < 0 || force_exact_pad()) return blws_svd_exact(w, warm, k, r, rng);
+        // Only keep < r failed: every other test of the exact path passed on the
+        // same values, so its result would be this call's kept leading columns
+        // (the leading columns of a QR depend only on the leading input columns)
+        // padded by adapt_subspace with the same Rng draws (block_lanczos.hpp:249-255).
+        // Reusing them saves recomputing the whole call.
+        DWarm part = make_warm(ctx, m, pn, kept_short);
+        if (kept_short > 0) {
+            copy(ctx, part.panel(), (graphed ? plan->next.view() : next.panel()).left(kept_short));
+            const double* hv = sl->h.data() + rec.vslot;
+            part.sigma.assign(hv, hv + kept_short);
+        }
+        BlwsResult out;
+        out.k_raised = sh.k_raised;
+        out.padded = true;
+        out.warm = adapt_subspace(ctx, kept_short > 0 ? &part : nullptr, r, m, n, rng,
+                                  w.row_sharded() ? &w.shard() : nullptr, w.col0(), w.col_sharded() ? pn : -1);
+        return out;
     }
     if (graphed) {
         next = make_warm(ctx, m, pn, sh.want);
