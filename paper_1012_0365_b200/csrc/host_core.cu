@@ -1,5 +1,6 @@
 // Operators, CholQR thin_qr, block Lanczos / BLWS and the cold Lanczos reseed.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -1758,12 +1759,28 @@ PartialSvd lanczos_partial_svd(LinearOperator& w, Index r, const LanczosOptions&
     Rng rng = Rng(opts.seed).split(11);
     LanczosStats stats;
     Index k_target = std::min(max_k, std::max<Index>(2 * r, 10));
+    static const bool lzdbg = std::getenv("BLWS_DEBUG_LZ") != nullptr;
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    const auto t_begin = now();
+    double t_steps = 0.0, t_cp = 0.0;
+    Index n_cp = 0;
     while (true) {
         if (!run.breakdown() && run.cols() < k_target) {
+            const auto t0 = now();
+            const Index c0 = run.cols();
             run.step_to(k_target);
+            const double dt = std::chrono::duration<double>(now() - t0).count();
+            t_steps += dt;
+            if (lzdbg)
+                std::fprintf(stderr, "  lanczos r %lld: steps %lld -> %lld in %.2f ms (%.1f us/step)\n",
+                             static_cast<long long>(r), static_cast<long long>(c0), static_cast<long long>(run.cols()),
+                             1e3 * dt, 1e6 * dt / std::max<Index>(1, run.cols() - c0));
             continue;
         }
+        const auto tc0 = now();
         Checkpoint cp = ritz_checkpoint(ctx, run, r, opts.tol);
+        t_cp += std::chrono::duration<double>(now() - tc0).count();
+        ++n_cp;
         bool done = cp.converged >= r || run.cols() >= max_k;
         if (!done) {
             if (run.breakdown()) {
@@ -1780,14 +1797,33 @@ PartialSvd lanczos_partial_svd(LinearOperator& w, Index r, const LanczosOptions&
             Index keep = 0;
             while (keep < avail && cp.values[static_cast<size_t>(keep)] > 0.0) ++keep;
             PartialSvd out;
+            const auto td0 = now();
             out.uv = make_warm(ctx, m, w.panel_n(), keep);
+            if (lzdbg) {
+                ctx.sync();
+                std::fprintf(stderr, "  done: make_warm %.2f ms\n", 1e3 * std::chrono::duration<double>(now() - td0).count());
+            }
             if (keep > 0) {
                 View B = run.basis();
+                const auto tg0 = now();
                 gemm(ctx, false, false, B.rows, keep, B.cols, std::sqrt(2.0), B.p, B.ld, cp.vecs.data(), cp.vecs.ld,
                      0.0, out.uv.uv.data(), out.uv.uv.ld);
+                if (lzdbg) {
+                    ctx.sync();
+                    std::fprintf(stderr, "  done: lift gemm %lld x %lld x %lld: %.2f ms\n", static_cast<long long>(B.rows),
+                                 static_cast<long long>(keep), static_cast<long long>(B.cols),
+                                 1e3 * std::chrono::duration<double>(now() - tg0).count());
+                }
                 std::copy(cp.values.begin(), cp.values.begin() + keep, out.uv.sigma.begin());
             }
             if (w.col_sharded()) out.uv = to_api_warm(w, out.uv);  // V whole for the caller
+            if (lzdbg) {
+                ctx.sync();
+                std::fprintf(stderr, "lanczos r %lld: %lld steps, total %.2f ms: steps %.2f, %lld checkpoints %.2f ms\n",
+                             static_cast<long long>(r), static_cast<long long>(run.cols()),
+                             1e3 * std::chrono::duration<double>(now() - t_begin).count(), 1e3 * t_steps,
+                             static_cast<long long>(n_cp), 1e3 * t_cp);
+            }
             stats.steps = run.cols();
             stats.converged = std::min(cp.converged, avail);
             stats.all_converged = avail == r && cp.converged >= r;

@@ -134,8 +134,8 @@ __global__ void __launch_bounds__(kRT, 1) lanczos_rows_k(RowArgs a) {
     double* qc = rs + RB;               // RB: q_l
     double* qp = qc + RB;               // RB: q_{l-1}
     double* acc2 = qp + RB;             // RB: spill sums
-    double* sp = acc2 + RB;             // kRW x 32
-    double* slot = sp + kRW * 32;       // 1
+    double* sp = acc2 + RB;             // 2 x kRW x 32 (the apply alternates halves)
+    double* slot = sp + 2 * kRW * 32;   // 1
     double* spb = a.spill + b * a.scap * RB;  // this CTA's spilled columns: spb[(p - CS) * RB + ii]
     // ---- prologue: owned rows of basis columns [0, l0] into the tile; q_l0, q_l0-1
     {
@@ -175,7 +175,8 @@ __global__ void __launch_bounds__(kRT, 1) lanczos_rows_k(RowArgs a) {
             const double* wrow = a.w + min(i, a.m - 1);  // clamped: loads stay unconditional
             const double yi = hasrow && !qzero ? qsrc[i] * qscale : 0.0;
             double acc = 0.0;
-            for (long jc = j0; jc < j1; jc += 32) {
+            int par = 0;  // the column-partial buffer alternates by chunk: one barrier per chunk
+            for (long jc = j0; jc < j1; jc += 32, par ^= 1) {
                 const long jl = jc + lane;
                 const double xl = jl < j1 && !qzero ? qsrc[a.mp + jl] * qscale : 0.0;
                 double bp[32];
@@ -187,16 +188,17 @@ __global__ void __launch_bounds__(kRT, 1) lanczos_rows_k(RowArgs a) {
                     bp[cc] = jc + cc < j1 ? bp[cc] * yi : 0.0;
                 }
                 const double colp = transpose_reduce(bp, lane);
-                sp[wid * 32 + lane] = colp;
+                double* spp = sp + par * (kRW * 32);
+                spp[wid * 32 + lane] = colp;
                 __syncthreads();
                 if (wid == 0 && jl < j1) {
                     double s = 0.0;
 #pragma unroll
-                    for (int w = 0; w < kRW; ++w) s += sp[w * 32 + lane];
+                    for (int w = 0; w < kRW; ++w) s += spp[w * 32 + lane];
                     a.pbot[rb * a.n + jl] = s;
                 }
-                __syncthreads();
             }
+            __syncthreads();  // warp 0's last partial read precedes any reuse of sp
             if (hasrow) a.ptop[cb * a.m + i] = acc;
         }
         grid.sync();
@@ -405,7 +407,7 @@ __global__ void __launch_bounds__(kRT, 1) lanczos_rows_k(RowArgs a) {
     }
 }
 
-size_t rows_smem_fixed(long RB, long cap) { return sizeof(double) * (cap + 4 * RB + kRW * 32 + 8); }
+size_t rows_smem_fixed(long RB, long cap) { return sizeof(double) * (cap + 4 * RB + 2 * kRW * 32 + 8); }
 
 }  // namespace
 
