@@ -317,6 +317,10 @@ __global__ void to_row_major_k(const double* X, long ld, long rows, long b, doub
 // row's nonzeros are taken 32 at a time: (column, value) pairs loaded coalesced,
 // shuffled out one by one; the X-row gathers of a batch are independent, so
 // several are in flight (two interleaved accumulators per slot, fixed order).
+#ifndef K8_UNROLL
+#define K8_UNROLL 32
+#endif
+constexpr int kK8Unroll = K8_UNROLL;
 template <int SLOTS>
 __global__ void csr_spmm_k(long rows, const std::int64_t* __restrict__ rowptr, const std::int32_t* __restrict__ colidx,
                            const double* __restrict__ val, long b, const double* __restrict__ xt, double* Y,
@@ -332,7 +336,7 @@ __global__ void csr_spmm_k(long rows, const std::int64_t* __restrict__ rowptr, c
             const long p = pb + lane;
             const int cj = p < p1 ? colidx[p] : 0;
             const double vj = p < p1 ? val[p] : 0.0;  // padding entries contribute 0
-#pragma unroll 8
+#pragma unroll(kK8Unroll)
             for (int t = 0; t < 32; ++t) {
                 const long col = __shfl_sync(0xffffffffu, cj, t);
                 const double v = __shfl_sync(0xffffffffu, vj, t);
