@@ -98,6 +98,26 @@ __device__ __forceinline__ double spmv_row(long b, long e, const std::int32_t* _
                                            const double* __restrict__ val, const double* __restrict__ x, int lane) {
     double s0 = 0.0, s1 = 0.0;
     long p = b + lane;
+    // 8 gathers in flight per lane; the accumulation order is the 4-wide loop's
+    // (two of its iterations per pass), so the sums are bitwise unchanged
+    for (; p + 224 < e; p += 256) {
+        int c[8];
+        double v[8], xv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            c[u] = idx[p + 32 * u];
+            v[u] = val[p + 32 * u];
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) xv[u] = x[c[u]];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            if (u & 1)
+                s1 = fma(v[u], xv[u], s1);
+            else
+                s0 = fma(v[u], xv[u], s0);
+        }
+    }
     for (; p + 96 < e; p += 128) {
         const int c0 = idx[p], c1 = idx[p + 32], c2 = idx[p + 64], c3 = idx[p + 96];
         const double v0 = val[p], v1 = val[p + 32], v2 = val[p + 64], v3 = val[p + 96];
