@@ -15,6 +15,7 @@
 // Staged in shared memory when it fits (b <= 116); the SH template parameter
 // keeps those accesses LDS/STS instead of generic loads.
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 
 #include "ops.cuh"
@@ -349,6 +350,11 @@ __global__ void __launch_bounds__(kCT) chol_inv_k(double* g, long ldg, double* r
 void chol_inv_upper(Context& ctx, View g, View rinv, int* status, double* diag, double skip_rel,
                     double* trace_out) {
     const int n = static_cast<int>(g.rows);
+    static const bool blocked = [] {
+        const char* e = std::getenv("BLWS_CHOL_BLOCKED");
+        return !(e && e[0] == '0');
+    }();
+    if (blocked && chol_blocked_fits(n)) return chol_inv_blocked(ctx, g, rinv, status, diag, trace_out);
     const long ld = n | 1;
     const long bytes = (2L * ld * n + 2L * n + 34) * 8;
     const bool on_chip = bytes <= kSmemBudget;

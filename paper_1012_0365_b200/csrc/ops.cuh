@@ -66,6 +66,11 @@ void potrf_upper(Context& ctx, View g, int* status, double* diag);
 /// factorising (device-predicated CholQR pass skip); tr(G) -> *trace_out if set.
 void chol_inv_upper(Context& ctx, View g, View rinv, int* status, double* diag, double skip_rel = 0.0,
                     double* trace_out = nullptr);
+/// The same for 112 < n <= 1024 by 112-column blocks (cholblk.cu): diagonal
+/// blocks on cholqr_factor_k, panels / trailing updates / R^{-1} on the GEMM;
+/// no whole-matrix skip mode. chol_inv_upper routes there (BLWS_CHOL_BLOCKED=0: not).
+bool chol_blocked_fits(Index n);
+void chol_inv_blocked(Context& ctx, View g, View rinv, int* status, double* diag, double* trace_out);
 /// One CholQR pass factor for n <= 112 (cholqr.cu): G <- R (upper), rinv <-
 /// R^{-1}; with r_prev, r_out <- R * r_prev (upper) when r_out is set and
 /// rank_out <- #diag(R * r_prev) > 1e-12 sqrt(trace_ref[0]) (trace_ref = null:
