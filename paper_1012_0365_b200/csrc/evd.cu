@@ -539,6 +539,7 @@ void sym_evd_top(Context& ctx, View t, Index want, double* values, View vectors)
         fill(ctx, vectors.left(1), 1.0);
         return;
     }
+    if (sytrd2_fits(n)) return sym_evd_top_two_stage(ctx, t, want, values, vectors);
     const long np = static_cast<long>(n) * (n + 1) / 2;
     const long head = (3L * n + 32 + (n <= 32 * kMaxRowsPerLane ? static_cast<long>(kWarps) * n : 0)) * 8;
     const bool on_chip = head + np * 8 <= kSmemBudget;

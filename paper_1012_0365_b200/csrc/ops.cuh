@@ -95,6 +95,12 @@ void count_diag_above(Context& ctx, View r, const double* sumsq_dev, double scal
 /// Top `want` eigenpairs (descending) of a dense symmetric n x n T:
 /// Householder tridiagonalisation + bisection / inverse iteration + back-transform.
 void sym_evd_top(Context& ctx, View t, Index want, double* values, View vectors);
+/// The same by two-stage tridiagonalisation (sytrd2.cu: dense -> band 8 on
+/// DMMA, bulge chasing as a warp wavefront, back-transformation bt2_k);
+/// sym_evd_top routes there when sytrd2_fits(n): opt-in, BLWS_EVD2=1 (n >= 16,
+/// on-chip sizes); slower than the one-stage kernel at order 200 (2.0 vs 0.74 ms).
+bool sytrd2_fits(Index n);
+void sym_evd_top_two_stage(Context& ctx, View t, Index want, double* values, View vectors);
 /// Top `want` eigenpairs of the symmetric tridiagonal (d, e): values
 /// descending, vectors n x want. Bisection + inverse iteration with cluster
 /// reorthogonalisation.

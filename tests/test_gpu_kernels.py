@@ -108,6 +108,27 @@ def test_sym_evd_matches_oracle(gpu, O, n):
     assert np.linalg.norm(vecs.T @ vecs - np.eye(n)) <= 1e-10
 
 
+@pytest.mark.parametrize("n", [16, 17, 40, 63, 96, 127, 150, 199, 200])
+def test_sym_evd_two_stage(gpu, O, n, monkeypatch):
+    # dense -> band 8 -> tridiagonal (sytrd2.cu), forced on for every order here
+    monkeypatch.setenv("BLWS_EVD2", "1")
+    g = O.Rng(57 + n).gaussian_matrix(n, n)
+    tn_cases = [0.5 * (g + g.T)]
+    # repeated eigenvalues and a zero block: Q diag(3,3,3,1,...,0,0) Q^T
+    q, _ = np.linalg.qr(O.Rng(5 + n).gaussian_matrix(n, n))
+    lam = np.concatenate([[3.0, 3.0, 3.0], np.linspace(1, 0, n - 3)])
+    lam[-min(4, n - 3):] = 0.0
+    tn_cases.append((q * lam) @ q.T)
+    for t in tn_cases:
+        t = 0.5 * (t + t.T)
+        vals, vecs = gpu.sym_evd_small(t)
+        ref_vals, _ = O.sym_evd_small(t)
+        tn = np.linalg.norm(t)
+        assert np.abs(vals - ref_vals).max() <= 1e-12 * tn
+        assert np.linalg.norm(t @ vecs - vecs * vals) <= 1e-10 * tn
+        assert np.linalg.norm(vecs.T @ vecs - np.eye(n)) <= 1e-10
+
+
 @pytest.mark.parametrize("n", [64, 110, 208, 260])
 def test_sym_evd_cluster_tridiagonalisation(gpu, O, n, monkeypatch):
     # opt-in cluster-distributed Householder stage (sytrd_cluster.cu)
