@@ -33,9 +33,11 @@ __global__ void colof_k(long n, const std::int64_t* __restrict__ colptr, std::in
 }
 
 // positions 0..nnz-1, the row histogram and the input checks (flags: bit 0 a
-// row index out of [0, m), bit 1 a non-finite value)
+// row index out of [0, m), bit 1 a non-finite value, bit 2 a column whose row
+// indices do not ascend -- not an error, but the tiled SpMM needs them sorted)
 __global__ void csr_prep_k(long nnz, long m, const std::int32_t* __restrict__ rowidx, const double* __restrict__ val,
-                           std::int64_t* iota, std::int64_t* counts, int* flags) {
+                           const std::int32_t* __restrict__ colof, std::int64_t* iota, std::int64_t* counts,
+                           int* flags) {
     int bad = 0;
     for (long p = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; p < nnz;
          p += static_cast<long>(gridDim.x) * blockDim.x) {
@@ -47,6 +49,7 @@ __global__ void csr_prep_k(long nnz, long m, const std::int32_t* __restrict__ ro
             atomicAdd(reinterpret_cast<unsigned long long*>(counts + r), 1ull);
         }
         if (!isfinite(val[p])) bad |= 2;
+        if (p > 0 && colof[p - 1] == colof[p] && rowidx[p - 1] > r) bad |= 4;
     }
     bad = __reduce_or_sync(0xffffffffu, bad);
     if ((threadIdx.x & 31) == 0 && bad) atomicOr(flags, bad);
@@ -61,9 +64,10 @@ __global__ void csr_colidx_k(long nnz, const std::int64_t* __restrict__ perm, co
 
 }  // namespace
 
-void build_csr_device(Context& ctx, Index m, Index n, Index nnz, const std::int64_t* colptr,
+bool build_csr_device(Context& ctx, Index m, Index n, Index nnz, const std::int64_t* colptr,
                       const std::int32_t* rowidx, const double* val, std::int64_t* rowptr, std::int32_t* colidx,
                       std::int64_t* perm, std::int32_t* colof) {
+    bool rows_ascend = true;
     DBuf<int> flags(ctx, 1);
     zero(ctx, flags.get(), sizeof(int));
     zero(ctx, rowptr, sizeof(std::int64_t) * static_cast<size_t>(m + 1));
@@ -78,7 +82,7 @@ void build_csr_device(Context& ctx, Index m, Index n, Index nnz, const std::int6
         DBuf<std::int64_t> iota(ctx, static_cast<size_t>(nnz)), counts(ctx, static_cast<size_t>(m + 1));
         DBuf<std::int32_t> keys_out(ctx, static_cast<size_t>(nnz));
         zero(ctx, counts.get(), sizeof(std::int64_t) * static_cast<size_t>(m + 1));
-        csr_prep_k<<<blocks_for(nnz), kT, 0, ctx.stream()>>>(nnz, m, rowidx, val, iota.get(), counts.get(),
+        csr_prep_k<<<blocks_for(nnz), kT, 0, ctx.stream()>>>(nnz, m, rowidx, val, colof, iota.get(), counts.get(),
                                                              flags.get());
         ctx.note_launch();
         ctx.check_launch("csr_prep_k");
@@ -87,6 +91,7 @@ void build_csr_device(Context& ctx, Index m, Index n, Index nnz, const std::int6
         ctx.sync();
         if (hf & 1) throw std::invalid_argument("SparseOperator: row index out of range");
         if (hf & 2) throw std::invalid_argument("SparseOperator: non-finite entries");
+        rows_ascend = !(hf & 4);
         int end_bit = 1;
         while (end_bit < 31 && (1L << end_bit) < m) ++end_bit;
         size_t tsort = 0, tscan = 0;
@@ -104,6 +109,7 @@ void build_csr_device(Context& ctx, Index m, Index n, Index nnz, const std::int6
         ctx.note_launch();
         ctx.check_launch("csr_colidx_k");
     }
+    return rows_ascend;
 }
 
 }  // namespace blws

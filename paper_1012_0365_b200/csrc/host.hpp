@@ -196,6 +196,7 @@ private:
     DBuf<std::int64_t> rowptr_, colptr_, perm_;  // perm: csr position -> csc position
     DBuf<std::int32_t> colidx_, rowidx_, colof_;
     DBuf<double> val_csr_, val_csc_;
+    bool csc_rows_ascend_ = true;  // the tiled SpMM may run on the CSC arrays (W^T x)
 };
 
 // ------------------------------------------------------------ warm start

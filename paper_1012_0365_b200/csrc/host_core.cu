@@ -469,8 +469,8 @@ SparseOperator::SparseOperator(Context& ctx, Index m, Index n, Index nnz, const 
         BLWS_CUDA(cudaMemcpyAsync(val_csc_.get(), values, sizeof(double) * nnz, cudaMemcpyHostToDevice,
                                   ctx.stream()));
     }
-    build_csr_device(ctx, m, n, nnz, colptr_.get(), rowidx_.get(), val_csc_.get(), rowptr_.get(), colidx_.get(),
-                     perm_.get(), colof_.get());
+    csc_rows_ascend_ = build_csr_device(ctx, m, n, nnz, colptr_.get(), rowidx_.get(), val_csc_.get(), rowptr_.get(),
+                                        colidx_.get(), perm_.get(), colof_.get());
     gather_values(ctx, nnz_, val_csr_.get(), val_csc_.get(), perm_.get());
     ctx.sync();
 }
@@ -506,10 +506,10 @@ void SparseOperator::pair_block_impl(View left, View right, View top, View bot) 
         {
             AuxScope aux(ctx_);
             csr_spmm(ctx_, n_, colptr_.get(), rowidx_.get(), val_csc_.get(), m_, b, left.p, left.ld, part.get(), npad,
-                     scratch2.get());
+                     scratch2.get(), csc_rows_ascend_ ? nnz_ : -1);
             aux.main();
             csr_spmm(ctx_, m_, rowptr_.get(), colidx_.get(), val_csr_.get(), n_, b, xfull.get(), npad, top.p, top.ld,
-                     scratch.get());
+                     scratch.get(), nnz_);
         }
         scatter_cols(*this, View{part.get(), npad, b, npad}, bot);
         return;
@@ -520,17 +520,17 @@ void SparseOperator::pair_block_impl(View left, View right, View top, View bot) 
     AuxScope aux(ctx_);  // W^T x on the auxiliary stream, overlapping W x
     if (reduce && bot.ld != n_) {
         csr_spmm(ctx_, n_, colptr_.get(), rowidx_.get(), val_csc_.get(), m_, b, left.p, left.ld, part.get(), n_,
-                 scratch2.get());
+                 scratch2.get(), csc_rows_ascend_ ? nnz_ : -1);
         ctx_.allreduce_sum(part.get(), static_cast<size_t>(n_ * b));
         copy(ctx_, bot, View{part.get(), n_, b, n_});
     } else {
         csr_spmm(ctx_, n_, colptr_.get(), rowidx_.get(), val_csc_.get(), m_, b, left.p, left.ld, bot.p, bot.ld,
-                 scratch2.get());
+                 scratch2.get(), csc_rows_ascend_ ? nnz_ : -1);
         if (reduce) ctx_.allreduce_sum(bot.p, static_cast<size_t>(n_ * b));
     }
     aux.main();
     csr_spmm(ctx_, m_, rowptr_.get(), colidx_.get(), val_csr_.get(), n_, b, right.p, right.ld, top.p, top.ld,
-             scratch.get());
+             scratch.get(), nnz_);
 }
 
 void SparseOperator::pair_impl(const double* left, const double* right, double* top, double* bot) {

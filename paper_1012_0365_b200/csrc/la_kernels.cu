@@ -2,6 +2,11 @@
 #include <algorithm>
 #include <cmath>
 
+#include <climits>
+#include <cstdlib>
+#include <cstring>
+
+#include "bulk.cuh"
 #include "ops.cuh"
 
 namespace blws {
@@ -321,6 +326,9 @@ __global__ void to_row_major_k(const double* X, long ld, long rows, long b, doub
 #define K8_UNROLL 32
 #endif
 constexpr int kK8Unroll = K8_UNROLL;
+#ifndef K8_DEFAULT_MODE
+#define K8_DEFAULT_MODE 0  // 0 gather, 1 tiled when it pays
+#endif
 template <int SLOTS>
 __global__ void csr_spmm_k(long rows, const std::int64_t* __restrict__ rowptr, const std::int32_t* __restrict__ colidx,
                            const double* __restrict__ val, long b, const double* __restrict__ xt, double* Y,
@@ -352,6 +360,168 @@ __global__ void csr_spmm_k(long rows, const std::int64_t* __restrict__ rowptr, c
         for (int q = 0; q < SLOTS; ++q) {
             const long c = lane + 32 * q;
             if (c < b) Y[i + c * ldy] = acc[q][0] + acc[q][1];
+        }
+    }
+}
+
+// K8, tiled. The gather kernel above re-reads a whole X row from L2 for every
+// nonzero (8 b bytes per nonzero: L2-bound). Here a CTA owns a group of rows
+// (kK8Warps consumer warps x RPW rows each, accumulators in registers) and
+// streams X through shared memory in tiles of T rows: bulk copies into a
+// kK8Stages-deep mbarrier ring, issued by one producer warp. The column indices
+// of a row ascend, so the row's nonzeros inside the current tile are the next
+// ones at its cursor. Each row keeps a 32-entry (column, value) batch in
+// registers, aligned as in csr_spmm_k, and entry t goes into accumulator t & 1:
+// the same sums in the same order as the gather kernel. L2 traffic drops from
+// 8 b nnz to (row groups) x 8 b ncols.
+constexpr int kK8Warps = 15;  // + the producer warp = 512 threads (128 registers each)
+constexpr int kK8Stages = 3;
+constexpr int kK8MaxRpw = 6;
+constexpr int kK8TileBytes = 64 * 1024;
+
+// the row's (column, value) stream comes from DRAM and is read once: the batch
+// after the one just loaded is pulled into L1, the one after that into L2, so
+// a reload does not stall its warp for a DRAM round trip
+__device__ __forceinline__ void k8_prefetch(const std::int32_t* colidx, const double* val, long base, int left,
+                                            int lane) {
+#ifndef K8T_NO_PREFETCH
+    if (lane + 32 < left) {
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(colidx + base + 32 + lane));
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(val + base + 32 + lane));
+    }
+    if (lane + 64 < left) {
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(colidx + base + 64 + lane));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(val + base + 64 + lane));
+    }
+#endif
+}
+
+template <int SLOTS, int RPW>
+__global__ void __launch_bounds__((kK8Warps + 1) * 32, 1)
+    csr_spmm_tiled_k(long rows, long ncols, const std::int64_t* __restrict__ rowptr,
+                     const std::int32_t* __restrict__ colidx, const double* __restrict__ val, int b,
+                     const double* __restrict__ xt, double* Y, long ldy, int T, long ngroups, long rpc) {
+    extern __shared__ __align__(128) unsigned char k8_smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(k8_smem);
+    uint64_t* empty = full + kK8Stages;
+    double* tiles = reinterpret_cast<double*>(k8_smem + 128);
+    const long tile_elems = static_cast<long>(T) * b;  // 8 T b is a multiple of 128 (T % 16 == 0)
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long ntiles = (ncols + T - 1) / T;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kK8Stages; ++s) {
+            gemm_tma::mbar_init(full + s, 1);
+            gemm_tma::mbar_init(empty + s, kK8Warps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    long it = 0;  // tiles this CTA has streamed: ring slot it % stages, use it / stages
+    if (warp == kK8Warps) {  // producer
+        if (lane == 0) {
+            for (long g = blockIdx.x; g < ngroups; g += gridDim.x)
+                for (long c = 0; c < ntiles; ++c, ++it) {
+                    const int s = static_cast<int>(it % kK8Stages);
+                    const long use = it / kK8Stages;
+                    if (use > 0) gemm_tma::mbar_wait(empty + s, static_cast<uint32_t>((use - 1) & 1));
+                    const long r0 = c * T;
+                    const long cnt = min(static_cast<long>(T), ncols - r0) * b;
+                    const long even = cnt & ~1L;  // bulk copies move 16-byte multiples
+                    double* dst = tiles + s * tile_elems;
+                    const double* src = xt + r0 * b;
+                    if (cnt & 1) dst[cnt - 1] = src[cnt - 1];  // ordered by the arrive below (release)
+                    gemm_tma::mbar_expect_tx(full + s, static_cast<uint32_t>(even * 8));
+                    if (even > 0) bulk_g2s(dst, src, static_cast<uint32_t>(even * 8), full + s);
+                }
+        }
+        return;
+    }
+    for (long g = blockIdx.x; g < ngroups; g += gridDim.x) {
+        const long gr0 = g * rpc, gr1 = min(rows, gr0 + rpc);
+        double acc[RPW][SLOTS][2];
+        long base[RPW];  // position of the batch's entry 0
+        int left[RPW];   // entries of the row from base on
+        int off[RPW];    // entries of the batch already consumed
+        int cj[RPW];
+        double vj[RPW];
+#pragma unroll
+        for (int r = 0; r < RPW; ++r) {
+#pragma unroll
+            for (int q = 0; q < SLOTS; ++q) acc[r][q][0] = acc[r][q][1] = 0.0;
+            const long i = gr0 + warp + static_cast<long>(r) * kK8Warps;
+            base[r] = i < gr1 ? rowptr[i] : 0;
+            left[r] = i < gr1 ? static_cast<int>(rowptr[i + 1] - base[r]) : 0;
+            off[r] = 0;
+            cj[r] = lane < left[r] ? colidx[base[r] + lane] : INT_MAX;
+            vj[r] = lane < left[r] ? val[base[r] + lane] : 0.0;
+            k8_prefetch(colidx, val, base[r], left[r], lane);
+        }
+        for (long c = 0; c < ntiles; ++c, ++it) {
+            const int s = static_cast<int>(it % kK8Stages);
+            gemm_tma::mbar_wait(full + s, static_cast<uint32_t>((it / kK8Stages) & 1));
+            const double* xs = tiles + s * tile_elems;
+            const int j0 = static_cast<int>(c * T);
+            const int j1 = static_cast<int>(min(ncols, static_cast<long>(j0) + T));
+#pragma unroll
+            for (int r = 0; r < RPW; ++r) {
+                while (true) {
+                    // ascending columns: the entries inside the tile are a run starting at off
+                    const int cnt = __popc(__ballot_sync(0xffffffffu, lane >= off[r] && cj[r] < j1));
+                    int t = off[r];
+                    const int te = t + cnt;
+#define K8_STEP(P, TT)                                                                      \
+    {                                                                                       \
+        const int col = __shfl_sync(0xffffffffu, cj[r], (TT)) - j0;                         \
+        const double v = __shfl_sync(0xffffffffu, vj[r], (TT));                             \
+        const double* xr = xs + col * b;                                                    \
+        _Pragma("unroll") for (int q = 0; q < SLOTS; ++q) {                                 \
+            const int cc = lane + 32 * q;                                                   \
+            if (cc < b) acc[r][q][P] = fma(v, xr[cc], acc[r][q][P]);                        \
+        }                                                                                   \
+    }
+                    if (t < te && (t & 1)) {
+                        K8_STEP(1, t);
+                        ++t;
+                    }
+                    for (; t + 3 < te; t += 4) {  // straight-line: the four entries' loads go out together
+                        K8_STEP(0, t);
+                        K8_STEP(1, t + 1);
+                        K8_STEP(0, t + 2);
+                        K8_STEP(1, t + 3);
+                    }
+                    if (t + 1 < te) {
+                        K8_STEP(0, t);
+                        K8_STEP(1, t + 1);
+                        t += 2;
+                    }
+                    if (t < te) K8_STEP(0, t);
+#undef K8_STEP
+                    off[r] = te;
+                    if (te == 32 && left[r] > 32) {  // batch used up, the row goes on
+                        base[r] += 32;
+                        left[r] -= 32;
+                        off[r] = 0;
+                        cj[r] = lane < left[r] ? colidx[base[r] + lane] : INT_MAX;
+                        vj[r] = lane < left[r] ? val[base[r] + lane] : 0.0;
+                        k8_prefetch(colidx, val, base[r], left[r], lane);
+                    } else {
+                        break;
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) gemm_tma::mbar_arrive(empty + s);
+        }
+#pragma unroll
+        for (int r = 0; r < RPW; ++r) {
+            const long i = gr0 + warp + static_cast<long>(r) * kK8Warps;
+            if (i < gr1) {
+#pragma unroll
+                for (int q = 0; q < SLOTS; ++q) {
+                    const int cc = lane + 32 * q;
+                    if (cc < b) Y[i + cc * ldy] = acc[r][q][0] + acc[r][q][1];
+                }
+            }
         }
     }
 }
@@ -591,11 +761,86 @@ void dot(Context& ctx, Index n, const double* x, const double* y, double* out) {
     LAUNCH(ctx, "reduce");
 }
 
+namespace {
+
+// BLWS_K8=gather keeps the L2 gather kernel, BLWS_K8=tiled forces the tiled one
+// wherever it can run; default: tiled when the X re-streaming is well below
+// the gather traffic
+int k8_mode() {
+    static const int mode = [] {
+        const char* e = std::getenv("BLWS_K8");
+        if (e && std::strcmp(e, "gather") == 0) return 0;
+        if (e && std::strcmp(e, "tiled") == 0) return 2;
+        return K8_DEFAULT_MODE;
+    }();
+    return mode;
+}
+
+template <int SLOTS, int RPW>
+void launch_k8_tiled(Context& ctx, unsigned grid, size_t smem, Index rows, Index ncols, const std::int64_t* rowptr,
+                     const std::int32_t* colidx, const double* val, Index b, const double* xt, double* Y, Index ldy,
+                     int T, long ngroups, long rpc) {
+    static bool once = [] {
+        BLWS_CUDA(cudaFuncSetAttribute(csr_spmm_tiled_k<SLOTS, RPW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       128 + kK8Stages * kK8TileBytes));
+        return true;
+    }();
+    (void)once;
+    csr_spmm_tiled_k<SLOTS, RPW><<<grid, (kK8Warps + 1) * 32, smem, ctx.stream()>>>(
+        rows, ncols, rowptr, colidx, val, static_cast<int>(b), xt, Y, ldy, T, ngroups, rpc);
+}
+
+template <int SLOTS>
+void launch_k8_tiled_rpw(int rpw, Context& ctx, unsigned grid, size_t smem, Index rows, Index ncols,
+                         const std::int64_t* rowptr, const std::int32_t* colidx, const double* val, Index b,
+                         const double* xt, double* Y, Index ldy, int T, long ngroups, long rpc) {
+#define K8_CASE(R)                                                                                              \
+    case R:                                                                                                     \
+        launch_k8_tiled<SLOTS, R>(ctx, grid, smem, rows, ncols, rowptr, colidx, val, b, xt, Y, ldy, T, ngroups, \
+                                  rpc);                                                                         \
+        break;
+    switch (rpw) {
+        K8_CASE(1) K8_CASE(2) K8_CASE(3) K8_CASE(4) K8_CASE(5) K8_CASE(6)
+        default: throw std::logic_error("csr_spmm_tiled: rows per warp");
+    }
+#undef K8_CASE
+}
+
+// true when the tiled kernel ran
+bool csr_spmm_tiled(Context& ctx, Index rows, const std::int64_t* rowptr, const std::int32_t* colidx,
+                    const double* val, Index ncols, Index b, const double* xt, double* Y, Index ldy, Index nnz) {
+    const int mode = k8_mode();
+    if (mode == 0 || nnz < 0 || b <= 8 || b > 64 || ncols >= INT_MAX) return false;
+    const long sms = ctx.sm_count();
+    // row groups: a multiple of the SM count, at most kK8Warps * kK8MaxRpw rows each
+    const long per = static_cast<long>(kK8Warps) * kK8MaxRpw;
+    const long ngroups = sms * ((rows + sms * per - 1) / (sms * per));
+    const long rpc = (rows + ngroups - 1) / ngroups;
+    const int rpw = static_cast<int>((rpc + kK8Warps - 1) / kK8Warps);
+    // every group streams X once: worth it when that is well below one X row per nonzero
+    if (mode == 1 && nnz < 4 * ngroups * ncols) return false;
+    int T = static_cast<int>((kK8TileBytes / (8 * b)) & ~15L);
+    T = static_cast<int>(std::min<long>(T, (ncols + 15) & ~15L));
+    const size_t smem = 128 + static_cast<size_t>(kK8Stages) * T * b * 8;
+    const unsigned grid = static_cast<unsigned>(std::min(ngroups, sms));
+    if (b <= 32)
+        launch_k8_tiled_rpw<1>(rpw, ctx, grid, smem, rows, ncols, rowptr, colidx, val, b, xt, Y, ldy, T, ngroups, rpc);
+    else
+        launch_k8_tiled_rpw<2>(rpw, ctx, grid, smem, rows, ncols, rowptr, colidx, val, b, xt, Y, ldy, T, ngroups, rpc);
+    return true;
+}
+
+}  // namespace
+
 void csr_spmm(Context& ctx, Index rows, const std::int64_t* rowptr, const std::int32_t* colidx, const double* val,
-              Index ncols, Index b, const double* X, Index ldx, double* Y, Index ldy, double* xt) {
+              Index ncols, Index b, const double* X, Index ldx, double* Y, Index ldy, double* xt, Index nnz) {
     if (rows <= 0 || b <= 0) return;
     to_row_major_k<<<grid_for(ncols * b), kThreads, 0, ctx.stream()>>>(X, ldx, ncols, b, xt);
     LAUNCH(ctx, "to_row_major");
+    if (csr_spmm_tiled(ctx, rows, rowptr, colidx, val, ncols, b, xt, Y, ldy, nnz)) {
+        LAUNCH(ctx, "csr_spmm_tiled");
+        return;
+    }
     const long warps_needed = rows;
     const unsigned blocks = static_cast<unsigned>(std::min<long>(8L * 1024, (warps_needed * 32 + kThreads - 1) / kThreads));
     if (b == 1)

@@ -116,14 +116,18 @@ void dot(Context& ctx, Index n, const double* x, const double* y, double* out);
 
 // ------------------------------------------------------------------ sparse (K8, K9)
 /// Y (rows x b) = S * X where S is CSR (rowptr, colidx, val); X col-major.
-/// xt is scratch of cols(S) * b doubles (row-major copy of X).
+/// xt is scratch of cols(S) * b doubles (row-major copy of X). nnz >= 0 with
+/// ascending column indices in every row allows the shared-memory tiled kernel
+/// (csr_spmm_tiled_k) when it pays; nnz < 0 keeps the L2 gather kernel.
 void csr_spmm(Context& ctx, Index rows, const std::int64_t* rowptr, const std::int32_t* colidx,
               const double* val, Index ncols, Index b, const double* X, Index ldx, double* Y, Index ldy,
-              double* xt);
+              double* xt, Index nnz = -1);
 /// CSR view of a CSC pattern on the device (csr_build.cu): rowptr (m + 1),
 /// colidx and perm (CSR slot -> CSC position) in column order within a row,
-/// colof (column of each CSC position); throws on bad row indices / non-finite values
-void build_csr_device(Context& ctx, Index m, Index n, Index nnz, const std::int64_t* colptr,
+/// colof (column of each CSC position); throws on bad row indices / non-finite values.
+/// Returns whether the row indices ascend within every column (the CSR columns
+/// within a row always do): what the tiled SpMM needs of the CSC arrays.
+bool build_csr_device(Context& ctx, Index m, Index n, Index nnz, const std::int64_t* colptr,
                       const std::int32_t* rowidx, const double* val, std::int64_t* rowptr, std::int32_t* colidx,
                       std::int64_t* perm, std::int32_t* colof);
 void gather_values(Context& ctx, Index nnz, double* dst, const double* src, const std::int64_t* perm);

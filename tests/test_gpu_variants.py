@@ -10,6 +10,7 @@ oracle on the same seeded inputs.
   BLWS_SYTRD=cluster the cluster tridiagonalisation below order 224
   BLWS_ORMTR=single one reflector at a time in the back-transformation (ormtr_full_k)
   BLWS_EXACT=1, BLWS_GRAPHS=0  the host-branching blws_svd path, no CUDA graphs
+  BLWS_K8=tiled     the shared-memory tiled SpMM (csr_spmm_tiled_k) wherever it can run
 """
 import os
 import subprocess
@@ -62,7 +63,7 @@ print("variant ok")
 
 @pytest.mark.parametrize("env", [{"BLWS_TMA": "0"}, {"BLWS_K7": "cpasync"}, {"BLWS_COOP": "cols"},
                                  {"BLWS_NO_COOP": "1"}, {"BLWS_SYTRD": "cluster"}, {"BLWS_ORMTR": "single"},
-                                 {"BLWS_EXACT": "1", "BLWS_GRAPHS": "0"}])
+                                 {"BLWS_EXACT": "1", "BLWS_GRAPHS": "0"}, {"BLWS_K8": "tiled"}])
 def test_switch_variant_matches_oracle(env):
     e = dict(os.environ)
     e.update(env)
@@ -101,3 +102,45 @@ def test_small_dense_limit(strict):
         assert "raised sym_evd_tridiagonal: too large" in r.stdout, r.stdout
     else:
         assert "completed 410" in r.stdout, r.stdout
+
+
+K8_CASE = r"""
+import sys, numpy as np, scipy.sparse as sp
+sys.path.insert(0, %(root)r)
+import paper_1012_0365_b200 as B
+out = {}
+for ci, (m, n, dens, b) in enumerate([(21000, 1500, 0.01, 9), (3001, 2999, 0.05, 33), (777, 20011, 0.03, 17),
+                                      (14300, 500, 0.2, 55), (5000, 5000, 0.1, 64)]):
+    rs = np.random.default_rng(7 * ci + b)
+    a = sp.random(m, n, density=dens, format="csc", random_state=rs, data_rvs=rs.standard_normal).tolil()
+    a[5, :] = rs.standard_normal(n)   # a dense row
+    a[:, 7] = 0.0                     # an empty column
+    a = a.tocsc(); a.sort_indices()
+    op = B.api.SparseOperator(m, n, a.indptr.astype(np.int64), a.indices.astype(np.int32), a.data.copy())
+    left, right = rs.standard_normal((m, b)), rs.standard_normal((n, b))
+    top, bot = op.apply_pair_block(left, right)
+    rt, rb = a @ right, a.T @ left
+    assert np.abs(top - rt).max() <= 1e-12 * np.abs(rt).max(), ci
+    assert np.abs(bot - rb).max() <= 1e-12 * np.abs(rb).max(), ci
+    out["top%%d" %% ci], out["bot%%d" %% ci] = top, bot
+np.savez(sys.argv[1], **out)
+print("k8 ok")
+"""
+
+
+def test_k8_tiled_bitwise_equals_gather(tmp_path):
+    # the tiled SpMM keeps the gather kernel's accumulation order: same bits,
+    # ragged shapes (more row groups than SMs, a dense row, an empty column,
+    # odd b so the last tile's bulk copy has a scalar tail)
+    import numpy as np
+
+    files = {}
+    for mode in ("gather", "tiled"):
+        e = dict(os.environ)
+        e["BLWS_K8"] = mode
+        files[mode] = str(tmp_path / (mode + ".npz"))
+        r = subprocess.run([sys.executable, "-c", K8_CASE % {"root": ROOT}, files[mode]], env=e,
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0 and "k8 ok" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
+    g, t = np.load(files["gather"]), np.load(files["tiled"])
+    assert all(np.array_equal(g[k], t[k]) for k in g.files)
