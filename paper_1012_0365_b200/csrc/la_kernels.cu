@@ -340,20 +340,28 @@ __global__ void csr_spmm_k(long rows, const std::int64_t* __restrict__ rowptr, c
         double acc[SLOTS][2];
 #pragma unroll
         for (int q = 0; q < SLOTS; ++q) acc[q][0] = acc[q][1] = 0.0;
+        // per slot, the lane's column of X^T as a byte pointer: an X-row element is then one
+        // 32 x 32 -> 64-bit multiply-add away (col * 8b). Lanes past b read column b - 1 and
+        // accumulate values that are never stored, so the loads and FMAs carry no predicate
+        // (the predicated form cost ~25 instructions per nonzero: 64-bit index arithmetic and
+        // a register-pair move after every predicated DFMA; ncu r02i)
+        const char* xl[SLOTS];
+#pragma unroll
+        for (int q = 0; q < SLOTS; ++q)
+            xl[q] = reinterpret_cast<const char*>(xt + min(static_cast<long>(lane + 32 * q), b - 1));
+        const unsigned bbytes = static_cast<unsigned>(b) * 8u;
         for (long pb = p0; pb < p1; pb += 32) {
             const long p = pb + lane;
             const int cj = p < p1 ? colidx[p] : 0;
             const double vj = p < p1 ? val[p] : 0.0;  // padding entries contribute 0
 #pragma unroll(kK8Unroll)
             for (int t = 0; t < 32; ++t) {
-                const long col = __shfl_sync(0xffffffffu, cj, t);
+                const unsigned long long ro =
+                    static_cast<unsigned long long>(static_cast<unsigned>(__shfl_sync(0xffffffffu, cj, t))) * bbytes;
                 const double v = __shfl_sync(0xffffffffu, vj, t);
-                const double* xr = xt + col * b;
 #pragma unroll
-                for (int q = 0; q < SLOTS; ++q) {
-                    const long c = lane + 32 * q;
-                    if (c < b) acc[q][t & 1] = fma(v, xr[c], acc[q][t & 1]);
-                }
+                for (int q = 0; q < SLOTS; ++q)
+                    acc[q][t & 1] = fma(v, *reinterpret_cast<const double*>(xl[q] + ro), acc[q][t & 1]);
             }
         }
 #pragma unroll
